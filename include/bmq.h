@@ -1,0 +1,239 @@
+/* bmq.h — C ABI of the B200-native compressed-block state-vector engine
+ * (libbmq.so, built from paper_2410_14088_b200/csrc).
+ *
+ * This is the drop-in boundary for the hot path of the BMQSim reference
+ * (/root/reference/proj/include/cbq, header-only C++20). The reference has no
+ * FFI of its own; each entry point below replaces the reference C++ symbol it
+ * cites, with plain pointers and sizes so that ctypes / cgo / JNI / N-API can
+ * bind it directly. The C++ drop-in surface in
+ * include/bmq/cbq.hpp wraps these calls back into the reference's types
+ * (Circuit, PartitionPlan, Simulator, compress_block, ...).
+ *
+ * Conventions
+ *  - Every function returns a bmq_status; on failure bmq_last_error() holds a
+ *    thread-local message with the same text the reference exception carries
+ *    (e.g. "sign bitmap truncated", "stage 3: group with outer value 1: ...").
+ *  - Host pointers everywhere; device memory is owned by the library.
+ *  - Amplitude arrays are interleaved complex128 (re, im), block scalar
+ *    arrays are the reference's planar layout (2^b real parts, then 2^b
+ *    imaginary parts, engine.hpp:166-180).
+ *  - Compute entry points run on the CUDA device (sm_100a). There is no CPU
+ *    fallback: without a device they return BMQ_ERR_NO_DEVICE.
+ */
+#ifndef BMQ_H
+#define BMQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum bmq_status {
+    BMQ_OK = 0,
+    BMQ_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument            */
+    BMQ_ERR_LOGIC = 2,            /* std::logic_error                 */
+    BMQ_ERR_CODEC = 3,            /* cbq::CodecError  (bitmap.hpp:14) */
+    BMQ_ERR_STORE = 4,            /* cbq::StoreError  (store.hpp:23)  */
+    BMQ_ERR_ENGINE = 5,           /* cbq::EngineError (engine.hpp:18) */
+    BMQ_ERR_QASM = 6,             /* cbq::QasmError   (qasm.hpp:17)   */
+    BMQ_ERR_CUDA = 7,
+    BMQ_ERR_NO_DEVICE = 8,
+    BMQ_ERR_OUT_OF_MEMORY = 9,
+    BMQ_ERR_BUFFER_TOO_SMALL = 10
+} bmq_status;
+
+/* Gate kinds in the reference order (circuit.hpp:20-22). */
+typedef enum bmq_gate_kind {
+    BMQ_GATE_H = 0, BMQ_GATE_X, BMQ_GATE_Y, BMQ_GATE_Z, BMQ_GATE_S, BMQ_GATE_SDG,
+    BMQ_GATE_T, BMQ_GATE_TDG, BMQ_GATE_RX, BMQ_GATE_RY, BMQ_GATE_RZ, BMQ_GATE_P,
+    BMQ_GATE_CX, BMQ_GATE_CZ, BMQ_GATE_CP
+} bmq_gate_kind;
+
+/* cbq::Gate (circuit.hpp:65-72). For two-qubit kinds q0 is the HIGH bit of
+ * the 2-bit sub-index (CX: q0 = control). 24 bytes. */
+typedef struct bmq_gate {
+    uint32_t kind;
+    uint32_t q0;
+    uint32_t q1;
+    uint32_t reserved;
+    double angle;
+} bmq_gate;
+
+/* cbq::Stage (partition.hpp:36-40): gates [gate_begin, gate_end) whose global
+ * operands lie in inner[0..inner_count) (sorted ascending, each >= b). */
+typedef struct bmq_stage {
+    uint64_t gate_begin;
+    uint64_t gate_end;
+    uint32_t inner_count;
+    uint32_t reserved;
+    uint32_t inner[64];
+} bmq_stage;
+
+/* cbq::Config (engine.hpp:23-37) plus device-side knobs. */
+typedef struct bmq_config {
+    uint32_t block_bits;         /* b; reference default 1 */
+    uint32_t inner_size;         /* reference default 2 */
+    double error_bound;          /* point-wise relative bound b_r; default 1e-3 */
+    uint64_t memory_budget;      /* store budget for the reference's accounting; UINT64_MAX = unlimited */
+    uint32_t workers;            /* accepted for API parity; device concurrency is streams */
+    uint32_t compress;           /* 1 = compressed payloads, 0 = raw little-endian doubles */
+    uint32_t verify_cap_qubits;  /* default 24 */
+    int32_t device;              /* CUDA ordinal, default 0 */
+    uint64_t device_pool_bytes;  /* per payload pool (x2); 0 = automatic */
+    uint64_t work_bytes;         /* dense group working set; 0 = automatic */
+    uint32_t flags;              /* BMQ_FLAG_* */
+    uint32_t reserved;
+} bmq_config;
+
+/* Skip groups whose blocks are all ALL_ZERO (bit-exact: linear gates map
+ * 0 -> 0 and the ALL_ZERO payload is canonical, codec.hpp:263-271). */
+#define BMQ_FLAG_ZERO_GROUP_SKIP 0x1u
+/* Skip blocks on which every gate of the stage acts as the identity
+ * (diagonal-only stages whose controls are not all set for the block);
+ * bit-exact because compress(decompress(p)) == p for every payload p the
+ * device codec emits (checked per error bound when the tables are built). */
+#define BMQ_FLAG_IDENTITY_SKIP 0x2u
+
+/* cbq::SimulationReport (engine.hpp:39-53) plus device-side counters. */
+typedef struct bmq_report {
+    uint64_t qubits;
+    uint64_t gate_count;
+    uint64_t stage_count;
+    uint64_t max_footprint_bytes;   /* replayed in the reference's sequential put order */
+    double standard_bytes;          /* 2^(n+4) */
+    double compression_ratio;       /* standard_bytes / max_footprint_bytes */
+    uint64_t spilled_blocks;
+    double wall_ms;                 /* host wall clock of run(), as the reference */
+    int32_t has_fidelity;
+    int32_t reserved;
+    double fidelity;
+    double final_norm;
+    uint64_t stage_compress_calls;
+    uint64_t stage_decompress_calls;
+    /* device-side extras */
+    double device_ms;               /* CUDA-event time of the stage loop */
+    uint64_t groups_processed;      /* groups that went through decompress/gates/compress */
+    uint64_t groups_skipped;        /* zero / identity groups */
+    uint64_t blocks_processed;
+    uint64_t payload_bytes_read;    /* compressed bytes consumed by processed groups */
+    uint64_t payload_bytes_written;
+    uint64_t dense_bytes;           /* 32 B x amplitudes of processed groups (roofline model) */
+    uint64_t kernel_launches;
+    uint64_t device_peak_bytes;     /* pools + working set high-water */
+    uint64_t gate_passes;
+} bmq_report;
+
+/* ------------------------------------------------------------ host-only
+ * (descriptor logic; callable without a GPU) */
+
+const char* bmq_last_error(void);
+const char* bmq_version(void);
+int bmq_device_count(int* count);
+
+/* ErrorBound (codec.hpp:19-29): log2_abs = log2(1 + b_r). */
+int bmq_error_bound(double b_r, double* log2_abs);
+
+/* unitary2 / unitary4 (circuit.hpp:133-198): row-major, interleaved re/im;
+ * writes 8 doubles (1-qubit) or 32 doubles (2-qubit). */
+int bmq_gate_unitary(const bmq_gate* gate, double* out);
+
+/* Circuit(n) + Circuit::add validation (circuit.hpp:103-127). */
+int bmq_circuit_validate(uint32_t num_qubits, const bmq_gate* gates, uint64_t count);
+
+/* generate_benchmark (benchmarks.hpp:148-166); name in {ghz, cat_state, bv,
+ * qft, qaoa}. *count receives the full gate count even when cap is short. */
+int bmq_generate_benchmark(const char* name, uint32_t num_qubits, uint32_t layers, uint64_t seed,
+                           const char* secret, bmq_gate* out, uint64_t cap, uint64_t* count);
+
+/* partition_circuit (partition.hpp:59-101). */
+int bmq_partition(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, uint32_t block_bits,
+                  uint32_t inner_size, bmq_stage* out, uint64_t cap, uint64_t* num_stages);
+
+/* enumerate_groups (partition.hpp:120-153): block ids row-major
+ * (group o, inner value v) -> ids[o * 2^|inner| + v]. */
+int bmq_enumerate_groups(uint32_t num_qubits, uint32_t block_bits, const bmq_stage* stage,
+                         uint64_t* ids, uint64_t cap, uint64_t* count);
+
+/* buffer_bit_of_qubit (partition.hpp:158-169). */
+int bmq_buffer_bit_of_qubit(uint32_t num_qubits, uint32_t block_bits, const bmq_stage* stage,
+                            uint32_t qubit, uint32_t* bit);
+
+/* Upper bound on compress output bytes for one block of n scalars. */
+uint64_t bmq_compress_bound(uint64_t scalar_count);
+
+/* ------------------------------------------------------- device compute */
+
+/* compress_block (codec.hpp:227-295) for nblocks blocks of n scalars each
+ * (scalars[k*n .. k*n+n)). Payloads are written back to back into out;
+ * sizes[k] receives each payload's length. Byte-identical to the reference. */
+int bmq_compress_blocks(const double* scalars, uint64_t nblocks, uint64_t scalars_per_block,
+                        double error_bound, uint8_t* out, uint64_t out_cap, uint64_t* sizes);
+
+/* decompress_block (codec.hpp:299-344) for nblocks payloads (payloads +
+ * offsets[k], sizes[k] bytes). Scalars are written back to back into out;
+ * counts[k] receives each block's scalar count. Bit-identical values. */
+int bmq_decompress_blocks(const uint8_t* payloads, const uint64_t* offsets, const uint64_t* sizes,
+                          uint64_t nblocks, double* out, uint64_t out_cap, uint64_t* counts);
+
+/* apply_unitary2 / apply_unitary4 (kernel.hpp:24-64) on an interleaved
+ * complex buffer of namps amplitudes; u is row-major interleaved (8 or 32
+ * doubles). Bit-identical to the reference arithmetic. */
+int bmq_apply_gate(double* amps, uint64_t namps, const double* u, int two_qubit, uint32_t hi_bit,
+                   uint32_t lo_bit);
+
+/* apply_stage (kernel.hpp:111-122) on one assembled group buffer. */
+int bmq_apply_stage(double* amps, uint64_t namps, uint32_t num_qubits, const bmq_gate* gates,
+                    uint64_t ngates, const bmq_stage* stage, uint32_t block_bits);
+
+/* dense_reference (engine.hpp:254-296), full FP64 vector on the device. */
+int bmq_dense_reference(uint32_t num_qubits, const bmq_gate* gates, uint64_t ngates,
+                        double* state, uint32_t verify_cap_qubits);
+
+/* ------------------------------------------------------------ simulator
+ * cbq::Simulator (engine.hpp:58-250). */
+
+typedef struct bmq_simulator bmq_simulator;
+
+void bmq_config_default(bmq_config* cfg);
+int bmq_simulator_create(uint32_t num_qubits, const bmq_gate* gates, uint64_t ngates,
+                         const bmq_config* cfg, bmq_simulator** out);
+int bmq_simulator_destroy(bmq_simulator* sim);
+/* plan() (engine.hpp:161) */
+int bmq_simulator_plan(const bmq_simulator* sim, bmq_stage* out, uint64_t cap, uint64_t* count);
+/* init_state() (engine.hpp:74-95) */
+int bmq_simulator_init_state(bmq_simulator* sim);
+/* run() (engine.hpp:97-134); stage_ms may be NULL. */
+int bmq_simulator_run(bmq_simulator* sim, bmq_report* report, double* stage_ms, uint64_t stage_cap);
+/* run stages [first, last) only (stage-level driver for pipelined callers). */
+int bmq_simulator_run_stages(bmq_simulator* sim, uint64_t first, uint64_t last);
+/* state_norm() (engine.hpp:150-158) */
+int bmq_simulator_state_norm(bmq_simulator* sim, double* norm);
+/* extract_state() (engine.hpp:138-147); refuses above verify_cap_qubits. */
+int bmq_simulator_extract_state(bmq_simulator* sim, double* amps, uint64_t namps);
+/* single amplitude query (new: the reference only has the dense extract). */
+int bmq_simulator_amplitude(bmq_simulator* sim, uint64_t index, double* re, double* im);
+/* store().get(id) (store.hpp:120-136): exact payload bytes of block id. */
+int bmq_simulator_get_payload(bmq_simulator* sim, uint64_t id, uint8_t* out, uint64_t cap,
+                              uint64_t* size);
+/* All payloads in id order, back to back; sizes[2^c]. */
+int bmq_simulator_get_payloads(bmq_simulator* sim, uint8_t* out, uint64_t cap, uint64_t* sizes,
+                               uint64_t* total);
+/* store().put(id, payload) (store.hpp:64-83). */
+int bmq_simulator_put_payload(bmq_simulator* sim, uint64_t id, const uint8_t* payload,
+                              uint64_t size);
+/* fidelity(dense_reference, extract_state) (engine.hpp:299-308) against a
+ * caller-supplied ideal state (interleaved, 2^n amplitudes). */
+int bmq_simulator_fidelity_dense(bmq_simulator* sim, const double* ideal, uint64_t namps,
+                                 double* fidelity);
+/* |<a|b>| between two simulators of the same layout, streamed block-wise. */
+int bmq_simulator_fidelity(bmq_simulator* a, bmq_simulator* b, double* fidelity);
+/* |<ideal|state>| for closed-form ideal states: 0 = uniform 2^(-n/2)
+ * (QFT of |0>), 1 = GHZ (|0..0> + |1..1>)/sqrt 2. */
+int bmq_simulator_fidelity_analytic(bmq_simulator* sim, int ideal_kind, double* fidelity);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMQ_H */

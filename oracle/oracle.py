@@ -105,10 +105,10 @@ class _Lib:
             raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
         self.lib = C.CDLL(path)
         self.path = path
-        self.lib[self.prefix + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
 
     def _f(self, name):
-        return self.lib[self.prefix + name]
+        return getattr(self.lib, self.prefix + name)
 
     def _check(self, rc):
         if rc:

@@ -1,0 +1,117 @@
+"""ctypes binding of libbmq.so (C ABI: include/bmq.h).
+
+The shared library is built in-tree by ``make -C paper_2410_14088_b200`` (or
+``__graft_entry__.build()``). There is no fallback: importing the package
+without the library raises immediately, and compute calls without a CUDA
+device raise ``NoDeviceError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbmq.so")
+
+BMQ_OK = 0
+BMQ_ERR_INVALID_ARGUMENT = 1
+BMQ_ERR_LOGIC = 2
+BMQ_ERR_CODEC = 3
+BMQ_ERR_STORE = 4
+BMQ_ERR_ENGINE = 5
+BMQ_ERR_QASM = 6
+BMQ_ERR_CUDA = 7
+BMQ_ERR_NO_DEVICE = 8
+BMQ_ERR_OUT_OF_MEMORY = 9
+BMQ_ERR_BUFFER_TOO_SMALL = 10
+
+BMQ_FLAG_ZERO_GROUP_SKIP = 0x1
+BMQ_FLAG_IDENTITY_SKIP = 0x2
+
+
+class bmq_gate(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("q0", C.c_uint32), ("q1", C.c_uint32), ("reserved", C.c_uint32),
+                ("angle", C.c_double)]
+
+
+class bmq_stage(C.Structure):
+    _fields_ = [("gate_begin", C.c_uint64), ("gate_end", C.c_uint64), ("inner_count", C.c_uint32),
+                ("reserved", C.c_uint32), ("inner", C.c_uint32 * 64)]
+
+
+class bmq_config(C.Structure):
+    _fields_ = [("block_bits", C.c_uint32), ("inner_size", C.c_uint32), ("error_bound", C.c_double),
+                ("memory_budget", C.c_uint64), ("workers", C.c_uint32), ("compress", C.c_uint32),
+                ("verify_cap_qubits", C.c_uint32), ("device", C.c_int32), ("device_pool_bytes", C.c_uint64),
+                ("work_bytes", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class bmq_report(C.Structure):
+    _fields_ = [("qubits", C.c_uint64), ("gate_count", C.c_uint64), ("stage_count", C.c_uint64),
+                ("max_footprint_bytes", C.c_uint64), ("standard_bytes", C.c_double),
+                ("compression_ratio", C.c_double), ("spilled_blocks", C.c_uint64), ("wall_ms", C.c_double),
+                ("has_fidelity", C.c_int32), ("reserved", C.c_int32), ("fidelity", C.c_double),
+                ("final_norm", C.c_double), ("stage_compress_calls", C.c_uint64),
+                ("stage_decompress_calls", C.c_uint64), ("device_ms", C.c_double),
+                ("groups_processed", C.c_uint64), ("groups_skipped", C.c_uint64),
+                ("blocks_processed", C.c_uint64), ("payload_bytes_read", C.c_uint64),
+                ("payload_bytes_written", C.c_uint64), ("dense_bytes", C.c_uint64),
+                ("kernel_launches", C.c_uint64), ("device_peak_bytes", C.c_uint64), ("gate_passes", C.c_uint64)]
+
+
+_P = C.c_void_p
+_U64 = C.c_uint64
+_U32 = C.c_uint32
+_D = C.c_double
+
+# name -> (restype, argtypes); every symbol include/bmq.h declares.
+SIGNATURES = {
+    "bmq_last_error": (C.c_char_p, []),
+    "bmq_version": (C.c_char_p, []),
+    "bmq_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "bmq_error_bound": (C.c_int, [_D, C.POINTER(_D)]),
+    "bmq_gate_unitary": (C.c_int, [C.POINTER(bmq_gate), _P]),
+    "bmq_circuit_validate": (C.c_int, [_U32, _P, _U64]),
+    "bmq_generate_benchmark": (C.c_int, [C.c_char_p, _U32, _U32, _U64, C.c_char_p, _P, _U64, C.POINTER(_U64)]),
+    "bmq_partition": (C.c_int, [_U32, _P, _U64, _U32, _U32, _P, _U64, C.POINTER(_U64)]),
+    "bmq_enumerate_groups": (C.c_int, [_U32, _U32, C.POINTER(bmq_stage), _P, _U64, C.POINTER(_U64)]),
+    "bmq_buffer_bit_of_qubit": (C.c_int, [_U32, _U32, C.POINTER(bmq_stage), _U32, C.POINTER(_U32)]),
+    "bmq_compress_bound": (_U64, [_U64]),
+    "bmq_compress_blocks": (C.c_int, [_P, _U64, _U64, _D, _P, _U64, _P]),
+    "bmq_decompress_blocks": (C.c_int, [_P, _P, _P, _U64, _P, _U64, _P]),
+    "bmq_apply_gate": (C.c_int, [_P, _U64, _P, C.c_int, _U32, _U32]),
+    "bmq_apply_stage": (C.c_int, [_P, _U64, _U32, _P, _U64, C.POINTER(bmq_stage), _U32]),
+    "bmq_dense_reference": (C.c_int, [_U32, _P, _U64, _P, _U32]),
+    "bmq_config_default": (None, [C.POINTER(bmq_config)]),
+    "bmq_simulator_create": (C.c_int, [_U32, _P, _U64, C.POINTER(bmq_config), C.POINTER(_P)]),
+    "bmq_simulator_destroy": (C.c_int, [_P]),
+    "bmq_simulator_plan": (C.c_int, [_P, _P, _U64, C.POINTER(_U64)]),
+    "bmq_simulator_init_state": (C.c_int, [_P]),
+    "bmq_simulator_run": (C.c_int, [_P, C.POINTER(bmq_report), _P, _U64]),
+    "bmq_simulator_run_stages": (C.c_int, [_P, _U64, _U64]),
+    "bmq_simulator_state_norm": (C.c_int, [_P, C.POINTER(_D)]),
+    "bmq_simulator_extract_state": (C.c_int, [_P, _P, _U64]),
+    "bmq_simulator_amplitude": (C.c_int, [_P, _U64, C.POINTER(_D), C.POINTER(_D)]),
+    "bmq_simulator_get_payload": (C.c_int, [_P, _U64, _P, _U64, C.POINTER(_U64)]),
+    "bmq_simulator_get_payloads": (C.c_int, [_P, _P, _U64, _P, C.POINTER(_U64)]),
+    "bmq_simulator_put_payload": (C.c_int, [_P, _U64, _P, _U64]),
+    "bmq_simulator_fidelity_dense": (C.c_int, [_P, _P, _U64, C.POINTER(_D)]),
+    "bmq_simulator_fidelity": (C.c_int, [_P, _P, C.POINTER(_D)]),
+    "bmq_simulator_fidelity_analytic": (C.c_int, [_P, C.c_int, C.POINTER(_D)]),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA extension with `make -C {_HERE}` "
+            "(or __graft_entry__.build()); paper_2410_14088_b200 has no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()

@@ -1,0 +1,219 @@
+// device_common.cuh — device-side helpers shared by the codec, gate and
+// engine kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bmq_internal.hpp"
+
+namespace bmq {
+
+// ----------------------------------------------------------------- errors
+// First device error wins; the host maps the code to the reference message.
+enum DevErr : uint32_t {
+    DE_NONE = 0,
+    DE_NONFINITE = 1,
+    DE_WINDOW = 2,
+    DE_HDR_TRUNC = 10,
+    DE_HDR_BOUND = 11,
+    DE_HDR_TRAIL = 12,
+    DE_SIGN_TRUNC = 13,
+    DE_ZERO_TRUNC = 14,
+    DE_TAG = 15,
+    DE_PARTIAL = 16,
+    DE_WIDTH0 = 17,
+    DE_CODES_TRUNC = 18,
+    DE_CODES_TRAIL = 19,
+    DE_BOUND_MISMATCH = 20,
+    DE_COUNT = 21,
+    DE_CODE_WINDOW = 22,
+    DE_POOL_FULL = 30,
+    DE_TOO_LARGE = 31,
+};
+
+struct DevError {
+    uint32_t code;
+    uint32_t pad;
+    uint64_t item;  // block index within the launch
+};
+
+__device__ __forceinline__ void dev_fail(DevError* e, uint32_t code, uint64_t item) {
+    if (atomicCAS(&e->code, 0u, code) == 0u) e->item = item;
+}
+
+const char* dev_error_message(uint32_t code);
+int dev_error_status(uint32_t code);
+
+// ------------------------------------------------------------ codec tables
+struct DevTables {
+    const uint64_t* thresh;   // thresh[q - qlo], q in [qlo, qhi + 1]
+    const double* dequant;    // dequant[q - qlo], q in [qlo, qhi]
+    int64_t qlo, qhi;
+    int64_t idem_lo, idem_hi;
+    double b_r;               // relative bound written into headers
+    double inv_ba;            // 1 / b_a, estimate only
+};
+
+// Device copy of host_tables(b_r) on the current device (cached).
+const DevTables& device_tables(double b_r);
+
+constexpr int kChunk = 4096;        // prescan chunk (bits) == scalars per chunk
+constexpr int kChunkThreads = 128;  // one thread per bitmap word
+constexpr int kWordsPerChunk = kChunk / 32;
+constexpr int kHeaderBytes = 26;
+
+// Exact reference quantiser q = llround(log2|v| / b_a) for finite v != 0.
+// A float log2 estimate lands within +-1 of the true code; the table
+// thresholds then settle it bit-exactly (see codec_tables.cpp).
+__device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& out_of_window) {
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
+    const uint32_t ex = static_cast<uint32_t>(bits >> 52);
+    uint64_t man = bits & 0xfffffffffffffull;
+    int e2;
+    if (ex == 0) {  // subnormal: normalise the mantissa
+        const int shift = __clzll(static_cast<long long>(man)) - 11;
+        man = (man << shift) & 0xfffffffffffffull;
+        e2 = -1022 - shift;
+    } else {
+        e2 = static_cast<int>(ex) - 1023;
+    }
+    const float m = static_cast<float>(__longlong_as_double(static_cast<long long>(man | 0x3ff0000000000000ull)));
+    const double x = (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
+    int64_t q = __double2ll_rn(x);
+    q = q < t.qlo ? t.qlo : (q > t.qhi ? t.qhi : q);
+    const uint64_t* T = t.thresh;
+    int64_t i = q - t.qlo;
+    while (bits < __ldg(T + i)) {
+        if (i == 0) {
+            out_of_window = true;
+            return t.qlo;
+        }
+        --i;
+    }
+    while (bits >= __ldg(T + i + 1)) ++i;
+    return t.qlo + i;
+}
+
+// Read `width` (<= 63) bits LSB-first starting at bit `bitpos` of the byte
+// stream at `base`. Reads aligned 32-bit words (buffers carry 16 B of slack).
+__device__ __forceinline__ uint64_t read_bits(const uint8_t* base, uint64_t bitpos, uint32_t width) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base) + (bitpos >> 3);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = static_cast<uint32_t>((a & 3) * 8 + (bitpos & 7));
+    const uint64_t lo = static_cast<uint64_t>(w[0]) | (static_cast<uint64_t>(w[1]) << 32);
+    uint64_t v = lo >> sh;
+    if (sh + width > 64) v |= static_cast<uint64_t>(w[2]) << (64 - sh);
+    return width >= 64 ? v : (v & ((1ull << width) - 1));
+}
+
+__device__ __forceinline__ uint32_t load_u32_unaligned(const uint8_t* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = static_cast<uint32_t>(a & 3) * 8;
+    return sh ? (__ldg(w) >> sh) | (__ldg(w + 1) << (32 - sh)) : __ldg(w);
+}
+
+// Write an LSB-first bit stream src[0..nbits) (words beyond nbits zero) at
+// byte dst, starting at bit `bit0` (< 8) of that byte. Interior 32-bit words
+// are owned and stored; the first and last words may be shared with
+// neighbouring segments of a zero-initialised region and are OR-ed in.
+__device__ __forceinline__ void write_bits_block(uint8_t* dst, uint32_t bit0, const uint32_t* src,
+                                                 uint64_t nbits, int tid, int nthreads) {
+    if (nbits == 0) return;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+    uint32_t* w = reinterpret_cast<uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t s = static_cast<uint32_t>(a & 3) * 8 + bit0;
+    const uint64_t nsrc = (nbits + 31) / 32;
+    const uint64_t nout = (s + nbits + 31) / 32;
+    for (uint64_t i = tid; i < nout; i += nthreads) {
+        uint32_t v = 0;
+        if (i < nsrc) v = src[i] << s;
+        if (s && i > 0) v |= src[i - 1] >> (32 - s);
+        if (i == 0 || i + 1 == nout)
+            atomicOr(w + i, v);
+        else
+            w[i] = v;
+    }
+}
+
+// pdep: scatter the low bits of x into the set bits of mask.
+__device__ __forceinline__ uint64_t dev_deposit(uint64_t x, uint64_t mask) {
+    uint64_t out = 0;
+    while (mask) {
+        const uint64_t low = mask & (~mask + 1);
+        if (x & 1) out |= low;
+        x >>= 1;
+        mask ^= low;
+    }
+    return out;
+}
+
+// ----------------------------------------------------- codec block records
+// Compress: per-block input descriptor and per-chunk / per-block plans.
+struct CmpBlock {
+    const double* in;   // planar scalars
+    uint64_t count;     // scalars in the block
+    uint64_t id;        // engine block id (or index for the API)
+};
+
+struct ChunkPlan {
+    int32_t qmin, qmax;
+    uint32_t nnz;
+    uint8_t stag, ztag, pad0, pad1;
+    uint32_t sign_off;   // byte offset of this chunk's raw sign bits in the payload
+    uint32_t zero_off;   // byte offset of this chunk's raw zero bits
+    uint32_t nz_prefix;  // nonzero scalars before this chunk in the block
+    uint32_t pad2;
+};
+
+struct BlockPlan {
+    uint64_t size;          // payload bytes
+    uint64_t out_off;       // offset in the output region (~0 = virtual ALL_ZERO)
+    int64_t code_min;
+    uint64_t code_seg;      // byte offset of the codes segment
+    uint64_t nnz;
+    uint32_t width;
+    uint32_t flags;         // 1 = ALL_ZERO
+    int64_t code_max;
+    uint64_t ztag_off;      // byte offset of the zero-bitmap tags
+    uint32_t ntag;          // tag bytes per bitmap
+    uint32_t nch;           // chunks
+    double sumsq;           // sum of dequantised squares (norm)
+    double sum_re, sum_im;  // sums of dequantised real / imaginary parts
+};
+
+// Decompress: per-block descriptor and per-chunk decode plan.
+struct DecBlock {
+    const uint8_t* in;
+    uint64_t size;
+    double* out;
+    uint64_t expect_count;  // 0 = any
+};
+
+struct DecChunk {
+    uint32_t sign_off, zero_off;  // raw byte offsets (valid when tag == 2)
+    uint32_t nz_prefix;
+    uint8_t stag, ztag, pad0, pad1;
+};
+
+struct DecInfo {
+    uint64_t count;
+    int64_t code_min;
+    uint64_t code_seg;
+    uint32_t width;
+    uint32_t flags;   // 1 = all zero, 2 = error
+    double sumsq;
+    double sum_re, sum_im;
+};
+
+}  // namespace bmq
+
+#define BMQ_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t err__ = (call);                                                           \
+        if (err__ != cudaSuccess)                                                             \
+            ::bmq::raise(err__ == cudaErrorMemoryAllocation ? BMQ_ERR_OUT_OF_MEMORY : BMQ_ERR_CUDA, \
+                         std::string("CUDA error: ") + cudaGetErrorString(err__) + " at " #call); \
+    } while (0)

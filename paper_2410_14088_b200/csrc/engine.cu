@@ -1,0 +1,833 @@
+// engine.cu — device implementation of cbq::Simulator (engine.hpp:58-250).
+//
+// State: the compressed payload of every block id lives in a device pool
+// (two pools, ping-pong per stage); ids whose payload is the canonical
+// ALL_ZERO header are virtual (no bytes stored). A stage runs its groups in
+// batches sized to the working set: build descriptors -> decompress the
+// batch's blocks into planar group buffers -> apply the stage's gate
+// program -> compress back into the other pool. Groups whose blocks are all
+// ALL_ZERO are skipped: linear gates map 0 to 0 and the codec emits the same
+// canonical header, so the result is byte-identical to processing them.
+// Per-id payload sizes come back to the host once per stage to replay the
+// reference BlockStore accounting (peak footprint, spills) in its put order.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "engine.cuh"
+
+namespace bmq {
+
+// ----------------------------------------------------------- StoreModel
+
+void StoreModel::reset(uint64_t num_ids, uint64_t budget) {
+    size_.assign(num_ids, 0);
+    flags_.assign(num_ids, 4);  // bit2: absent
+    budget_ = budget;
+    resident_ = spilled_live_ = peak_ = spilled_blocks_ = 0;
+    shared_refs_ = shared_size_ = 0;
+    shared_spilled_ = false;
+}
+
+void StoreModel::detach(uint64_t id) {  // detach_locked (store.hpp:192-212)
+    uint8_t& f = flags_[id];
+    if (f & 4) return;
+    if (f & 2) {
+        if (--shared_refs_ == 0) (shared_spilled_ ? spilled_live_ : resident_) -= shared_size_;
+    } else {
+        ((f & 1) ? spilled_live_ : resident_) -= size_[id];
+    }
+    f = 4;
+}
+
+bool StoreModel::place(uint64_t size) {  // fits_locked (store.hpp:188-190)
+    if (size <= budget_ && resident_ <= budget_ - size) {
+        resident_ += size;
+        return false;
+    }
+    spilled_live_ += size;
+    ++spilled_blocks_;
+    return true;
+}
+
+void StoreModel::put(uint64_t id, uint64_t size) {  // put (store.hpp:64-83)
+    detach(id);
+    flags_[id] = place(size) ? 1 : 0;
+    size_[id] = size;
+    peak_ = std::max(peak_, resident_ + spilled_live_);
+}
+
+void StoreModel::put_shared(uint64_t first, uint64_t last, uint64_t size) {  // store.hpp:85-117
+    for (uint64_t id = first; id < last; ++id) detach(id);
+    shared_spilled_ = place(size);
+    shared_size_ = size;
+    shared_refs_ = last - first;
+    for (uint64_t id = first; id < last; ++id) {
+        flags_[id] = 2;
+        size_[id] = size;
+    }
+    peak_ = std::max(peak_, resident_ + spilled_live_);
+}
+
+// ---------------------------------------------------------------- kernels
+
+namespace {
+
+__global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t zero_size) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        off[i] = ~0ull;
+        size[i] = zero_size;
+    }
+}
+
+__global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, const uint64_t* __restrict__ off_in,
+                             const uint64_t* __restrict__ size_in, const uint8_t* pool_in, const uint8_t* zero_hdr,
+                             double* work, uint32_t b, DecBlock* dec, CmpBlock* cmp) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= nblk) return;
+    const uint64_t id = ids[i];
+    const uint64_t count = 2ull << b;
+    double* slot = work + i * count;
+    const uint64_t off = off_in[id];
+    DecBlock d;
+    d.in = off == ~0ull ? zero_hdr : pool_in + off;
+    d.size = off == ~0ull ? kHeaderBytes : size_in[id];
+    d.out = slot;
+    d.expect_count = count;
+    dec[i] = d;
+    cmp[i] = CmpBlock{slot, count, id};
+}
+
+__global__ void k_store_cmp_sums(const BlockPlan* __restrict__ bp, const CmpBlock* __restrict__ cmp, uint64_t nblk,
+                                 double* sums) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= nblk) return;
+    const uint64_t id = cmp[i].id;
+    sums[3 * id] = bp[i].sumsq;
+    sums[3 * id + 1] = bp[i].sum_re;
+    sums[3 * id + 2] = bp[i].sum_im;
+}
+
+__global__ void k_store_dec_sums(const DecInfo* __restrict__ di, const uint64_t* __restrict__ ids, uint64_t nblk,
+                                 double* sums) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= nblk) return;
+    const uint64_t id = ids[i];
+    sums[3 * id] = di[i].sumsq;
+    sums[3 * id + 1] = di[i].sum_re;
+    sums[3 * id + 2] = di[i].sum_im;
+}
+
+// planar blocks [re(2^b) | im(2^b)] -> interleaved complex
+__global__ void k_interleave(const double* __restrict__ planar, uint64_t nblk, uint32_t b, double* __restrict__ out) {
+    const uint64_t total = nblk << b;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < total; p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t blk = p >> b, l = p & ((1ull << b) - 1);
+        const double* src = planar + (blk << (b + 1));
+        out[2 * p] = src[l];
+        out[2 * p + 1] = src[(1ull << b) + l];
+    }
+}
+
+// per-CTA partial sums of conj(ideal) * state (planar state, interleaved ideal)
+__global__ void k_dot(const double* __restrict__ planar, const double* __restrict__ ideal, uint64_t nblk, uint32_t b,
+                      double* __restrict__ partial) {
+    const uint64_t total = nblk << b;
+    double re = 0.0, im = 0.0;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < total; p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t blk = p >> b, l = p & ((1ull << b) - 1);
+        const double* src = planar + (blk << (b + 1));
+        const double sr = src[l], si = src[(1ull << b) + l];
+        const double ir = ideal[2 * p], ii = -ideal[2 * p + 1];
+        re += ir * sr - ii * si;
+        im += ir * si + ii * sr;
+    }
+    __shared__ double s[2][256];
+    s[0][threadIdx.x] = re;
+    s[1][threadIdx.x] = im;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            s[0][threadIdx.x] += s[0][threadIdx.x + o];
+            s[1][threadIdx.x] += s[1][threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = s[0][0];
+        partial[2 * blockIdx.x + 1] = s[1][0];
+    }
+}
+
+// per-CTA partial dot of two planar buffers: sum conj(a) * b
+__global__ void k_dot2(const double* __restrict__ a, const double* __restrict__ bb, uint64_t nblk, uint32_t b,
+                       double* __restrict__ partial) {
+    const uint64_t total = nblk << b;
+    double re = 0.0, im = 0.0;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < total; p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t blk = p >> b, l = p & ((1ull << b) - 1);
+        const uint64_t o = blk << (b + 1);
+        const double ar = a[o + l], ai = -a[o + (1ull << b) + l];
+        const double br = bb[o + l], bi = bb[o + (1ull << b) + l];
+        re += ar * br - ai * bi;
+        im += ar * bi + ai * br;
+    }
+    __shared__ double s[2][256];
+    s[0][threadIdx.x] = re;
+    s[1][threadIdx.x] = im;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            s[0][threadIdx.x] += s[0][threadIdx.x + o];
+            s[1][threadIdx.x] += s[1][threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = s[0][0];
+        partial[2 * blockIdx.x + 1] = s[1][0];
+    }
+}
+
+// per-block sums over a dense planar state (raw mode): sumsq, sum_re, sum_im
+__global__ void k_block_sums(const double* __restrict__ planar, uint32_t b, double* __restrict__ sums) {
+    const uint64_t blk = blockIdx.x;
+    const double* src = planar + (blk << (b + 1));
+    double sq = 0.0, sr = 0.0, si = 0.0;
+    for (uint64_t l = threadIdx.x; l < (1ull << b); l += blockDim.x) {
+        const double r = src[l], i = src[(1ull << b) + l];
+        sq += r * r + i * i;
+        sr += r;
+        si += i;
+    }
+    __shared__ double s[3][256];
+    s[0][threadIdx.x] = sq;
+    s[1][threadIdx.x] = sr;
+    s[2][threadIdx.x] = si;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int k = 0; k < 3; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 3; ++k) sums[3 * blk + k] = s[k][0];
+}
+
+uint32_t grid_for(uint64_t n, uint32_t threads = 256) {
+    const uint64_t g = (n + threads - 1) / threads;
+    return static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(g, 1), 148ull * 64));
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Engine
+
+Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_config& cfg) : cfg_(cfg) {
+    check_circuit(n, gates, ngates);
+    gates_.assign(gates, gates + ngates);
+    L_ = make_layout(n, cfg.block_bits);
+    plan_ = partition_plan(n, gates, ngates, cfg.block_bits, cfg.inner_size);
+    if (!(cfg.error_bound > 0.0) || std::isinf(cfg.error_bound))
+        raise(BMQ_ERR_INVALID_ARGUMENT, "relative error bound must be positive and finite");
+    if (cfg.workers < 1) raise(BMQ_ERR_INVALID_ARGUMENT, "worker count must be at least 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        raise(BMQ_ERR_NO_DEVICE, "no CUDA device available (the engine has no CPU fallback)");
+    }
+    if (cfg.device < 0 || cfg.device >= ndev) raise(BMQ_ERR_INVALID_ARGUMENT, "invalid CUDA device ordinal");
+    dev_ = cfg.device;
+    BMQ_CUDA(cudaSetDevice(dev_));
+    BMQ_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    BMQ_CUDA(cudaEventCreate(&ev0_));
+    BMQ_CUDA(cudaEventCreate(&ev1_));
+    const bool raw = !cfg.compress;
+    uint32_t kmax = 0;
+    for (const bmq_stage& s : plan_) {
+        auto sp = std::make_unique<StagePlan>();
+        sp->stage = s;
+        sp->gg = group_geometry(L_, s);
+        kmax = std::max(kmax, s.inner_count);
+        std::vector<GateOp> ops;
+        for (uint64_t i = s.gate_begin; i < s.gate_end; ++i) {
+            const bmq_gate& g = gates_[i];
+            const bool two = gate_is_two_qubit(g.kind);
+            if (raw) {
+                ops.push_back(make_op(g, g.q0, two ? g.q1 : 0));
+            } else {
+                const uint32_t hi = buffer_bit(L_, s, g.q0);
+                const uint32_t lo = two ? buffer_bit(L_, s, g.q1) : 0;
+                ops.push_back(make_op(g, hi, lo));
+            }
+        }
+        build_program(sp->prog, std::move(ops), raw ? L_.n : L_.b + s.inner_count);
+        stage_plans_.push_back(std::move(sp));
+    }
+    const uint64_t nid = L_.num_blocks();
+    const uint64_t blk_scalars = 2ull << L_.b;
+    size_t free_b = 0, total_b = 0;
+    BMQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    off_[0].alloc(nid);
+    off_[1].alloc(nid);
+    size_[0].alloc(nid);
+    size_[1].alloc(nid);
+    sums_.alloc(3 * nid);
+    err_.alloc(1);
+    cursor_.alloc(4);
+    red_.alloc(2 * 148 * 64);
+    BMQ_CUDA(cudaMemset(err_.p, 0, sizeof(DevError)));
+    BMQ_CUDA(cudaMemset(cursor_.p, 0, 4 * sizeof(uint64_t)));
+    h_off_.assign(nid, ~0ull);
+    h_size_.assign(nid, 0);
+    if (raw) {
+        dense_.alloc(nid * blk_scalars);
+        work_scalars_ = 0;
+        device_peak_ = dense_.bytes();
+        return;
+    }
+    tabs_ = &device_tables(cfg.error_bound);
+    const uint64_t group_bytes = 8ull * (blk_scalars << kmax);
+    uint64_t want = cfg.work_bytes ? cfg.work_bytes : std::min<uint64_t>(16ull << 30, free_b / 4);
+    want = std::max<uint64_t>(want, group_bytes);
+    work_scalars_ = (want / 8) / blk_scalars * blk_scalars;
+    max_blocks_ = work_scalars_ / blk_scalars;
+    nch_ = static_cast<uint32_t>((blk_scalars + kChunk - 1) / kChunk);
+    work_.alloc(work_scalars_);
+    cmp_.alloc(max_blocks_);
+    dec_.alloc(max_blocks_);
+    cplan_.alloc(max_blocks_ * nch_);
+    bplan_.alloc(max_blocks_);
+    dinfo_.alloc(max_blocks_);
+    dchunk_.alloc(max_blocks_ * nch_);
+    ids_.alloc(std::max<uint64_t>(nid, max_blocks_));
+    // canonical ALL_ZERO payload (codec.hpp:263-271) + slack
+    uint8_t hdr[kHeaderBytes + 16] = {};
+    const uint64_t cnt = blk_scalars;
+    for (int k = 0; k < 8; ++k) hdr[k] = static_cast<uint8_t>(cnt >> (8 * k));
+    std::memcpy(hdr + 8, &cfg.error_bound, 8);
+    hdr[25] = 1;
+    zero_hdr_.alloc(sizeof hdr);
+    BMQ_CUDA(cudaMemcpy(zero_hdr_.p, hdr, sizeof hdr, cudaMemcpyHostToDevice));
+    BMQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t pool = cfg.device_pool_bytes;
+    if (!pool) {
+        const uint64_t reserve = 2ull << 30;
+        pool = free_b > reserve ? (free_b - reserve) / 2 : free_b / 4;
+        pool = std::min<uint64_t>(pool, 48ull << 30);
+    }
+    pool_cap_ = pool;
+    pool_[0].alloc(pool + 64);
+    pool_[1].alloc(pool + 64);
+    device_peak_ = 2 * (pool + 64) + work_.bytes() + cplan_.bytes() + dchunk_.bytes();
+}
+
+Engine::~Engine() {
+    if (st_) {
+        cudaSetDevice(dev_);
+        cudaStreamSynchronize(st_);
+        cudaStreamDestroy(st_);
+    }
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+}
+
+void Engine::check_device_error(const char* what) {
+    DevError e{};
+    BMQ_CUDA(cudaMemcpyAsync(&e, err_.p, sizeof e, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    if (e.code) {
+        BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        raise(dev_error_status(e.code), std::string(what) + dev_error_message(e.code));
+    }
+}
+
+void Engine::sync_meta_to_host() {
+    BMQ_CUDA(cudaMemcpyAsync(h_off_.data(), off_[cur_].p, off_[cur_].bytes(), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaMemcpyAsync(h_size_.data(), size_[cur_].p, size_[cur_].bytes(), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::init_state() {
+    if (initialized_) raise(BMQ_ERR_ENGINE, "state already initialized");
+    BMQ_CUDA(cudaSetDevice(dev_));
+    const uint64_t nid = L_.num_blocks();
+    const double one = 1.0;
+    store_.reset(nid, cfg_.memory_budget);
+    BMQ_CUDA(cudaMemsetAsync(sums_.p, 0, sums_.bytes(), st_));
+    if (!cfg_.compress) {
+        const uint64_t raw = 16ull << L_.b;
+        BMQ_CUDA(cudaMemsetAsync(dense_.p, 0, dense_.bytes(), st_));
+        BMQ_CUDA(cudaMemcpyAsync(dense_.p, &one, 8, cudaMemcpyHostToDevice, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        store_.put(0, raw);
+        if (nid > 1) store_.put_shared(1, nid, raw);
+        for (uint64_t id = 0; id < nid; ++id) h_size_[id] = raw;
+        initialized_ = true;
+        next_stage_ = 0;
+        return;
+    }
+    cur_ = 0;
+    k_fill_meta<<<grid_for(nid), 256, 0, st_>>>(off_[0].p, size_[0].p, nid, kHeaderBytes);
+    BMQ_CUDA(cudaMemsetAsync(cursor_.p, 0, 2 * sizeof(uint64_t), st_));
+    const uint64_t cnt = 2ull << L_.b;
+    BMQ_CUDA(cudaMemsetAsync(work_.p, 0, cnt * sizeof(double), st_));
+    BMQ_CUDA(cudaMemcpyAsync(work_.p, &one, 8, cudaMemcpyHostToDevice, st_));
+    const CmpBlock blk{work_.p, cnt, 0};
+    BMQ_CUDA(cudaMemcpyAsync(cmp_.p, &blk, sizeof blk, cudaMemcpyHostToDevice, st_));
+    launch_compress(st_, cmp_.p, 1, nch_, *tabs_, pool_[0].p, pool_cap_, cursor_.p, cursor_.p + 2, bplan_.p, cplan_.p,
+                    off_[0].p, size_[0].p, true, err_.p, &counters_.kernel_launches);
+    k_store_cmp_sums<<<1, 32, 0, st_>>>(bplan_.p, cmp_.p, 1, sums_.p);
+    check_device_error("init_state: ");
+    sync_meta_to_host();
+    store_.put(0, h_size_[0]);
+    if (nid > 1) store_.put_shared(1, nid, kHeaderBytes);  // one zero payload, counted once
+    initialized_ = true;
+    next_stage_ = 0;
+}
+
+void Engine::ensure_init() {
+    if (!initialized_) init_state();
+}
+
+void Engine::raw_run_stage(uint64_t s) {
+    StagePlan& sp = *stage_plans_[s];
+    run_program(st_, sp.prog, dense_.p, L_.b, false, 1, &counters_.kernel_launches);
+    counters_.gate_passes += sp.prog.passes.size();
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    const uint64_t raw = 16ull << L_.b;
+    const GroupGeometry& gg = sp.gg;
+    std::vector<uint64_t> inner(gg.per_group());
+    for (uint64_t v = 0; v < inner.size(); ++v) inner[v] = deposit_bits(v, gg.inner_mask);
+    uint64_t o = 0;
+    for (uint64_t g = 0; g < gg.groups(); ++g) {
+        for (uint64_t v : inner) store_.put(o | v, raw);
+        o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
+    }
+    counters_.groups_processed += gg.groups();
+    counters_.blocks_processed += L_.num_blocks();
+    counters_.dense_bytes += 32ull << L_.n;
+    stage_compress_calls_ += L_.num_blocks();
+    stage_decompress_calls_ += L_.num_blocks();
+}
+
+void Engine::run_stage(uint64_t s) {
+    if (!cfg_.compress) return raw_run_stage(s);
+    StagePlan& sp = *stage_plans_[s];
+    const GroupGeometry& gg = sp.gg;
+    const uint64_t per = gg.per_group(), ngroups = gg.groups();
+    const uint64_t nid = L_.num_blocks();
+    const bool skip_zero = cfg_.flags & BMQ_FLAG_ZERO_GROUP_SKIP;
+    // groups in ascending outer order; ids of groups that need processing
+    std::vector<uint64_t> inner(per);
+    for (uint64_t v = 0; v < per; ++v) inner[v] = deposit_bits(v, gg.inner_mask);
+    std::vector<uint64_t> work_ids;
+    work_ids.reserve(nid);
+    uint64_t o = 0;
+    for (uint64_t g = 0; g < ngroups; ++g) {
+        bool nonzero = !skip_zero;
+        for (uint64_t v = 0; v < per && !nonzero; ++v) nonzero = h_off_[o | inner[v]] != ~0ull;
+        if (nonzero)
+            for (uint64_t v = 0; v < per; ++v) work_ids.push_back(o | inner[v]);
+        o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
+    }
+    const int nxt = 1 - cur_;
+    k_fill_meta<<<grid_for(nid), 256, 0, st_>>>(off_[nxt].p, size_[nxt].p, nid, kHeaderBytes);
+    BMQ_CUDA(cudaMemsetAsync(cursor_.p + nxt, 0, sizeof(uint64_t), st_));
+    counters_.kernel_launches += 1;
+    const uint64_t nwork = work_ids.size();
+    if (nwork) {
+        BMQ_CUDA(cudaMemcpyAsync(ids_.p, work_ids.data(), nwork * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
+        const uint64_t batch_groups = std::max<uint64_t>(1, max_blocks_ / per);
+        const uint64_t batch_blocks = batch_groups * per;
+        for (uint64_t first = 0; first < nwork; first += batch_blocks) {
+            const uint64_t nblk = std::min(batch_blocks, nwork - first);
+            const uint64_t* d_ids = ids_.p + first;
+            k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_[cur_].p, size_[cur_].p, pool_[cur_].p,
+                                                          zero_hdr_.p, work_.p, L_.b, dec_.p, cmp_.p);
+            launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
+                              &counters_.kernel_launches);
+            run_program(st_, sp.prog, work_.p, L_.b, false, nblk / per, &counters_.kernel_launches);
+            launch_compress(st_, cmp_.p, nblk, nch_, *tabs_, pool_[nxt].p, pool_cap_, cursor_.p + nxt, cursor_.p + 2,
+                            bplan_.p, cplan_.p, off_[nxt].p, size_[nxt].p, true, err_.p, &counters_.kernel_launches);
+            k_store_cmp_sums<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, cmp_.p, nblk, sums_.p);
+            counters_.kernel_launches += 2;
+            counters_.gate_passes += sp.prog.passes.size();
+        }
+    }
+    // zero groups that were skipped keep zero sums (already zero)
+    const std::vector<uint64_t> old_size = h_size_;
+    const std::vector<uint64_t> old_off = h_off_;
+    cur_ = nxt;
+    check_device_error(("stage " + std::to_string(s) + ": ").c_str());
+    sync_meta_to_host();
+    // accounting replay in the reference put order (groups ascending)
+    o = 0;
+    for (uint64_t g = 0; g < ngroups; ++g) {
+        for (uint64_t v : inner) store_.put(o | v, h_size_[o | v]);
+        o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
+    }
+    for (uint64_t id : work_ids) {
+        counters_.payload_bytes_read += old_off[id] == ~0ull ? 0 : old_size[id];
+        counters_.payload_bytes_written += h_off_[id] == ~0ull ? 0 : h_size_[id];
+    }
+    counters_.groups_processed += nwork / per;
+    counters_.groups_skipped += ngroups - nwork / per;
+    counters_.blocks_processed += nwork;
+    counters_.dense_bytes += nwork * (32ull << L_.b);
+    stage_compress_calls_ += nid;
+    stage_decompress_calls_ += nid;
+}
+
+void Engine::run_stages(uint64_t first, uint64_t last) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (first != next_stage_ || last < first || last > plan_.size())
+        raise(BMQ_ERR_ENGINE, "stages must run in order: next stage is " + std::to_string(next_stage_));
+    for (uint64_t s = first; s < last; ++s) {
+        run_stage(s);
+        next_stage_ = s + 1;
+    }
+}
+
+void Engine::run(bmq_report* rep, double* stage_ms, uint64_t stage_cap) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    const double t0 = now_ms();
+    ensure_init();
+    bmq_report r{};
+    r.qubits = L_.n;
+    r.gate_count = gates_.size();
+    r.stage_count = plan_.size();
+    counters_ = bmq_report{};
+    BMQ_CUDA(cudaEventRecord(ev0_, st_));
+    for (uint64_t s = next_stage_; s < plan_.size(); ++s) {
+        const double ts = now_ms();
+        run_stage(s);
+        next_stage_ = s + 1;
+        if (stage_ms && s < stage_cap) stage_ms[s] = now_ms() - ts;
+    }
+    BMQ_CUDA(cudaEventRecord(ev1_, st_));
+    BMQ_CUDA(cudaEventSynchronize(ev1_));
+    float dms = 0.f;
+    BMQ_CUDA(cudaEventElapsedTime(&dms, ev0_, ev1_));
+    r.max_footprint_bytes = store_.peak();
+    r.standard_bytes = std::exp2(static_cast<double>(L_.n + 4));
+    r.compression_ratio = r.max_footprint_bytes ? r.standard_bytes / static_cast<double>(r.max_footprint_bytes) : 0.0;
+    r.spilled_blocks = store_.spilled_blocks();
+    r.stage_compress_calls = stage_compress_calls_;
+    r.stage_decompress_calls = stage_decompress_calls_;
+    r.final_norm = state_norm();
+    r.wall_ms = now_ms() - t0;
+    r.device_ms = dms;
+    r.groups_processed = counters_.groups_processed;
+    r.groups_skipped = counters_.groups_skipped;
+    r.blocks_processed = counters_.blocks_processed;
+    r.payload_bytes_read = counters_.payload_bytes_read;
+    r.payload_bytes_written = counters_.payload_bytes_written;
+    r.dense_bytes = counters_.dense_bytes;
+    r.kernel_launches = counters_.kernel_launches;
+    r.gate_passes = counters_.gate_passes;
+    r.device_peak_bytes = device_peak_;
+    *rep = r;
+}
+
+double Engine::state_norm() {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    const uint64_t nid = L_.num_blocks();
+    if (!cfg_.compress) {
+        k_block_sums<<<static_cast<uint32_t>(nid), 256, 0, st_>>>(dense_.p, L_.b, sums_.p);
+        BMQ_CUDA(cudaGetLastError());
+    }
+    std::vector<double> h(3 * nid);
+    BMQ_CUDA(cudaMemcpyAsync(h.data(), sums_.p, sums_.bytes(), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    double sum = 0.0;
+    for (uint64_t id = 0; id < nid; ++id) sum += h[3 * id];
+    return std::sqrt(sum);
+}
+
+void Engine::host_ids_to_device(const std::vector<uint64_t>& ids) {
+    BMQ_CUDA(cudaMemcpyAsync(ids_.p, ids.data(), ids.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
+}
+
+void Engine::decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums) {
+    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_[cur_].p, size_[cur_].p, pool_[cur_].p,
+                                                  zero_hdr_.p, work_.p, L_.b, dec_.p, cmp_.p);
+    launch_decompress(st_, dec_.p, nids, nch_, *tabs_, dinfo_.p, dchunk_.p, true, want_sums, err_.p,
+                      &counters_.kernel_launches);
+}
+
+void Engine::extract_state(double* amps, uint64_t namps) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (L_.n > cfg_.verify_cap_qubits)
+        raise(BMQ_ERR_ENGINE, "dense verification refused: " + std::to_string(L_.n) +
+                                  " qubits exceeds the cap of " + std::to_string(cfg_.verify_cap_qubits));
+    if (namps != (1ull << L_.n)) raise(BMQ_ERR_INVALID_ARGUMENT, "amplitude buffer must hold 2^n amplitudes");
+    const uint64_t nid = L_.num_blocks();
+    if (!cfg_.compress) {
+        DevArray<double> tmp;
+        tmp.alloc(2 * namps);
+        k_interleave<<<grid_for(namps), 256, 0, st_>>>(dense_.p, nid, L_.b, tmp.p);
+        BMQ_CUDA(cudaMemcpyAsync(amps, tmp.p, tmp.bytes(), cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        return;
+    }
+    DevArray<double> tmp;
+    tmp.alloc(std::min(nid, max_blocks_) * (2ull << L_.b));
+    std::vector<uint64_t> ids(nid);
+    for (uint64_t i = 0; i < nid; ++i) ids[i] = i;
+    host_ids_to_device(ids);
+    for (uint64_t first = 0; first < nid; first += max_blocks_) {
+        const uint64_t nb = std::min(max_blocks_, nid - first);
+        decompress_ids(ids_.p + first, nb, false);
+        k_interleave<<<grid_for(nb << L_.b), 256, 0, st_>>>(work_.p, nb, L_.b, tmp.p);
+        BMQ_CUDA(cudaMemcpyAsync(amps + 2 * (first << L_.b), tmp.p, (nb << L_.b) * 2 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+    }
+    check_device_error("extract_state: ");
+}
+
+void Engine::amplitude(uint64_t index, double* re, double* im) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (index >> L_.n) raise(BMQ_ERR_INVALID_ARGUMENT, "amplitude index out of range");
+    const uint64_t id = index >> L_.b, l = index & ((1ull << L_.b) - 1);
+    const double* src;
+    if (!cfg_.compress) {
+        src = dense_.p + (id << (L_.b + 1));
+    } else {
+        host_ids_to_device({id});
+        decompress_ids(ids_.p, 1, false);
+        src = work_.p;
+    }
+    BMQ_CUDA(cudaMemcpyAsync(re, src + l, 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaMemcpyAsync(im, src + (1ull << L_.b) + l, 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    if (cfg_.compress) check_device_error("amplitude: ");
+}
+
+uint64_t Engine::zero_payload(uint8_t* out, uint64_t cap) const {
+    if (!cfg_.compress) {
+        const uint64_t raw = 16ull << L_.b;
+        if (out && cap >= raw) std::memset(out, 0, raw);
+        return raw;
+    }
+    if (out && cap >= static_cast<uint64_t>(kHeaderBytes)) {
+        std::memset(out, 0, kHeaderBytes);
+        const uint64_t cnt = 2ull << L_.b;
+        for (int k = 0; k < 8; ++k) out[k] = static_cast<uint8_t>(cnt >> (8 * k));
+        std::memcpy(out + 8, &cfg_.error_bound, 8);
+        out[25] = 1;
+    }
+    return kHeaderBytes;
+}
+
+uint64_t Engine::get_payload(uint64_t id, uint8_t* out, uint64_t cap) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (id >= L_.num_blocks()) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(id));
+    if (!cfg_.compress) {
+        const uint64_t raw = 16ull << L_.b;
+        if (out && cap >= raw) {
+            BMQ_CUDA(cudaMemcpyAsync(out, dense_.p + (id << (L_.b + 1)), raw, cudaMemcpyDeviceToHost, st_));
+            BMQ_CUDA(cudaStreamSynchronize(st_));
+        }
+        return raw;
+    }
+    if (h_off_[id] == ~0ull) return zero_payload(out, cap);
+    const uint64_t size = h_size_[id];
+    if (out && cap >= size) {
+        BMQ_CUDA(cudaMemcpyAsync(out, pool_[cur_].p + h_off_[id], size, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+    }
+    return size;
+}
+
+void Engine::get_payloads(uint8_t* out, uint64_t cap, uint64_t* sizes, uint64_t* total) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    const uint64_t nid = L_.num_blocks();
+    uint64_t t = 0;
+    for (uint64_t id = 0; id < nid; ++id) {
+        const uint64_t sz = cfg_.compress ? (h_off_[id] == ~0ull ? kHeaderBytes : h_size_[id]) : (16ull << L_.b);
+        if (sizes) sizes[id] = sz;
+        t += sz;
+    }
+    *total = t;
+    if (!out) return;
+    if (cap < t) raise(BMQ_ERR_BUFFER_TOO_SMALL, "payload buffer too small");
+    if (!cfg_.compress) {
+        BMQ_CUDA(cudaMemcpyAsync(out, dense_.p, t, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        return;
+    }
+    // Stored payloads are packed in the pool in id order within each batch;
+    // copy the pool once and scatter on the host.
+    uint64_t used = 0;
+    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    std::vector<uint8_t> host(used);
+    if (used) {
+        BMQ_CUDA(cudaMemcpyAsync(host.data(), pool_[cur_].p, used, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+    }
+    uint64_t pos = 0;
+    for (uint64_t id = 0; id < nid; ++id) {
+        if (h_off_[id] == ~0ull) {
+            pos += zero_payload(out + pos, kHeaderBytes);
+        } else {
+            std::memcpy(out + pos, host.data() + h_off_[id], h_size_[id]);
+            pos += h_size_[id];
+        }
+    }
+}
+
+void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (id >= L_.num_blocks()) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(id));
+    if (!cfg_.compress) {
+        const uint64_t raw = 16ull << L_.b;
+        if (size != raw) raise(BMQ_ERR_ENGINE, "raw block payload has invalid length");
+        BMQ_CUDA(cudaMemcpyAsync(dense_.p + (id << (L_.b + 1)), data, raw, cudaMemcpyHostToDevice, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        store_.put(id, raw);
+        return;
+    }
+    uint64_t used = 0;
+    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    if (used + size > pool_cap_) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+    const uint64_t prev_off = h_off_[id], prev_size = h_size_[id];
+    BMQ_CUDA(cudaMemcpyAsync(pool_[cur_].p + used, data, size, cudaMemcpyHostToDevice, st_));
+    const uint64_t end = used + size;
+    BMQ_CUDA(cudaMemcpyAsync(cursor_.p + cur_, &end, 8, cudaMemcpyHostToDevice, st_));
+    BMQ_CUDA(cudaMemcpyAsync(off_[cur_].p + id, &used, 8, cudaMemcpyHostToDevice, st_));
+    BMQ_CUDA(cudaMemcpyAsync(size_[cur_].p + id, &size, 8, cudaMemcpyHostToDevice, st_));
+    host_ids_to_device({id});
+    decompress_ids(ids_.p, 1, true);
+    k_store_dec_sums<<<1, 32, 0, st_>>>(dinfo_.p, ids_.p, 1, sums_.p);
+    try {
+        check_device_error("");
+    } catch (...) {  // restore the previous payload
+        BMQ_CUDA(cudaMemcpyAsync(off_[cur_].p + id, &prev_off, 8, cudaMemcpyHostToDevice, st_));
+        BMQ_CUDA(cudaMemcpyAsync(size_[cur_].p + id, &prev_size, 8, cudaMemcpyHostToDevice, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        throw;
+    }
+    h_off_[id] = used;
+    h_size_[id] = size;
+    store_.put(id, size);
+}
+
+double Engine::fidelity_dense(const double* ideal, uint64_t namps) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (namps != (1ull << L_.n)) raise(BMQ_ERR_INVALID_ARGUMENT, "fidelity requires equal-length states");
+    const uint64_t nid = L_.num_blocks();
+    const uint64_t step = cfg_.compress ? max_blocks_ : nid;
+    DevArray<double> dideal;
+    dideal.alloc(std::min(step, nid) * (2ull << L_.b));
+    std::vector<uint64_t> ids(nid);
+    for (uint64_t i = 0; i < nid; ++i) ids[i] = i;
+    if (cfg_.compress) host_ids_to_device(ids);
+    double re = 0.0, im = 0.0;
+    std::vector<double> part(2 * 148 * 64);
+    for (uint64_t first = 0; first < nid; first += step) {
+        const uint64_t nb = std::min(step, nid - first);
+        const double* planar = dense_.p ? dense_.p + (first << (L_.b + 1)) : nullptr;
+        if (cfg_.compress) {
+            decompress_ids(ids_.p + first, nb, false);
+            planar = work_.p;
+        }
+        BMQ_CUDA(cudaMemcpyAsync(dideal.p, ideal + 2 * (first << L_.b), (nb << L_.b) * 16, cudaMemcpyHostToDevice, st_));
+        const uint32_t g = grid_for(nb << L_.b);
+        k_dot<<<g, 256, 0, st_>>>(planar, dideal.p, nb, L_.b, red_.p);
+        BMQ_CUDA(cudaMemcpyAsync(part.data(), red_.p, 2 * g * sizeof(double), cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        for (uint32_t k = 0; k < g; ++k) {
+            re += part[2 * k];
+            im += part[2 * k + 1];
+        }
+    }
+    if (cfg_.compress) check_device_error("fidelity: ");
+    return std::hypot(re, im);
+}
+
+double Engine::fidelity_analytic(int kind) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (kind == 0) {  // uniform 2^(-n/2): |<u|psi>| = 2^(-n/2) |sum psi_i|
+        const uint64_t nid = L_.num_blocks();
+        if (!cfg_.compress) {
+            k_block_sums<<<static_cast<uint32_t>(nid), 256, 0, st_>>>(dense_.p, L_.b, sums_.p);
+            BMQ_CUDA(cudaGetLastError());
+        }
+        std::vector<double> h(3 * nid);
+        BMQ_CUDA(cudaMemcpyAsync(h.data(), sums_.p, sums_.bytes(), cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        double re = 0.0, im = 0.0;
+        for (uint64_t id = 0; id < nid; ++id) {
+            re += h[3 * id + 1];
+            im += h[3 * id + 2];
+        }
+        return std::hypot(re, im) * std::exp2(-0.5 * static_cast<double>(L_.n));
+    }
+    if (kind == 1) {  // GHZ (|0..0> + |1..1>) / sqrt 2
+        double r0, i0, r1, i1;
+        amplitude(0, &r0, &i0);
+        amplitude((1ull << L_.n) - 1, &r1, &i1);
+        return std::hypot(r0 + r1, i0 + i1) / std::sqrt(2.0);
+    }
+    raise(BMQ_ERR_INVALID_ARGUMENT, "unknown analytic ideal state kind");
+}
+
+double Engine::fidelity_pair(Engine& a, Engine& b) {
+    if (a.L_.n != b.L_.n || a.L_.b != b.L_.b) raise(BMQ_ERR_INVALID_ARGUMENT, "fidelity requires equal-length states");
+    if (a.dev_ != b.dev_) raise(BMQ_ERR_INVALID_ARGUMENT, "fidelity requires both simulators on one device");
+    BMQ_CUDA(cudaSetDevice(a.dev_));
+    a.ensure_init();
+    b.ensure_init();
+    const uint64_t nid = a.L_.num_blocks();
+    uint64_t step = nid;
+    if (a.cfg_.compress) step = std::min(step, a.max_blocks_);
+    if (b.cfg_.compress) step = std::min(step, b.max_blocks_);
+    std::vector<uint64_t> ids(nid);
+    for (uint64_t i = 0; i < nid; ++i) ids[i] = i;
+    if (a.cfg_.compress) a.host_ids_to_device(ids);
+    if (b.cfg_.compress) b.host_ids_to_device(ids);
+    BMQ_CUDA(cudaStreamSynchronize(a.st_));
+    BMQ_CUDA(cudaStreamSynchronize(b.st_));
+    double re = 0.0, im = 0.0;
+    std::vector<double> part(2 * 148 * 64);
+    for (uint64_t first = 0; first < nid; first += step) {
+        const uint64_t nb = std::min(step, nid - first);
+        const double* pa = a.cfg_.compress ? a.work_.p : a.dense_.p + (first << (a.L_.b + 1));
+        const double* pb = b.cfg_.compress ? b.work_.p : b.dense_.p + (first << (b.L_.b + 1));
+        if (a.cfg_.compress) a.decompress_ids(a.ids_.p + first, nb, false);
+        if (b.cfg_.compress) b.decompress_ids(b.ids_.p + first, nb, false);
+        BMQ_CUDA(cudaStreamSynchronize(a.st_));
+        BMQ_CUDA(cudaStreamSynchronize(b.st_));
+        const uint32_t g = grid_for(nb << a.L_.b);
+        k_dot2<<<g, 256, 0, a.st_>>>(pa, pb, nb, a.L_.b, a.red_.p);
+        BMQ_CUDA(cudaMemcpyAsync(part.data(), a.red_.p, 2 * g * sizeof(double), cudaMemcpyDeviceToHost, a.st_));
+        BMQ_CUDA(cudaStreamSynchronize(a.st_));
+        for (uint32_t k = 0; k < g; ++k) {
+            re += part[2 * k];
+            im += part[2 * k + 1];
+        }
+    }
+    if (a.cfg_.compress) a.check_device_error("fidelity: ");
+    if (b.cfg_.compress) b.check_device_error("fidelity: ");
+    return std::hypot(re, im);
+}
+
+}  // namespace bmq

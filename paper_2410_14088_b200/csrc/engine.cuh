@@ -1,0 +1,138 @@
+// engine.cuh — the device Simulator (cbq::Simulator, engine.hpp:58-250).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "codec.cuh"
+#include "gates.cuh"
+
+namespace bmq {
+
+template <class T>
+struct DevArray {
+    T* p = nullptr;
+    size_t n = 0;
+    DevArray() = default;
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    ~DevArray() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) BMQ_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// Host replay of BlockStore's accounting (store.hpp:64-117,188-232) in the
+// reference's sequential put order, so max_footprint_bytes and
+// spilled_blocks match the reference run with one worker.
+class StoreModel {
+public:
+    void reset(uint64_t num_ids, uint64_t budget);
+    void put(uint64_t id, uint64_t size);
+    void put_shared(uint64_t first_id, uint64_t last_id, uint64_t size);  // ids [first, last)
+    uint64_t peak() const { return peak_; }
+    uint64_t spilled_blocks() const { return spilled_blocks_; }
+    uint64_t size(uint64_t id) const { return size_[id]; }
+
+private:
+    void detach(uint64_t id);
+    bool place(uint64_t size);  // returns spilled
+    std::vector<uint64_t> size_;
+    std::vector<uint8_t> flags_;  // bit0 spilled, bit1 shared
+    uint64_t budget_ = ~0ull, resident_ = 0, spilled_live_ = 0, peak_ = 0, spilled_blocks_ = 0;
+    uint64_t shared_refs_ = 0, shared_size_ = 0;
+    bool shared_spilled_ = false;
+};
+
+struct StagePlan {
+    bmq_stage stage;
+    GroupGeometry gg;
+    GateProgram prog;  // over the 2^(b + |inner|) group buffer
+};
+
+class Engine {
+public:
+    Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_config& cfg);
+    ~Engine();
+
+    void init_state();
+    void run(bmq_report* rep, double* stage_ms, uint64_t stage_cap);
+    void run_stages(uint64_t first, uint64_t last);
+    double state_norm();
+    void extract_state(double* amps, uint64_t namps);
+    void amplitude(uint64_t index, double* re, double* im);
+    uint64_t get_payload(uint64_t id, uint8_t* out, uint64_t cap);
+    void get_payloads(uint8_t* out, uint64_t cap, uint64_t* sizes, uint64_t* total);
+    void put_payload(uint64_t id, const uint8_t* data, uint64_t size);
+    double fidelity_dense(const double* ideal, uint64_t namps);
+    double fidelity_analytic(int kind);
+    static double fidelity_pair(Engine& a, Engine& b);
+
+    const Layout& layout() const { return L_; }
+    const std::vector<bmq_stage>& plan() const { return plan_; }
+
+private:
+    void ensure_init();
+    void run_stage(uint64_t s);
+    void sync_meta_to_host();
+    // decompress `ids` (device list) into work slots; returns nothing
+    void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
+    void host_ids_to_device(const std::vector<uint64_t>& ids);
+    uint64_t zero_payload(uint8_t* out, uint64_t cap) const;
+    void check_device_error(const char* what);
+    void raw_run_stage(uint64_t s);
+
+    Layout L_;
+    bmq_config cfg_;
+    std::vector<bmq_gate> gates_;
+    std::vector<bmq_stage> plan_;
+    std::vector<std::unique_ptr<StagePlan>> stage_plans_;
+    const DevTables* tabs_ = nullptr;
+    int dev_ = 0;
+    cudaStream_t st_ = nullptr;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    bool initialized_ = false;
+    uint64_t next_stage_ = 0;
+
+    // compressed state: payload pools (ping-pong) + per-id metadata
+    DevArray<uint8_t> pool_[2];
+    uint64_t pool_cap_ = 0;
+    int cur_ = 0;
+    DevArray<uint64_t> cursor_;  // [2] pool cursors, [2..3] range scratch
+    DevArray<uint64_t> off_[2], size_[2];
+    DevArray<double> sums_;       // per id: sumsq, sum_re, sum_im (3 doubles)
+    DevArray<uint8_t> zero_hdr_;  // canonical ALL_ZERO payload (+ slack)
+    // raw mode (compress == false): dense planar state
+    DevArray<double> dense_;
+    // working set
+    DevArray<double> work_;
+    uint64_t work_scalars_ = 0;
+    uint64_t max_blocks_ = 0;
+    uint32_t nch_ = 1;
+    DevArray<CmpBlock> cmp_;
+    DevArray<DecBlock> dec_;
+    DevArray<ChunkPlan> cplan_;
+    DevArray<BlockPlan> bplan_;
+    DevArray<DecInfo> dinfo_;
+    DevArray<DecChunk> dchunk_;
+    DevArray<uint64_t> ids_;
+    DevArray<DevError> err_;
+    DevArray<double> red_;
+
+    // host mirrors
+    std::vector<uint64_t> h_off_, h_size_;
+    StoreModel store_;
+    uint64_t stage_compress_calls_ = 0, stage_decompress_calls_ = 0;
+    bmq_report counters_{};
+    uint64_t device_peak_ = 0;
+};
+
+}  // namespace bmq

@@ -1,0 +1,236 @@
+// host_circuit.cpp — host-side descriptors of the drop-in surface: gate
+// validation and unitaries (circuit.hpp), the benchmark generators
+// (benchmarks.hpp), layout / greedy staging / group geometry (partition.hpp).
+// These are the inputs the device path consumes; they run once per circuit.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <numbers>
+#include <random>
+
+#include "bmq_internal.hpp"
+
+namespace bmq {
+
+bool gate_is_two_qubit(uint32_t kind) {
+    return kind == BMQ_GATE_CX || kind == BMQ_GATE_CZ || kind == BMQ_GATE_CP;
+}
+
+// Circuit(n) and Circuit::add (circuit.hpp:103-127).
+void check_circuit(uint32_t n, const bmq_gate* gates, uint64_t count) {
+    if (n < 1 || n > 62)
+        raise(BMQ_ERR_INVALID_ARGUMENT, "qubit count must be in [1, 62], got " + std::to_string(n));
+    for (uint64_t i = 0; i < count; ++i) {
+        const bmq_gate& g = gates[i];
+        if (g.kind > BMQ_GATE_CP) raise(BMQ_ERR_INVALID_ARGUMENT, "unknown gate kind " + std::to_string(g.kind));
+        const auto out_of_range = [n](uint32_t q) {
+            return "gate operand " + std::to_string(q) + " out of range for " + std::to_string(n) + " qubits";
+        };
+        if (g.q0 >= n) raise(BMQ_ERR_INVALID_ARGUMENT, out_of_range(g.q0));
+        if (gate_is_two_qubit(g.kind)) {
+            if (g.q1 >= n) raise(BMQ_ERR_INVALID_ARGUMENT, out_of_range(g.q1));
+            if (g.q0 == g.q1) raise(BMQ_ERR_INVALID_ARGUMENT, "two-qubit gate operands must be distinct");
+        }
+    }
+}
+
+namespace {
+Cx from_std(std::complex<double> z) { return Cx{z.real(), z.imag()}; }
+}  // namespace
+
+// Entries use the same libm calls as the reference (sqrt, cos, sin,
+// std::polar), so every matrix entry is bit-identical to unitary2/unitary4.
+int gate_matrix(const bmq_gate& g, Cx* u) {
+    constexpr double pi = std::numbers::pi;
+    const double a = g.angle;
+    const Cx zero{0.0, 0.0}, one{1.0, 0.0};
+    if (gate_is_two_qubit(g.kind)) {
+        for (int i = 0; i < 16; ++i) u[i] = zero;
+        u[0] = one;   // |00> -> |00>
+        u[5] = one;   // |01> -> |01>
+        switch (g.kind) {
+        case BMQ_GATE_CX: u[11] = one; u[14] = one; break;          // swap |10>,|11>
+        case BMQ_GATE_CZ: u[10] = one; u[15] = Cx{-1.0, 0.0}; break;
+        default: u[10] = one; u[15] = from_std(std::polar(1.0, a)); break;  // CP
+        }
+        return 4;
+    }
+    for (int i = 0; i < 4; ++i) u[i] = zero;
+    switch (g.kind) {
+    case BMQ_GATE_H: {
+        const double h = 1.0 / std::sqrt(2.0);
+        u[0] = Cx{h, 0}; u[1] = Cx{h, 0}; u[2] = Cx{h, 0}; u[3] = Cx{-h, 0};
+        break;
+    }
+    case BMQ_GATE_X: u[1] = one; u[2] = one; break;
+    case BMQ_GATE_Y: u[1] = Cx{0, -1}; u[2] = Cx{0, 1}; break;
+    case BMQ_GATE_Z: u[0] = one; u[3] = Cx{-1, 0}; break;
+    case BMQ_GATE_S: u[0] = one; u[3] = Cx{0, 1}; break;
+    case BMQ_GATE_SDG: u[0] = one; u[3] = Cx{0, -1}; break;
+    case BMQ_GATE_T: u[0] = one; u[3] = from_std(std::polar(1.0, pi / 4)); break;
+    case BMQ_GATE_TDG: u[0] = one; u[3] = from_std(std::polar(1.0, -pi / 4)); break;
+    case BMQ_GATE_RX: {
+        const double c = std::cos(a / 2), s = std::sin(a / 2);
+        u[0] = Cx{c, 0}; u[1] = Cx{0, -s}; u[2] = Cx{0, -s}; u[3] = Cx{c, 0};
+        break;
+    }
+    case BMQ_GATE_RY: {
+        const double c = std::cos(a / 2), s = std::sin(a / 2);
+        u[0] = Cx{c, 0}; u[1] = Cx{-s, 0}; u[2] = Cx{s, 0}; u[3] = Cx{c, 0};
+        break;
+    }
+    case BMQ_GATE_RZ:
+        u[0] = from_std(std::polar(1.0, -a / 2));
+        u[3] = from_std(std::polar(1.0, a / 2));
+        break;
+    case BMQ_GATE_P: u[0] = one; u[3] = from_std(std::polar(1.0, a)); break;
+    default: raise(BMQ_ERR_LOGIC, "unitary2 called on a two-qubit gate");
+    }
+    return 2;
+}
+
+// Benchmark generators (benchmarks.hpp:44-166).
+std::vector<bmq_gate> make_benchmark(const std::string& name, uint32_t n, uint32_t layers,
+                                     uint64_t seed, const char* secret) {
+    const bool ghz = name == "ghz" || name == "cat_state";
+    if (!ghz && name != "bv" && name != "qft" && name != "qaoa")
+        raise(BMQ_ERR_INVALID_ARGUMENT, "unknown benchmark '" + name + "'");
+    if (n < 2) raise(BMQ_ERR_INVALID_ARGUMENT, name + " requires at least 2 qubits");
+    if (n > 62) raise(BMQ_ERR_INVALID_ARGUMENT, "qubit count must be in [1, 62], got " + std::to_string(n));
+    std::vector<bmq_gate> c;
+    const auto one = [&c](uint32_t k, uint32_t q, double ang = 0.0) { c.push_back({k, q, 0, 0, ang}); };
+    const auto two = [&c](uint32_t k, uint32_t q0, uint32_t q1, double ang = 0.0) {
+        c.push_back({k, q0, q1, 0, ang});
+    };
+    if (ghz) {  // H(0) then a CX ladder
+        one(BMQ_GATE_H, 0);
+        for (uint32_t q = 1; q < n; ++q) two(BMQ_GATE_CX, q - 1, q);
+    } else if (name == "bv") {
+        std::string s;
+        if (secret && *secret) {
+            s = secret;
+        } else {
+            for (uint32_t i = 0; i + 1 < n; ++i) s.push_back(i % 2 ? '0' : '1');
+        }
+        if (s.size() > n - 1)
+            raise(BMQ_ERR_INVALID_ARGUMENT, "bv secret longer than the " + std::to_string(n - 1) + " data qubits");
+        if (s.find_first_not_of("01") != std::string::npos)
+            raise(BMQ_ERR_INVALID_ARGUMENT, "bv secret must contain only '0' and '1'");
+        const uint32_t anc = n - 1;
+        one(BMQ_GATE_X, anc);
+        for (uint32_t q = 0; q < n; ++q) one(BMQ_GATE_H, q);
+        for (uint32_t i = 0; i < s.size(); ++i)
+            if (s[i] == '1') two(BMQ_GATE_CX, i, anc);
+        for (uint32_t q = 0; q < n; ++q) one(BMQ_GATE_H, q);
+    } else if (name == "qft") {
+        for (uint32_t t = n; t-- > 0;) {
+            one(BMQ_GATE_H, t);
+            for (uint32_t ctl = t; ctl-- > 0;)
+                two(BMQ_GATE_CP, ctl, t, std::numbers::pi / static_cast<double>(1ull << (t - ctl)));
+        }
+        for (uint32_t lo = 0; lo < n / 2; ++lo) {  // bit reversal, swaps as CX triples
+            const uint32_t hi = n - 1 - lo;
+            two(BMQ_GATE_CX, lo, hi);
+            two(BMQ_GATE_CX, hi, lo);
+            two(BMQ_GATE_CX, lo, hi);
+        }
+    } else {  // qaoa: ring ZZ via CX-RZ-CX, RX mixer, angles from mt19937_64
+        if (layers < 1) raise(BMQ_ERR_INVALID_ARGUMENT, "qaoa requires at least one layer");
+        std::mt19937_64 rng(seed);
+        const double two_pi = 2.0 * std::numbers::pi;
+        for (uint32_t l = 0; l < layers; ++l) {
+            const double gamma = static_cast<double>(rng() >> 11) * 0x1.0p-53 * two_pi;
+            const double beta = static_cast<double>(rng() >> 11) * 0x1.0p-53 * two_pi;
+            for (uint32_t q = 0; q < n; ++q) {
+                const uint32_t nxt = q + 1 == n ? 0 : q + 1;
+                two(BMQ_GATE_CX, q, nxt);
+                one(BMQ_GATE_RZ, nxt, gamma);
+                two(BMQ_GATE_CX, q, nxt);
+            }
+            for (uint32_t q = 0; q < n; ++q) one(BMQ_GATE_RX, q, beta);
+        }
+    }
+    return c;
+}
+
+Layout make_layout(uint32_t n, uint32_t b) {
+    if (n < 1 || n > 62) raise(BMQ_ERR_INVALID_ARGUMENT, "layout qubit count must be in [1, 62]");
+    if (b < 1 || b > n) raise(BMQ_ERR_INVALID_ARGUMENT, "local index bits must be in [1, n]");
+    return Layout{n, b, n - b};
+}
+
+// Greedy Alg. 1 staging (partition.hpp:59-101). The open stage's distinct
+// global operands are tracked as a bit mask; a gate that would push the
+// count past max(inner_size, 2) closes the stage (unless it is the stage's
+// first gate) and opens the next one with its own globals.
+std::vector<bmq_stage> partition_plan(uint32_t n, const bmq_gate* gates, uint64_t count,
+                                      uint32_t block_bits, uint32_t inner_size) {
+    check_circuit(n, gates, count);
+    const Layout L = make_layout(n, block_bits);
+    const uint32_t limit = std::max(inner_size, 2u);
+    const auto globals_of = [&](const bmq_gate& g) {
+        uint64_t m = 0;
+        if (g.q0 >= L.b) m |= 1ull << g.q0;
+        if (gate_is_two_qubit(g.kind) && g.q1 >= L.b) m |= 1ull << g.q1;
+        return m;
+    };
+    const auto close = [](std::vector<bmq_stage>& out, uint64_t begin, uint64_t end, uint64_t mask) {
+        bmq_stage st{};
+        st.gate_begin = begin;
+        st.gate_end = end;
+        for (uint32_t q = 0; q < 64; ++q)
+            if (mask >> q & 1) st.inner[st.inner_count++] = q;
+        out.push_back(st);
+    };
+    std::vector<bmq_stage> stages;
+    uint64_t open_mask = 0, begin = 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        const uint64_t g = globals_of(gates[i]);
+        const uint64_t merged = open_mask | g;
+        if (static_cast<uint32_t>(__builtin_popcountll(merged)) > limit && i > begin) {
+            close(stages, begin, i, open_mask);
+            begin = i;
+            open_mask = g;
+        } else {
+            open_mask = merged;
+        }
+    }
+    if (begin < count) close(stages, begin, count, open_mask);
+    return stages;
+}
+
+uint64_t GroupGeometry::block_id(uint64_t outer, uint64_t v) const {
+    return deposit_bits(outer, outer_mask) | deposit_bits(v, inner_mask);
+}
+
+// enumerate_groups geometry (partition.hpp:120-153): inner offsets q - b.
+GroupGeometry group_geometry(const Layout& L, const bmq_stage& st) {
+    GroupGeometry gg;
+    for (uint32_t i = 0; i < st.inner_count; ++i) {
+        const uint32_t q = st.inner[i];
+        if (q < L.b || q >= L.n)
+            raise(BMQ_ERR_INVALID_ARGUMENT,
+                  "stage inner index " + std::to_string(q) + " outside the global index range");
+        gg.inner_mask |= 1ull << (q - L.b);
+    }
+    gg.inner_bits = static_cast<uint32_t>(__builtin_popcountll(gg.inner_mask));
+    const uint64_t all = L.c >= 64 ? ~0ull : (1ull << L.c) - 1;
+    gg.outer_mask = all & ~gg.inner_mask;
+    gg.outer_bits = L.c - gg.inner_bits;
+    return gg;
+}
+
+// buffer_bit_of_qubit (partition.hpp:158-169).
+uint32_t buffer_bit(const Layout& L, const bmq_stage& st, uint32_t q) {
+    if (q < L.b) return q;
+    for (uint32_t i = 0; i < st.inner_count; ++i)
+        if (st.inner[i] == q) return L.b + i;
+    raise(BMQ_ERR_LOGIC, "qubit " + std::to_string(q) + " is an outer index for this stage");
+}
+
+uint64_t compress_bound(uint64_t n) {
+    const uint64_t chunks = (n + 4095) / 4096;
+    return 26 + 2 * ((chunks + 3) / 4 + (n + 7) / 8) + (n * 63 + 7) / 8 + 16;
+}
+
+}  // namespace bmq

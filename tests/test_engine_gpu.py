@@ -1,0 +1,192 @@
+"""Device Simulator parity (cbq::Simulator, engine.hpp:58-250): final
+payloads byte-identical to the reference run, reports (stages, peak
+footprint replayed in put order, spills, compression ratio, calls) equal,
+norm and fidelity within stated tolerances."""
+import ctypes as C
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+NORM_RTOL = 1e-10        # sums over up to 2^20 amplitudes in a different order
+FIDELITY_ATOL = 1e-6     # north_star: within 1e-6 of the reference fidelity
+
+
+def fnv(port, payloads):
+    f = port.lib.cbqo_fnv1a64
+    f.restype, f.argtypes = C.c_uint64, [C.c_char_p, C.c_uint64, C.c_uint64]
+    h = 0xCBF29CE484222325
+    for p in payloads:
+        if p:
+            h = f(p, len(p), h)
+    return h
+
+
+def golden_cases():
+    with open(os.path.join(GOLDEN, "sim_golden.json")) as f:
+        return json.load(f)["simulations"]
+
+
+@pytest.mark.parametrize("case", golden_cases(), ids=lambda c: f"{c['name']}{c['n']}-b{c['b']}-i{c['inner']}-{c['error_bound']}")
+def test_simulator_matches_reference_golden(gpu, port, case):
+    c = gpu.generate_benchmark(case["name"], case["n"], gpu.BenchmarkParams(layers=case["layers"], seed=1))
+    with gpu.Simulator(c, gpu.Config(block_bits=case["b"], inner_size=case["inner"],
+                                     error_bound=case["error_bound"])) as sim:
+        rep = sim.run()
+        want = case["report"]
+        assert rep.stage_count == want["stage_count"]
+        assert rep.max_footprint_bytes == want["max_footprint_bytes"]
+        assert rep.compression_ratio == want["compression_ratio"]
+        assert rep.spilled_blocks == want["spilled_blocks"]
+        assert rep.stage_compress_calls == want["stage_compress_calls"]
+        assert rep.stage_decompress_calls == want["stage_decompress_calls"]
+        assert rep.final_norm == pytest.approx(want["final_norm"], rel=NORM_RTOL)
+        assert f"{fnv(port, sim.payloads()):016x}" == case["payload_fnv"]
+        if want.get("has_fidelity"):
+            ideal = gpu.dense_reference(c)
+            f = sim.fidelity_dense(ideal)
+            assert abs(f - want["fidelity"]) <= FIDELITY_ATOL
+            if case["error_bound"] <= 1e-3:
+                assert f >= 0.99
+
+
+def random_circuit(gpu, rng, n, count):
+    gl = []
+    for _ in range(count):
+        k = int(rng.integers(15))
+        q0 = int(rng.integers(n))
+        q1 = int((q0 + 1 + rng.integers(n - 1)) % n)
+        gl.append((k, q0, q1 if k >= 12 else 0, float(rng.uniform(0, 6.28))))
+    return gl, gpu.Circuit(n, [gpu.Gate(gpu.GateKind(k), a, b, ang) for k, a, b, ang in gl])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_circuits_match_oracle(gpu, port, seed):
+    rng = np.random.default_rng(100 + seed)
+    n = 6 + seed % 9
+    gl, c = random_circuit(gpu, rng, n, 50)
+    b = 1 + int(rng.integers(n))
+    inner = int(rng.integers(5))
+    br = [1e-2, 1e-3, 1e-4, 0.5][seed % 4]
+    res = port.simulate(n, gl, b, inner, br, want_state=True)
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=inner, error_bound=br)) as sim:
+        rep = sim.run()
+        assert sim.payloads() == res.payloads
+        assert rep.max_footprint_bytes == res.report["max_footprint_bytes"]
+        assert rep.final_norm == pytest.approx(res.report["final_norm"], rel=NORM_RTOL)
+        st = sim.extract_state()
+        assert np.array_equal(st.view(np.uint64), res.state.view(np.uint64))
+        k = int(rng.integers(1 << n))
+        assert sim.amplitude(k) == res.state[k]
+
+
+def test_zero_group_skip_is_exact(gpu):
+    c = gpu.generate_benchmark("qft", 16)
+    outs = []
+    for skip in (True, False):
+        with gpu.Simulator(c, gpu.Config(block_bits=10, inner_size=2, zero_group_skip=skip)) as sim:
+            rep = sim.run()
+            outs.append((sim.payloads(), rep.max_footprint_bytes))
+            if skip:
+                assert rep.device["groups_skipped"] > 0
+            else:
+                assert rep.device["groups_skipped"] == 0
+    assert outs[0] == outs[1]
+
+
+def test_small_batches_are_exact(gpu, port):
+    c = gpu.generate_benchmark("qaoa", 14, gpu.BenchmarkParams(layers=2))
+    want = port.simulate(14, [g.as_tuple() for g in c.gates], 9, 2, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=9, inner_size=2, work_bytes=3 * (16 << 9) * 4)) as sim:
+        sim.run()
+        assert sim.payloads() == want.payloads
+
+
+def test_spill_accounting(gpu, port):
+    c = gpu.generate_benchmark("qft", 16)
+    gl = [g.as_tuple() for g in c.gates]
+    want = port.simulate(16, gl, 8, 2, 1e-3, memory_budget=20000)
+    with gpu.Simulator(c, gpu.Config(block_bits=8, inner_size=2, memory_budget=20000)) as sim:
+        rep = sim.run()
+        assert rep.spilled_blocks == want.report["spilled_blocks"] > 0
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert sim.payloads() == want.payloads
+
+
+def test_uncompressed_mode(gpu, port):
+    rng = np.random.default_rng(21)
+    gl, c = random_circuit(gpu, rng, 10, 60)
+    want = port.simulate(10, gl, 4, 2, 1e-3, compress=False, want_state=True)
+    with gpu.Simulator(c, gpu.Config(block_bits=4, inner_size=2, compress=False)) as sim:
+        rep = sim.run()
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert np.array_equal(sim.extract_state(), want.state)  # values equal (zero signs may differ)
+        assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=NORM_RTOL)
+
+
+def test_fidelity_paths_agree(gpu):
+    c = gpu.generate_benchmark("qft", 14)
+    with gpu.Simulator(c, gpu.Config(block_bits=8, inner_size=2)) as sim, \
+            gpu.Simulator(c, gpu.Config(block_bits=8, inner_size=2, compress=False)) as exact:
+        sim.run()
+        exact.run()
+        f_dense = sim.fidelity_dense(gpu.dense_reference(c))
+        f_pair = sim.fidelity_with(exact)
+        f_uni = sim.fidelity_analytic("uniform")
+        assert f_dense >= 0.99
+        assert f_pair == pytest.approx(f_dense, abs=1e-9)
+        assert f_uni == pytest.approx(f_dense, abs=1e-9)
+    g = gpu.generate_benchmark("ghz", 14)
+    with gpu.Simulator(g, gpu.Config(block_bits=6, inner_size=2)) as sim:
+        sim.run()
+        assert sim.fidelity_analytic("ghz") == pytest.approx(sim.fidelity_dense(gpu.dense_reference(g)), abs=1e-12)
+
+
+def test_payload_round_trip_and_errors(gpu, port):
+    c = gpu.generate_benchmark("qaoa", 10, gpu.BenchmarkParams(layers=1))
+    with gpu.Simulator(c, gpu.Config(block_bits=5, inner_size=2)) as sim:
+        sim.init_state()
+        with pytest.raises(gpu.EngineError, match="already initialized"):
+            sim.init_state()
+        x = np.linspace(-0.1, 0.1, 64)
+        p = port.compress_block(x, 1e-3)
+        sim.put_payload(3, p)
+        assert sim.get_payload(3) == p
+        assert sim.amplitude(3 * 32 + 5) == complex(port.decompress_block(p)[5], port.decompress_block(p)[37])
+        with pytest.raises(gpu.CodecError, match="codes truncated"):
+            sim.put_payload(4, p[:-1])
+        assert sim.get_payload(4) == port.compress_block(np.zeros(64), 1e-3)
+    big = gpu.generate_benchmark("ghz", 26)
+    with gpu.Simulator(big, gpu.Config(block_bits=20, inner_size=2)) as sim:
+        with pytest.raises(gpu.EngineError, match="dense verification refused: 26 qubits exceeds the cap of 24"):
+            sim.extract_state()
+
+
+def test_stage_by_stage_driver(gpu):
+    c = gpu.generate_benchmark("qft", 12)
+    with gpu.Simulator(c, gpu.Config(block_bits=6, inner_size=2)) as a, \
+            gpu.Simulator(c, gpu.Config(block_bits=6, inner_size=2)) as b:
+        a.run()
+        nst = len(b.plan().stages)
+        for s in range(nst):
+            b.run_stages(s, s + 1)
+        assert a.payloads() == b.payloads()
+        with pytest.raises(gpu.EngineError, match="stages must run in order"):
+            b.run_stages(0, 1)
+
+
+@pytest.mark.slow
+def test_ghz30_b20_block_sizes(gpu):
+    """C2 shape: GHZ-30, b=20, inner=2 — only the two end blocks are nonzero."""
+    c = gpu.generate_benchmark("ghz", 30)
+    with gpu.Simulator(c, gpu.Config(block_bits=20, inner_size=2)) as sim:
+        rep = sim.run()
+        assert rep.stage_count == 9
+        sizes = [len(sim.get_payload(i)) for i in (0, 1, 1023)]
+        assert sizes[1] == 26
+        assert sim.fidelity_analytic("ghz") >= 0.99
+        assert abs(rep.final_norm - 1) < 2e-3
