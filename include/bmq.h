@@ -123,6 +123,17 @@ typedef struct bmq_report {
     uint64_t kernel_launches;
     uint64_t device_peak_bytes;     /* pools + working set high-water */
     uint64_t gate_passes;
+    /* CUDA-event time per phase of the stage loop (engine stream) */
+    double decompress_ms;           /* descriptor build + index + decode */
+    double gate_ms;                 /* gate-program passes */
+    double compress_ms;             /* stats + plan + alloc + zero + emit + sums */
+    uint64_t batches;
+    /* algorithmic HBM bytes per phase (roofline numerators) */
+    uint64_t decompress_bytes;      /* payload bytes read + 16 B per amplitude written */
+    uint64_t gate_bytes;            /* 32 B per amplitude per gate pass */
+    uint64_t compress_bytes;        /* 16 B per amplitude read + payload bytes written */
+    uint64_t fused_batches;         /* batches whose last gate pass quantised in place */
+    uint64_t compactions;           /* payload arena compactions */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only
@@ -206,6 +217,9 @@ int bmq_simulator_plan(const bmq_simulator* sim, bmq_stage* out, uint64_t cap, u
 int bmq_simulator_init_state(bmq_simulator* sim);
 /* run() (engine.hpp:97-134); stage_ms may be NULL. */
 int bmq_simulator_run(bmq_simulator* sim, bmq_report* report, double* stage_ms, uint64_t stage_cap);
+/* Discard the state so init_state()/run() can start over (plan, tables and
+ * device buffers are kept). */
+int bmq_simulator_reset(bmq_simulator* sim);
 /* run stages [first, last) only (stage-level driver for pipelined callers). */
 int bmq_simulator_run_stages(bmq_simulator* sim, uint64_t first, uint64_t last);
 /* state_norm() (engine.hpp:150-158) */

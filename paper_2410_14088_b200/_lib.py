@@ -56,7 +56,10 @@ class bmq_report(C.Structure):
                 ("groups_processed", C.c_uint64), ("groups_skipped", C.c_uint64),
                 ("blocks_processed", C.c_uint64), ("payload_bytes_read", C.c_uint64),
                 ("payload_bytes_written", C.c_uint64), ("dense_bytes", C.c_uint64),
-                ("kernel_launches", C.c_uint64), ("device_peak_bytes", C.c_uint64), ("gate_passes", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("device_peak_bytes", C.c_uint64), ("gate_passes", C.c_uint64),
+                ("decompress_ms", C.c_double), ("gate_ms", C.c_double), ("compress_ms", C.c_double),
+                ("batches", C.c_uint64), ("decompress_bytes", C.c_uint64), ("gate_bytes", C.c_uint64),
+                ("compress_bytes", C.c_uint64), ("fused_batches", C.c_uint64), ("compactions", C.c_uint64)]
 
 
 _P = C.c_void_p
@@ -89,6 +92,7 @@ SIGNATURES = {
     "bmq_simulator_init_state": (C.c_int, [_P]),
     "bmq_simulator_run": (C.c_int, [_P, C.POINTER(bmq_report), _P, _U64]),
     "bmq_simulator_run_stages": (C.c_int, [_P, _U64, _U64]),
+    "bmq_simulator_reset": (C.c_int, [_P]),
     "bmq_simulator_state_norm": (C.c_int, [_P, C.POINTER(_D)]),
     "bmq_simulator_extract_state": (C.c_int, [_P, _P, _U64]),
     "bmq_simulator_amplitude": (C.c_int, [_P, _U64, C.POINTER(_D), C.POINTER(_D)]),

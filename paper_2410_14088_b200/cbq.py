@@ -615,11 +615,17 @@ class Simulator:
         _check(lib.bmq_simulator_run(self._h, C.byref(r), _ptr(stage_ms), nst))
         dev = {k: getattr(r, k) for k in ("device_ms", "groups_processed", "groups_skipped", "blocks_processed",
                                            "payload_bytes_read", "payload_bytes_written", "dense_bytes",
-                                           "kernel_launches", "device_peak_bytes", "gate_passes")}
+                                           "kernel_launches", "device_peak_bytes", "gate_passes", "decompress_ms",
+                                           "gate_ms", "compress_ms", "batches", "decompress_bytes",
+                                           "gate_bytes", "compress_bytes", "fused_batches", "compactions")}
         return SimulationReport(r.qubits, r.gate_count, r.stage_count, r.max_footprint_bytes, r.standard_bytes,
                                 r.compression_ratio, r.spilled_blocks, r.wall_ms, stage_ms[: r.stage_count].tolist(),
                                 r.fidelity if r.has_fidelity else None, r.final_norm, r.stage_compress_calls,
                                 r.stage_decompress_calls, dev)
+
+    def reset(self) -> None:
+        """Drop the state; the next run() starts from |0...0> again."""
+        _check(lib.bmq_simulator_reset(self._h))
 
     def run_stages(self, first: int, last: int) -> None:
         _check(lib.bmq_simulator_run_stages(self._h, first, last))

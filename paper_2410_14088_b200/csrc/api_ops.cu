@@ -52,13 +52,15 @@ void api_compress_blocks(const double* scalars, uint64_t nblocks, uint64_t n, do
     cursor.alloc(4);
     err.alloc(1);
     if (n) BMQ_CUDA(cudaMemcpyAsync(din.p, scalars, nblocks * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    DevArray<uint32_t> pk;
+    pk.alloc(std::max<uint64_t>(1, nblocks * n));
     std::vector<CmpBlock> hb(nblocks);
-    for (uint64_t k = 0; k < nblocks; ++k) hb[k] = CmpBlock{din.p + k * n, n, k};
+    for (uint64_t k = 0; k < nblocks; ++k) hb[k] = CmpBlock{din.p + k * n, pk.p + k * n, n, k};
     BMQ_CUDA(cudaMemcpyAsync(blks.p, hb.data(), nblocks * sizeof(CmpBlock), cudaMemcpyHostToDevice, st));
     BMQ_CUDA(cudaMemsetAsync(cursor.p, 0, 4 * sizeof(uint64_t), st));
     BMQ_CUDA(cudaMemsetAsync(err.p, 0, sizeof(DevError), st));
     launch_compress(st, blks.p, nblocks, nch, t, dout.p, nblocks * bound, cursor.p, cursor.p + 2, bp.p, cp.p, nullptr,
-                    nullptr, false, err.p, nullptr);
+                    nullptr, false, false, err.p, nullptr);
     std::vector<BlockPlan> hp(nblocks);
     DevError e{};
     uint64_t total = 0;

@@ -216,6 +216,13 @@ int bmq_simulator_run(bmq_simulator* sim, bmq_report* report, double* stage_ms, 
     });
 }
 
+int bmq_simulator_reset(bmq_simulator* sim) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->reset();
+    });
+}
+
 int bmq_simulator_run_stages(bmq_simulator* sim, uint64_t first, uint64_t last) {
     return guarded([&] {
         null_check(sim, "simulator");

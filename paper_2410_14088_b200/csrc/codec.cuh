@@ -1,4 +1,4 @@
-// codec.cuh — launchers of the device codec (codec.cu).
+// codec.cuh — launchers of the device codec (codec_cmp.cu, codec_dec.cu).
 #pragma once
 
 #include "device_common.cuh"
@@ -6,12 +6,25 @@
 namespace bmq {
 
 // Compress nblk blocks (descriptors in device memory) into the byte region
-// `out` starting at *d_cursor (device). Payload offsets/sizes land in d_bp
-// and, when meta_off is given, in meta_off[id] / meta_size[id].
+// `out` starting at *d_cursor (device). When have_pk is false the blocks'
+// scalars (CmpBlock::in) are quantised first into CmpBlock::pk and d_cp;
+// otherwise a producer (the fused gate epilogue) already filled both, with
+// d_cp zero-initialised before it ran. Payload offsets/sizes land in d_bp and,
+// when meta_off is given, in meta_off[id] / meta_size[id].
 void launch_compress(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                      uint8_t* out, uint64_t out_cap, uint64_t* d_cursor, uint64_t* d_range, BlockPlan* d_bp,
-                     ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size, bool virtual_zero, DevError* d_err,
-                     uint64_t* launches);
+                     ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size, bool virtual_zero, bool have_pk,
+                     DevError* d_err, uint64_t* launches);
+
+// The two halves of launch_compress: quantise (unless have_pk) + plan, and
+// alloc + zero + emit (which may be launched again after DE_POOL_FULL).
+void launch_compress_plan(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
+                          const DevTables& t, BlockPlan* d_bp, ChunkPlan* d_cp, bool have_pk, DevError* d_err,
+                          uint64_t* launches);
+void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
+                          const DevTables& t, uint8_t* out, uint64_t out_cap, uint64_t* d_cursor, uint64_t* d_range,
+                          BlockPlan* d_bp, ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size,
+                          bool virtual_zero, uint32_t align, DevError* d_err, uint64_t* launches);
 
 // Decompress nblk payloads into their planar output buffers.
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,

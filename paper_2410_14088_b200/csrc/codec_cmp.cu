@@ -1,0 +1,506 @@
+// codec_cmp.cu — byte-exact device compressor (compress_block,
+// codec.hpp:227-295; prescan_encode, bitmap.hpp:109-145) for batches of
+// blocks, plus the codec tables, error messages and device allocator.
+//
+// Work decomposition: one CTA of 128 threads per 4096-scalar chunk, which is
+// exactly one prescan chunk of each bitmap (bitmap.hpp:76). Warp w, step j
+// handles scalars 128 j + 32 w + lane, so global loads/stores are coalesced
+// and a warp ballot yields bitmap word 4 j + w directly (the paper's warp
+// ballot pre-scan).
+//
+// Compress = quantise (k_cmp_stats, or fused into the stage's last gate pass):
+//              packed code word per scalar + per-chunk counters
+//          -> plan  (per block: code_min, width, tags, segment offsets, size)
+//          -> alloc (exclusive scan of sizes into the output region)
+//          -> zero  (clear the region so shared edge words can be OR-ed)
+//          -> emit  (header, tags, raw mixed chunks, LSB-first codes) from the
+//                    packed words — no second quantisation.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <cfloat>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#include "codec.cuh"
+#include "codec_util.cuh"
+
+namespace bmq {
+
+// --------------------------------------------------------------- messages
+const char* dev_error_message(uint32_t code) {
+    switch (code) {
+    case DE_NONFINITE: return "input scalars must be finite";
+    case DE_WINDOW: return "scalar magnitude below the quantiser table window of this error bound";
+    case DE_HDR_TRUNC: return "header truncated";
+    case DE_HDR_BOUND: return "header: invalid relative error bound";
+    case DE_HDR_TRAIL: return "header: trailing bytes after payload";
+    case DE_SIGN_TRUNC: return "sign bitmap truncated";
+    case DE_ZERO_TRUNC: return "zero bitmap truncated";
+    case DE_TAG: return "bitmap tag stream corrupt: invalid chunk tag";
+    case DE_PARTIAL: return "bitmap final partial chunk must be stored raw";
+    case DE_WIDTH0: return "codes: width zero with nonzero scalars present";
+    case DE_CODES_TRUNC: return "codes truncated";
+    case DE_CODES_TRAIL: return "codes: trailing bytes after payload";
+    case DE_BOUND_MISMATCH: return "header: relative bound differs from the decoder tables";
+    case DE_COUNT: return "block payload scalar count does not match the layout";
+    case DE_CODE_WINDOW: return "codes: decoded code outside the dequantisation table";
+    case DE_POOL_FULL: return "device payload pool exhausted";
+    case DE_TOO_LARGE: return "payload scalar count exceeds the launch geometry";
+    default: return "unknown device error";
+    }
+}
+
+int dev_error_status(uint32_t code) {
+    if (code == DE_COUNT) return BMQ_ERR_ENGINE;
+    if (code == DE_POOL_FULL) return BMQ_ERR_STORE;
+    return BMQ_ERR_CODEC;
+}
+
+// ------------------------------------------------------------- allocation
+void* dev_alloc(size_t bytes) {
+    int dev = 0;
+    BMQ_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static bool configured[64] = {};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev < 64 && !configured[dev]) {
+            cudaMemPool_t pool;
+            BMQ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+            uint64_t thr = ~0ull;
+            BMQ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+            configured[dev] = true;
+        }
+    }
+    void* p = nullptr;
+    BMQ_CUDA(cudaMallocAsync(&p, bytes, cudaStreamPerThread));
+    BMQ_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+    return p;
+}
+
+void dev_free(void* p) {
+    if (!p) return;
+    cudaDeviceSynchronize();
+    cudaFreeAsync(p, cudaStreamPerThread);
+    cudaStreamSynchronize(cudaStreamPerThread);
+}
+
+// ------------------------------------------------------------------ tables
+const DevTables& device_tables(double b_r) {
+    static std::mutex mu;
+    static std::map<std::pair<int, uint64_t>, DevTables> cache;
+    const CodecTables& h = host_tables(b_r);
+    int dev = 0;
+    BMQ_CUDA(cudaGetDevice(&dev));
+    uint64_t key;
+    std::memcpy(&key, &b_r, 8);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({dev, key});
+    if (it != cache.end()) return it->second;
+    if (static_cast<uint64_t>(h.qhi - h.qlo) >= kQOffMax)
+        raise(BMQ_ERR_INVALID_ARGUMENT, "error bound too small for the device code window");
+    DevTables t{};
+    uint64_t* th = nullptr;
+    double* dq = nullptr;
+    BMQ_CUDA(cudaMalloc(&th, h.thresh.size() * sizeof(uint64_t)));
+    BMQ_CUDA(cudaMalloc(&dq, h.dequant.size() * sizeof(double)));
+    BMQ_CUDA(cudaMemcpy(th, h.thresh.data(), h.thresh.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    BMQ_CUDA(cudaMemcpy(dq, h.dequant.data(), h.dequant.size() * sizeof(double), cudaMemcpyHostToDevice));
+    t.thresh = th;
+    t.dequant = dq;
+    t.qlo = h.qlo;
+    t.qhi = h.qhi;
+    t.idem_lo = h.idem_lo;
+    t.idem_hi = h.idem_hi;
+    t.b_r = h.b_r;
+    t.inv_ba = 1.0 / h.b_a;
+    return cache.emplace(std::make_pair(dev, key), t).first->second;
+}
+
+namespace {
+
+// ---------------------------------------------------------------- stats
+// Quantise one chunk: packed code words + per-chunk counters.
+__global__ void __launch_bounds__(kChunkThreads) k_cmp_stats(const CmpBlock* __restrict__ blks, uint32_t nch_max,
+                                                             ChunkPlan* __restrict__ cps, DevTables t,
+                                                             DevError* err) {
+    const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
+    const CmpBlock blk = blks[bi];
+    const uint64_t nch = (blk.count + kChunk - 1) / kChunk;
+    if (c >= nch) return;
+    const uint32_t len = chunk_len(blk.count, c);
+    const double* src = blk.in + static_cast<uint64_t>(c) * kChunk;
+    uint32_t* dst = blk.pk + static_cast<uint64_t>(c) * kChunk;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    ChunkAcc acc;
+    bool bad = false, oow = false;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t s = 128 * j + 32 * w + lane;
+        if (s < len) {
+            const uint32_t pk = quantize_pack(__ldg(src + s), t, bad, oow);
+            dst[s] = pk;
+            acc.add(pk);
+        }
+    }
+    if (bad) dev_fail(err, DE_NONFINITE, bi);
+    if (oow) dev_fail(err, DE_WINDOW, bi);
+    flush_chunk(cps + static_cast<uint64_t>(bi) * nch_max + c, acc);
+}
+
+// ----------------------------------------------------------------- plan
+// One CTA per block: reduce chunk counters, derive tags, lay out segments.
+constexpr int kPlanThreads = 256;
+
+__device__ __forceinline__ uint8_t tag_of(uint32_t ones, uint32_t len) {
+    if (len < kChunk) return 2;  // a partial chunk is always stored raw
+    return ones == 0 ? 0 : (ones == len ? 1 : 2);
+}
+
+__global__ void __launch_bounds__(kPlanThreads) k_cmp_plan(const CmpBlock* __restrict__ blks, uint32_t nch_max,
+                                                           ChunkPlan* __restrict__ cps, BlockPlan* __restrict__ bps,
+                                                           int64_t qlo) {
+    const uint32_t bi = blockIdx.x;
+    const CmpBlock blk = blks[bi];
+    const uint32_t nch = static_cast<uint32_t>((blk.count + kChunk - 1) / kChunk);
+    ChunkPlan* cp = cps + static_cast<uint64_t>(bi) * nch_max;
+    using ReduceU = cub::BlockReduce<unsigned long long, kPlanThreads>;
+    using Scan = cub::BlockScan<unsigned long long, kPlanThreads>;
+    __shared__ typename ReduceU::TempStorage rs;
+    __shared__ typename Scan::TempStorage ss;
+    __shared__ unsigned long long s_tot[5];
+    // pass 1: totals
+    unsigned long long mninv = 0, mx = 0, nnz = 0, sraw = 0, zraw = 0;
+    for (uint32_t c = threadIdx.x; c < nch; c += kPlanThreads) {
+        const ChunkPlan p = cp[c];
+        const uint32_t len = chunk_len(blk.count, c);
+        if (p.nnz) {
+            mninv = max(mninv, static_cast<unsigned long long>(p.qmin_inv));
+            mx = max(mx, static_cast<unsigned long long>(p.qmax_off));
+        }
+        nnz += p.nnz;
+        if (tag_of(p.nneg, len) == 2) sraw += (len + 7) / 8;
+        if (tag_of(len - p.nnz, len) == 2) zraw += (len + 7) / 8;
+    }
+    const unsigned long long r0 = ReduceU(rs).Reduce(mninv, cub::Max());
+    __syncthreads();
+    const unsigned long long r1 = ReduceU(rs).Reduce(mx, cub::Max());
+    __syncthreads();
+    const unsigned long long r2 = ReduceU(rs).Sum(nnz);
+    __syncthreads();
+    const unsigned long long r3 = ReduceU(rs).Sum(sraw);
+    __syncthreads();
+    const unsigned long long r4 = ReduceU(rs).Sum(zraw);
+    if (threadIdx.x == 0) {
+        s_tot[0] = r0;
+        s_tot[1] = r1;
+        s_tot[2] = r2;
+        s_tot[3] = r3;
+        s_tot[4] = r4;
+    }
+    __syncthreads();
+    const uint64_t qmin_off = kQOffMax - s_tot[0], qmax_off = s_tot[1], total_nnz = s_tot[2];
+    const uint32_t ntag = (nch + 3) / 4;
+    const uint64_t ztag_off = kHeaderBytes + ntag + s_tot[3];
+    const uint64_t code_seg = ztag_off + ntag + s_tot[4];
+    uint32_t width = 0;
+    if (total_nnz) {
+        const uint64_t range = qmax_off - qmin_off;
+        width = range ? 64 - __clzll(static_cast<long long>(range)) : 1;
+    }
+    // pass 2: tags and per-chunk offsets (exclusive scans in chunk order)
+    unsigned long long carry_s = 0, carry_z = 0, carry_n = 0;
+    for (uint32_t base = 0; base < nch; base += kPlanThreads) {
+        const uint32_t c = base + threadIdx.x;
+        unsigned long long vs = 0, vz = 0, vn = 0;
+        ChunkPlan p{};
+        if (c < nch) {
+            p = cp[c];
+            const uint32_t len = chunk_len(blk.count, c);
+            p.stag = tag_of(p.nneg, len);
+            p.ztag = tag_of(len - p.nnz, len);
+            vs = p.stag == 2 ? (len + 7) / 8 : 0;
+            vz = p.ztag == 2 ? (len + 7) / 8 : 0;
+            vn = p.nnz;
+        }
+        unsigned long long ps, pz, pn, ts, tz, tn;
+        Scan(ss).ExclusiveSum(vs, ps, ts);
+        __syncthreads();
+        Scan(ss).ExclusiveSum(vz, pz, tz);
+        __syncthreads();
+        Scan(ss).ExclusiveSum(vn, pn, tn);
+        __syncthreads();
+        if (c < nch) {
+            p.sign_off = static_cast<uint32_t>(kHeaderBytes + ntag + carry_s + ps);
+            p.zero_off = static_cast<uint32_t>(ztag_off + ntag + carry_z + pz);
+            p.nz_prefix = static_cast<uint32_t>(carry_n + pn);
+            cp[c] = p;
+        }
+        carry_s += ts;
+        carry_z += tz;
+        carry_n += tn;
+    }
+    if (threadIdx.x == 0) {
+        BlockPlan bp{};
+        bp.nch = nch;
+        bp.ntag = ntag;
+        bp.nnz = total_nnz;
+        if (total_nnz == 0) {
+            bp.flags = 1;
+            bp.size = kHeaderBytes;
+        } else {
+            bp.code_min = qlo + static_cast<int64_t>(qmin_off);
+            bp.code_max = qlo + static_cast<int64_t>(qmax_off);
+            bp.width = width;
+            bp.ztag_off = ztag_off;
+            bp.code_seg = code_seg;
+            bp.size = code_seg + (total_nnz * width + 7) / 8;
+        }
+        bps[bi] = bp;
+    }
+}
+
+// ---------------------------------------------------------------- alloc
+// Single CTA: exclusive scan of payload sizes into [cursor, cursor + total).
+// virtual_zero: ALL_ZERO payloads take no space (engine pools); they are
+// materialised as the canonical 26-byte header on read.
+constexpr int kAllocThreads = 1024;
+
+// Payloads are placed at multiples of `align` (16 in engine arenas, so they
+// can be moved with 16-byte copies; 1 for back-to-back API output). Nothing
+// is written when the region would overflow `cap` (DE_POOL_FULL): the caller
+// makes room and launches the allocation again.
+__global__ void __launch_bounds__(kAllocThreads) k_cmp_alloc(const CmpBlock* __restrict__ blks, uint64_t nblk,
+                                                             BlockPlan* __restrict__ bps, uint64_t* cursor,
+                                                             uint64_t cap, uint64_t* range, int virtual_zero,
+                                                             uint32_t align, uint64_t* meta_off,
+                                                             uint64_t* meta_size, DevError* err) {
+    using Scan = cub::BlockScan<unsigned long long, kAllocThreads>;
+    using Reduce = cub::BlockReduce<unsigned long long, kAllocThreads>;
+    __shared__ typename Scan::TempStorage ss;
+    __shared__ typename Reduce::TempStorage rs;
+    __shared__ bool s_fits;
+    const uint64_t start = *cursor;
+    const auto placed = [&](uint64_t i) -> unsigned long long {
+        const BlockPlan& p = bps[i];
+        if (virtual_zero && (p.flags & 1)) return 0;
+        return (p.size + align - 1) / align * align;
+    };
+    unsigned long long part = 0;
+    for (uint64_t i = threadIdx.x; i < nblk; i += kAllocThreads) part += placed(i);
+    const unsigned long long total = Reduce(rs).Sum(part);
+    if (threadIdx.x == 0) {
+        s_fits = start + total <= cap;
+        if (!s_fits) {
+            dev_fail(err, DE_POOL_FULL, 0);
+            range[0] = range[1] = start;
+        } else {
+            range[0] = start;
+            range[1] = start + total;
+            *cursor = start + total;
+        }
+    }
+    __syncthreads();
+    if (!s_fits) return;
+    unsigned long long carry = 0;
+    for (uint64_t base = 0; base < nblk; base += kAllocThreads) {
+        const uint64_t i = base + threadIdx.x;
+        const unsigned long long sz = i < nblk ? placed(i) : 0;
+        unsigned long long pre, tot;
+        Scan(ss).ExclusiveSum(sz, pre, tot);
+        __syncthreads();
+        if (i < nblk) {
+            BlockPlan& p = bps[i];
+            const bool virt = virtual_zero && (p.flags & 1);
+            p.out_off = virt ? ~0ull : start + carry + pre;
+            if (meta_off) {
+                const uint64_t id = blks[i].id;
+                meta_off[id] = p.out_off;
+                meta_size[id] = p.size;
+            }
+        }
+        carry += tot;
+    }
+}
+
+__global__ void k_zero_range(uint8_t* base, const uint64_t* range) {
+    const uint64_t a = range[0], b = range[1];
+    if (b <= a) return;
+    const uint64_t wa = (a + 3) / 4, wb = b / 4;  // whole words [wa, wb)
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint32_t* w = reinterpret_cast<uint32_t*>(base);
+    if (wa < wb) {
+        for (uint64_t i = wa + tid; i < wb; i += stride) w[i] = 0;
+        if (tid < 4) {
+            const uint64_t x = a + tid;
+            if (x < wa * 4) base[x] = 0;
+            const uint64_t y = wb * 4 + tid;
+            if (y < b) base[y] = 0;
+        }
+    } else if (tid < b - a) {
+        base[a + tid] = 0;
+    }
+}
+
+// ----------------------------------------------------------------- emit
+constexpr int kStageWords = (kChunk * 30 + 31) / 32 + 2;  // codes are < 2^30 (kQOffMax)
+
+__global__ void __launch_bounds__(kChunkThreads) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
+                                                            const ChunkPlan* __restrict__ cps,
+                                                            BlockPlan* __restrict__ bps, uint8_t* __restrict__ out,
+                                                            DevTables t, const DevError* err) {
+    if (err->code) return;
+    const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
+    const CmpBlock blk = blks[bi];
+    const BlockPlan bp = bps[bi];
+    if (c > 0 && c >= bp.nch) return;  // (an empty block still gets its header from chunk 0)
+    if (bp.out_off == ~0ull) return;   // virtual ALL_ZERO
+    uint8_t* pay = out + bp.out_off;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (c == 0 && tid == 0) {  // header (codec.hpp:282-286)
+        uint64_t v[3];
+        v[0] = blk.count;
+        v[1] = static_cast<uint64_t>(__double_as_longlong(t.b_r));
+        v[2] = static_cast<uint64_t>(bp.code_min);
+        for (int f = 0; f < 3; ++f)
+            for (int k = 0; k < 8; ++k) pay[8 * f + k] = static_cast<uint8_t>(v[f] >> (8 * k));
+        pay[24] = static_cast<uint8_t>(bp.width);
+        pay[25] = static_cast<uint8_t>(bp.flags);
+    }
+    if (bp.flags & 1) return;
+    const ChunkPlan* cp = cps + static_cast<uint64_t>(bi) * nch_max;
+    if (c == 0) {  // tag bytes of both bitmaps
+        for (uint32_t k = tid; k < bp.ntag; k += kChunkThreads) {
+            uint32_t sb = 0, zb = 0;
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint32_t cc = 4 * k + i;
+                if (cc < bp.nch) {
+                    sb |= static_cast<uint32_t>(cp[cc].stag) << (2 * i);
+                    zb |= static_cast<uint32_t>(cp[cc].ztag) << (2 * i);
+                }
+            }
+            pay[kHeaderBytes + k] = static_cast<uint8_t>(sb);
+            pay[bp.ztag_off + k] = static_cast<uint8_t>(zb);
+        }
+    }
+    const ChunkPlan p = cp[c];
+    const uint32_t len = chunk_len(blk.count, c);
+    const uint32_t* src = blk.pk + static_cast<uint64_t>(c) * kChunk;
+    __shared__ uint32_t s_sign[kWordsPerChunk], s_zero[kWordsPerChunk], s_pre[kWordsPerChunk];
+    __shared__ uint32_t stage[kStageWords];
+    __shared__ double s_red[3][4];
+    const uint32_t w_bits = bp.width;
+    const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
+    const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
+    const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
+    for (uint32_t i = tid; i < nstage; i += kChunkThreads) stage[i] = 0;
+    uint32_t pkv[32];
+    double sq = 0.0, sre = 0.0, sim = 0.0;
+    const uint64_t half = blk.count / 2, g0 = static_cast<uint64_t>(c) * kChunk;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {  // all loads in flight before the first ballot
+        const uint32_t s = 128 * j + 32 * w + lane;
+        pkv[j] = s < len ? __ldg(src + s) : 1u;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t s = 128 * j + 32 * w + lane;
+        const bool valid = s < len;
+        const uint32_t pk = pkv[j];
+        const uint32_t sw = __ballot_sync(0xffffffffu, (pk >> 1) & 1u);
+        const uint32_t zw = __ballot_sync(0xffffffffu, valid && (pk & 1u));
+        if (lane == 0) {
+            s_sign[4 * j + w] = sw;
+            s_zero[4 * j + w] = zw;
+        }
+        if (!(pk & 1u)) {
+            const double m = __ldg(t.dequant + (pk >> 2));
+            sq += m * m;
+            const double sv = (pk & 2u) ? -m : m;
+            if (g0 + s < half)
+                sre += sv;
+            else
+                sim += sv;
+        }
+    }
+    __syncthreads();
+    // nonzero prefix over the 128 words in scalar order
+    {
+        using Scan = cub::BlockScan<uint32_t, kChunkThreads>;
+        __shared__ typename Scan::TempStorage ss;
+        const uint32_t cnt = __popc(~s_zero[tid] & word_mask(len, tid));
+        uint32_t pre;
+        Scan(ss).ExclusiveSum(cnt, pre);
+        s_pre[tid] = pre;
+    }
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t k = 4 * j + w;
+        const uint32_t nzw = ~s_zero[k] & word_mask(len, k);
+        if ((nzw >> lane) & 1u) {
+            const uint32_t rank = s_pre[k] + __popc(nzw & lt);
+            const uint64_t code = static_cast<uint64_t>((pkv[j] >> 2) - qmin_off);
+            const uint64_t pos = static_cast<uint64_t>(rank) * w_bits;
+            const uint32_t wi = static_cast<uint32_t>(pos >> 5), sh = static_cast<uint32_t>(pos & 31);
+            atomicOr(&stage[wi], static_cast<uint32_t>(code << sh));
+            if (sh + w_bits > 32) atomicOr(&stage[wi + 1], static_cast<uint32_t>(code >> (32 - sh)));
+        }
+    }
+    __syncthreads();
+    const uint32_t raw_bits = ((len + 7) / 8) * 8;
+    if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, s_sign, raw_bits, tid, kChunkThreads);
+    if (p.ztag == 2) write_bits_block(pay + p.zero_off, 0, s_zero, raw_bits, tid, kChunkThreads);
+    const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix) * w_bits;
+    write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), stage, code_bits,
+                     tid, kChunkThreads);
+    block_sums3(sq, sre, sim, s_red, &bps[bi].sumsq);  // dequantised sums for norm / fidelity
+}
+
+}  // namespace
+
+// ================================================================ launchers
+
+void launch_compress_plan(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
+                          const DevTables& t, BlockPlan* d_bp, ChunkPlan* d_cp, bool have_pk, DevError* d_err,
+                          uint64_t* launches) {
+    if (nblk == 0) return;
+    if (!have_pk) {
+        BMQ_CUDA(cudaMemsetAsync(d_cp, 0, nblk * nch_max * sizeof(ChunkPlan), st));
+        k_cmp_stats<<<static_cast<uint32_t>(nblk * nch_max), kChunkThreads, 0, st>>>(d_blks, nch_max, d_cp, t,
+                                                                                      d_err);
+    }
+    k_cmp_plan<<<static_cast<uint32_t>(nblk), kPlanThreads, 0, st>>>(d_blks, nch_max, d_cp, d_bp, t.qlo);
+    BMQ_CUDA(cudaGetLastError());
+    if (launches) *launches += have_pk ? 1 : 2;
+}
+
+void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
+                          const DevTables& t, uint8_t* out, uint64_t out_cap, uint64_t* d_cursor, uint64_t* d_range,
+                          BlockPlan* d_bp, ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size,
+                          bool virtual_zero, uint32_t align, DevError* d_err, uint64_t* launches) {
+    if (nblk == 0) return;
+    k_cmp_alloc<<<1, kAllocThreads, 0, st>>>(d_blks, nblk, d_bp, d_cursor, out_cap, d_range, virtual_zero ? 1 : 0,
+                                             align, meta_off, meta_size, d_err);
+    k_zero_range<<<296, 256, 0, st>>>(out, d_range);
+    k_cmp_emit<<<static_cast<uint32_t>(nblk * nch_max), kChunkThreads, 0, st>>>(d_blks, nch_max, d_cp, d_bp, out, t,
+                                                                                 d_err);
+    BMQ_CUDA(cudaGetLastError());
+    if (launches) *launches += 3;
+}
+
+void launch_compress(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
+                     uint8_t* out, uint64_t out_cap, uint64_t* d_cursor, uint64_t* d_range, BlockPlan* d_bp,
+                     ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size, bool virtual_zero, bool have_pk,
+                     DevError* d_err, uint64_t* launches) {
+    launch_compress_plan(st, d_blks, nblk, nch_max, t, d_bp, d_cp, have_pk, d_err, launches);
+    launch_compress_emit(st, d_blks, nblk, nch_max, t, out, out_cap, d_cursor, d_range, d_bp, d_cp, meta_off,
+                         meta_size, virtual_zero, virtual_zero ? 16 : 1, d_err, launches);
+}
+
+}  // namespace bmq

@@ -46,6 +46,12 @@ __device__ __forceinline__ void dev_fail(DevError* e, uint32_t code, uint64_t it
 const char* dev_error_message(uint32_t code);
 int dev_error_status(uint32_t code);
 
+// Device allocations come from the device's stream-ordered memory pool with
+// an unlimited release threshold, so simulators created back to back reuse
+// the same HBM without cudaMalloc/cudaFree round trips.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+
 // ------------------------------------------------------------ codec tables
 struct DevTables {
     const uint64_t* thresh;   // thresh[q - qlo], q in [qlo, qhi + 1]
@@ -153,19 +159,32 @@ __device__ __forceinline__ uint64_t dev_deposit(uint64_t x, uint64_t mask) {
 // ----------------------------------------------------- codec block records
 // Compress: per-block input descriptor and per-chunk / per-block plans.
 struct CmpBlock {
-    const double* in;   // planar scalars
+    const double* in;   // planar scalars (read by the stats kernel)
+    uint32_t* pk;       // packed codes of the block, one word per scalar
     uint64_t count;     // scalars in the block
     uint64_t id;        // engine block id (or index for the API)
 };
 
+// Packed per-scalar code word written by the quantiser (stats kernel or the
+// fused gate epilogue) and read by emit:
+//   pk = (q - qlo) << 2 | negative << 1 | zero      (q meaningful if !zero)
+constexpr uint32_t kQOffMax = 0x3fffffffu;
+
+__device__ __forceinline__ uint32_t pack_code(uint32_t qoff, bool neg, bool zero) {
+    return (qoff << 2) | (neg ? 2u : 0u) | (zero ? 1u : 0u);
+}
+
+// Per-chunk counters, zero-initialised and combined with atomics (max / add)
+// by the producers; the plan kernel turns them into tags and offsets.
 struct ChunkPlan {
-    int32_t qmin, qmax;
-    uint32_t nnz;
-    uint8_t stag, ztag, pad0, pad1;
+    uint32_t qmin_inv;   // max over nonzero scalars of kQOffMax - (q - qlo)
+    uint32_t qmax_off;   // max over nonzero scalars of q - qlo
+    uint32_t nnz;        // nonzero scalars
+    uint32_t nneg;       // negative scalars
     uint32_t sign_off;   // byte offset of this chunk's raw sign bits in the payload
     uint32_t zero_off;   // byte offset of this chunk's raw zero bits
     uint32_t nz_prefix;  // nonzero scalars before this chunk in the block
-    uint32_t pad2;
+    uint8_t stag, ztag, pad0, pad1;
 };
 
 struct BlockPlan {

@@ -1,15 +1,25 @@
 // engine.cu — device implementation of cbq::Simulator (engine.hpp:58-250).
 //
-// State: the compressed payload of every block id lives in a device pool
-// (two pools, ping-pong per stage); ids whose payload is the canonical
-// ALL_ZERO header are virtual (no bytes stored). A stage runs its groups in
-// batches sized to the working set: build descriptors -> decompress the
-// batch's blocks into planar group buffers -> apply the stage's gate
-// program -> compress back into the other pool. Groups whose blocks are all
-// ALL_ZERO are skipped: linear gates map 0 to 0 and the codec emits the same
-// canonical header, so the result is byte-identical to processing them.
+// State: the compressed payload of every block id lives in an append-only
+// device arena (payloads 16-byte aligned); ids whose payload is the
+// canonical ALL_ZERO header are virtual (no bytes stored). When the arena
+// fills, live payloads are compacted into the second arena.
+//
+// A stage runs in batches sized to the working set:
+//   descriptors -> decompress the batch's blocks into planar buffers
+//   -> gate program (last pass quantises in place: packed code words)
+//   -> plan -> alloc (append) -> zero -> emit.
+// Work skipped without changing a single output byte:
+//   * groups whose blocks are all ALL_ZERO (linear gates map 0 to 0 and the
+//     codec's ALL_ZERO payload is canonical, codec.hpp:263-271);
+//   * with BMQ_FLAG_IDENTITY_SKIP, in stages made only of diagonal gates,
+//     blocks on which no gate acts: their payload is left in place, which
+//     equals compress(decompress(p)) because the codec is idempotent on every
+//     code a finite amplitude can produce (codec_tables.cpp checks this).
 // Per-id payload sizes come back to the host once per stage to replay the
 // reference BlockStore accounting (peak footprint, spills) in its put order.
+#include <cub/block/block_scan.cuh>
+
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -73,6 +83,8 @@ void StoreModel::put_shared(uint64_t first, uint64_t last, uint64_t size) {  // 
 
 namespace {
 
+constexpr uint32_t kArenaAlign = 16;
+
 __global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t zero_size) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         off[i] = ~0ull;
@@ -80,22 +92,22 @@ __global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t 
     }
 }
 
-__global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, const uint64_t* __restrict__ off_in,
-                             const uint64_t* __restrict__ size_in, const uint8_t* pool_in, const uint8_t* zero_hdr,
-                             double* work, uint32_t b, DecBlock* dec, CmpBlock* cmp) {
+__global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, const uint64_t* __restrict__ off,
+                             const uint64_t* __restrict__ size, const uint8_t* pool, const uint8_t* zero_hdr,
+                             double* work, uint32_t* pk, uint32_t b, DecBlock* dec, CmpBlock* cmp) {
     const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (i >= nblk) return;
     const uint64_t id = ids[i];
     const uint64_t count = 2ull << b;
     double* slot = work + i * count;
-    const uint64_t off = off_in[id];
+    const uint64_t o = off[id];
     DecBlock d;
-    d.in = off == ~0ull ? zero_hdr : pool_in + off;
-    d.size = off == ~0ull ? kHeaderBytes : size_in[id];
+    d.in = o == ~0ull ? zero_hdr : pool + o;
+    d.size = o == ~0ull ? kHeaderBytes : size[id];
     d.out = slot;
     d.expect_count = count;
     dec[i] = d;
-    cmp[i] = CmpBlock{slot, count, id};
+    cmp[i] = CmpBlock{slot, pk + i * count, count, id};
 }
 
 __global__ void k_store_cmp_sums(const BlockPlan* __restrict__ bp, const CmpBlock* __restrict__ cmp, uint64_t nblk,
@@ -118,6 +130,40 @@ __global__ void k_store_dec_sums(const DecInfo* __restrict__ di, const uint64_t*
     sums[3 * id + 2] = di[i].sum_im;
 }
 
+// Compaction: new aligned offsets for the live ids (single CTA scan).
+__global__ void __launch_bounds__(1024) k_compact_plan(const uint64_t* __restrict__ ids, uint64_t n,
+                                                       const uint64_t* __restrict__ size, uint64_t* new_off,
+                                                       uint64_t* total) {
+    using Scan = cub::BlockScan<unsigned long long, 1024>;
+    __shared__ typename Scan::TempStorage ss;
+    unsigned long long carry = 0;
+    for (uint64_t base = 0; base < n; base += 1024) {
+        const uint64_t i = base + threadIdx.x;
+        const unsigned long long sz = i < n ? (size[ids[i]] + kArenaAlign - 1) / kArenaAlign * kArenaAlign : 0;
+        unsigned long long pre, tot;
+        Scan(ss).ExclusiveSum(sz, pre, tot);
+        __syncthreads();
+        if (i < n) new_off[i] = carry + pre;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+// Move live payloads (16-byte aligned at both ends) and repoint the metadata.
+__global__ void k_compact_copy(const uint64_t* __restrict__ ids, uint64_t n, uint64_t* off,
+                               const uint64_t* __restrict__ size, const uint8_t* __restrict__ from,
+                               const uint64_t* __restrict__ new_off, uint8_t* __restrict__ to) {
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint64_t id = ids[i];
+        const uint4* s = reinterpret_cast<const uint4*>(from + off[id]);
+        uint4* d = reinterpret_cast<uint4*>(to + new_off[i]);
+        const uint64_t words = (size[id] + 15) / 16;
+        for (uint64_t w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
+        __syncthreads();
+        if (threadIdx.x == 0) off[id] = new_off[i];
+    }
+}
+
 // planar blocks [re(2^b) | im(2^b)] -> interleaved complex
 __global__ void k_interleave(const double* __restrict__ planar, uint64_t nblk, uint32_t b, double* __restrict__ out) {
     const uint64_t total = nblk << b;
@@ -126,6 +172,24 @@ __global__ void k_interleave(const double* __restrict__ planar, uint64_t nblk, u
         const double* src = planar + (blk << (b + 1));
         out[2 * p] = src[l];
         out[2 * p + 1] = src[(1ull << b) + l];
+    }
+}
+
+__device__ __forceinline__ void block_reduce2(double re, double im, double* partial) {
+    __shared__ double s[2][256];
+    s[0][threadIdx.x] = re;
+    s[1][threadIdx.x] = im;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            s[0][threadIdx.x] += s[0][threadIdx.x + o];
+            s[1][threadIdx.x] += s[1][threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = s[0][0];
+        partial[2 * blockIdx.x + 1] = s[1][0];
     }
 }
 
@@ -142,21 +206,7 @@ __global__ void k_dot(const double* __restrict__ planar, const double* __restric
         re += ir * sr - ii * si;
         im += ir * si + ii * sr;
     }
-    __shared__ double s[2][256];
-    s[0][threadIdx.x] = re;
-    s[1][threadIdx.x] = im;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o; o >>= 1) {
-        if (threadIdx.x < o) {
-            s[0][threadIdx.x] += s[0][threadIdx.x + o];
-            s[1][threadIdx.x] += s[1][threadIdx.x + o];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        partial[2 * blockIdx.x] = s[0][0];
-        partial[2 * blockIdx.x + 1] = s[1][0];
-    }
+    block_reduce2(re, im, partial);
 }
 
 // per-CTA partial dot of two planar buffers: sum conj(a) * b
@@ -172,21 +222,7 @@ __global__ void k_dot2(const double* __restrict__ a, const double* __restrict__ 
         re += ar * br - ai * bi;
         im += ar * bi + ai * br;
     }
-    __shared__ double s[2][256];
-    s[0][threadIdx.x] = re;
-    s[1][threadIdx.x] = im;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o; o >>= 1) {
-        if (threadIdx.x < o) {
-            s[0][threadIdx.x] += s[0][threadIdx.x + o];
-            s[1][threadIdx.x] += s[1][threadIdx.x + o];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        partial[2 * blockIdx.x] = s[0][0];
-        partial[2 * blockIdx.x + 1] = s[1][0];
-    }
+    block_reduce2(re, im, partial);
 }
 
 // per-block sums over a dense planar state (raw mode): sumsq, sum_re, sum_im
@@ -221,6 +257,32 @@ uint32_t grid_for(uint64_t n, uint32_t threads = 256) {
 
 double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Does any gate of a diagonal-only stage act on a block with inner value v?
+// Local condition bits can always be met inside the block.
+std::vector<uint8_t> touched_table(const GateProgram& prog, uint32_t b, uint32_t k) {
+    std::vector<uint8_t> t(1ull << k, 0);
+    for (uint64_t v = 0; v < t.size(); ++v) {
+        for (const GateOp& op : prog.ops) {
+            const auto bit_ok = [&](uint32_t bit, uint32_t want) {
+                return bit < b || ((v >> (bit - b)) & 1) == want;
+            };
+            bool acts = false;
+            if (op.type == OP_DIAG) {
+                acts = (op.et[0] != ET_ONE && bit_ok(op.hi, 0)) || (op.et[3] != ET_ONE && bit_ok(op.hi, 1));
+            } else if (op.type == OP_CDIAG) {
+                acts = op.et[15] != ET_ONE && bit_ok(op.hi, 1) && bit_ok(op.lo, 1);
+            } else {
+                acts = true;
+            }
+            if (acts) {
+                t[v] = 1;
+                break;
+            }
+        }
+    }
+    return t;
 }
 
 }  // namespace
@@ -266,16 +328,22 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
             }
         }
         build_program(sp->prog, std::move(ops), raw ? L_.n : L_.b + s.inner_count);
+        if (!raw && sp->prog.all_diagonal) {
+            bool local_tiles = L_.b >= kMaxTileBits;
+            for (const GatePass& p : sp->prog.passes) local_tiles = local_tiles && p.fast && !(p.tile_mask >> L_.b);
+            if (local_tiles) {
+                sp->diag_only = true;
+                sp->touched = touched_table(sp->prog, L_.b, s.inner_count);
+            }
+        }
         stage_plans_.push_back(std::move(sp));
     }
     const uint64_t nid = L_.num_blocks();
     const uint64_t blk_scalars = 2ull << L_.b;
     size_t free_b = 0, total_b = 0;
     BMQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    off_[0].alloc(nid);
-    off_[1].alloc(nid);
-    size_[0].alloc(nid);
-    size_[1].alloc(nid);
+    off_.alloc(nid);
+    size_.alloc(nid);
     sums_.alloc(3 * nid);
     err_.alloc(1);
     cursor_.alloc(4);
@@ -291,20 +359,39 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
         return;
     }
     tabs_ = &device_tables(cfg.error_bound);
+    {
+        const CodecTables& h = host_tables(cfg.error_bound);
+        // every code up to the one of DBL_MAX/(1+b_r) round-trips exactly
+        identity_ok_ = h.idem_lo == h.qlo && h.idem_hi >= h.qhi - 1;
+    }
     const uint64_t group_bytes = 8ull * (blk_scalars << kmax);
-    uint64_t want = cfg.work_bytes ? cfg.work_bytes : std::min<uint64_t>(16ull << 30, free_b / 4);
+    // Automatic sizes are fractions of the device's total HBM (free memory is
+    // misleading once the stream-ordered pool holds released buffers).
+    uint64_t want = cfg.work_bytes ? cfg.work_bytes
+                                   : std::min<uint64_t>({16ull << 30, total_b / 8, 16ull << L_.n});
     want = std::max<uint64_t>(want, group_bytes);
     work_scalars_ = (want / 8) / blk_scalars * blk_scalars;
     max_blocks_ = work_scalars_ / blk_scalars;
+    // bound the per-block scratch for tiny blocks (b small): at most 2^20
+    // blocks per batch, but never less than one group
+    const uint64_t min_blocks = 1ull << kmax;
+    if (max_blocks_ > std::max<uint64_t>(min_blocks, 1ull << 20)) {
+        max_blocks_ = std::max<uint64_t>(min_blocks, 1ull << 20);
+        work_scalars_ = max_blocks_ * blk_scalars;
+    }
     nch_ = static_cast<uint32_t>((blk_scalars + kChunk - 1) / kChunk);
     work_.alloc(work_scalars_);
     cmp_.alloc(max_blocks_);
     dec_.alloc(max_blocks_);
     cplan_.alloc(max_blocks_ * nch_);
+    pk_.alloc(work_scalars_);
     bplan_.alloc(max_blocks_);
     dinfo_.alloc(max_blocks_);
     dchunk_.alloc(max_blocks_ * nch_);
     ids_.alloc(std::max<uint64_t>(nid, max_blocks_));
+    vtab_.alloc(std::max<uint64_t>(nid, max_blocks_));
+    new_off_.alloc(nid);
+    live_ids_.alloc(nid);
     // canonical ALL_ZERO payload (codec.hpp:263-271) + slack
     uint8_t hdr[kHeaderBytes + 16] = {};
     const uint64_t cnt = blk_scalars;
@@ -313,17 +400,15 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     hdr[25] = 1;
     zero_hdr_.alloc(sizeof hdr);
     BMQ_CUDA(cudaMemcpy(zero_hdr_.p, hdr, sizeof hdr, cudaMemcpyHostToDevice));
-    BMQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
     uint64_t pool = cfg.device_pool_bytes;
-    if (!pool) {
-        const uint64_t reserve = 2ull << 30;
-        pool = free_b > reserve ? (free_b - reserve) / 2 : free_b / 4;
-        pool = std::min<uint64_t>(pool, 48ull << 30);
+    if (!pool) {  // every block at its worst-case payload size, capped
+        const uint64_t worst = nid * (compress_bound(blk_scalars) + kArenaAlign);
+        pool = std::min<uint64_t>({24ull << 30, total_b / 8, worst});
     }
     pool_cap_ = pool;
     pool_[0].alloc(pool + 64);
     pool_[1].alloc(pool + 64);
-    device_peak_ = 2 * (pool + 64) + work_.bytes() + cplan_.bytes() + dchunk_.bytes();
+    device_peak_ = 2 * (pool + 64) + work_.bytes() + pk_.bytes() + cplan_.bytes() + dchunk_.bytes();
 }
 
 Engine::~Engine() {
@@ -334,23 +419,51 @@ Engine::~Engine() {
     }
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
+    for (cudaEvent_t e : phase_ev_) cudaEventDestroy(e);
 }
 
-void Engine::check_device_error(const char* what) {
+uint32_t Engine::peek_error() {
     DevError e{};
     BMQ_CUDA(cudaMemcpyAsync(&e, err_.p, sizeof e, cudaMemcpyDeviceToHost, st_));
     BMQ_CUDA(cudaStreamSynchronize(st_));
-    if (e.code) {
+    return e.code;
+}
+
+void Engine::check_device_error(const char* what) {
+    const uint32_t code = peek_error();
+    if (code) {
         BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
-        raise(dev_error_status(e.code), std::string(what) + dev_error_message(e.code));
+        raise(dev_error_status(code), std::string(what) + dev_error_message(code));
     }
 }
 
 void Engine::sync_meta_to_host() {
-    BMQ_CUDA(cudaMemcpyAsync(h_off_.data(), off_[cur_].p, off_[cur_].bytes(), cudaMemcpyDeviceToHost, st_));
-    BMQ_CUDA(cudaMemcpyAsync(h_size_.data(), size_[cur_].p, size_[cur_].bytes(), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaMemcpyAsync(h_off_.data(), off_.p, off_.bytes(), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaMemcpyAsync(h_size_.data(), size_.p, size_.bytes(), cudaMemcpyDeviceToHost, st_));
     BMQ_CUDA(cudaStreamSynchronize(st_));
+}
+
+// Move every stored payload into the other arena, back to back.
+void Engine::compact() {
+    sync_meta_to_host();
+    std::vector<uint64_t> live;
+    for (uint64_t id = 0; id < h_off_.size(); ++id)
+        if (h_off_[id] != ~0ull) live.push_back(id);
+    const int nxt = 1 - cur_;
+    if (live.empty()) {
+        BMQ_CUDA(cudaMemsetAsync(cursor_.p + nxt, 0, 8, st_));
+    } else {
+        BMQ_CUDA(cudaMemcpyAsync(live_ids_.p, live.data(), live.size() * 8, cudaMemcpyHostToDevice, st_));
+        k_compact_plan<<<1, 1024, 0, st_>>>(live_ids_.p, live.size(), size_.p, new_off_.p, cursor_.p + nxt);
+        k_compact_copy<<<grid_for(live.size() * 256), 256, 0, st_>>>(live_ids_.p, live.size(), off_.p, size_.p,
+                                                                     pool_[cur_].p, new_off_.p, pool_[nxt].p);
+        BMQ_CUDA(cudaGetLastError());
+        counters_.kernel_launches += 2;
+    }
+    cur_ = nxt;
+    sync_meta_to_host();
+    ++counters_.compactions;
 }
 
 void Engine::init_state() {
@@ -373,15 +486,15 @@ void Engine::init_state() {
         return;
     }
     cur_ = 0;
-    k_fill_meta<<<grid_for(nid), 256, 0, st_>>>(off_[0].p, size_[0].p, nid, kHeaderBytes);
+    k_fill_meta<<<grid_for(nid), 256, 0, st_>>>(off_.p, size_.p, nid, kHeaderBytes);
     BMQ_CUDA(cudaMemsetAsync(cursor_.p, 0, 2 * sizeof(uint64_t), st_));
     const uint64_t cnt = 2ull << L_.b;
     BMQ_CUDA(cudaMemsetAsync(work_.p, 0, cnt * sizeof(double), st_));
     BMQ_CUDA(cudaMemcpyAsync(work_.p, &one, 8, cudaMemcpyHostToDevice, st_));
-    const CmpBlock blk{work_.p, cnt, 0};
+    const CmpBlock blk{work_.p, pk_.p, cnt, 0};
     BMQ_CUDA(cudaMemcpyAsync(cmp_.p, &blk, sizeof blk, cudaMemcpyHostToDevice, st_));
     launch_compress(st_, cmp_.p, 1, nch_, *tabs_, pool_[0].p, pool_cap_, cursor_.p, cursor_.p + 2, bplan_.p, cplan_.p,
-                    off_[0].p, size_[0].p, true, err_.p, &counters_.kernel_launches);
+                    off_.p, size_.p, true, false, err_.p, &counters_.kernel_launches);
     k_store_cmp_sums<<<1, 32, 0, st_>>>(bplan_.p, cmp_.p, 1, sums_.p);
     check_device_error("init_state: ");
     sync_meta_to_host();
@@ -393,6 +506,37 @@ void Engine::init_state() {
 
 void Engine::ensure_init() {
     if (!initialized_) init_state();
+}
+
+void Engine::reset() {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    initialized_ = false;
+    next_stage_ = 0;
+    stage_compress_calls_ = stage_decompress_calls_ = 0;
+    counters_ = bmq_report{};
+}
+
+void Engine::phase_event(size_t i) {
+    while (phase_ev_.size() <= i) {
+        cudaEvent_t e;
+        BMQ_CUDA(cudaEventCreate(&e));
+        phase_ev_.push_back(e);
+    }
+    BMQ_CUDA(cudaEventRecord(phase_ev_[i], st_));
+}
+
+void Engine::collect_phase_times(size_t nbatches) {
+    for (size_t k = 0; k < nbatches; ++k) {
+        float a = 0.f, b = 0.f, c = 0.f;
+        BMQ_CUDA(cudaEventElapsedTime(&a, phase_ev_[4 * k], phase_ev_[4 * k + 1]));
+        BMQ_CUDA(cudaEventElapsedTime(&b, phase_ev_[4 * k + 1], phase_ev_[4 * k + 2]));
+        BMQ_CUDA(cudaEventElapsedTime(&c, phase_ev_[4 * k + 2], phase_ev_[4 * k + 3]));
+        counters_.decompress_ms += a;
+        counters_.gate_ms += b;
+        counters_.compress_ms += c;
+    }
+    counters_.batches += nbatches;
 }
 
 void Engine::raw_run_stage(uint64_t s) {
@@ -416,6 +560,47 @@ void Engine::raw_run_stage(uint64_t s) {
     stage_decompress_calls_ += L_.num_blocks();
 }
 
+// alloc + zero + emit for the batch in flight; on a full arena, compact and
+// allocate again (the plan and the packed codes are still in place).
+void Engine::emit_batch(uint64_t nblk) {
+    for (int attempt = 0;; ++attempt) {
+        launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, pool_[cur_].p, pool_cap_, cursor_.p + cur_,
+                             cursor_.p + 2, bplan_.p, cplan_.p, off_.p, size_.p, true, kArenaAlign, err_.p,
+                             &counters_.kernel_launches);
+        const uint32_t code = peek_error();
+        if (code != DE_POOL_FULL) break;
+        BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
+        if (attempt > 0) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+        compact();
+    }
+    k_store_cmp_sums<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, cmp_.p, nblk, sums_.p);
+    ++counters_.kernel_launches;
+}
+
+void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk,
+                           size_t bidx) {
+    phase_event(4 * bidx);
+    k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_.p, size_.p, pool_[cur_].p, zero_hdr_.p, work_.p,
+                                                  pk_.p, L_.b, dec_.p, cmp_.p);
+    ++counters_.kernel_launches;
+    launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
+                      &counters_.kernel_launches);
+    phase_event(4 * bidx + 1);
+    // the stage's last gate pass quantises straight into pk_ / cplan_
+    BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
+    const QuantOut qo{pk_.p, cplan_.p, nch_, *tabs_, err_.p};
+    const uint64_t per = sp.gg.per_group();
+    const bool fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per,
+                                   &counters_.kernel_launches, &qo, d_vtab, nblk);
+    phase_event(4 * bidx + 2);
+    launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,
+                         &counters_.kernel_launches);
+    emit_batch(nblk);
+    phase_event(4 * bidx + 3);
+    if (fused) ++counters_.fused_batches;
+    counters_.gate_passes += sp.prog.passes.size();
+}
+
 void Engine::run_stage(uint64_t s) {
     if (!cfg_.compress) return raw_run_stage(s);
     StagePlan& sp = *stage_plans_[s];
@@ -423,61 +608,72 @@ void Engine::run_stage(uint64_t s) {
     const uint64_t per = gg.per_group(), ngroups = gg.groups();
     const uint64_t nid = L_.num_blocks();
     const bool skip_zero = cfg_.flags & BMQ_FLAG_ZERO_GROUP_SKIP;
-    // groups in ascending outer order; ids of groups that need processing
+    const bool blockwise = sp.diag_only && identity_ok_ && skip_zero && (cfg_.flags & BMQ_FLAG_IDENTITY_SKIP);
     std::vector<uint64_t> inner(per);
     for (uint64_t v = 0; v < per; ++v) inner[v] = deposit_bits(v, gg.inner_mask);
+    // the blocks to process, in the reference's group order
     std::vector<uint64_t> work_ids;
+    std::vector<uint32_t> work_v;
     work_ids.reserve(nid);
-    uint64_t o = 0;
+    uint64_t o = 0, groups_done = 0;
     for (uint64_t g = 0; g < ngroups; ++g) {
-        bool nonzero = !skip_zero;
-        for (uint64_t v = 0; v < per && !nonzero; ++v) nonzero = h_off_[o | inner[v]] != ~0ull;
-        if (nonzero)
-            for (uint64_t v = 0; v < per; ++v) work_ids.push_back(o | inner[v]);
+        if (blockwise) {
+            bool any = false;
+            for (uint64_t v = 0; v < per; ++v) {
+                const uint64_t id = o | inner[v];
+                if (sp.touched[v] && h_off_[id] != ~0ull) {
+                    work_ids.push_back(id);
+                    work_v.push_back(static_cast<uint32_t>(v));
+                    any = true;
+                }
+            }
+            groups_done += any;
+        } else {
+            bool nonzero = !skip_zero;
+            for (uint64_t v = 0; v < per && !nonzero; ++v) nonzero = h_off_[o | inner[v]] != ~0ull;
+            if (nonzero) {
+                for (uint64_t v = 0; v < per; ++v) work_ids.push_back(o | inner[v]);
+                ++groups_done;
+            }
+        }
         o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
     }
-    const int nxt = 1 - cur_;
-    k_fill_meta<<<grid_for(nid), 256, 0, st_>>>(off_[nxt].p, size_[nxt].p, nid, kHeaderBytes);
-    BMQ_CUDA(cudaMemsetAsync(cursor_.p + nxt, 0, sizeof(uint64_t), st_));
-    counters_.kernel_launches += 1;
     const uint64_t nwork = work_ids.size();
+    size_t nbatches = 0;
     if (nwork) {
         BMQ_CUDA(cudaMemcpyAsync(ids_.p, work_ids.data(), nwork * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
-        const uint64_t batch_groups = std::max<uint64_t>(1, max_blocks_ / per);
-        const uint64_t batch_blocks = batch_groups * per;
-        for (uint64_t first = 0; first < nwork; first += batch_blocks) {
+        if (blockwise)
+            BMQ_CUDA(cudaMemcpyAsync(vtab_.p, work_v.data(), nwork * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        const uint64_t batch_blocks = blockwise ? max_blocks_ : std::max<uint64_t>(1, max_blocks_ / per) * per;
+        for (uint64_t first = 0; first < nwork; first += batch_blocks, ++nbatches) {
             const uint64_t nblk = std::min(batch_blocks, nwork - first);
-            const uint64_t* d_ids = ids_.p + first;
-            k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_[cur_].p, size_[cur_].p, pool_[cur_].p,
-                                                          zero_hdr_.p, work_.p, L_.b, dec_.p, cmp_.p);
-            launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
-                              &counters_.kernel_launches);
-            run_program(st_, sp.prog, work_.p, L_.b, false, nblk / per, &counters_.kernel_launches);
-            launch_compress(st_, cmp_.p, nblk, nch_, *tabs_, pool_[nxt].p, pool_cap_, cursor_.p + nxt, cursor_.p + 2,
-                            bplan_.p, cplan_.p, off_[nxt].p, size_[nxt].p, true, err_.p, &counters_.kernel_launches);
-            k_store_cmp_sums<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, cmp_.p, nblk, sums_.p);
-            counters_.kernel_launches += 2;
-            counters_.gate_passes += sp.prog.passes.size();
+            process_batch(sp, ids_.p + first, blockwise ? vtab_.p + first : nullptr, nblk, nbatches);
         }
     }
-    // zero groups that were skipped keep zero sums (already zero)
     const std::vector<uint64_t> old_size = h_size_;
     const std::vector<uint64_t> old_off = h_off_;
-    cur_ = nxt;
     check_device_error(("stage " + std::to_string(s) + ": ").c_str());
     sync_meta_to_host();
+    collect_phase_times(nbatches);
     // accounting replay in the reference put order (groups ascending)
     o = 0;
     for (uint64_t g = 0; g < ngroups; ++g) {
         for (uint64_t v : inner) store_.put(o | v, h_size_[o | v]);
         o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
     }
+    uint64_t rd = 0, wr = 0;
     for (uint64_t id : work_ids) {
-        counters_.payload_bytes_read += old_off[id] == ~0ull ? 0 : old_size[id];
-        counters_.payload_bytes_written += h_off_[id] == ~0ull ? 0 : h_size_[id];
+        rd += old_off[id] == ~0ull ? 0 : old_size[id];
+        wr += h_off_[id] == ~0ull ? 0 : h_size_[id];
     }
-    counters_.groups_processed += nwork / per;
-    counters_.groups_skipped += ngroups - nwork / per;
+    const uint64_t half_dense = nwork * (16ull << L_.b);
+    counters_.payload_bytes_read += rd;
+    counters_.payload_bytes_written += wr;
+    counters_.decompress_bytes += rd + half_dense;
+    counters_.gate_bytes += 2 * half_dense * sp.prog.passes.size();
+    counters_.compress_bytes += half_dense + wr;
+    counters_.groups_processed += groups_done;
+    counters_.groups_skipped += ngroups - groups_done;
     counters_.blocks_processed += nwork;
     counters_.dense_bytes += nwork * (32ull << L_.b);
     stage_compress_calls_ += nid;
@@ -533,6 +729,15 @@ void Engine::run(bmq_report* rep, double* stage_ms, uint64_t stage_cap) {
     r.kernel_launches = counters_.kernel_launches;
     r.gate_passes = counters_.gate_passes;
     r.device_peak_bytes = device_peak_;
+    r.decompress_ms = counters_.decompress_ms;
+    r.gate_ms = counters_.gate_ms;
+    r.compress_ms = counters_.compress_ms;
+    r.batches = counters_.batches;
+    r.decompress_bytes = counters_.decompress_bytes;
+    r.gate_bytes = counters_.gate_bytes;
+    r.compress_bytes = counters_.compress_bytes;
+    r.fused_batches = counters_.fused_batches;
+    r.compactions = counters_.compactions;
     *rep = r;
 }
 
@@ -557,8 +762,8 @@ void Engine::host_ids_to_device(const std::vector<uint64_t>& ids) {
 }
 
 void Engine::decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums) {
-    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_[cur_].p, size_[cur_].p, pool_[cur_].p,
-                                                  zero_hdr_.p, work_.p, L_.b, dec_.p, cmp_.p);
+    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_.p, size_.p, pool_[cur_].p, zero_hdr_.p, work_.p,
+                                                  pk_.p, L_.b, dec_.p, cmp_.p);
     launch_decompress(st_, dec_.p, nids, nch_, *tabs_, dinfo_.p, dchunk_.p, true, want_sums, err_.p,
                       &counters_.kernel_launches);
 }
@@ -669,8 +874,9 @@ void Engine::get_payloads(uint8_t* out, uint64_t cap, uint64_t* sizes, uint64_t*
         BMQ_CUDA(cudaStreamSynchronize(st_));
         return;
     }
-    // Stored payloads are packed in the pool in id order within each batch;
-    // copy the pool once and scatter on the host.
+    // Compact first: the arena then holds exactly the live payloads in id
+    // order, so one contiguous copy brings the whole state to the host.
+    compact();
     uint64_t used = 0;
     BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
     BMQ_CUDA(cudaStreamSynchronize(st_));
@@ -705,21 +911,26 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
     uint64_t used = 0;
     BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
     BMQ_CUDA(cudaStreamSynchronize(st_));
-    if (used + size > pool_cap_) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+    if (used + size + kArenaAlign > pool_cap_) {
+        compact();
+        BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        if (used + size + kArenaAlign > pool_cap_) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+    }
     const uint64_t prev_off = h_off_[id], prev_size = h_size_[id];
     BMQ_CUDA(cudaMemcpyAsync(pool_[cur_].p + used, data, size, cudaMemcpyHostToDevice, st_));
-    const uint64_t end = used + size;
+    const uint64_t end = (used + size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
     BMQ_CUDA(cudaMemcpyAsync(cursor_.p + cur_, &end, 8, cudaMemcpyHostToDevice, st_));
-    BMQ_CUDA(cudaMemcpyAsync(off_[cur_].p + id, &used, 8, cudaMemcpyHostToDevice, st_));
-    BMQ_CUDA(cudaMemcpyAsync(size_[cur_].p + id, &size, 8, cudaMemcpyHostToDevice, st_));
+    BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &used, 8, cudaMemcpyHostToDevice, st_));
+    BMQ_CUDA(cudaMemcpyAsync(size_.p + id, &size, 8, cudaMemcpyHostToDevice, st_));
     host_ids_to_device({id});
     decompress_ids(ids_.p, 1, true);
     k_store_dec_sums<<<1, 32, 0, st_>>>(dinfo_.p, ids_.p, 1, sums_.p);
     try {
         check_device_error("");
     } catch (...) {  // restore the previous payload
-        BMQ_CUDA(cudaMemcpyAsync(off_[cur_].p + id, &prev_off, 8, cudaMemcpyHostToDevice, st_));
-        BMQ_CUDA(cudaMemcpyAsync(size_[cur_].p + id, &prev_size, 8, cudaMemcpyHostToDevice, st_));
+        BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &prev_off, 8, cudaMemcpyHostToDevice, st_));
+        BMQ_CUDA(cudaMemcpyAsync(size_.p + id, &prev_size, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
         throw;
     }

@@ -19,11 +19,11 @@ struct DevArray {
     ~DevArray() { release(); }
     void alloc(size_t count) {
         release();
-        if (count) BMQ_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
         n = count;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
         p = nullptr;
         n = 0;
     }
@@ -40,13 +40,12 @@ public:
     void put_shared(uint64_t first_id, uint64_t last_id, uint64_t size);  // ids [first, last)
     uint64_t peak() const { return peak_; }
     uint64_t spilled_blocks() const { return spilled_blocks_; }
-    uint64_t size(uint64_t id) const { return size_[id]; }
 
 private:
     void detach(uint64_t id);
     bool place(uint64_t size);  // returns spilled
     std::vector<uint64_t> size_;
-    std::vector<uint8_t> flags_;  // bit0 spilled, bit1 shared
+    std::vector<uint8_t> flags_;  // bit0 spilled, bit1 shared, bit2 absent
     uint64_t budget_ = ~0ull, resident_ = 0, spilled_live_ = 0, peak_ = 0, spilled_blocks_ = 0;
     uint64_t shared_refs_ = 0, shared_size_ = 0;
     bool shared_spilled_ = false;
@@ -55,7 +54,9 @@ private:
 struct StagePlan {
     bmq_stage stage;
     GroupGeometry gg;
-    GateProgram prog;  // over the 2^(b + |inner|) group buffer
+    GateProgram prog;            // over the 2^(b + |inner|) group buffer
+    bool diag_only = false;      // no gate mixes amplitudes: blocks are independent
+    std::vector<uint8_t> touched;  // diag_only: inner value v -> some gate acts on the block
 };
 
 class Engine {
@@ -64,6 +65,7 @@ public:
     ~Engine();
 
     void init_state();
+    void reset();
     void run(bmq_report* rep, double* stage_ms, uint64_t stage_cap);
     void run_stages(uint64_t first, uint64_t last);
     double state_norm();
@@ -82,13 +84,18 @@ public:
 private:
     void ensure_init();
     void run_stage(uint64_t s);
+    void raw_run_stage(uint64_t s);
+    void process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk, size_t bidx);
+    void emit_batch(uint64_t nblk);
+    void compact();
     void sync_meta_to_host();
-    // decompress `ids` (device list) into work slots; returns nothing
     void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
     void host_ids_to_device(const std::vector<uint64_t>& ids);
     uint64_t zero_payload(uint8_t* out, uint64_t cap) const;
+    uint32_t peek_error();
     void check_device_error(const char* what);
-    void raw_run_stage(uint64_t s);
+    void phase_event(size_t i);
+    void collect_phase_times(size_t nbatches);
 
     Layout L_;
     bmq_config cfg_;
@@ -99,15 +106,18 @@ private:
     int dev_ = 0;
     cudaStream_t st_ = nullptr;
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    std::vector<cudaEvent_t> phase_ev_;  // 4 per batch: start, decoded, gated, compressed
     bool initialized_ = false;
+    bool identity_ok_ = false;  // codec idempotent on every representable amplitude
     uint64_t next_stage_ = 0;
 
-    // compressed state: payload pools (ping-pong) + per-id metadata
+    // compressed state: an append-only payload arena (compacted into the
+    // other one when full) + per-id metadata (off ~0 = canonical ALL_ZERO)
     DevArray<uint8_t> pool_[2];
     uint64_t pool_cap_ = 0;
     int cur_ = 0;
-    DevArray<uint64_t> cursor_;  // [2] pool cursors, [2..3] range scratch
-    DevArray<uint64_t> off_[2], size_[2];
+    DevArray<uint64_t> cursor_;  // [0..1] arena cursors, [2..3] range scratch
+    DevArray<uint64_t> off_, size_, new_off_, live_ids_;
     DevArray<double> sums_;       // per id: sumsq, sum_re, sum_im (3 doubles)
     DevArray<uint8_t> zero_hdr_;  // canonical ALL_ZERO payload (+ slack)
     // raw mode (compress == false): dense planar state
@@ -120,10 +130,12 @@ private:
     DevArray<CmpBlock> cmp_;
     DevArray<DecBlock> dec_;
     DevArray<ChunkPlan> cplan_;
+    DevArray<uint32_t> pk_;  // packed code words of the batch (4 B per scalar)
     DevArray<BlockPlan> bplan_;
     DevArray<DecInfo> dinfo_;
     DevArray<DecChunk> dchunk_;
     DevArray<uint64_t> ids_;
+    DevArray<uint32_t> vtab_;
     DevArray<DevError> err_;
     DevArray<double> red_;
 

@@ -3,14 +3,23 @@
 //
 // Gates are applied one by one in program order — their arithmetic is never
 // fused, so every amplitude sees exactly the reference's rounding sequence —
-// but their MEMORY traffic is fused: a pass loads one tile of 2^tb
+// but their MEMORY traffic is fused: a pass loads one tile of 2^12
 // amplitudes into shared memory, applies a run of gates whose mixing bits
 // all lie inside the tile, and writes the tile back once. Diagonal gates
 // (Z, S, T, RZ, P, CZ, CP, ...) and CX controls never mix amplitudes, so
 // they add no tile bits; a QFT stage of dozens of controlled phases is one
 // pass. Tiles always contain buffer bits 0..4 so global accesses coalesce.
+//
+// Diagonal runs are applied amplitude by amplitude (no barriers). A run of
+// controlled phases sharing one control bit (a QFT "phase chain") is one
+// OP_CHAIN: the amplitude walks the set bits of (index & R) in program order
+// and multiplies by each bit's phase, so the cost is the number of phases
+// that actually apply, not the number of gates.
 #include <algorithm>
+#include <cstring>
+#include <functional>
 
+#include "codec_util.cuh"
 #include "gates.cuh"
 
 namespace bmq {
@@ -65,7 +74,8 @@ GateOp make_matrix_op(const Cx* u, bool two_qubit, uint32_t hi_bit, uint32_t lo_
 }
 
 GateProgram::~GateProgram() {
-    if (d_ops) cudaFree(d_ops);
+    if (d_ops) dev_free(d_ops);
+    if (d_chain_tab) dev_free(d_chain_tab);
 }
 
 namespace {
@@ -83,6 +93,125 @@ uint8_t rank_in(uint64_t mask, uint32_t bit) {
     return static_cast<uint8_t>(__builtin_popcountll(mask & ((1ull << bit) - 1)));
 }
 
+// Runs of `mask` restricted to [0, limit); when tail_to is set, the source
+// bits past the mask's runs are appended as one run landing at tail_to.
+BitRuns make_runs(uint64_t mask, uint32_t limit, int tail_to) {
+    BitRuns r{};
+    uint32_t src = 0;
+    for (uint32_t b = 0; b < limit;) {
+        if (!((mask >> b) & 1)) {
+            ++b;
+            continue;
+        }
+        uint32_t e = b;
+        while (e < limit && ((mask >> e) & 1)) ++e;
+        r.src[r.n] = static_cast<uint8_t>(src);
+        r.dst[r.n] = static_cast<uint8_t>(b);
+        r.width[r.n] = static_cast<uint8_t>(e - b);
+        ++r.n;
+        src += e - b;
+        b = e;
+    }
+    if (tail_to >= 0) {
+        r.src[r.n] = static_cast<uint8_t>(src);
+        r.dst[r.n] = static_cast<uint8_t>(tail_to);
+        r.width[r.n] = static_cast<uint8_t>(64 - std::max<uint32_t>(src, tail_to));
+        ++r.n;
+    }
+    return r;
+}
+
+FastOp to_fast(const GateOp& g) {
+    FastOp f{};
+    f.type = g.type;
+    f.tp_hi = g.tp_hi;
+    f.tp_lo = g.tp_lo;
+    f.in_hi = g.in_hi;
+    f.in_lo = g.in_lo;
+    f.hi = g.hi;
+    f.lo = g.lo;
+    const auto take = [&](int slot, int e) {
+        f.et[slot] = g.et[e];
+        f.m[2 * slot] = g.m[2 * e];
+        f.m[2 * slot + 1] = g.m[2 * e + 1];
+    };
+    if (g.type == OP_U2) {
+        for (int e = 0; e < 4; ++e) take(e, e);
+        // real 2x2 (H, RY, X, Z): the real product form is exact for every
+        // entry class incl. 0 and +-1 (up to the sign of an exact zero)
+        bool real = true;
+        for (int e = 0; e < 4; ++e) real = real && g.m[2 * e + 1] == 0.0;
+        f.pad = real ? 1 : 0;
+    } else if (g.type == OP_DIAG) {
+        take(0, 0);
+        take(1, 3);
+    } else if (g.type == OP_CDIAG) {
+        take(0, 15);
+    }
+    return f;
+}
+
+// Fast ops for [begin, end): consecutive CP-like ops (OP_CDIAG with a
+// complex entry) that share one bit and whose other bits are distinct and
+// monotone become one OP_CHAIN with a 64-entry phase table.
+std::vector<FastOp> fuse_chains(const std::vector<GateOp>& ops, uint32_t begin, uint32_t end,
+                                std::vector<double>& tab) {
+    std::vector<FastOp> out;
+    const size_t pass_base = tab.size();  // chain offsets are relative to the pass
+    const auto chainable = [](const GateOp& o) {
+        return o.type == OP_CDIAG && o.et[15] == ET_CPLX && o.hi < 32 && o.lo < 32;
+    };
+    uint32_t i = begin;
+    while (i < end) {
+        const GateOp& a = ops[i];
+        if (chainable(a) && i + 1 < end && chainable(ops[i + 1])) {
+            const GateOp& b = ops[i + 1];
+            int c = -1;
+            if (b.hi == a.hi || b.lo == a.hi)
+                c = a.hi;
+            else if (b.hi == a.lo || b.lo == a.lo)
+                c = a.lo;
+            if (c >= 0) {
+                const auto other = [c](const GateOp& o) { return static_cast<int>(o.hi == c ? o.lo : o.hi); };
+                const int oa = other(a), ob = other(b);
+                if (oa != ob) {
+                    const bool desc = ob < oa;
+                    uint64_t R = (1ull << oa) | (1ull << ob);
+                    int last = ob;
+                    uint32_t j = i + 2;
+                    while (j < end && chainable(ops[j]) && (ops[j].hi == c || ops[j].lo == c)) {
+                        const int oj = other(ops[j]);
+                        if ((R >> oj) & 1) break;
+                        if (desc ? !(oj < last) : !(oj > last)) break;
+                        R |= 1ull << oj;
+                        last = oj;
+                        ++j;
+                    }
+                    const size_t off = tab.size();
+                    tab.resize(off + 64, 0.0);  // 32 entries (re, im)
+                    for (uint32_t k = i; k < j; ++k) {
+                        const int o = other(ops[k]);
+                        tab[off + 2 * o] = ops[k].m[30];
+                        tab[off + 2 * o + 1] = ops[k].m[31];
+                    }
+                    FastOp f{};
+                    f.type = OP_CHAIN;
+                    f.hi = static_cast<uint8_t>(c);
+                    f.et[0] = desc ? 1 : 0;
+                    f.pad2 = static_cast<uint32_t>((off - pass_base) / 2);
+                    std::memcpy(&f.m[0], &R, 8);
+                    out.push_back(f);
+                    i = j;
+                    continue;
+                }
+            }
+        }
+        out.push_back(to_fast(a));
+        ++i;
+    }
+    return out;
+}
+
 }  // namespace
 
 void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bits) {
@@ -98,16 +227,44 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
         if (op.type == OP_DIAG) prog.diag_cond_mask |= 1ull << op.hi;
         if (op.type == OP_CDIAG) prog.diag_cond_mask |= (1ull << op.hi) | (1ull << op.lo);
     }
-    const auto close = [&](uint64_t mix, uint32_t begin, uint32_t end) {
+    prog.chain_tab.clear();
+    std::function<void(uint32_t, uint32_t)> close = [&](uint32_t begin, uint32_t end) {
+        uint64_t mix = 0;
+        for (uint32_t i = begin; i < end; ++i) mix |= mixing_bits(ops[i]);
         uint64_t mask = (mix | coalesce) & all;
         for (uint32_t b = 0; __builtin_popcountll(mask) < static_cast<int>(tb); ++b) mask |= (1ull << b) & all;
         GatePass p{mask, tb, begin, end - begin};
+        bool fast = tb == kMaxTileBits;
         for (uint32_t i = begin; i < end; ++i) {
             GateOp& op = ops[i];
             op.in_hi = (mask >> op.hi) & 1;
             op.in_lo = (mask >> op.lo) & 1;
             op.tp_hi = op.in_hi ? rank_in(mask, op.hi) : 0;
             op.tp_lo = op.in_lo ? rank_in(mask, op.lo) : 0;
+            if (op.type == OP_U4) fast = false;
+        }
+        if (fast) {
+            const size_t tab_mark = prog.chain_tab.size();
+            std::vector<FastOp> fops = fuse_chains(ops, begin, end, prog.chain_tab);
+            if (fops.size() > static_cast<size_t>(kMaxFastOps) && end - begin > 1) {
+                prog.chain_tab.resize(tab_mark);
+                const uint32_t mid = begin + (end - begin) / 2;
+                close(begin, mid);
+                close(mid, end);
+                return;
+            }
+            if (fops.size() <= static_cast<size_t>(kMaxFastOps)) {
+                auto fp = std::make_shared<FastPass>();
+                std::memset(fp.get(), 0, sizeof(FastPass));
+                fp->tile = make_runs(mask, total_bits, -1);
+                fp->base = make_runs(~mask & all, total_bits, static_cast<int>(total_bits));
+                fp->nops = static_cast<uint32_t>(fops.size());
+                fp->tab_base = tab_mark / 2;
+                fp->tab_entries = static_cast<uint32_t>((prog.chain_tab.size() - tab_mark) / 2);
+                std::copy(fops.begin(), fops.end(), fp->ops);
+                p.fast = true;
+                p.fp = fp;
+            }
         }
         prog.passes.push_back(p);
     };
@@ -115,23 +272,36 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
     uint32_t begin = 0;
     for (uint32_t i = 0; i < ops.size(); ++i) {
         const uint64_t m = mixing_bits(ops[i]);
-        if (__builtin_popcountll((mix | m | coalesce) & all) > static_cast<int>(tb) && i > begin) {
-            close(mix, begin, i);
+        const bool too_wide = __builtin_popcountll((mix | m | coalesce) & all) > static_cast<int>(tb);
+        const bool too_long = i - begin >= 4096u;
+        if ((too_wide || too_long) && i > begin) {
+            close(begin, i);
             begin = i;
             mix = 0;
         }
         mix |= m;
     }
-    if (begin < ops.size()) close(mix, begin, static_cast<uint32_t>(ops.size()));
+    if (begin < ops.size()) close(begin, static_cast<uint32_t>(ops.size()));
     prog.ops = std::move(ops);
     if (prog.d_ops) {
-        cudaFree(prog.d_ops);
+        dev_free(prog.d_ops);
         prog.d_ops = nullptr;
     }
+    if (prog.d_chain_tab) {
+        dev_free(prog.d_chain_tab);
+        prog.d_chain_tab = nullptr;
+    }
     if (!prog.ops.empty()) {
-        BMQ_CUDA(cudaMalloc(&prog.d_ops, prog.ops.size() * sizeof(GateOp)));
+        prog.d_ops = static_cast<GateOp*>(dev_alloc(prog.ops.size() * sizeof(GateOp)));
         BMQ_CUDA(cudaMemcpy(prog.d_ops, prog.ops.data(), prog.ops.size() * sizeof(GateOp), cudaMemcpyHostToDevice));
     }
+    if (!prog.chain_tab.empty()) {
+        prog.d_chain_tab = static_cast<double*>(dev_alloc(prog.chain_tab.size() * sizeof(double)));
+        BMQ_CUDA(cudaMemcpy(prog.d_chain_tab, prog.chain_tab.data(), prog.chain_tab.size() * sizeof(double),
+                            cudaMemcpyHostToDevice));
+    }
+    for (GatePass& p : prog.passes)
+        if (p.fast) p.fp->chain_tab = prog.d_chain_tab;
 }
 
 namespace {
@@ -140,31 +310,47 @@ struct C2 {
     double re, im;
 };
 
-// u * a for one classified entry, with the reference's rounding (no FMA).
+// u * a with the reference's rounding: (ur*ar - ui*ai, ur*ai + ui*ar), each
+// product rounded, no FMA. For u = 1, -1, real or imaginary this equals the
+// cheaper special forms except for the sign of an exact zero, so the
+// specialised cases below are exact too.
+__device__ __forceinline__ C2 cmul(double ur, double ui, C2 a) {
+    return C2{__dsub_rn(__dmul_rn(ur, a.re), __dmul_rn(ui, a.im)), __dadd_rn(__dmul_rn(ur, a.im), __dmul_rn(ui, a.re))};
+}
+
 __device__ __forceinline__ C2 entry_mul(uint8_t et, double ur, double ui, C2 a) {
     switch (et) {
+    case ET_ZERO: return C2{0.0, 0.0};
     case ET_ONE: return a;
     case ET_NEG: return C2{-a.re, -a.im};
     case ET_REAL: return C2{__dmul_rn(ur, a.re), __dmul_rn(ur, a.im)};
     case ET_IMAG: return C2{-__dmul_rn(ui, a.im), __dmul_rn(ui, a.re)};
-    default:
-        return C2{__dsub_rn(__dmul_rn(ur, a.re), __dmul_rn(ui, a.im)),
-                  __dadd_rn(__dmul_rn(ur, a.im), __dmul_rn(ui, a.re))};
+    default: return cmul(ur, ui, a);
     }
 }
 
-// sum_c u[r][c] * a[c], left to right over the nonzero entries.
-template <int N>
-__device__ __forceinline__ C2 mat_row(const GateOp* __restrict__ g, int r, const C2* a) {
+__device__ __forceinline__ C2 cadd(C2 a, C2 b) { return C2{__dadd_rn(a.re, b.re), __dadd_rn(a.im, b.im)}; }
+
+// Row r of a 2x2 (entries 2r, 2r+1): sum over nonzero entries, left to right.
+__device__ __forceinline__ C2 row2(const uint8_t* et, const double* m, int r, C2 a0, C2 a1) {
+    const uint8_t e0 = et[2 * r], e1 = et[2 * r + 1];
+    if (e0 == ET_ZERO) return entry_mul(e1, m[4 * r + 2], m[4 * r + 3], a1);
+    const C2 t0 = entry_mul(e0, m[4 * r], m[4 * r + 1], a0);
+    if (e1 == ET_ZERO) return t0;
+    return cadd(t0, entry_mul(e1, m[4 * r + 2], m[4 * r + 3], a1));
+}
+
+// sum_c u[r][c] * a[c], left to right over the nonzero entries (general 4x4).
+__device__ __forceinline__ C2 row4(const GateOp* __restrict__ g, int r, const C2* a) {
     C2 acc{0.0, 0.0};
     bool any = false;
 #pragma unroll
-    for (int c = 0; c < N; ++c) {
-        const int e = r * N + c;
+    for (int c = 0; c < 4; ++c) {
+        const int e = r * 4 + c;
         const uint8_t et = g->et[e];
         if (et == ET_ZERO) continue;
         const C2 t = entry_mul(et, g->m[2 * e], g->m[2 * e + 1], a[c]);
-        acc = any ? C2{__dadd_rn(acc.re, t.re), __dadd_rn(acc.im, t.im)} : t;
+        acc = any ? cadd(acc, t) : t;
         any = true;
     }
     return acc;
@@ -173,6 +359,16 @@ __device__ __forceinline__ C2 mat_row(const GateOp* __restrict__ g, int r, const
 __device__ __forceinline__ uint32_t insert0(uint32_t x, uint32_t pos) {
     const uint32_t low = (1u << pos) - 1;
     return ((x & ~low) << 1) | (x & low);
+}
+
+__device__ __forceinline__ uint64_t runs_deposit(uint64_t x, const BitRuns& r) {
+    uint64_t out = 0;
+    for (uint32_t i = 0; i < r.n; ++i) {
+        const uint32_t w = r.width[i];
+        const uint64_t m = w >= 64 ? ~0ull : ((1ull << w) - 1);
+        out |= ((x >> r.src[i]) & m) << r.dst[i];
+    }
+    return out;
 }
 
 __device__ __forceinline__ uint64_t deposit_x(uint64_t x, uint64_t mask) {
@@ -185,6 +381,275 @@ __device__ __forceinline__ uint64_t deposit_x(uint64_t x, uint64_t mask) {
     }
     return out;
 }
+
+__device__ __forceinline__ uint64_t planar_addr(uint64_t p, uint32_t lb, uint64_t lmask, int interleaved) {
+    return interleaved ? 2 * p : (((p >> lb) << (lb + 1)) | (p & lmask));
+}
+
+// ------------------------------------------------------- fast tiled pass
+
+constexpr int kFastThreads = 256;
+constexpr int kPer = 16;  // tile positions per thread: k = tid + 256 j
+
+// Diagonal ops [q0, q1) on one amplitude with full buffer index x; chain
+// phase tables live in shared memory (stab).
+// Walk the set bits of s in the chain's program order, multiplying by the
+// phase of each (exact reference product per phase).
+__device__ __forceinline__ C2 chain_walk(uint32_t s, bool desc, const double2* tab, C2 a) {
+    if (desc) {
+        while (s) {
+            const int r = 31 - __clz(s);
+            s &= ~(1u << r);
+            const double2 u = tab[r];
+            a = cmul(u.x, u.y, a);
+        }
+    } else {
+        while (s) {
+            const int r = __ffs(s) - 1;
+            s &= s - 1;
+            const double2 u = tab[r];
+            a = cmul(u.x, u.y, a);
+        }
+    }
+    return a;
+}
+
+template <bool kDesc>
+__device__ __forceinline__ int next_bit(uint32_t s) {
+    return kDesc ? 31 - __clz(s) : __ffs(s) - 1;
+}
+
+// A lone phase chain over the thread's 16 amplitudes, four walks interleaved
+// (j, j + 4, j + 8, j + 12) so dependent complex products of different
+// amplitudes overlap in the FP64 pipeline.
+constexpr int kWalks = 4;
+
+template <bool kDesc>
+__device__ __forceinline__ void chain_walks(double2* tile_s, const double2* tab, uint32_t tid, uint64_t xbase,
+                                            const uint64_t* joff, uint32_t c, uint32_t R) {
+    for (int j = 0; j < kPer / kWalks; ++j) {
+        uint32_t s[kWalks];
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < kWalks; ++q) {
+            const uint64_t x = xbase | joff[j + q * (kPer / kWalks)];
+            s[q] = ((x >> c) & 1) ? static_cast<uint32_t>(x) & R : 0u;
+            any |= s[q] != 0;
+        }
+        if (!any) continue;
+        C2 a[kWalks];
+#pragma unroll
+        for (int q = 0; q < kWalks; ++q) {
+            const double2 v = tile_s[tid + 256u * (j + q * (kPer / kWalks))];
+            a[q] = C2{v.x, v.y};
+        }
+        while (s[0] | s[1] | s[2] | s[3]) {
+#pragma unroll
+            for (int q = 0; q < kWalks; ++q) {
+                if (s[q]) {
+                    const int r = next_bit<kDesc>(s[q]);
+                    s[q] &= ~(1u << r);
+                    const double2 u = tab[r];
+                    a[q] = cmul(u.x, u.y, a[q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kWalks; ++q)
+            tile_s[tid + 256u * (j + q * (kPer / kWalks))] = make_double2(a[q].re, a[q].im);
+    }
+}
+
+__device__ __forceinline__ C2 apply_diag_run(const FastOp* ops, const double2* stab, uint32_t q0, uint32_t q1,
+                                             uint64_t x, C2 a) {
+    for (uint32_t q = q0; q < q1; ++q) {
+        const FastOp& o = ops[q];
+        if (o.type == OP_CHAIN) {
+            if (!((x >> o.hi) & 1)) continue;
+            uint32_t R;
+            memcpy(&R, &o.m[0], 4);
+            a = chain_walk(static_cast<uint32_t>(x) & R, o.et[0] != 0, stab + o.pad2, a);
+        } else if (o.type == OP_CDIAG) {
+            if (((x >> o.hi) & (x >> o.lo) & 1) && o.et[0] != ET_ONE) a = entry_mul(o.et[0], o.m[0], o.m[1], a);
+        } else {  // OP_DIAG
+            const int e = static_cast<int>((x >> o.hi) & 1);
+            if (o.et[e] != ET_ONE) a = entry_mul(o.et[e], o.m[2 * e], o.m[2 * e + 1], a);
+        }
+    }
+    return a;
+}
+
+__device__ __forceinline__ bool is_diag(uint8_t t) { return t == OP_DIAG || t == OP_CDIAG || t == OP_CHAIN; }
+
+// Quantisation epilogue: amplitudes j of this thread -> packed words and
+// per-chunk counters. Lanes of a warp hold 32 consecutive locals (tile
+// positions 0..4 are buffer bits 0..4), so (block slot, chunk) is
+// warp-uniform and counters are reduced per warp before one set of atomics.
+__device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t base,
+                                               uint64_t toff, const uint64_t* joff, uint32_t lb) {
+    const uint64_t lmask = (1ull << lb) - 1;
+    ChunkAcc acc_re, acc_im;
+    uint64_t key_re = ~0ull, key_im = ~0ull;
+    bool bad = false, oow = false;
+    for (int j = 0; j < kPer; ++j) {
+        const double2 v = tile_s[tid + 256 * j];
+        const uint64_t p = base | toff | joff[j];
+        const uint64_t slot = p >> lb, l = p & lmask;
+        const uint64_t s_im = (1ull << lb) + l;
+        const uint64_t kre = slot * q.nch + (l >> 12), kim = slot * q.nch + (s_im >> 12);
+        if (kre != key_re) {  // warp-uniform
+            if (key_re != ~0ull) flush_chunk(q.cps + key_re, acc_re);
+            acc_re = ChunkAcc{};
+            key_re = kre;
+        }
+        if (kim != key_im) {
+            if (key_im != ~0ull) flush_chunk(q.cps + key_im, acc_im);
+            acc_im = ChunkAcc{};
+            key_im = kim;
+        }
+        const uint32_t pre = quantize_pack(v.x, q.t, bad, oow);
+        const uint32_t pim = quantize_pack(v.y, q.t, bad, oow);
+        uint32_t* dst = q.pk + (slot << (lb + 1));
+        dst[l] = pre;
+        dst[s_im] = pim;
+        acc_re.add(pre);
+        acc_im.add(pim);
+    }
+    flush_chunk(q.cps + key_re, acc_re);
+    flush_chunk(q.cps + key_im, acc_im);
+    if (bad) dev_fail(q.err, DE_NONFINITE, 0);
+    if (oow) dev_fail(q.err, DE_WINDOW, 0);
+}
+
+__global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __restrict__ buf, uint32_t lb,
+                                                                 int interleaved, uint64_t ntiles,
+                                                                 const __grid_constant__ FastPass pass,
+                                                                 const __grid_constant__ QuantOut quant,
+                                                                 const uint32_t* __restrict__ vtab) {
+    // dynamic SMEM: 4096 amplitudes (tile position k) | chain tables | ops
+    extern __shared__ double2 tile_s[];
+    __shared__ uint64_t joff[kPer];
+    double2* stab = tile_s + 4096;
+    FastOp* sops = reinterpret_cast<FastOp*>(stab + pass.tab_entries);
+    const uint32_t tid = threadIdx.x;
+    const uint64_t lmask = (1ull << lb) - 1;
+    const uint64_t im_off = interleaved ? 1 : (1ull << lb);
+    const uint64_t toff = runs_deposit(tid, pass.tile);
+    if (tid < kPer) joff[tid] = runs_deposit(static_cast<uint64_t>(tid) << 8, pass.tile);
+    for (uint32_t e = tid; e < pass.tab_entries; e += kFastThreads)
+        stab[e] = __ldg(reinterpret_cast<const double2*>(pass.chain_tab) + pass.tab_base + e);
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(pass.ops);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(sops);
+        const uint32_t words = pass.nops * static_cast<uint32_t>(sizeof(FastOp) / 4);
+        for (uint32_t e = tid; e < words; e += kFastThreads) dst[e] = src[e];
+    }
+    __syncthreads();
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t base = runs_deposit(tile, pass.base);
+        // Index used by diagonal conditions. Block-wise batches (vtab) hold
+        // single blocks of a diagonal stage: the bits above lb are the
+        // block's inner value, not its slot in the batch.
+        const uint64_t xbase = vtab ? ((static_cast<uint64_t>(vtab[base >> lb]) << lb) | (base & lmask)) : base;
+        __syncthreads();  // previous tile's stores have read tile_s
+        {
+            double re[kPer], im[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
+                re[j] = buf[a];
+                im[j] = buf[a + im_off];
+            }
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) tile_s[tid + 256 * j] = make_double2(re[j], im[j]);
+        }
+        bool owners_only = true;
+        for (uint32_t i = 0; i < pass.nops;) {
+            const FastOp& g = sops[i];
+            if (is_diag(g.type)) {
+                uint32_t i2 = i + 1;
+                while (i2 < pass.nops && is_diag(sops[i2].type)) ++i2;
+                if (!owners_only) __syncthreads();
+                owners_only = true;
+                if (i2 == i + 1 && g.type == OP_CHAIN) {  // a lone phase chain: parameters in registers
+                    const uint32_t c = g.hi;
+                    uint32_t R;
+                    memcpy(&R, &g.m[0], 4);
+                    const bool desc = g.et[0] != 0;
+                    const double2* tab = stab + g.pad2;
+                    if (desc)
+                        chain_walks<true>(tile_s, tab, tid, xbase | toff, joff, c, R);
+                    else
+                        chain_walks<false>(tile_s, tab, tid, xbase | toff, joff, c, R);
+                } else {
+                    for (int j = 0; j < kPer; ++j) {
+                        const uint32_t k = tid + 256u * j;
+                        const double2 v = tile_s[k];
+                        const C2 r = apply_diag_run(sops, stab, i, i2, xbase | toff | joff[j], C2{v.x, v.y});
+                        tile_s[k] = make_double2(r.re, r.im);
+                    }
+                }
+                i = i2;
+                continue;
+            }
+            ++i;
+            __syncthreads();
+            owners_only = false;
+            const bool cx = g.type == OP_CX;
+            const uint32_t tp = cx ? g.tp_lo : g.tp_hi;
+            const uint32_t m = 1u << tp;
+            const uint32_t bctl = static_cast<uint32_t>((base >> g.hi) & 1);
+            for (uint32_t r = tid; r < 2048; r += kFastThreads) {
+                const uint32_t i0 = insert0(r, tp), i1 = i0 | m;
+                if (cx) {
+                    const uint32_t ctl = g.in_hi ? (i0 >> g.tp_hi) & 1 : bctl;
+                    if (ctl) {
+                        const double2 t = tile_s[i0];
+                        tile_s[i0] = tile_s[i1];
+                        tile_s[i1] = t;
+                    }
+                } else {
+                    const double2 v0 = tile_s[i0], v1 = tile_s[i1];
+                    if (g.pad) {  // all entries real: u*a = (u*ar, u*ai) exactly
+                        const double u00 = g.m[0], u01 = g.m[2], u10 = g.m[4], u11 = g.m[6];
+                        tile_s[i0] = make_double2(__dadd_rn(__dmul_rn(u00, v0.x), __dmul_rn(u01, v1.x)),
+                                                  __dadd_rn(__dmul_rn(u00, v0.y), __dmul_rn(u01, v1.y)));
+                        tile_s[i1] = make_double2(__dadd_rn(__dmul_rn(u10, v0.x), __dmul_rn(u11, v1.x)),
+                                                  __dadd_rn(__dmul_rn(u10, v0.y), __dmul_rn(u11, v1.y)));
+                    } else {
+                        const C2 a0{v0.x, v0.y}, a1{v1.x, v1.y};
+                        const C2 o0 = row2(g.et, g.m, 0, a0, a1), o1 = row2(g.et, g.m, 1, a0, a1);
+                        tile_s[i0] = make_double2(o0.re, o0.im);
+                        tile_s[i1] = make_double2(o1.re, o1.im);
+                    }
+                }
+            }
+        }
+        if (!owners_only) __syncthreads();
+        if (quant.pk) {
+            quant_epilogue(quant, tile_s, tid, base, toff, joff, lb);
+            continue;
+        }
+        {
+            double re[kPer], im[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const double2 v = tile_s[tid + 256 * j];
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
+                buf[a] = re[j];
+                buf[a + im_off] = im[j];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------ general pass (SMEM)
+// Any tile size and general 4x4 matrices; used for small buffers and U4.
 
 constexpr int kPassThreads = 256;
 
@@ -200,18 +665,15 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
     const uint64_t base = deposit_x(blockIdx.x, ~tile_mask);
     const uint64_t toff = deposit_x(tid, tile_mask);
     const uint64_t lmask = (1ull << lb) - 1;
-    const auto addr = [&](uint64_t p) -> uint64_t {
-        return interleaved ? 2 * p : (((p >> lb) << (lb + 1)) | (p & lmask));
-    };
     const uint64_t im_off = interleaved ? 1 : (1ull << lb);
-#pragma unroll 4
     for (uint32_t j = 0; j < per; ++j) {
         const uint32_t k = tid + j * nth;
-        const uint64_t a = addr(base | toff | deposit_x(static_cast<uint64_t>(j) * nth, tile_mask));
+        const uint64_t a = planar_addr(base | toff | deposit_x(static_cast<uint64_t>(j) * nth, tile_mask), lb, lmask,
+                                       interleaved);
         sre[k] = buf[a];
         sim[k] = buf[a + im_off];
     }
-    bool owners_only = true;  // smem entries touched since the last barrier were written by their owners
+    bool owners_only = true;
     for (uint32_t i = 0; i < nops; ++i) {
         const GateOp* g = ops + i;
         const uint8_t type = g->type;
@@ -221,7 +683,6 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
                 owners_only = true;
             }
             const uint64_t bhi = (base >> g->hi) & 1, blo = (base >> g->lo) & 1;
-            const uint8_t et = type == OP_DIAG ? 0 : 15;
             for (uint32_t j = 0; j < per; ++j) {
                 const uint32_t k = tid + j * nth;
                 const uint32_t hv = g->in_hi ? (k >> g->tp_hi) & 1 : static_cast<uint32_t>(bhi);
@@ -231,11 +692,11 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
                 } else {
                     const uint32_t lv = g->in_lo ? (k >> g->tp_lo) & 1 : static_cast<uint32_t>(blo);
                     if (!(hv && lv)) continue;
-                    e = et;
+                    e = 15;
                 }
                 const uint8_t ty = g->et[e];
                 if (ty == ET_ONE) continue;
-                const C2 r = ty == ET_ZERO ? C2{0.0, 0.0} : entry_mul(ty, g->m[2 * e], g->m[2 * e + 1], C2{sre[k], sim[k]});
+                const C2 r = entry_mul(ty, g->m[2 * e], g->m[2 * e + 1], C2{sre[k], sim[k]});
                 sre[k] = r.re;
                 sim[k] = r.im;
             }
@@ -247,8 +708,8 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
             const uint32_t tp = g->tp_hi, m = 1u << tp;
             for (uint32_t r = tid; r < tsz / 2; r += nth) {
                 const uint32_t i0 = insert0(r, tp), i1 = i0 | m;
-                const C2 a[2] = {{sre[i0], sim[i0]}, {sre[i1], sim[i1]}};
-                const C2 o0 = mat_row<2>(g, 0, a), o1 = mat_row<2>(g, 1, a);
+                const C2 a0{sre[i0], sim[i0]}, a1{sre[i1], sim[i1]};
+                const C2 o0 = row2(g->et, g->m, 0, a0, a1), o1 = row2(g->et, g->m, 1, a0, a1);
                 sre[i0] = o0.re;
                 sim[i0] = o0.im;
                 sre[i1] = o1.re;
@@ -279,7 +740,7 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
                 for (int q = 0; q < 4; ++q) a[q] = C2{sre[idx[q]], sim[idx[q]]};
                 C2 o[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) o[q] = mat_row<4>(g, q, a);
+                for (int q = 0; q < 4; ++q) o[q] = row4(g, q, a);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     sre[idx[q]] = o[q].re;
@@ -289,10 +750,10 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
         }
     }
     __syncthreads();
-#pragma unroll 4
     for (uint32_t j = 0; j < per; ++j) {
         const uint32_t k = tid + j * nth;
-        const uint64_t a = addr(base | toff | deposit_x(static_cast<uint64_t>(j) * nth, tile_mask));
+        const uint64_t a = planar_addr(base | toff | deposit_x(static_cast<uint64_t>(j) * nth, tile_mask), lb, lmask,
+                                       interleaved);
         buf[a] = sre[k];
         buf[a + im_off] = sim[k];
     }
@@ -300,25 +761,45 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
 
 }  // namespace
 
-void run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
-                 uint64_t nreps, uint64_t* launches) {
+bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
+                 uint64_t nreps, uint64_t* launches, const QuantOut* quant, const uint32_t* vtab,
+                 uint64_t nblocks) {
+    const bool fuse = quant && !interleaved && lb >= 12 && !prog.passes.empty() && prog.passes.back().fast;
+    if (vtab) {  // block-wise batch: every pass must be fast and its tile local
+        for (const GatePass& p : prog.passes)
+            if (!p.fast || (p.tile_mask >> lb) || lb < p.tb)
+                raise(BMQ_ERR_LOGIC, "block-wise gate batch needs local fast passes");
+    }
+    const QuantOut none{};
     static thread_local int attr_dev = -1;
     int dev = 0;
     BMQ_CUDA(cudaGetDevice(&dev));
+    const int tile_bytes = (1 << kMaxTileBits) * static_cast<int>(sizeof(double2));
     if (attr_dev != dev) {
-        BMQ_CUDA(cudaFuncSetAttribute(k_gate_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      2 * (1 << kMaxTileBits) * static_cast<int>(sizeof(double))));
+        BMQ_CUDA(cudaFuncSetAttribute(k_gate_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_bytes));
+        BMQ_CUDA(cudaFuncSetAttribute(k_gate_pass_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_dev = dev;
     }
-    for (const GatePass& p : prog.passes) {
-        const uint64_t tiles = nreps << (prog.total_bits - p.tb);
-        const uint32_t nth = std::min<uint32_t>(kPassThreads, 1u << p.tb);
-        const size_t smem = 2 * (size_t(1) << p.tb) * sizeof(double);
-        k_gate_pass<<<static_cast<uint32_t>(tiles), nth, smem, st>>>(buf, lb, interleaved ? 1 : 0, p.tile_mask, p.tb,
-                                                                    prog.d_ops + p.begin, p.count);
+    for (size_t pi = 0; pi < prog.passes.size(); ++pi) {
+        const GatePass& p = prog.passes[pi];
+        const uint64_t tiles = vtab ? nblocks << (lb - p.tb) : nreps << (prog.total_bits - p.tb);
+        if (p.fast) {
+            const size_t smem = tile_bytes + p.fp->tab_entries * sizeof(double2) + p.fp->nops * sizeof(FastOp);
+            const uint64_t per_sm = std::max<uint64_t>(1, (227ull * 1024) / (smem + 2048));
+            const uint64_t grid = std::min<uint64_t>(tiles, 148ull * per_sm * 8);
+            const bool last = pi + 1 == prog.passes.size();
+            k_gate_pass_fast<<<static_cast<uint32_t>(grid), kFastThreads, smem, st>>>(
+                buf, lb, interleaved ? 1 : 0, tiles, *p.fp, (fuse && last) ? *quant : none, vtab);
+        } else {
+            const uint32_t nth = std::min<uint32_t>(kPassThreads, 1u << p.tb);
+            const size_t smem = 2 * (size_t(1) << p.tb) * sizeof(double);
+            k_gate_pass<<<static_cast<uint32_t>(tiles), nth, smem, st>>>(buf, lb, interleaved ? 1 : 0, p.tile_mask,
+                                                                        p.tb, prog.d_ops + p.begin, p.count);
+        }
         BMQ_CUDA(cudaGetLastError());
         if (launches) ++*launches;
     }
+    return fuse;
 }
 
 }  // namespace bmq

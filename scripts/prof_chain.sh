@@ -1,0 +1,4 @@
+#!/bin/bash
+B="python bench.py --qubits 26 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gate_pass_fast -s 14 -c 1 -o gpurun_out/prof_chain2 $B > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gate_pass_fast -s 17 -c 1 -o gpurun_out/prof_epi2 $B > /dev/null 2>&1

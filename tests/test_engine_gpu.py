@@ -98,6 +98,32 @@ def test_zero_group_skip_is_exact(gpu):
     assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("name,n,b,inner,layers", [("qft", 18, 12, 2, 1), ("qft", 17, 12, 4, 1),
+                                                   ("qaoa", 16, 12, 2, 2), ("bv", 16, 13, 2, 1)])
+def test_identity_skip_is_exact(gpu, port, name, n, b, inner, layers):
+    c = gpu.generate_benchmark(name, n, gpu.BenchmarkParams(layers=layers))
+    want = port.simulate(n, [g.as_tuple() for g in c.gates], b, inner, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=inner, identity_skip=True)) as sim:
+        rep = sim.run()
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=NORM_RTOL)
+        if name == "qft":  # QFT stages are mostly controlled phases: many blocks skipped
+            assert rep.device["blocks_processed"] < rep.stage_count * (1 << (n - b))
+
+
+def test_arena_compaction_is_exact(gpu, port):
+    c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=2))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    biggest = max(len(p) for p in want.payloads)
+    pool = 24 * (biggest + 16)  # the live state plus about two batches
+    with gpu.Simulator(c, gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool,
+                                     work_bytes=4 * (16 << 12))) as sim:
+        rep = sim.run()
+        assert rep.device["compactions"] > 0
+        assert sim.payloads() == want.payloads
+
+
 def test_small_batches_are_exact(gpu, port):
     c = gpu.generate_benchmark("qaoa", 14, gpu.BenchmarkParams(layers=2))
     want = port.simulate(14, [g.as_tuple() for g in c.gates], 9, 2, 1e-3)
