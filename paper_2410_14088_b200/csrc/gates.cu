@@ -419,44 +419,44 @@ __device__ __forceinline__ int next_bit(uint32_t s) {
     return kDesc ? 31 - __clz(s) : __ffs(s) - 1;
 }
 
-// A lone phase chain over the thread's 16 amplitudes, four walks interleaved
-// (j, j + 4, j + 8, j + 12) so dependent complex products of different
-// amplitudes overlap in the FP64 pipeline.
-constexpr int kWalks = 4;
+// A lone phase chain over the thread's 16 amplitudes, eight at a time held
+// in registers. The chain's bits are visited once per thread in program
+// order (one bit scan and one phase load shared by eight amplitudes); each
+// amplitude multiplies when its own bit is set. The eight products of one
+// step are independent, so the FP64 pipeline stays busy.
+constexpr int kLanesPerStep = 8;
 
 template <bool kDesc>
 __device__ __forceinline__ void chain_walks(double2* tile_s, const double2* tab, uint32_t tid, uint64_t xbase,
                                             const uint64_t* joff, uint32_t c, uint32_t R) {
-    for (int j = 0; j < kPer / kWalks; ++j) {
-        uint32_t s[kWalks];
-        bool any = false;
+    for (int h = 0; h < kPer / kLanesPerStep; ++h) {
+        uint32_t xs[kLanesPerStep];
+        uint32_t any = 0;
 #pragma unroll
-        for (int q = 0; q < kWalks; ++q) {
-            const uint64_t x = xbase | joff[j + q * (kPer / kWalks)];
-            s[q] = ((x >> c) & 1) ? static_cast<uint32_t>(x) & R : 0u;
-            any |= s[q] != 0;
+        for (int q = 0; q < kLanesPerStep; ++q) {
+            const uint64_t x = xbase | joff[h * kLanesPerStep + q];
+            xs[q] = ((x >> c) & 1) ? static_cast<uint32_t>(x) & R : 0u;
+            any |= xs[q];
         }
         if (!any) continue;
-        C2 a[kWalks];
+        C2 a[kLanesPerStep];
 #pragma unroll
-        for (int q = 0; q < kWalks; ++q) {
-            const double2 v = tile_s[tid + 256u * (j + q * (kPer / kWalks))];
+        for (int q = 0; q < kLanesPerStep; ++q) {
+            const double2 v = tile_s[tid + 256u * (h * kLanesPerStep + q)];
             a[q] = C2{v.x, v.y};
         }
-        while (s[0] | s[1] | s[2] | s[3]) {
+        uint32_t rem = any;  // bits of R set in at least one of the eight
+        while (rem) {
+            const int r = next_bit<kDesc>(rem);
+            rem &= ~(1u << r);
+            const double2 u = tab[r];
 #pragma unroll
-            for (int q = 0; q < kWalks; ++q) {
-                if (s[q]) {
-                    const int r = next_bit<kDesc>(s[q]);
-                    s[q] &= ~(1u << r);
-                    const double2 u = tab[r];
-                    a[q] = cmul(u.x, u.y, a[q]);
-                }
-            }
+            for (int q = 0; q < kLanesPerStep; ++q)
+                if ((xs[q] >> r) & 1u) a[q] = cmul(u.x, u.y, a[q]);
         }
 #pragma unroll
-        for (int q = 0; q < kWalks; ++q)
-            tile_s[tid + 256u * (j + q * (kPer / kWalks))] = make_double2(a[q].re, a[q].im);
+        for (int q = 0; q < kLanesPerStep; ++q)
+            tile_s[tid + 256u * (h * kLanesPerStep + q)] = make_double2(a[q].re, a[q].im);
     }
 }
 
