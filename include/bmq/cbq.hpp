@@ -1,0 +1,360 @@
+// bmq/cbq.hpp — C++ drop-in surface for the reference's `namespace cbq`
+// (/root/reference/proj/include/cbq), backed by libbmq.so (include/bmq.h).
+//
+// A reference user replaces
+//     #include "cbq/engine.hpp"   (and codec.hpp, partition.hpp, ...)
+// with
+//     #include "bmq/cbq.hpp"
+// and links -lbmq. Types, function names, argument meaning and exception
+// types follow the reference; Simulator::run executes on the B200.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "bmq.h"
+
+namespace cbq {
+
+using Complex = std::complex<double>;
+using Mat2 = std::array<Complex, 4>;
+using Mat4 = std::array<Complex, 16>;
+
+// -------------------------------------------------------------- exceptions
+class CodecError : public std::runtime_error {  // bitmap.hpp:14-17
+public:
+    using std::runtime_error::runtime_error;
+};
+class StoreError : public std::runtime_error {  // store.hpp:23-26
+public:
+    using std::runtime_error::runtime_error;
+};
+class EngineError : public std::runtime_error {  // engine.hpp:18-21
+public:
+    using std::runtime_error::runtime_error;
+};
+class DeviceError : public std::runtime_error {  // CUDA / no device (new)
+public:
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+[[noreturn]] inline void rethrow(int rc) {
+    const std::string msg = bmq_last_error();
+    switch (rc) {
+    case BMQ_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case BMQ_ERR_LOGIC: throw std::logic_error(msg);
+    case BMQ_ERR_CODEC: throw CodecError(msg);
+    case BMQ_ERR_STORE: throw StoreError(msg);
+    case BMQ_ERR_ENGINE: throw EngineError(msg);
+    default: throw DeviceError(msg);
+    }
+}
+inline void check(int rc) {
+    if (rc != BMQ_OK) rethrow(rc);
+}
+}  // namespace detail
+
+// ----------------------------------------------------------------- circuit
+enum class GateKind : std::uint8_t { H, X, Y, Z, S, Sdg, T, Tdg, RX, RY, RZ, P, CX, CZ, CP };
+
+constexpr bool is_two_qubit(GateKind k) { return k == GateKind::CX || k == GateKind::CZ || k == GateKind::CP; }
+
+struct Gate {  // circuit.hpp:65-72
+    GateKind kind{};
+    std::uint32_t q0 = 0;
+    std::uint32_t q1 = 0;
+    double angle = 0.0;
+    bool operator==(const Gate&) const = default;
+    bmq_gate c() const { return bmq_gate{static_cast<uint32_t>(kind), q0, is_two_qubit(kind) ? q1 : 0u, 0u, angle}; }
+};
+
+struct Circuit {  // circuit.hpp:97-130
+    std::uint32_t num_qubits = 1;
+    std::vector<Gate> gates;
+    Circuit() = default;
+    explicit Circuit(std::uint32_t n) : num_qubits(n) { detail::check(bmq_circuit_validate(n, nullptr, 0)); }
+    void add(const Gate& g) {
+        const bmq_gate cg = g.c();
+        detail::check(bmq_circuit_validate(num_qubits, &cg, 1));
+        gates.push_back(g);
+    }
+    std::vector<bmq_gate> c_gates() const {
+        std::vector<bmq_gate> v;
+        v.reserve(gates.size());
+        for (const Gate& g : gates) v.push_back(g.c());
+        return v;
+    }
+    bool operator==(const Circuit&) const = default;
+};
+
+inline Mat2 unitary2(const Gate& g) {  // circuit.hpp:133-170
+    if (is_two_qubit(g.kind)) throw std::logic_error("unitary2 called on a two-qubit gate");
+    const bmq_gate cg = g.c();
+    double m[32];
+    detail::check(bmq_gate_unitary(&cg, m));
+    Mat2 u;
+    for (int i = 0; i < 4; ++i) u[i] = Complex(m[2 * i], m[2 * i + 1]);
+    return u;
+}
+
+inline Mat4 unitary4(const Gate& g) {  // circuit.hpp:174-198
+    if (!is_two_qubit(g.kind)) throw std::logic_error("unitary4 called on a single-qubit gate");
+    const bmq_gate cg = g.c();
+    double m[32];
+    detail::check(bmq_gate_unitary(&cg, m));
+    Mat4 u;
+    for (int i = 0; i < 16; ++i) u[i] = Complex(m[2 * i], m[2 * i + 1]);
+    return u;
+}
+
+enum class Benchmark { Ghz, CatState, Bv, Qft, Qaoa };
+
+struct BenchmarkParams {  // benchmarks.hpp:24-28
+    std::uint32_t layers = 1;
+    std::optional<std::string> secret;
+    std::uint64_t seed = 1;
+};
+
+inline Circuit generate_benchmark(Benchmark b, std::uint32_t n, const BenchmarkParams& p = {}) {
+    static const char* names[] = {"ghz", "cat_state", "bv", "qft", "qaoa"};
+    const char* name = names[static_cast<int>(b)];
+    const std::string secret = p.secret.value_or("");
+    std::uint64_t count = 0;
+    int rc = bmq_generate_benchmark(name, n, p.layers, p.seed, secret.c_str(), nullptr, 0, &count);
+    if (rc != BMQ_OK && rc != BMQ_ERR_BUFFER_TOO_SMALL) detail::rethrow(rc);
+    std::vector<bmq_gate> v(count);
+    detail::check(bmq_generate_benchmark(name, n, p.layers, p.seed, secret.c_str(), v.data(), count, &count));
+    Circuit c(n);
+    for (const bmq_gate& g : v) c.gates.push_back(Gate{static_cast<GateKind>(g.kind), g.q0, g.q1, g.angle});
+    return c;
+}
+
+// --------------------------------------------------------------- partition
+struct Layout {  // partition.hpp:14-21
+    std::uint32_t n = 1, b = 1, c = 0;
+    std::uint64_t num_blocks() const { return 1ull << c; }
+    std::uint64_t block_size() const { return 1ull << b; }
+};
+
+inline Layout make_layout(std::uint32_t n, std::uint32_t b) {
+    if (n < 1 || n > 62) throw std::invalid_argument("layout qubit count must be in [1, 62]");
+    if (b < 1 || b > n) throw std::invalid_argument("local index bits must be in [1, n]");
+    return Layout{n, b, n - b};
+}
+
+struct Stage {  // partition.hpp:36-40
+    std::size_t gate_begin = 0, gate_end = 0;
+    std::vector<std::uint32_t> inner;
+    bmq_stage c() const {
+        bmq_stage s{};
+        s.gate_begin = gate_begin;
+        s.gate_end = gate_end;
+        s.inner_count = static_cast<uint32_t>(inner.size());
+        for (std::size_t i = 0; i < inner.size(); ++i) s.inner[i] = inner[i];
+        return s;
+    }
+};
+
+struct PartitionPlan {  // partition.hpp:42-46
+    Layout layout;
+    std::uint32_t inner_size = 0;
+    std::vector<Stage> stages;
+};
+
+struct SVGroup {  // partition.hpp:50-53
+    std::uint64_t outer_value = 0;
+    std::vector<std::uint64_t> block_ids;
+};
+
+inline PartitionPlan partition_circuit(const Circuit& c, std::uint32_t block_bits, std::uint32_t inner_size) {
+    const auto g = c.c_gates();
+    std::vector<bmq_stage> out(std::max<std::size_t>(1, g.size()));
+    std::uint64_t ns = 0;
+    detail::check(bmq_partition(c.num_qubits, g.data(), g.size(), block_bits, inner_size, out.data(), out.size(), &ns));
+    PartitionPlan plan{make_layout(c.num_qubits, block_bits), inner_size, {}};
+    for (std::uint64_t i = 0; i < ns; ++i)
+        plan.stages.push_back(Stage{out[i].gate_begin, out[i].gate_end,
+                                    std::vector<std::uint32_t>(out[i].inner, out[i].inner + out[i].inner_count)});
+    return plan;
+}
+
+inline std::vector<SVGroup> enumerate_groups(const Stage& stage, const Layout& layout) {
+    const bmq_stage s = stage.c();
+    std::vector<std::uint64_t> ids(layout.num_blocks());
+    std::uint64_t count = 0;
+    detail::check(bmq_enumerate_groups(layout.n, layout.b, &s, ids.data(), ids.size(), &count));
+    const std::uint64_t per = 1ull << stage.inner.size();
+    std::vector<SVGroup> groups(count / per);
+    for (std::uint64_t o = 0; o < groups.size(); ++o) {
+        groups[o].outer_value = o;
+        groups[o].block_ids.assign(ids.begin() + o * per, ids.begin() + (o + 1) * per);
+    }
+    return groups;
+}
+
+inline std::uint32_t buffer_bit_of_qubit(const Stage& stage, const Layout& layout, std::uint32_t q) {
+    const bmq_stage s = stage.c();
+    std::uint32_t bit = 0;
+    detail::check(bmq_buffer_bit_of_qubit(layout.n, layout.b, &s, q, &bit));
+    return bit;
+}
+
+// ------------------------------------------------------------------- codec
+struct ErrorBound {  // codec.hpp:19-29
+    double relative;
+    double log2_abs;
+    explicit ErrorBound(double b_r) : relative(b_r), log2_abs(0.0) { detail::check(bmq_error_bound(b_r, &log2_abs)); }
+};
+
+inline std::vector<std::uint8_t> compress_block(std::span<const double> scalars, const ErrorBound& bound) {
+    std::vector<std::uint8_t> out(bmq_compress_bound(scalars.size()));
+    std::uint64_t size = 0;
+    detail::check(bmq_compress_blocks(scalars.data(), 1, scalars.size(), bound.relative, out.data(), out.size(), &size));
+    out.resize(size);
+    return out;
+}
+
+inline std::vector<double> decompress_block(std::span<const std::uint8_t> payload) {
+    const std::uint64_t off = 0, size = payload.size();
+    std::uint64_t count = 0;
+    double dummy = 0.0;
+    int rc = bmq_decompress_blocks(payload.data(), &off, &size, 1, &dummy, 0, &count);
+    if (rc != BMQ_OK && rc != BMQ_ERR_BUFFER_TOO_SMALL) detail::rethrow(rc);
+    std::vector<double> out(count);
+    if (count) detail::check(bmq_decompress_blocks(payload.data(), &off, &size, 1, out.data(), count, &count));
+    return out;
+}
+
+// ------------------------------------------------------------------ engine
+inline constexpr std::uint64_t kUnlimitedBudget = std::numeric_limits<std::uint64_t>::max();
+
+struct Config {  // engine.hpp:23-37 (+ device knobs)
+    std::uint32_t block_bits = 1;
+    std::uint32_t inner_size = 2;
+    double error_bound = 1e-3;
+    std::uint64_t memory_budget = kUnlimitedBudget;
+    unsigned workers = 1;
+    bool compress = true;
+    std::uint32_t verify_cap_qubits = 24;
+    int device = 0;
+    bool identity_skip = false;
+};
+
+struct SimulationReport {  // engine.hpp:39-53
+    std::uint64_t qubits = 0, gate_count = 0, stage_count = 0, max_footprint_bytes = 0;
+    double standard_bytes = 0.0, compression_ratio = 0.0;
+    std::uint64_t spilled_blocks = 0;
+    double wall_ms = 0.0;
+    std::vector<double> stage_ms;
+    std::optional<double> fidelity;
+    double final_norm = 0.0;
+    std::uint64_t stage_compress_calls = 0, stage_decompress_calls = 0;
+    bmq_report device{};
+};
+
+class Simulator {  // engine.hpp:58-250
+public:
+    Simulator(Circuit circuit, Config config) : circuit_(std::move(circuit)), config_(config) {
+        bmq_config c;
+        bmq_config_default(&c);
+        c.block_bits = config_.block_bits;
+        c.inner_size = config_.inner_size;
+        c.error_bound = config_.error_bound;
+        c.memory_budget = config_.memory_budget;
+        c.workers = config_.workers;
+        c.compress = config_.compress ? 1u : 0u;
+        c.verify_cap_qubits = config_.verify_cap_qubits;
+        c.device = config_.device;
+        if (config_.identity_skip) c.flags |= BMQ_FLAG_IDENTITY_SKIP;
+        const auto g = circuit_.c_gates();
+        detail::check(bmq_simulator_create(circuit_.num_qubits, g.data(), g.size(), &c, &sim_));
+    }
+    Simulator(const Simulator&) = delete;
+    Simulator& operator=(const Simulator&) = delete;
+    ~Simulator() { bmq_simulator_destroy(sim_); }
+
+    void init_state() { detail::check(bmq_simulator_init_state(sim_)); }
+
+    SimulationReport run() {
+        bmq_report r{};
+        std::vector<double> stage_ms(std::max<std::size_t>(1, circuit_.gates.size()));
+        detail::check(bmq_simulator_run(sim_, &r, stage_ms.data(), stage_ms.size()));
+        SimulationReport out;
+        out.qubits = r.qubits;
+        out.gate_count = r.gate_count;
+        out.stage_count = r.stage_count;
+        out.max_footprint_bytes = r.max_footprint_bytes;
+        out.standard_bytes = r.standard_bytes;
+        out.compression_ratio = r.compression_ratio;
+        out.spilled_blocks = r.spilled_blocks;
+        out.wall_ms = r.wall_ms;
+        out.stage_ms.assign(stage_ms.begin(), stage_ms.begin() + static_cast<std::ptrdiff_t>(r.stage_count));
+        out.final_norm = r.final_norm;
+        out.stage_compress_calls = r.stage_compress_calls;
+        out.stage_decompress_calls = r.stage_decompress_calls;
+        out.device = r;
+        return out;
+    }
+
+    std::vector<Complex> extract_state() const {
+        std::vector<Complex> st(1ull << circuit_.num_qubits);
+        detail::check(bmq_simulator_extract_state(sim_, reinterpret_cast<double*>(st.data()), st.size()));
+        return st;
+    }
+
+    double state_norm() const {
+        double n = 0.0;
+        detail::check(bmq_simulator_state_norm(sim_, &n));
+        return n;
+    }
+
+    Complex amplitude(std::uint64_t index) const {
+        double re = 0.0, im = 0.0;
+        detail::check(bmq_simulator_amplitude(sim_, index, &re, &im));
+        return {re, im};
+    }
+
+    std::vector<std::uint8_t> get_payload(std::uint64_t id) const {  // store().get(id)
+        std::uint64_t size = 0;
+        detail::check(bmq_simulator_get_payload(sim_, id, nullptr, 0, &size));
+        std::vector<std::uint8_t> out(size);
+        detail::check(bmq_simulator_get_payload(sim_, id, out.data(), out.size(), &size));
+        return out;
+    }
+
+    void put_payload(std::uint64_t id, std::span<const std::uint8_t> p) {  // store().put(id, p)
+        detail::check(bmq_simulator_put_payload(sim_, id, p.data(), p.size()));
+    }
+
+    Layout layout() const { return make_layout(circuit_.num_qubits, config_.block_bits); }
+    PartitionPlan plan() const { return partition_circuit(circuit_, config_.block_bits, config_.inner_size); }
+
+private:
+    mutable bmq_simulator* sim_ = nullptr;
+    Circuit circuit_;
+    Config config_;
+};
+
+inline std::vector<Complex> dense_reference(const Circuit& c, std::uint32_t verify_cap_qubits = 24) {
+    if (c.num_qubits > verify_cap_qubits)
+        throw EngineError("dense reference refused: " + std::to_string(c.num_qubits) +
+                          " qubits exceeds the cap of " + std::to_string(verify_cap_qubits));
+    std::vector<Complex> st(1ull << c.num_qubits);
+    const auto g = c.c_gates();
+    detail::check(bmq_dense_reference(c.num_qubits, g.data(), g.size(), reinterpret_cast<double*>(st.data()),
+                                      verify_cap_qubits));
+    return st;
+}
+
+}  // namespace cbq

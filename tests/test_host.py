@@ -135,6 +135,22 @@ def test_validation_messages(cbq):
         cbq.enumerate_groups(cbq.Stage(0, 0, [1]), cbq.make_layout(6, 2))
 
 
+def test_cpp_dropin_header(cbq, tmp_path):
+    """include/bmq/cbq.hpp compiles like the reference headers and agrees with them."""
+    from paper_2410_14088_b200 import _lib
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    exe = tmp_path / "dropin"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ROOT}/include", f"{ROOT}/tests/cpp/dropin_host.cpp",
+                    f"-L{libdir}", "-lbmq", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines()
+    assert "qft34_gates 646" in out
+    assert "stages 14 2 200" in out and "stages 20 2 98" in out and "stages 20 6 21" in out
+    assert "group0 0 2 8 10" in out
+    assert "h00 0.70710678118654746" in out
+    assert "invalid_argument two-qubit gate operands must be distinct" in out
+    assert "logic_error qubit 4 is an outer index for this stage" in out
+
+
 def test_no_cpu_fallback_without_device(cbq):
     if cbq.device_count() > 0:
         pytest.skip("a CUDA device is present")
