@@ -171,6 +171,18 @@ int bmq_enumerate_groups(uint32_t num_qubits, uint32_t block_bits, const bmq_sta
 int bmq_buffer_bit_of_qubit(uint32_t num_qubits, uint32_t block_bits, const bmq_stage* stage,
                             uint32_t qubit, uint32_t* bit);
 
+/* parse_qasm (qasm.hpp:387-389): OPENQASM 2.0 subset. On BMQ_ERR_QASM the
+ * message is "line L, col C: ..." (cbq::QasmError). *count receives the full
+ * gate count even when cap is short; warnings (e.g. ignored measure) are
+ * written '\n'-separated into `warnings` (may be NULL). */
+int bmq_parse_qasm(const char* text, uint32_t* num_qubits, bmq_gate* out, uint64_t cap, uint64_t* count,
+                   char* warnings, uint64_t warnings_cap, uint64_t* num_warnings);
+
+/* emit_qasm (qasm.hpp:392-411): parse_qasm(emit_qasm(c)) == c. *size gets the
+ * text length (without the terminating NUL, which is written when it fits). */
+int bmq_emit_qasm(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, char* out, uint64_t cap,
+                  uint64_t* size);
+
 /* Upper bound on compress output bytes for one block of n scalars. */
 uint64_t bmq_compress_bound(uint64_t scalar_count);
 

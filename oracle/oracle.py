@@ -346,3 +346,23 @@ def ref() -> Ref:
 
 def have_ref() -> bool:
     return os.path.exists(REF_SO)
+
+
+def ref_parse_qasm(text: str):
+    """Reference parse_qasm through oracle/_ref: (num_qubits, gates, n_warnings) or raises OracleError."""
+    r = ref()
+    cap = 1 << 16
+    arr = (Gate * cap)()
+    nq, cnt, nw = C.c_uint32(), C.c_uint64(), C.c_uint64()
+    r._check(r._f("parse_qasm")(text.encode(), C.byref(nq), arr, C.c_uint64(cap), C.byref(cnt), C.byref(nw)))
+    return nq.value, gates_to_list(arr, cnt.value), nw.value
+
+
+def ref_emit_qasm(n: int, gates) -> str:
+    r = ref()
+    arr = gates_array(gates)
+    cap = 64 * (len(gates) + 8)
+    buf = C.create_string_buffer(cap)
+    size = C.c_uint64()
+    r._check(r._f("emit_qasm")(C.c_uint32(n), arr, C.c_uint64(len(gates)), buf, C.c_uint64(cap), C.byref(size)))
+    return buf.value.decode()

@@ -79,6 +79,9 @@ SIGNATURES = {
     "bmq_partition": (C.c_int, [_U32, _P, _U64, _U32, _U32, _P, _U64, C.POINTER(_U64)]),
     "bmq_enumerate_groups": (C.c_int, [_U32, _U32, C.POINTER(bmq_stage), _P, _U64, C.POINTER(_U64)]),
     "bmq_buffer_bit_of_qubit": (C.c_int, [_U32, _U32, C.POINTER(bmq_stage), _U32, C.POINTER(_U32)]),
+    "bmq_parse_qasm": (C.c_int, [C.c_char_p, C.POINTER(_U32), _P, _U64, C.POINTER(_U64), C.c_char_p, _U64,
+                                 C.POINTER(_U64)]),
+    "bmq_emit_qasm": (C.c_int, [_U32, _P, _U64, C.c_char_p, _U64, C.POINTER(_U64)]),
     "bmq_compress_bound": (_U64, [_U64]),
     "bmq_compress_blocks": (C.c_int, [_P, _U64, _U64, _D, _P, _U64, _P]),
     "bmq_decompress_blocks": (C.c_int, [_P, _P, _P, _U64, _P, _U64, _P]),

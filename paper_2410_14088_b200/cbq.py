@@ -67,7 +67,15 @@ class EngineError(BmqError):
 
 
 class QasmError(BmqError):
+    """cbq::QasmError (qasm.hpp:17-31): message 'line L, col C: ...'."""
     code = _lib.BMQ_ERR_QASM
+
+    def __init__(self, msg):
+        super().__init__(msg)
+        import re
+        m = re.match(r"line (\d+), col (\d+): ", msg)
+        self.line = int(m.group(1)) if m else 0
+        self.col = int(m.group(2)) if m else 0
 
 
 class CudaError(BmqError):
@@ -273,6 +281,35 @@ def generate_benchmark(bench, n: int, params: BenchmarkParams | None = None) -> 
     c = Circuit(n)
     c.gates = [_gate_from_c(arr[i]) for i in range(count.value)]
     return c
+
+
+def parse_qasm(text: str, warnings: list | None = None) -> Circuit:
+    """parse_qasm (qasm.hpp:387-389): OPENQASM 2.0 subset, parsed by libbmq's host C++."""
+    data = text.encode()
+    nq, count, nw = C.c_uint32(), C.c_uint64(), C.c_uint64()
+    wbuf = C.create_string_buffer(4096)
+    rc = lib.bmq_parse_qasm(data, C.byref(nq), None, 0, C.byref(count), wbuf, 4096, C.byref(nw))
+    if rc and rc != _lib.BMQ_ERR_BUFFER_TOO_SMALL:
+        _check(rc)
+    arr = (bmq_gate * max(1, count.value))()
+    _check(lib.bmq_parse_qasm(data, C.byref(nq), arr, count.value, C.byref(count), wbuf, 4096, C.byref(nw)))
+    if warnings is not None and nw.value:
+        warnings.extend(wbuf.value.decode().split("\n"))
+    c = Circuit(nq.value)
+    c.gates = [_gate_from_c(arr[i]) for i in range(count.value)]
+    return c
+
+
+def emit_qasm(circuit: Circuit) -> str:
+    """emit_qasm (qasm.hpp:392-411)."""
+    size = C.c_uint64()
+    rc = lib.bmq_emit_qasm(circuit.num_qubits, circuit.c_array(), len(circuit.gates), None, 0, C.byref(size))
+    if rc and rc != _lib.BMQ_ERR_BUFFER_TOO_SMALL:
+        _check(rc)
+    buf = C.create_string_buffer(size.value + 1)
+    _check(lib.bmq_emit_qasm(circuit.num_qubits, circuit.c_array(), len(circuit.gates), buf, size.value + 1,
+                             C.byref(size)))
+    return buf.value.decode()
 
 
 # ------------------------------------------------------------- partition

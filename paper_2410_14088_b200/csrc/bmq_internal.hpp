@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "bmq.h"
@@ -85,5 +86,14 @@ const CodecTables& host_tables(double b_r);
 
 // ------------------------------------------------------------------- stats
 uint64_t compress_bound(uint64_t n);
+
+// -------------------------------------------------------------------- qasm
+struct QasmCircuit {
+    uint32_t num_qubits = 0;
+    std::vector<bmq_gate> gates;
+    std::vector<std::string> warnings;
+};
+QasmCircuit parse_qasm_text(std::string_view text);
+std::string emit_qasm_text(uint32_t n, const bmq_gate* gates, uint64_t count);
 
 }  // namespace bmq

@@ -130,6 +130,36 @@ int bmq_buffer_bit_of_qubit(uint32_t num_qubits, uint32_t block_bits, const bmq_
     });
 }
 
+int bmq_parse_qasm(const char* text, uint32_t* num_qubits, bmq_gate* out, uint64_t cap, uint64_t* count,
+                   char* warnings, uint64_t warnings_cap, uint64_t* num_warnings) {
+    return guarded([&] {
+        null_check(text, "text");
+        const bmq::QasmCircuit c = bmq::parse_qasm_text(text);
+        *num_qubits = c.num_qubits;
+        *count = c.gates.size();
+        if (num_warnings) *num_warnings = c.warnings.size();
+        if (warnings && warnings_cap) {
+            std::string joined;
+            for (size_t i = 0; i < c.warnings.size(); ++i) joined += (i ? "\n" : "") + c.warnings[i];
+            const size_t n = std::min<size_t>(joined.size(), warnings_cap - 1);
+            std::memcpy(warnings, joined.data(), n);
+            warnings[n] = 0;
+        }
+        if (c.gates.size() > cap) bmq::raise(BMQ_ERR_BUFFER_TOO_SMALL, "gate buffer too small");
+        std::memcpy(out, c.gates.data(), c.gates.size() * sizeof(bmq_gate));
+    });
+}
+
+int bmq_emit_qasm(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, char* out, uint64_t cap,
+                  uint64_t* size) {
+    return guarded([&] {
+        const std::string s = bmq::emit_qasm_text(num_qubits, gates, count);
+        *size = s.size();
+        if (s.size() + 1 > cap) bmq::raise(BMQ_ERR_BUFFER_TOO_SMALL, "text buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
+    });
+}
+
 uint64_t bmq_compress_bound(uint64_t scalar_count) { return bmq::compress_bound(scalar_count); }
 
 int bmq_compress_blocks(const double* scalars, uint64_t nblocks, uint64_t scalars_per_block, double error_bound,
