@@ -85,6 +85,11 @@ typedef struct bmq_config {
     uint64_t work_bytes;         /* dense group working set; 0 = automatic */
     uint32_t flags;              /* BMQ_FLAG_* */
     uint32_t reserved;
+    /* Second level of the two-level store (store.hpp:47-300): pinned host
+     * memory that receives payloads when the device arena is full (0 = no
+     * host level: a full device arena is a StoreError). Device kernels read
+     * and write it directly through the mapped address. */
+    uint64_t host_pool_bytes;
 } bmq_config;
 
 /* Skip groups whose blocks are all ALL_ZERO (bit-exact: linear gates map
@@ -134,6 +139,8 @@ typedef struct bmq_report {
     uint64_t compress_bytes;        /* 16 B per amplitude read + payload bytes written */
     uint64_t fused_batches;         /* batches whose last gate pass quantised in place */
     uint64_t compactions;           /* payload arena compactions */
+    uint64_t host_spill_bytes;      /* payload bytes placed in the pinned host arena */
+    uint64_t host_spill_batches;    /* batches whose payloads went to the host arena */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

@@ -43,7 +43,8 @@ class bmq_config(C.Structure):
     _fields_ = [("block_bits", C.c_uint32), ("inner_size", C.c_uint32), ("error_bound", C.c_double),
                 ("memory_budget", C.c_uint64), ("workers", C.c_uint32), ("compress", C.c_uint32),
                 ("verify_cap_qubits", C.c_uint32), ("device", C.c_int32), ("device_pool_bytes", C.c_uint64),
-                ("work_bytes", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32)]
+                ("work_bytes", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32),
+                ("host_pool_bytes", C.c_uint64)]
 
 
 class bmq_report(C.Structure):
@@ -59,7 +60,8 @@ class bmq_report(C.Structure):
                 ("kernel_launches", C.c_uint64), ("device_peak_bytes", C.c_uint64), ("gate_passes", C.c_uint64),
                 ("decompress_ms", C.c_double), ("gate_ms", C.c_double), ("compress_ms", C.c_double),
                 ("batches", C.c_uint64), ("decompress_bytes", C.c_uint64), ("gate_bytes", C.c_uint64),
-                ("compress_bytes", C.c_uint64), ("fused_batches", C.c_uint64), ("compactions", C.c_uint64)]
+                ("compress_bytes", C.c_uint64), ("fused_batches", C.c_uint64), ("compactions", C.c_uint64),
+                ("host_spill_bytes", C.c_uint64), ("host_spill_batches", C.c_uint64)]
 
 
 _P = C.c_void_p

@@ -571,6 +571,7 @@ class Config:
     work_bytes: int = 0
     zero_group_skip: bool = True
     identity_skip: bool = False
+    host_pool_bytes: int = 0
 
     def to_c(self) -> bmq_config:
         c = bmq_config()
@@ -579,6 +580,7 @@ class Config:
         c.memory_budget, c.workers, c.compress = self.memory_budget, self.workers, int(self.compress)
         c.verify_cap_qubits, c.device = self.verify_cap_qubits, self.device
         c.device_pool_bytes, c.work_bytes = self.device_pool_bytes, self.work_bytes
+        c.host_pool_bytes = self.host_pool_bytes
         c.flags = (_lib.BMQ_FLAG_ZERO_GROUP_SKIP if self.zero_group_skip else 0) | \
                   (_lib.BMQ_FLAG_IDENTITY_SKIP if self.identity_skip else 0)
         return c
@@ -654,7 +656,8 @@ class Simulator:
                                            "payload_bytes_read", "payload_bytes_written", "dense_bytes",
                                            "kernel_launches", "device_peak_bytes", "gate_passes", "decompress_ms",
                                            "gate_ms", "compress_ms", "batches", "decompress_bytes",
-                                           "gate_bytes", "compress_bytes", "fused_batches", "compactions")}
+                                           "gate_bytes", "compress_bytes", "fused_batches", "compactions",
+                                           "host_spill_bytes", "host_spill_batches")}
         return SimulationReport(r.qubits, r.gate_count, r.stage_count, r.max_footprint_bytes, r.standard_bytes,
                                 r.compression_ratio, r.spilled_blocks, r.wall_ms, stage_ms[: r.stage_count].tolist(),
                                 r.fidelity if r.has_fidelity else None, r.final_norm, r.stage_compress_calls,

@@ -24,7 +24,8 @@ void launch_compress_plan(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk
 void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
                           const DevTables& t, uint8_t* out, uint64_t out_cap, uint64_t* d_cursor, uint64_t* d_range,
                           BlockPlan* d_bp, ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size,
-                          bool virtual_zero, uint32_t align, DevError* d_err, uint64_t* launches);
+                          bool virtual_zero, uint32_t align, DevError* d_err, uint64_t* launches,
+                          uint64_t meta_base = 0, uint64_t meta_tag = 0);
 
 // Decompress nblk payloads into their planar output buffers.
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,

@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(kAllocThreads) k_cmp_alloc(const CmpBlock* __r
                                                              BlockPlan* __restrict__ bps, uint64_t* cursor,
                                                              uint64_t cap, uint64_t* range, int virtual_zero,
                                                              uint32_t align, uint64_t* meta_off,
-                                                             uint64_t* meta_size, DevError* err) {
+                                                             uint64_t* meta_size, uint64_t meta_base,
+                                                             uint64_t meta_tag, DevError* err) {
     using Scan = cub::BlockScan<unsigned long long, kAllocThreads>;
     using Reduce = cub::BlockReduce<unsigned long long, kAllocThreads>;
     __shared__ typename Scan::TempStorage ss;
@@ -316,9 +317,9 @@ __global__ void __launch_bounds__(kAllocThreads) k_cmp_alloc(const CmpBlock* __r
             BlockPlan& p = bps[i];
             const bool virt = virtual_zero && (p.flags & 1);
             p.out_off = virt ? ~0ull : start + carry + pre;
-            if (meta_off) {
+            if (meta_off) {  // metadata may point into another arena (staged host spill)
                 const uint64_t id = blks[i].id;
-                meta_off[id] = p.out_off;
+                meta_off[id] = virt ? ~0ull : ((meta_base + p.out_off) | meta_tag);
                 meta_size[id] = p.size;
             }
         }
@@ -483,10 +484,11 @@ void launch_compress_plan(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk
 void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
                           const DevTables& t, uint8_t* out, uint64_t out_cap, uint64_t* d_cursor, uint64_t* d_range,
                           BlockPlan* d_bp, ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size,
-                          bool virtual_zero, uint32_t align, DevError* d_err, uint64_t* launches) {
+                          bool virtual_zero, uint32_t align, DevError* d_err, uint64_t* launches,
+                          uint64_t meta_base, uint64_t meta_tag) {
     if (nblk == 0) return;
     k_cmp_alloc<<<1, kAllocThreads, 0, st>>>(d_blks, nblk, d_bp, d_cursor, out_cap, d_range, virtual_zero ? 1 : 0,
-                                             align, meta_off, meta_size, d_err);
+                                             align, meta_off, meta_size, meta_base, meta_tag, d_err);
     k_zero_range<<<296, 256, 0, st>>>(out, d_range);
     k_cmp_emit<<<static_cast<uint32_t>(nblk * nch_max), kChunkThreads, 0, st>>>(d_blks, nch_max, d_cp, d_bp, out, t,
                                                                                  d_err);

@@ -84,6 +84,7 @@ void StoreModel::put_shared(uint64_t first, uint64_t last, uint64_t size) {  // 
 namespace {
 
 constexpr uint32_t kArenaAlign = 16;
+constexpr uint64_t kHostTag = 1ull << 62;  // payload offset refers to the pinned host arena
 
 __global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t zero_size) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -93,8 +94,9 @@ __global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t 
 }
 
 __global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, const uint64_t* __restrict__ off,
-                             const uint64_t* __restrict__ size, const uint8_t* pool, const uint8_t* zero_hdr,
-                             double* work, uint32_t* pk, uint32_t b, DecBlock* dec, CmpBlock* cmp) {
+                             const uint64_t* __restrict__ size, const uint8_t* pool, const uint8_t* host_pool,
+                             const uint8_t* zero_hdr, double* work, uint32_t* pk, uint32_t b, DecBlock* dec,
+                             CmpBlock* cmp) {
     const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (i >= nblk) return;
     const uint64_t id = ids[i];
@@ -102,7 +104,7 @@ __global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, co
     double* slot = work + i * count;
     const uint64_t o = off[id];
     DecBlock d;
-    d.in = o == ~0ull ? zero_hdr : pool + o;
+    d.in = o == ~0ull ? zero_hdr : ((o & kHostTag) ? host_pool + (o & ~kHostTag) : pool + o);
     d.size = o == ~0ull ? kHeaderBytes : size[id];
     d.out = slot;
     d.expect_count = count;
@@ -346,7 +348,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     size_.alloc(nid);
     sums_.alloc(3 * nid);
     err_.alloc(1);
-    cursor_.alloc(4);
+    cursor_.alloc(8);
     red_.alloc(2 * 148 * 64);
     BMQ_CUDA(cudaMemset(err_.p, 0, sizeof(DevError)));
     BMQ_CUDA(cudaMemset(cursor_.p, 0, 4 * sizeof(uint64_t)));
@@ -420,6 +422,7 @@ Engine::~Engine() {
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     for (cudaEvent_t e : phase_ev_) cudaEventDestroy(e);
+    if (host_pool_) cudaFreeHost(host_pool_);
 }
 
 uint32_t Engine::peek_error() {
@@ -449,7 +452,7 @@ void Engine::compact() {
     sync_meta_to_host();
     std::vector<uint64_t> live;
     for (uint64_t id = 0; id < h_off_.size(); ++id)
-        if (h_off_[id] != ~0ull) live.push_back(id);
+        if (h_off_[id] != ~0ull && !(h_off_[id] & kHostTag)) live.push_back(id);  // device payloads only
     const int nxt = 1 - cur_;
     if (live.empty()) {
         BMQ_CUDA(cudaMemsetAsync(cursor_.p + nxt, 0, 8, st_));
@@ -472,6 +475,7 @@ void Engine::init_state() {
     const uint64_t nid = L_.num_blocks();
     const double one = 1.0;
     store_.reset(nid, cfg_.memory_budget);
+    host_cursor_ = 0;
     BMQ_CUDA(cudaMemsetAsync(sums_.p, 0, sums_.bytes(), st_));
     if (!cfg_.compress) {
         const uint64_t raw = 16ull << L_.b;
@@ -563,25 +567,57 @@ void Engine::raw_run_stage(uint64_t s) {
 // alloc + zero + emit for the batch in flight; on a full arena, compact and
 // allocate again (the plan and the packed codes are still in place).
 void Engine::emit_batch(uint64_t nblk) {
-    for (int attempt = 0;; ++attempt) {
+    bool placed = false;
+    for (int attempt = 0; attempt < 2 && !placed; ++attempt) {
         launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, pool_[cur_].p, pool_cap_, cursor_.p + cur_,
                              cursor_.p + 2, bplan_.p, cplan_.p, off_.p, size_.p, true, kArenaAlign, err_.p,
                              &counters_.kernel_launches);
         const uint32_t code = peek_error();
-        if (code != DE_POOL_FULL) break;
+        placed = code != DE_POOL_FULL;
+        if (placed) break;
         BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
-        if (attempt > 0) raise(BMQ_ERR_STORE, "device payload pool exhausted");
-        compact();
+        if (attempt == 0) compact();
+    }
+    if (!placed) {
+        // Second level: emit into the (now dead) dense work buffer, then move
+        // the batch's payloads to the pinned host arena in one copy.
+        if (!cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+        ensure_host_pool();
+        BMQ_CUDA(cudaMemsetAsync(cursor_.p + 4, 0, 8, st_));
+        uint8_t* staging = reinterpret_cast<uint8_t*>(work_.p);
+        launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, staging, work_.bytes() - 64, cursor_.p + 4,
+                             cursor_.p + 2, bplan_.p, cplan_.p, off_.p, size_.p, true, kArenaAlign, err_.p,
+                             &counters_.kernel_launches, host_cursor_, kHostTag);
+        if (peek_error() == DE_POOL_FULL) {
+            BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
+            raise(BMQ_ERR_STORE, "payload batch exceeds the staging buffer");
+        }
+        uint64_t total = 0;
+        BMQ_CUDA(cudaMemcpyAsync(&total, cursor_.p + 4, 8, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        if (host_cursor_ + total > host_cap_) raise(BMQ_ERR_STORE, "host payload pool exhausted");
+        BMQ_CUDA(cudaMemcpyAsync(host_pool_ + host_cursor_, staging, total, cudaMemcpyDeviceToHost, st_));
+        host_cursor_ += total;
+        counters_.host_spill_bytes += total;
+        ++counters_.host_spill_batches;
     }
     k_store_cmp_sums<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, cmp_.p, nblk, sums_.p);
     ++counters_.kernel_launches;
 }
 
+void Engine::ensure_host_pool() {
+    if (host_pool_) return;
+    host_cap_ = cfg_.host_pool_bytes;
+    BMQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool_), host_cap_ + 64,
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    host_cursor_ = 0;
+}
+
 void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk,
                            size_t bidx) {
     phase_event(4 * bidx);
-    k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_.p, size_.p, pool_[cur_].p, zero_hdr_.p, work_.p,
-                                                  pk_.p, L_.b, dec_.p, cmp_.p);
+    k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_.p, size_.p, pool_[cur_].p, host_pool_,
+                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p);
     ++counters_.kernel_launches;
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
                       &counters_.kernel_launches);
@@ -738,6 +774,8 @@ void Engine::run(bmq_report* rep, double* stage_ms, uint64_t stage_cap) {
     r.compress_bytes = counters_.compress_bytes;
     r.fused_batches = counters_.fused_batches;
     r.compactions = counters_.compactions;
+    r.host_spill_bytes = counters_.host_spill_bytes;
+    r.host_spill_batches = counters_.host_spill_batches;
     *rep = r;
 }
 
@@ -762,8 +800,8 @@ void Engine::host_ids_to_device(const std::vector<uint64_t>& ids) {
 }
 
 void Engine::decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums) {
-    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_.p, size_.p, pool_[cur_].p, zero_hdr_.p, work_.p,
-                                                  pk_.p, L_.b, dec_.p, cmp_.p);
+    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_.p, size_.p, pool_[cur_].p, host_pool_,
+                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p);
     launch_decompress(st_, dec_.p, nids, nch_, *tabs_, dinfo_.p, dchunk_.p, true, want_sums, err_.p,
                       &counters_.kernel_launches);
 }
@@ -850,8 +888,13 @@ uint64_t Engine::get_payload(uint64_t id, uint8_t* out, uint64_t cap) {
     if (h_off_[id] == ~0ull) return zero_payload(out, cap);
     const uint64_t size = h_size_[id];
     if (out && cap >= size) {
-        BMQ_CUDA(cudaMemcpyAsync(out, pool_[cur_].p + h_off_[id], size, cudaMemcpyDeviceToHost, st_));
-        BMQ_CUDA(cudaStreamSynchronize(st_));
+        if (h_off_[id] & kHostTag) {
+            BMQ_CUDA(cudaStreamSynchronize(st_));
+            std::memcpy(out, host_pool_ + (h_off_[id] & ~kHostTag), size);
+        } else {
+            BMQ_CUDA(cudaMemcpyAsync(out, pool_[cur_].p + h_off_[id], size, cudaMemcpyDeviceToHost, st_));
+            BMQ_CUDA(cudaStreamSynchronize(st_));
+        }
     }
     return size;
 }
@@ -889,6 +932,9 @@ void Engine::get_payloads(uint8_t* out, uint64_t cap, uint64_t* sizes, uint64_t*
     for (uint64_t id = 0; id < nid; ++id) {
         if (h_off_[id] == ~0ull) {
             pos += zero_payload(out + pos, kHeaderBytes);
+        } else if (h_off_[id] & kHostTag) {
+            std::memcpy(out + pos, host_pool_ + (h_off_[id] & ~kHostTag), h_size_[id]);
+            pos += h_size_[id];
         } else {
             std::memcpy(out + pos, host.data() + h_off_[id], h_size_[id]);
             pos += h_size_[id];

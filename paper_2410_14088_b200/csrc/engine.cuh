@@ -116,7 +116,12 @@ private:
     DevArray<uint8_t> pool_[2];
     uint64_t pool_cap_ = 0;
     int cur_ = 0;
-    DevArray<uint64_t> cursor_;  // [0..1] arena cursors, [2..3] range scratch
+    DevArray<uint64_t> cursor_;  // [0..1] arena cursors, [2..3] range scratch, [4] staging cursor
+    // second level: pinned, mapped host arena (payload offsets tagged with
+    // kHostTag), allocated on the first spill; append-only this round
+    uint8_t* host_pool_ = nullptr;
+    uint64_t host_cap_ = 0, host_cursor_ = 0;
+    void ensure_host_pool();
     DevArray<uint64_t> off_, size_, new_off_, live_ids_;
     DevArray<double> sums_;       // per id: sumsq, sum_re, sum_im (3 doubles)
     DevArray<uint8_t> zero_hdr_;  // canonical ALL_ZERO payload (+ slack)

@@ -124,6 +124,30 @@ def test_arena_compaction_is_exact(gpu, port):
         assert sim.payloads() == want.payloads
 
 
+def test_host_spill_is_exact(gpu, port):
+    """Two-level store (store.hpp:47-300): with a device arena far smaller than
+    the live state, payloads land in the pinned host arena and are read back
+    from there by the next stage; the result is unchanged byte for byte."""
+    c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=2))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    biggest = max(len(p) for p in want.payloads)
+    pool = 6 * (biggest + 16)  # about one batch: most payloads must go to the host
+    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, work_bytes=4 * (16 << 12),
+                     host_pool_bytes=64 << 20)
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run()
+        assert rep.device["host_spill_batches"] > 0
+        assert rep.device["host_spill_bytes"] > 0
+        assert sim.payloads() == want.payloads
+        for i in (0, 3, 15):
+            assert sim.get_payload(i) == want.payloads[i]
+        assert abs(sim.state_norm() - want.report["final_norm"]) <= NORM_RTOL * want.report["final_norm"]
+    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, work_bytes=4 * (16 << 12))
+    with gpu.Simulator(c, cfg) as sim:
+        with pytest.raises(gpu.StoreError):
+            sim.run()
+
+
 def test_small_batches_are_exact(gpu, port):
     c = gpu.generate_benchmark("qaoa", 14, gpu.BenchmarkParams(layers=2))
     want = port.simulate(14, [g.as_tuple() for g in c.gates], 9, 2, 1e-3)
