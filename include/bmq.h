@@ -266,6 +266,40 @@ int bmq_simulator_fidelity(bmq_simulator* a, bmq_simulator* b, double* fidelity)
  * (QFT of |0>), 1 = GHZ (|0..0> + |1..1>)/sqrt 2. */
 int bmq_simulator_fidelity_analytic(bmq_simulator* sim, int ideal_kind, double* fidelity);
 
+/* ---- sharded runs (one simulator per rank) ----
+ * The reference runs one process (engine.hpp:97-134); these entry points let a
+ * shard driver (paper_2410_14088_b200/shard.py) spread its stage loop over
+ * `world` ranks. Stage s's groups belong to the rank whose bits are the values
+ * of log2(world) "device qubits" (outer qubits of s); payloads whose owner
+ * changes between stages move through the driver's collective. */
+
+/* Device qubits of every stage: device_qubits[s * log2(world) + j] is the
+ * qubit whose value is bit j of the owning rank. Host-only. */
+int bmq_shard_plan(uint32_t num_qubits, uint32_t block_bits, const bmq_stage* stages, uint64_t num_stages,
+                   uint32_t world, uint32_t* device_qubits);
+/* Make `sim` rank `rank` of `world` (before the state is initialized).
+ * run() is then refused: drive stages with run_stages + export/import. */
+int bmq_simulator_shard(bmq_simulator* sim, uint32_t rank, uint32_t world);
+/* meta[4 i .. 4 i + 3] = {payload size (0 = ALL_ZERO, no bytes), then the
+ * block's sum |a|^2, sum re, sum im as f64 bit patterns}. With dst != NULL
+ * (device or host memory, 16-byte aligned) the payloads are packed at
+ * 16-byte aligned offsets in id-list order; cap >= sum of rounded sizes. */
+int bmq_simulator_export(bmq_simulator* sim, const uint64_t* ids, uint64_t n, uint64_t* meta, void* dst,
+                         uint64_t cap);
+/* Store payloads packed as by export (src device or host memory). */
+int bmq_simulator_import(bmq_simulator* sim, const uint64_t* ids, uint64_t n, const uint64_t* meta,
+                         const void* src);
+/* Forget payloads (the ids become ALL_ZERO with zero sums). */
+int bmq_simulator_drop(bmq_simulator* sim, const uint64_t* ids, uint64_t n);
+/* sizes[id] = payload size of every id this rank owns under stage s, else 0. */
+int bmq_simulator_stage_sizes(bmq_simulator* sim, uint64_t stage, uint64_t* sizes);
+/* Replay BlockStore::put of stage s (store.hpp:64-83) with global sizes. */
+int bmq_simulator_account_stage(bmq_simulator* sim, uint64_t stage, const uint64_t* sizes);
+/* {sum |a|^2, sum re, sum im} over the blocks this rank holds. */
+int bmq_simulator_partial_sums(bmq_simulator* sim, double* sums3);
+/* Report of the stages run so far (final_norm, wall_ms, device_ms = 0). */
+int bmq_simulator_report(bmq_simulator* sim, bmq_report* report);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,15 @@ SIGNATURES = {
     "bmq_simulator_fidelity_dense": (C.c_int, [_P, _P, _U64, C.POINTER(_D)]),
     "bmq_simulator_fidelity": (C.c_int, [_P, _P, C.POINTER(_D)]),
     "bmq_simulator_fidelity_analytic": (C.c_int, [_P, C.c_int, C.POINTER(_D)]),
+    "bmq_shard_plan": (C.c_int, [C.c_uint32, C.c_uint32, C.POINTER(bmq_stage), _U64, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "bmq_simulator_shard": (C.c_int, [_P, C.c_uint32, C.c_uint32]),
+    "bmq_simulator_export": (C.c_int, [_P, C.POINTER(_U64), _U64, C.POINTER(_U64), C.c_void_p, _U64]),
+    "bmq_simulator_import": (C.c_int, [_P, C.POINTER(_U64), _U64, C.POINTER(_U64), C.c_void_p]),
+    "bmq_simulator_drop": (C.c_int, [_P, C.POINTER(_U64), _U64]),
+    "bmq_simulator_stage_sizes": (C.c_int, [_P, _U64, C.POINTER(_U64)]),
+    "bmq_simulator_account_stage": (C.c_int, [_P, _U64, C.POINTER(_U64)]),
+    "bmq_simulator_partial_sums": (C.c_int, [_P, C.POINTER(_D)]),
+    "bmq_simulator_report": (C.c_int, [_P, C.POINTER(bmq_report)]),
 }
 
 

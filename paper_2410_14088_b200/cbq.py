@@ -605,6 +605,21 @@ class SimulationReport:
     device: dict = field(default_factory=dict)
 
 
+DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks_processed",
+                      "payload_bytes_read", "payload_bytes_written", "dense_bytes", "kernel_launches",
+                      "device_peak_bytes", "gate_passes", "decompress_ms", "gate_ms", "compress_ms", "batches",
+                      "decompress_bytes", "gate_bytes", "compress_bytes", "fused_batches", "compactions",
+                      "host_spill_bytes", "host_spill_batches")
+
+
+def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:
+    dev = {k: getattr(r, k) for k in DEVICE_REPORT_KEYS}
+    return SimulationReport(r.qubits, r.gate_count, r.stage_count, r.max_footprint_bytes, r.standard_bytes,
+                            r.compression_ratio, r.spilled_blocks, r.wall_ms, stage_ms,
+                            r.fidelity if r.has_fidelity else None, r.final_norm, r.stage_compress_calls,
+                            r.stage_decompress_calls, dev)
+
+
 class Simulator:
     """cbq::Simulator (engine.hpp:58-250) running on one B200."""
 
@@ -652,16 +667,7 @@ class Simulator:
         nst = max(1, len(self.circuit.gates))
         stage_ms = np.zeros(nst)
         _check(lib.bmq_simulator_run(self._h, C.byref(r), _ptr(stage_ms), nst))
-        dev = {k: getattr(r, k) for k in ("device_ms", "groups_processed", "groups_skipped", "blocks_processed",
-                                           "payload_bytes_read", "payload_bytes_written", "dense_bytes",
-                                           "kernel_launches", "device_peak_bytes", "gate_passes", "decompress_ms",
-                                           "gate_ms", "compress_ms", "batches", "decompress_bytes",
-                                           "gate_bytes", "compress_bytes", "fused_batches", "compactions",
-                                           "host_spill_bytes", "host_spill_batches")}
-        return SimulationReport(r.qubits, r.gate_count, r.stage_count, r.max_footprint_bytes, r.standard_bytes,
-                                r.compression_ratio, r.spilled_blocks, r.wall_ms, stage_ms[: r.stage_count].tolist(),
-                                r.fidelity if r.has_fidelity else None, r.final_norm, r.stage_compress_calls,
-                                r.stage_decompress_calls, dev)
+        return report_from_c(r, stage_ms[: r.stage_count].tolist())
 
     def reset(self) -> None:
         """Drop the state; the next run() starts from |0...0> again."""

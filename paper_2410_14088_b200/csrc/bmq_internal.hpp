@@ -52,6 +52,14 @@ struct GroupGeometry {
     uint64_t block_id(uint64_t outer, uint64_t v) const;
 };
 GroupGeometry group_geometry(const Layout& L, const bmq_stage& st);
+
+// Device bits (block-id bit positions, log2(world) per stage) of a sharded run.
+std::vector<uint32_t> shard_plan(const Layout& L, const std::vector<bmq_stage>& plan, uint32_t world);
+inline uint32_t shard_owner(uint64_t id, const uint32_t* bits, uint32_t m) {
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < m; ++j) r |= static_cast<uint32_t>(id >> bits[j] & 1) << j;
+    return r;
+}
 uint32_t buffer_bit(const Layout& L, const bmq_stage& st, uint32_t q);
 
 inline uint64_t deposit_bits(uint64_t x, uint64_t mask) {

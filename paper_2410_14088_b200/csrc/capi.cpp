@@ -326,4 +326,78 @@ int bmq_simulator_fidelity_analytic(bmq_simulator* sim, int ideal_kind, double* 
     });
 }
 
+int bmq_shard_plan(uint32_t num_qubits, uint32_t block_bits, const bmq_stage* stages, uint64_t num_stages,
+                   uint32_t world, uint32_t* device_qubits) {
+    return guarded([&] {
+        const bmq::Layout L = bmq::make_layout(num_qubits, block_bits);
+        std::vector<bmq_stage> plan(stages, stages + num_stages);
+        for (const bmq_stage& st : plan) {
+            if (st.inner_count > 64) bmq::raise(BMQ_ERR_INVALID_ARGUMENT, "stage has too many inner qubits");
+            for (uint32_t i = 0; i < st.inner_count; ++i)
+                if (st.inner[i] < L.b || st.inner[i] >= L.n)
+                    bmq::raise(BMQ_ERR_INVALID_ARGUMENT, "inner qubit is not a global qubit");
+        }
+        const auto bits = bmq::shard_plan(L, plan, world);
+        for (size_t i = 0; i < bits.size(); ++i) device_qubits[i] = bits[i] + L.b;
+    });
+}
+
+int bmq_simulator_shard(bmq_simulator* sim, uint32_t rank, uint32_t world) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->shard(rank, world);
+    });
+}
+
+int bmq_simulator_export(bmq_simulator* sim, const uint64_t* ids, uint64_t n, uint64_t* meta, void* dst,
+                         uint64_t cap) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->export_payloads(ids, n, meta, dst, cap);
+    });
+}
+
+int bmq_simulator_import(bmq_simulator* sim, const uint64_t* ids, uint64_t n, const uint64_t* meta,
+                         const void* src) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->import_payloads(ids, n, meta, src);
+    });
+}
+
+int bmq_simulator_drop(bmq_simulator* sim, const uint64_t* ids, uint64_t n) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->drop_payloads(ids, n);
+    });
+}
+
+int bmq_simulator_stage_sizes(bmq_simulator* sim, uint64_t stage, uint64_t* sizes) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->stage_sizes(stage, sizes);
+    });
+}
+
+int bmq_simulator_account_stage(bmq_simulator* sim, uint64_t stage, const uint64_t* sizes) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->account_stage(stage, sizes);
+    });
+}
+
+int bmq_simulator_partial_sums(bmq_simulator* sim, double* sums3) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->partial_sums(sums3);
+    });
+}
+
+int bmq_simulator_report(bmq_simulator* sim, bmq_report* report) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->report(report, 0.0);
+    });
+}
+
 }  // extern "C"

@@ -166,6 +166,55 @@ __global__ void k_compact_copy(const uint64_t* __restrict__ ids, uint64_t n, uin
     }
 }
 
+// Shard transfers: one CTA per payload, 16-byte words (arena payloads and
+// transfer slots are 16-byte aligned; sizes are rounded up to whole words).
+struct Xfer {
+    uint64_t id, xoff, size;  // xoff: offset in the transfer buffer
+    uint64_t dst;             // import: arena offset (tag included)
+    double sums[3];
+};
+
+__global__ void k_pack_payloads(const Xfer* __restrict__ xs, uint64_t n, const uint64_t* __restrict__ off,
+                                const uint8_t* pool, const uint8_t* host_pool, uint8_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const Xfer x = xs[i];
+        if (!x.size) continue;
+        const uint64_t o = off[x.id];
+        const uint4* s = reinterpret_cast<const uint4*>((o & kHostTag) ? host_pool + (o & ~kHostTag) : pool + o);
+        uint4* d = reinterpret_cast<uint4*>(out + x.xoff);
+        const uint64_t words = (x.size + 15) / 16;
+        for (uint64_t w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
+    }
+}
+
+__global__ void k_unpack_payloads(const Xfer* __restrict__ xs, uint64_t n, const uint8_t* __restrict__ in,
+                                  uint8_t* to, uint64_t tag, uint64_t* off, uint64_t* size, double* sums) {
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const Xfer x = xs[i];
+        if (x.size) {
+            const uint4* s = reinterpret_cast<const uint4*>(in + x.xoff);
+            uint4* d = reinterpret_cast<uint4*>(to + x.dst);
+            const uint64_t words = (x.size + 15) / 16;
+            for (uint64_t w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
+        }
+        if (threadIdx.x == 0) {
+            off[x.id] = x.size ? (x.dst | tag) : ~0ull;
+            size[x.id] = x.size ? x.size : kHeaderBytes;
+            for (int k = 0; k < 3; ++k) sums[3 * x.id + k] = x.sums[k];
+        }
+    }
+}
+
+__global__ void k_drop_payloads(const uint64_t* __restrict__ ids, uint64_t n, uint64_t* off, uint64_t* size,
+                                double* sums) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t id = ids[i];
+    off[id] = ~0ull;
+    size[id] = kHeaderBytes;
+    sums[3 * id] = sums[3 * id + 1] = sums[3 * id + 2] = 0.0;
+}
+
 // planar blocks [re(2^b) | im(2^b)] -> interleaved complex
 __global__ void k_interleave(const double* __restrict__ planar, uint64_t nblk, uint32_t b, double* __restrict__ out) {
     const uint64_t total = nblk << b;
@@ -506,6 +555,10 @@ void Engine::init_state() {
     if (nid > 1) store_.put_shared(1, nid, kHeaderBytes);  // one zero payload, counted once
     initialized_ = true;
     next_stage_ = 0;
+    if (sharded() && owner(0, 0) != shard_rank_) {
+        const uint64_t id0 = 0;
+        drop_payloads(&id0, 1);
+    }
 }
 
 void Engine::ensure_init() {
@@ -651,8 +704,13 @@ void Engine::run_stage(uint64_t s) {
     std::vector<uint64_t> work_ids;
     std::vector<uint32_t> work_v;
     work_ids.reserve(nid);
-    uint64_t o = 0, groups_done = 0;
+    uint64_t o = 0, groups_done = 0, groups_owned = 0;
     for (uint64_t g = 0; g < ngroups; ++g) {
+        if (sharded() && owner(o, s) != shard_rank_) {  // device bits are outer bits: o decides
+            o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
+            continue;
+        }
+        ++groups_owned;
         if (blockwise) {
             bool any = false;
             for (uint64_t v = 0; v < per; ++v) {
@@ -691,12 +749,9 @@ void Engine::run_stage(uint64_t s) {
     check_device_error(("stage " + std::to_string(s) + ": ").c_str());
     sync_meta_to_host();
     collect_phase_times(nbatches);
-    // accounting replay in the reference put order (groups ascending)
-    o = 0;
-    for (uint64_t g = 0; g < ngroups; ++g) {
-        for (uint64_t v : inner) store_.put(o | v, h_size_[o | v]);
-        o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
-    }
+    // accounting replay in the reference put order (groups ascending); a
+    // sharded run replays the gathered global sizes in account_stage()
+    if (!sharded()) account_stage(s, h_size_.data());
     uint64_t rd = 0, wr = 0;
     for (uint64_t id : work_ids) {
         rd += old_off[id] == ~0ull ? 0 : old_size[id];
@@ -709,7 +764,7 @@ void Engine::run_stage(uint64_t s) {
     counters_.gate_bytes += 2 * half_dense * sp.prog.passes.size();
     counters_.compress_bytes += half_dense + wr;
     counters_.groups_processed += groups_done;
-    counters_.groups_skipped += ngroups - groups_done;
+    counters_.groups_skipped += groups_owned - groups_done;
     counters_.blocks_processed += nwork;
     counters_.dense_bytes += nwork * (32ull << L_.b);
     stage_compress_calls_ += nid;
@@ -729,12 +784,9 @@ void Engine::run_stages(uint64_t first, uint64_t last) {
 
 void Engine::run(bmq_report* rep, double* stage_ms, uint64_t stage_cap) {
     BMQ_CUDA(cudaSetDevice(dev_));
+    if (sharded()) raise(BMQ_ERR_ENGINE, "a sharded simulator is driven stage by stage by its shard driver");
     const double t0 = now_ms();
     ensure_init();
-    bmq_report r{};
-    r.qubits = L_.n;
-    r.gate_count = gates_.size();
-    r.stage_count = plan_.size();
     counters_ = bmq_report{};
     BMQ_CUDA(cudaEventRecord(ev0_, st_));
     for (uint64_t s = next_stage_; s < plan_.size(); ++s) {
@@ -747,15 +799,24 @@ void Engine::run(bmq_report* rep, double* stage_ms, uint64_t stage_cap) {
     BMQ_CUDA(cudaEventSynchronize(ev1_));
     float dms = 0.f;
     BMQ_CUDA(cudaEventElapsedTime(&dms, ev0_, ev1_));
+    report(rep, dms);
+    rep->final_norm = state_norm();
+    rep->wall_ms = now_ms() - t0;
+}
+
+// The report of the stages run so far (final_norm / wall_ms left to the caller).
+void Engine::report(bmq_report* rep, double device_ms) {
+    bmq_report r{};
+    r.qubits = L_.n;
+    r.gate_count = gates_.size();
+    r.stage_count = plan_.size();
+    r.device_ms = device_ms;
     r.max_footprint_bytes = store_.peak();
     r.standard_bytes = std::exp2(static_cast<double>(L_.n + 4));
     r.compression_ratio = r.max_footprint_bytes ? r.standard_bytes / static_cast<double>(r.max_footprint_bytes) : 0.0;
     r.spilled_blocks = store_.spilled_blocks();
     r.stage_compress_calls = stage_compress_calls_;
     r.stage_decompress_calls = stage_decompress_calls_;
-    r.final_norm = state_norm();
-    r.wall_ms = now_ms() - t0;
-    r.device_ms = dms;
     r.groups_processed = counters_.groups_processed;
     r.groups_skipped = counters_.groups_skipped;
     r.blocks_processed = counters_.blocks_processed;
@@ -1085,6 +1146,170 @@ double Engine::fidelity_pair(Engine& a, Engine& b) {
     if (a.cfg_.compress) a.check_device_error("fidelity: ");
     if (b.cfg_.compress) b.check_device_error("fidelity: ");
     return std::hypot(re, im);
+}
+
+// ------------------------------------------------------------ sharded runs
+
+void Engine::shard(uint32_t rank, uint32_t world) {
+    if (initialized_) raise(BMQ_ERR_ENGINE, "shard() must be called before the state is initialized");
+    if (!cfg_.compress) raise(BMQ_ERR_INVALID_ARGUMENT, "sharded runs require compression");
+    dev_bits_ = shard_plan(L_, plan_, world);
+    if (rank >= world) raise(BMQ_ERR_INVALID_ARGUMENT, "shard rank out of range");
+    shard_rank_ = rank;
+    shard_world_ = world;
+    shard_m_ = 0;
+    while ((1u << shard_m_) < world) ++shard_m_;
+}
+
+void Engine::export_payloads(const uint64_t* ids, uint64_t n, uint64_t* meta, void* dst, uint64_t cap) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (!cfg_.compress) raise(BMQ_ERR_INVALID_ARGUMENT, "payload export requires compression");
+    const uint64_t nid = L_.num_blocks();
+    std::vector<double> sums(3 * nid);
+    BMQ_CUDA(cudaMemcpyAsync(sums.data(), sums_.p, sums_.bytes(), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    std::vector<Xfer> xs(n);
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t id = ids[i];
+        if (id >= nid) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(id));
+        const uint64_t size = h_off_[id] == ~0ull ? 0 : h_size_[id];
+        xs[i] = Xfer{id, pos, size, 0, {sums[3 * id], sums[3 * id + 1], sums[3 * id + 2]}};
+        meta[4 * i] = size;
+        std::memcpy(meta + 4 * i + 1, &sums[3 * id], 24);
+        pos += (size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+    }
+    if (!dst || !n) return;
+    if (reinterpret_cast<uintptr_t>(dst) % kArenaAlign) raise(BMQ_ERR_INVALID_ARGUMENT, "transfer buffer must be 16-byte aligned");
+    if (cap < pos) raise(BMQ_ERR_BUFFER_TOO_SMALL, "transfer buffer too small");
+    DevArray<Xfer> dx;
+    dx.alloc(n);
+    BMQ_CUDA(cudaMemcpyAsync(dx.p, xs.data(), n * sizeof(Xfer), cudaMemcpyHostToDevice, st_));
+    k_pack_payloads<<<static_cast<uint32_t>(std::min<uint64_t>(n, 148 * 16)), 256, 0, st_>>>(
+        dx.p, n, off_.p, pool_[cur_].p, host_pool_, static_cast<uint8_t*>(dst));
+    ++counters_.kernel_launches;
+    BMQ_CUDA(cudaGetLastError());
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* meta, const void* src) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (!cfg_.compress) raise(BMQ_ERR_INVALID_ARGUMENT, "payload import requires compression");
+    if (!n) return;
+    const uint64_t nid = L_.num_blocks();
+    if (src && reinterpret_cast<uintptr_t>(src) % kArenaAlign)
+        raise(BMQ_ERR_INVALID_ARGUMENT, "transfer buffer must be 16-byte aligned");
+    std::vector<Xfer> xs(n);
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (ids[i] >= nid) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(ids[i]));
+        Xfer x{ids[i], pos, meta[4 * i], pos, {}};
+        std::memcpy(x.sums, meta + 4 * i + 1, 24);
+        if (x.size && !src) raise(BMQ_ERR_INVALID_ARGUMENT, "payload bytes missing");
+        xs[i] = x;
+        pos += (x.size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+    }
+    // place the batch back to back: device arena (after compaction if
+    // needed), else the pinned host arena
+    uint64_t used = 0;
+    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    if (used + pos > pool_cap_) {
+        compact();
+        BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+    }
+    uint8_t* to = pool_[cur_].p;
+    uint64_t tag = 0, base = used;
+    if (used + pos > pool_cap_) {
+        if (!cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+        ensure_host_pool();
+        if (host_cursor_ + pos > host_cap_) raise(BMQ_ERR_STORE, "host payload pool exhausted");
+        to = host_pool_;
+        tag = kHostTag;
+        base = host_cursor_;
+        host_cursor_ += pos;
+        counters_.host_spill_bytes += pos;
+        ++counters_.host_spill_batches;
+    } else {
+        const uint64_t end = used + pos;
+        BMQ_CUDA(cudaMemcpyAsync(cursor_.p + cur_, &end, 8, cudaMemcpyHostToDevice, st_));
+    }
+    for (Xfer& x : xs) x.dst = base + x.dst;
+    DevArray<Xfer> dx;
+    dx.alloc(n);
+    BMQ_CUDA(cudaMemcpyAsync(dx.p, xs.data(), n * sizeof(Xfer), cudaMemcpyHostToDevice, st_));
+    k_unpack_payloads<<<static_cast<uint32_t>(std::min<uint64_t>(n, 148 * 16)), 256, 0, st_>>>(
+        dx.p, n, static_cast<const uint8_t*>(src), to, tag, off_.p, size_.p, sums_.p);
+    ++counters_.kernel_launches;
+    BMQ_CUDA(cudaGetLastError());
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    for (const Xfer& x : xs) {
+        h_off_[x.id] = x.size ? (x.dst | tag) : ~0ull;
+        h_size_[x.id] = x.size ? x.size : kHeaderBytes;
+    }
+}
+
+void Engine::drop_payloads(const uint64_t* ids, uint64_t n) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    if (!cfg_.compress) raise(BMQ_ERR_INVALID_ARGUMENT, "payload drop requires compression");
+    if (!n) return;
+    const uint64_t nid = L_.num_blocks();
+    for (uint64_t i = 0; i < n; ++i)
+        if (ids[i] >= nid) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(ids[i]));
+    DevArray<uint64_t> d;
+    d.alloc(n);
+    BMQ_CUDA(cudaMemcpyAsync(d.p, ids, n * 8, cudaMemcpyHostToDevice, st_));
+    k_drop_payloads<<<grid_for(n), 256, 0, st_>>>(d.p, n, off_.p, size_.p, sums_.p);
+    ++counters_.kernel_launches;
+    BMQ_CUDA(cudaGetLastError());
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    for (uint64_t i = 0; i < n; ++i) {
+        h_off_[ids[i]] = ~0ull;
+        h_size_[ids[i]] = kHeaderBytes;
+    }
+}
+
+// Sizes of the ids this rank owns under stage s (0 elsewhere), so a sum over
+// ranks yields every id's size.
+void Engine::stage_sizes(uint64_t s, uint64_t* sizes) {
+    if (s >= plan_.size()) raise(BMQ_ERR_INVALID_ARGUMENT, "stage index out of range");
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    for (uint64_t id = 0; id < L_.num_blocks(); ++id)
+        sizes[id] = owner(id, s) == shard_rank_ ? (cfg_.compress ? h_size_[id] : 16ull << L_.b) : 0;
+}
+
+// BlockStore puts of stage s in the reference order (groups ascending,
+// block_ids order; engine.hpp:114-115, store.hpp:64-83).
+void Engine::account_stage(uint64_t s, const uint64_t* sizes) {
+    if (s >= plan_.size()) raise(BMQ_ERR_INVALID_ARGUMENT, "stage index out of range");
+    const GroupGeometry& gg = stage_plans_[s]->gg;
+    std::vector<uint64_t> inner(gg.per_group());
+    for (uint64_t v = 0; v < inner.size(); ++v) inner[v] = deposit_bits(v, gg.inner_mask);
+    uint64_t o = 0;
+    for (uint64_t g = 0; g < gg.groups(); ++g) {
+        for (uint64_t v : inner) store_.put(o | v, sizes[o | v]);
+        o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
+    }
+}
+
+void Engine::partial_sums(double* out3) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    const uint64_t nid = L_.num_blocks();
+    if (!cfg_.compress) {
+        k_block_sums<<<static_cast<uint32_t>(nid), 256, 0, st_>>>(dense_.p, L_.b, sums_.p);
+        BMQ_CUDA(cudaGetLastError());
+    }
+    std::vector<double> h(3 * nid);
+    BMQ_CUDA(cudaMemcpyAsync(h.data(), sums_.p, sums_.bytes(), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    out3[0] = out3[1] = out3[2] = 0.0;
+    for (uint64_t id = 0; id < nid; ++id)
+        for (int k = 0; k < 3; ++k) out3[k] += h[3 * id + k];
 }
 
 }  // namespace bmq

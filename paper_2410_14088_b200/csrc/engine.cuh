@@ -78,10 +78,32 @@ public:
     double fidelity_analytic(int kind);
     static double fidelity_pair(Engine& a, Engine& b);
 
+    // Sharded runs (one engine per rank). A sharded engine only
+    // processes the groups of its rank under each stage's device bits; ids it
+    // does not own hold ALL_ZERO with zero sums, so local reductions are
+    // partial sums. The host driver moves payloads between stages.
+    void shard(uint32_t rank, uint32_t world);
+    const std::vector<uint32_t>& device_bits() const { return dev_bits_; }
+    // meta per id: {size (0 = ALL_ZERO), sumsq, sum_re, sum_im (f64 bits)}
+    void export_payloads(const uint64_t* ids, uint64_t n, uint64_t* meta, void* dst, uint64_t cap);
+    void import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* meta, const void* src);
+    void drop_payloads(const uint64_t* ids, uint64_t n);
+    void stage_sizes(uint64_t s, uint64_t* sizes);
+    void account_stage(uint64_t s, const uint64_t* sizes);
+    void partial_sums(double* out3);
+    void report(bmq_report* rep, double device_ms);
+
     const Layout& layout() const { return L_; }
     const std::vector<bmq_stage>& plan() const { return plan_; }
 
 private:
+    bool sharded() const { return shard_world_ > 1; }
+    uint32_t owner(uint64_t id, uint64_t s) const {
+        return shard_m_ ? shard_owner(id, dev_bits_.data() + s * shard_m_, shard_m_) : 0;
+    }
+    uint32_t shard_rank_ = 0, shard_world_ = 1, shard_m_ = 0;
+    std::vector<uint32_t> dev_bits_;  // shard_m_ block-id bits per stage
+
     void ensure_init();
     void run_stage(uint64_t s);
     void raw_run_stage(uint64_t s);

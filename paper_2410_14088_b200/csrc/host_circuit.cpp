@@ -228,6 +228,59 @@ uint32_t buffer_bit(const Layout& L, const bmq_stage& st, uint32_t q) {
     raise(BMQ_ERR_LOGIC, "qubit " + std::to_string(q) + " is an outer index for this stage");
 }
 
+// Device-bit plan for `world` shards. The reference is
+// single-node; its stage loop (engine.hpp:109-120) only needs every group of a
+// stage on one worker, which holds iff the device bits are outer bits of that
+// stage. Slot j of stage s holds the id bit whose value is bit j of the owning
+// rank. A slot is only re-chosen when the stage needs its bit as an inner
+// bit, and then gets the free bit used furthest in the future (Belady);
+// ties go to the highest bit, so the plan is deterministic on every rank.
+std::vector<uint32_t> shard_plan(const Layout& L, const std::vector<bmq_stage>& plan, uint32_t world) {
+    if (world == 0 || (world & (world - 1))) raise(BMQ_ERR_INVALID_ARGUMENT, "shard count must be a power of two");
+    uint32_t m = 0;
+    while ((1u << m) < world) ++m;
+    const uint64_t ns = plan.size();
+    std::vector<uint32_t> out(ns * m);
+    if (!m) return out;
+    std::vector<uint64_t> inner_mask(ns, 0);
+    for (uint64_t s = 0; s < ns; ++s) {
+        for (uint32_t i = 0; i < plan[s].inner_count; ++i) inner_mask[s] |= 1ull << (plan[s].inner[i] - L.b);
+        if (L.c - plan[s].inner_count < m)
+            raise(BMQ_ERR_INVALID_ARGUMENT, "stage " + std::to_string(s) + " leaves " +
+                                                std::to_string(L.c - plan[s].inner_count) +
+                                                " outer bits, too few for " + std::to_string(world) + " shards");
+    }
+    const auto next_use = [&](uint32_t bit, uint64_t from) {
+        for (uint64_t s = from; s < ns; ++s)
+            if (inner_mask[s] >> bit & 1) return s;
+        return ns;
+    };
+    std::vector<uint32_t> slots;
+    uint64_t held = 0;
+    const auto pick = [&](uint64_t s) {
+        uint32_t best = ~0u;
+        uint64_t best_use = 0;
+        for (uint32_t bit = L.c; bit-- > 0;) {
+            if ((inner_mask[s] >> bit & 1) || (held >> bit & 1)) continue;
+            const uint64_t u = next_use(bit, s);
+            if (best == ~0u || u > best_use) best = bit, best_use = u;
+        }
+        held |= 1ull << best;
+        return best;
+    };
+    for (uint32_t j = 0; j < m; ++j) slots.push_back(pick(0));
+    std::sort(slots.begin(), slots.end());
+    for (uint64_t s = 0; s < ns; ++s) {
+        for (uint32_t j = 0; j < m; ++j) {
+            if (!(inner_mask[s] >> slots[j] & 1)) continue;
+            held &= ~(1ull << slots[j]);
+            slots[j] = pick(s);
+        }
+        for (uint32_t j = 0; j < m; ++j) out[s * m + j] = slots[j];
+    }
+    return out;
+}
+
 uint64_t compress_bound(uint64_t n) {
     const uint64_t chunks = (n + 4095) / 4096;
     return 26 + 2 * ((chunks + 3) / 4 + (n + 7) / 8) + (n * 63 + 7) / 8 + 16;
