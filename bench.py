@@ -103,7 +103,7 @@ def dist_setup():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return world, rank, local, dist
     return 1, 0, 0, None
 
@@ -194,6 +194,121 @@ def cpu_baseline(seconds_hint=20.0):
             "extrapolated_full_run_s": (1 << w["n"]) * len(plan) / value}
 
 
+def phase_roofline(d, t_dev):
+    """Dominant device phase: algorithmic bytes / CUDA-event time."""
+    peak, peak_kind = load_peaks()
+    phases = {"decompress": (d["decompress_ms"], d["decompress_bytes"]),
+              "gate": (d["gate_ms"], d["gate_bytes"]),
+              "compress": (d["compress_ms"], d["compress_bytes"])}
+    dom = max(phases, key=lambda k: phases[k][0])
+    ms, nbytes = phases[dom]
+    achieved = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(dom)
+        except Exception:
+            traffic = None
+    model_bytes = d["payload_bytes_read"] + d["payload_bytes_written"] + d["dense_bytes"]
+    return {"bound": "hbm", "kernel": f"{dom} phase", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_source": peak_kind, "traffic": traffic,
+            "stage_loop": {"model_bytes": model_bytes,
+                           "achieved_gbs": model_bytes / (t_dev / 1e3) / 1e9,
+                           "frac": model_bytes / (t_dev / 1e3) / 1e9 / peak},
+            "phase_ms": {k: v[0] for k, v in phases.items()},
+            "phase_bytes": {k: v[1] for k, v in phases.items()}}
+
+
+def main_sharded(args, world, rank, local, dist):
+    """N GPUs, one simulation: the stage loop sharded over device qubits with
+    payload remaps over NCCL (paper_2410_14088_b200/shard.py). Total work is
+    fixed (strong scaling); value = amp-stages of the one simulation / the
+    max over ranks of the device-timed run."""
+    import torch
+    from paper_2410_14088_b200 import cbq
+    from paper_2410_14088_b200.shard import EngineShard, ShardedSimulator, TorchCollective
+    if dist is None:  # --sharded at N=1: a one-rank NCCL group
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+    w = WORKLOAD
+    circ = cbq.generate_benchmark(w["name"], w["n"])
+    cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
+                     identity_skip=not args.no_identity_skip)
+    col = TorchCollective(torch.device("cuda", local))
+    be = EngineShard(circ, cfg, rank, world)
+    ssim = ShardedSimulator(be, col)
+    stages = len(ssim.stages)
+    amp_stages = (1 << w["n"]) * stages
+    for _ in range(args.warmup):
+        ssim.run()
+    reps, dev_ms = [], []
+    barrier_sync(dist)
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            barrier_sync(dist)
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            reps.append(ssim.run())
+            torch.cuda.synchronize()
+            ev1.record()
+            ev1.synchronize()
+            dev_ms.append(ev0.elapsed_time(ev1))
+        barrier_sync(dist)
+    t_dev = max_over_ranks(dist, statistics.median(dev_ms))
+    rep = reps[-1]
+    local_rep = be.report()
+    fidelity = ssim.fidelity_uniform() if w["name"] == "qft" else None
+    value = amp_stages / (t_dev / 1e3)
+    be.close()
+    e2e = None
+    if not args.no_e2e:
+        times, h2d, d2h = [], 0, 0
+        gates_arr = circ.c_array()
+        for step in range(max(1, min(args.steps, 3)) + 1):
+            barrier_sync(dist)
+            t0 = time.perf_counter()
+            b2 = EngineShard(circ, cfg, rank, world)
+            s2 = ShardedSimulator(b2, col)
+            s2.run()
+            pays = s2.gather_payloads(0)
+            b2.close()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if step > 0:
+                times.append(dt)
+            h2d = len(bytes(gates_arr)) + 8
+            d2h = sum(len(p) for p in pays) + 8 * len(pays) if pays else 0
+        t_e2e = max_over_ranks(dist, statistics.median(times))
+        e2e = {"value": amp_stages / t_e2e, "unit": "amp-stages/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "seconds": t_e2e}
+    line = {
+        "metric": "amp-stages/s (QFT-34, b=20, inner=2, b_r=1e-3)", "value": value, "unit": "amp-stages/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (QFT|0> circuit generated in-process; no datasets)",
+        "config": {"workload": f"qft{w['n']}_b{w['b']}_i{w['inner']}_br1e-3", "stages": stages,
+                   "parallelism": f"shard{world} (device qubits, NCCL payload remaps)",
+                   "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
+                   "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},
+        "sim_time_s": t_dev / 1e3, "compression_ratio": rep.compression_ratio,
+        "max_footprint_bytes": rep.max_footprint_bytes, "fidelity": fidelity, "final_norm": rep.final_norm,
+        "gpu_launches": int(rep.device["kernel_launches"]),
+        "groups_processed": rep.device["groups_processed"], "groups_skipped": rep.device["groups_skipped"],
+        "remaps": ssim.remaps, "exchange_ms_rank0": ssim.exchange_ms, "account_ms_rank0": ssim.account_ms,
+        "roofline": dict(phase_roofline(local_rep.device, t_dev), scope="rank 0"),
+        "clocks": clocks.summary(), "e2e": e2e,
+    }
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -207,6 +322,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-identity-skip", action="store_true",
                     help="process every block of every nonzero group (no diagonal-stage block skipping)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent full simulations instead of one sharded simulation")
+    ap.add_argument("--sharded", action="store_true", help="use the sharded driver even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -214,6 +332,8 @@ def main():
     world, rank, local, dist = dist_setup()
     import torch
     torch.cuda.set_device(local)
+    if (world > 1 and not args.replicas) or args.sharded:
+        return main_sharded(args, world, rank, local, dist)
     from paper_2410_14088_b200 import cbq
     w = WORKLOAD
     circ = cbq.generate_benchmark(w["name"], w["n"])
@@ -262,31 +382,7 @@ def main():
         t_e2e = max_over_ranks(dist, statistics.median(times))
         e2e = {"value": world * amp_stages / t_e2e, "unit": "amp-stages/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "seconds": t_e2e}
-    # ----------------------------------------------------------- roofline
-    peak, peak_kind = load_peaks()
-    d = rep.device
-    phases = {"decompress": (d["decompress_ms"], d["decompress_bytes"]),
-              "gate": (d["gate_ms"], d["gate_bytes"]),
-              "compress": (d["compress_ms"], d["compress_bytes"])}
-    dom = max(phases, key=lambda k: phases[k][0])
-    ms, nbytes = phases[dom]
-    achieved = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                traffic = json.load(f).get(dom)
-        except Exception:
-            traffic = None
-    model_bytes = d["payload_bytes_read"] + d["payload_bytes_written"] + d["dense_bytes"]
-    roofline = {"bound": "hbm", "kernel": f"{dom} phase", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_source": peak_kind, "traffic": traffic,
-                "stage_loop": {"model_bytes": model_bytes,
-                               "achieved_gbs": model_bytes / (t_dev / 1e3) / 1e9,
-                               "frac": model_bytes / (t_dev / 1e3) / 1e9 / peak},
-                "phase_ms": {k: v[0] for k, v in phases.items()},
-                "phase_bytes": {k: v[1] for k, v in phases.items()}}
+    roofline = phase_roofline(rep.device, t_dev)
     line = {
         "metric": "amp-stages/s (QFT-34, b=20, inner=2, b_r=1e-3)", "value": value, "unit": "amp-stages/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev,

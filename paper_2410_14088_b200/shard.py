@@ -194,6 +194,9 @@ class EngineShard:
     def init(self):
         self.sim.init_state()
 
+    def reset(self):
+        self.sim.reset()
+
     def run_stage(self, s: int):
         cbq._check(lib.bmq_simulator_run_stages(self._h, s, s + 1))
 
@@ -268,6 +271,7 @@ class ShardedSimulator:
         if hasattr(backend, "set_bits"):  # backends that do not plan themselves
             backend.set_bits(self.bits)
         self._own = {}
+        self._ran = False
         self.remaps = 0
         self.moved_bytes = 0  # payload bytes this rank sent
         self.exchange_ms = 0.0
@@ -319,6 +323,10 @@ class ShardedSimulator:
     def run(self) -> cbq.SimulationReport:
         be, col = self.backend, self.col
         t0 = time.perf_counter()
+        if self._ran:
+            be.reset()
+        self._ran = True
+        self.remaps, self.moved_bytes, self.exchange_ms, self.account_ms = 0, 0, 0.0, 0.0
         be.init()
         stage_ms = []
         for s in range(len(self.stages)):
