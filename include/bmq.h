@@ -100,6 +100,12 @@ typedef struct bmq_config {
  * bit-exact because compress(decompress(p)) == p for every payload p the
  * device codec emits (checked per error bound when the tables are built). */
 #define BMQ_FLAG_IDENTITY_SKIP 0x2u
+/* Run stages made only of gates whose matrix entries are 0 or units
+ * (X, Y, Z, S, Sdg, CX, CZ) on the quantiser codes: such gates only move
+ * real/imaginary parts and flip signs, so every decompressed scalar +-E[q]
+ * lands on another scalar with the same code. Bit-exact under the same
+ * idempotence check as BMQ_FLAG_IDENTITY_SKIP; default on. */
+#define BMQ_FLAG_CODE_DOMAIN 0x4u
 
 /* cbq::SimulationReport (engine.hpp:39-53) plus device-side counters. */
 typedef struct bmq_report {
@@ -141,6 +147,7 @@ typedef struct bmq_report {
     uint64_t compactions;           /* payload arena compactions */
     uint64_t host_spill_bytes;      /* payload bytes placed in the pinned host arena */
     uint64_t host_spill_batches;    /* batches whose payloads went to the host arena */
+    uint64_t code_domain_batches;   /* batches run on quantiser codes (BMQ_FLAG_CODE_DOMAIN) */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

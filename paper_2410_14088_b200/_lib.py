@@ -27,6 +27,7 @@ BMQ_ERR_BUFFER_TOO_SMALL = 10
 
 BMQ_FLAG_ZERO_GROUP_SKIP = 0x1
 BMQ_FLAG_IDENTITY_SKIP = 0x2
+BMQ_FLAG_CODE_DOMAIN = 0x4
 
 
 class bmq_gate(C.Structure):
@@ -61,7 +62,8 @@ class bmq_report(C.Structure):
                 ("decompress_ms", C.c_double), ("gate_ms", C.c_double), ("compress_ms", C.c_double),
                 ("batches", C.c_uint64), ("decompress_bytes", C.c_uint64), ("gate_bytes", C.c_uint64),
                 ("compress_bytes", C.c_uint64), ("fused_batches", C.c_uint64), ("compactions", C.c_uint64),
-                ("host_spill_bytes", C.c_uint64), ("host_spill_batches", C.c_uint64)]
+                ("host_spill_bytes", C.c_uint64), ("host_spill_batches", C.c_uint64),
+                ("code_domain_batches", C.c_uint64)]
 
 
 _P = C.c_void_p

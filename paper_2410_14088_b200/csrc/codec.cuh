@@ -27,9 +27,11 @@ void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk
                           bool virtual_zero, uint32_t align, DevError* d_err, uint64_t* launches,
                           uint64_t meta_base = 0, uint64_t meta_tag = 0);
 
-// Decompress nblk payloads into their planar output buffers.
+// Decompress nblk payloads into their planar output buffers. mode 0: doubles;
+// 1: packed code words, 4 bytes per scalar, in DecBlock::out reinterpreted as
+// uint32_t*; 2: no output, dequantised sums only (DecInfo::sumsq, ...).
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
-                       uint64_t* launches);
+                       uint64_t* launches, int mode = 0);
 
 }  // namespace bmq

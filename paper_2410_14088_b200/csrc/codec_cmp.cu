@@ -350,7 +350,104 @@ __global__ void k_zero_range(uint8_t* base, const uint64_t* range) {
 // ----------------------------------------------------------------- emit
 constexpr int kStageWords = (kChunk * 30 + 31) / 32 + 2;  // codes are < 2^30 (kQOffMax)
 
-__global__ void __launch_bounds__(kChunkThreads) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
+// The scalar part of emit for one chunk (kFull: all 4096 scalars valid).
+struct EmitSmem {
+    uint32_t sign[kWordsPerChunk], zero[kWordsPerChunk], pre[kWordsPerChunk];
+    uint32_t stage[kStageWords];
+    uint32_t cmp[kChunkThreads / 32][32];
+};
+
+template <bool kFull>
+__device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, const uint32_t* __restrict__ src,
+                                           const BlockPlan& bp, uint8_t* pay, const DevTables& t, EmitSmem& sm) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t* s_sign = sm.sign;
+    uint32_t* s_zero = sm.zero;
+    uint32_t* s_pre = sm.pre;
+    uint32_t* stage = sm.stage;
+    auto& s_cmp = sm.cmp;
+    const uint32_t w_bits = bp.width;
+    const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
+    const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
+    const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
+    for (uint32_t i = tid; i < nstage; i += kChunkThreads) stage[i] = 0;
+    uint32_t pkv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {  // all loads in flight before the first ballot
+        const uint32_t s = 128 * j + 32 * w + lane;
+        pkv[j] = (kFull || s < len) ? __ldcs(src + s) : 1u;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t pk = pkv[j];
+        const uint32_t sw = __ballot_sync(0xffffffffu, (pk >> 1) & 1u);
+        const uint32_t zw = __ballot_sync(0xffffffffu, pk & 1u) & (kFull ? ~0u : word_mask(len, 4 * j + w));
+        if (lane == 0) {
+            s_sign[4 * j + w] = sw;
+            s_zero[4 * j + w] = zw;
+        }
+    }
+    __syncthreads();
+    // nonzero prefix over the 128 words in scalar order
+    {
+        using Scan = cub::BlockScan<uint32_t, kChunkThreads>;
+        __shared__ typename Scan::TempStorage ss;
+        const uint32_t cnt = __popc(~s_zero[tid] & (kFull ? ~0u : word_mask(len, tid)));
+        uint32_t pre;
+        Scan(ss).ExclusiveSum(cnt, pre);
+        s_pre[tid] = pre;
+    }
+    __syncthreads();
+    // Warp-cooperative packing: the nonzero codes of one bitmap word are
+    // compacted by rank, then lane i assembles stage word i of the word's
+    // contiguous bit range; edge words are shared with neighbouring warps.
+    const uint32_t lt = (1u << lane) - 1;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t k = 4 * j + w;
+        const uint32_t nzw = ~s_zero[k] & (kFull ? ~0u : word_mask(len, k));
+        const uint32_t cnt = __popc(nzw);
+        if (!cnt) continue;  // warp-uniform
+        const bool mine = (nzw >> lane) & 1u;
+        const uint32_t code = (pkv[j] >> 2) - qmin_off;
+        const uint32_t a0 = s_pre[k] * w_bits;  // chunk-relative bit of this word's first code
+        const uint32_t off0 = a0 & 31, wbase = a0 >> 5;
+        if (w_bits == 1 && cnt == 32) {
+            const uint32_t bits = __ballot_sync(0xffffffffu, code & 1u);
+            if (lane == 0 && bits) {
+                atomicOr(&stage[wbase], bits << off0);
+                if (off0) atomicOr(&stage[wbase + 1], bits >> (32 - off0));
+            }
+            continue;
+        }
+        if (mine) s_cmp[w][__popc(nzw & lt)] = code;
+        __syncwarp();
+        const uint32_t nwords = (off0 + cnt * w_bits + 31) >> 5;
+        if (lane < nwords) {
+            const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);  // word start, code-range relative
+            const uint32_t m_lo = wb > 0 ? static_cast<uint32_t>(wb) / w_bits : 0;
+            const uint32_t m_hi = min(cnt - 1, static_cast<uint32_t>(wb + 31) / w_bits);
+            uint32_t v = 0;
+            for (uint32_t m = m_lo; m <= m_hi; ++m) {
+                const int pos = static_cast<int>(m * w_bits) - wb;
+                const uint32_t cv = s_cmp[w][m];
+                v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
+            }
+            if (v) atomicOr(&stage[wbase + lane], v);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    const uint32_t raw_bits = ((len + 7) / 8) * 8;
+    if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, s_sign, raw_bits, tid, kChunkThreads);
+    if (p.ztag == 2) write_bits_block(pay + p.zero_off, 0, s_zero, raw_bits, tid, kChunkThreads);
+    const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix) * w_bits;
+    write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), stage, code_bits,
+                     tid, kChunkThreads);
+}
+
+
+__global__ void __launch_bounds__(kChunkThreads, 6) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
                                                             const ChunkPlan* __restrict__ cps,
                                                             BlockPlan* __restrict__ bps, uint8_t* __restrict__ out,
                                                             DevTables t, const DevError* err) {
@@ -361,7 +458,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_cmp_emit(const CmpBlock* __re
     if (c > 0 && c >= bp.nch) return;  // (an empty block still gets its header from chunk 0)
     if (bp.out_off == ~0ull) return;   // virtual ALL_ZERO
     uint8_t* pay = out + bp.out_off;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int tid = threadIdx.x;
     if (c == 0 && tid == 0) {  // header (codec.hpp:282-286)
         uint64_t v[3];
         v[0] = blk.count;
@@ -390,77 +487,11 @@ __global__ void __launch_bounds__(kChunkThreads) k_cmp_emit(const CmpBlock* __re
     }
     const ChunkPlan p = cp[c];
     const uint32_t len = chunk_len(blk.count, c);
-    const uint32_t* src = blk.pk + static_cast<uint64_t>(c) * kChunk;
-    __shared__ uint32_t s_sign[kWordsPerChunk], s_zero[kWordsPerChunk], s_pre[kWordsPerChunk];
-    __shared__ uint32_t stage[kStageWords];
-    __shared__ double s_red[3][4];
-    const uint32_t w_bits = bp.width;
-    const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
-    const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
-    const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
-    for (uint32_t i = tid; i < nstage; i += kChunkThreads) stage[i] = 0;
-    uint32_t pkv[32];
-    double sq = 0.0, sre = 0.0, sim = 0.0;
-    const uint64_t half = blk.count / 2, g0 = static_cast<uint64_t>(c) * kChunk;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {  // all loads in flight before the first ballot
-        const uint32_t s = 128 * j + 32 * w + lane;
-        pkv[j] = s < len ? __ldg(src + s) : 1u;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t s = 128 * j + 32 * w + lane;
-        const bool valid = s < len;
-        const uint32_t pk = pkv[j];
-        const uint32_t sw = __ballot_sync(0xffffffffu, (pk >> 1) & 1u);
-        const uint32_t zw = __ballot_sync(0xffffffffu, valid && (pk & 1u));
-        if (lane == 0) {
-            s_sign[4 * j + w] = sw;
-            s_zero[4 * j + w] = zw;
-        }
-        if (!(pk & 1u)) {
-            const double m = __ldg(t.dequant + (pk >> 2));
-            sq += m * m;
-            const double sv = (pk & 2u) ? -m : m;
-            if (g0 + s < half)
-                sre += sv;
-            else
-                sim += sv;
-        }
-    }
-    __syncthreads();
-    // nonzero prefix over the 128 words in scalar order
-    {
-        using Scan = cub::BlockScan<uint32_t, kChunkThreads>;
-        __shared__ typename Scan::TempStorage ss;
-        const uint32_t cnt = __popc(~s_zero[tid] & word_mask(len, tid));
-        uint32_t pre;
-        Scan(ss).ExclusiveSum(cnt, pre);
-        s_pre[tid] = pre;
-    }
-    __syncthreads();
-    const uint32_t lt = (1u << lane) - 1;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t k = 4 * j + w;
-        const uint32_t nzw = ~s_zero[k] & word_mask(len, k);
-        if ((nzw >> lane) & 1u) {
-            const uint32_t rank = s_pre[k] + __popc(nzw & lt);
-            const uint64_t code = static_cast<uint64_t>((pkv[j] >> 2) - qmin_off);
-            const uint64_t pos = static_cast<uint64_t>(rank) * w_bits;
-            const uint32_t wi = static_cast<uint32_t>(pos >> 5), sh = static_cast<uint32_t>(pos & 31);
-            atomicOr(&stage[wi], static_cast<uint32_t>(code << sh));
-            if (sh + w_bits > 32) atomicOr(&stage[wi + 1], static_cast<uint32_t>(code >> (32 - sh)));
-        }
-    }
-    __syncthreads();
-    const uint32_t raw_bits = ((len + 7) / 8) * 8;
-    if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, s_sign, raw_bits, tid, kChunkThreads);
-    if (p.ztag == 2) write_bits_block(pay + p.zero_off, 0, s_zero, raw_bits, tid, kChunkThreads);
-    const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix) * w_bits;
-    write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), stage, code_bits,
-                     tid, kChunkThreads);
-    block_sums3(sq, sre, sim, s_red, &bps[bi].sumsq);  // dequantised sums for norm / fidelity
+    __shared__ EmitSmem sm;
+    if (len == kChunk)
+        emit_chunk<true>(p, len, blk.pk + static_cast<uint64_t>(c) * kChunk, bp, pay, t, sm);
+    else
+        emit_chunk<false>(p, len, blk.pk + static_cast<uint64_t>(c) * kChunk, bp, pay, t, sm);
 }
 
 }  // namespace

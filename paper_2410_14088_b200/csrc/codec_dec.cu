@@ -197,6 +197,85 @@ __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __r
     }
 }
 
+// Output modes: kDoubles writes the planar scalars; kCodes writes packed
+// code words (CmpBlock::pk layout, (q - qlo) << 2 | negative << 1 | zero)
+// for code-domain stages — codes must lie in the tables' idempotent window
+// so that compress(decompress) reproduces them; kSumsOnly writes nothing and
+// only accumulates the dequantised sums (norm / fidelity).
+enum DecMode : int { kDoubles = 0, kCodes = 1, kSumsOnly = 2 };
+
+// Warp-cooperative code fetch: the nonzero scalars of one 32-scalar bitmap
+// word hold consecutive ranks, so their codes are one contiguous bit range.
+// Each lane loads one aligned 32-bit word of that range; lane j's code is
+// then two shuffles and a funnel shift away (width <= 30). All 32 lanes call.
+__device__ __forceinline__ uint32_t warp_codes(const uint32_t* cs32, uint64_t a0, uint32_t cnt, uint32_t width,
+                                               uint32_t rank_in_word, uint32_t lane) {
+    const uint32_t off0 = static_cast<uint32_t>(a0 & 31);
+    const uint64_t w0 = a0 >> 5;
+    const uint32_t nwords = (off0 + cnt * width + 31) >> 5;
+    const uint32_t wv = lane < nwords ? __ldg(cs32 + w0 + lane) : 0u;
+    const uint32_t a = off0 + rank_in_word * width;
+    const uint32_t rel = (a >> 5) & 31, sh = a & 31;
+    const uint32_t lo = __shfl_sync(0xffffffffu, wv, rel), hi = __shfl_sync(0xffffffffu, wv, (rel + 1) & 31);
+    return __funnelshift_r(lo, hi, sh) & ((1u << width) - 1);
+}
+
+// Per-scalar loop of one chunk. kFull: a whole 4096-scalar chunk (no
+// partial words). check: some code of the block may fall outside the window
+// (block-uniform; decided from code_min and the width).
+template <int kMode, bool kFull>
+__device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32_t* s_nz, const uint32_t* s_pre,
+                                            const uint8_t* codes, uint32_t width, uint32_t nz_prefix, uint32_t len,
+                                            int64_t qbase, int64_t lo, int64_t hi, bool check, const DevTables& t,
+                                            double* dst, uint32_t* cdst, uint64_t half, uint64_t g0, bool sums,
+                                            double& sq, double& sre, double& sim, bool& bad) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uintptr_t cs = reinterpret_cast<uintptr_t>(codes);
+    const uint32_t* cs32 = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3));
+    const uint32_t bit0 = static_cast<uint32_t>(cs & 3) * 8;
+    const bool coop = width <= 30;  // block-uniform
+    const uint32_t lt = (1u << lane) - 1;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t k = 4 * j + w;
+        if (!kFull && k * 32 >= len) break;  // warp-uniform; later words are empty too
+        const uint32_t s = 32 * k + lane;
+        const uint32_t nzw = s_nz[k];
+        const bool mine = (nzw >> lane) & 1u;
+        const uint32_t rw = __popc(nzw & lt);
+        uint64_t code = 0;
+        if (coop) {
+            const uint32_t cnt = __popc(nzw);
+            if (cnt) code = warp_codes(cs32, bit0 + (static_cast<uint64_t>(nz_prefix) + s_pre[k]) * width, cnt, width, rw, lane);
+        } else if (mine) {
+            code = read_bits(codes, (static_cast<uint64_t>(nz_prefix) + s_pre[k] + rw) * width, width);
+        }
+        // packed word / table index of the code: q - qlo (qbase = code_min - qlo)
+        const int64_t qo = qbase + static_cast<int64_t>(code);
+        if (check && mine && (qo < lo || qo > hi)) bad = true;
+        const bool neg = (s_sign[k] >> lane) & 1u;
+        if constexpr (kMode == kCodes) {
+            const uint32_t pkw = mine ? pack_code(static_cast<uint32_t>(qo), neg, false) : 1u;
+            if (kFull || s < len) cdst[s] = pkw;
+        } else {
+            double v = 0.0;
+            if (mine && !(check && (qo < lo || qo > hi))) {
+                const double m = __ldg(t.dequant + qo);
+                v = neg ? -m : m;
+                if (kMode == kSumsOnly || sums) {
+                    sq += m * m;
+                    if (g0 + s < half)
+                        sre += v;
+                    else
+                        sim += v;
+                }
+            }
+            if (kMode == kDoubles && (kFull || s < len)) dst[s] = v;
+        }
+    }
+}
+
+template <int kMode>
 __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __restrict__ blks, uint32_t nch_max,
                                                              DecInfo* __restrict__ infos,
                                                              const DecChunk* __restrict__ dcs, DevTables t,
@@ -209,13 +288,21 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     const DecBlock blk = blks[bi];
     const uint32_t len = chunk_len(info.count, c);
     double* dst = blk.out + static_cast<uint64_t>(c) * kChunk;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t* cdst = reinterpret_cast<uint32_t*>(blk.out) + static_cast<uint64_t>(c) * kChunk;
+    const int tid = threadIdx.x;
     if (info.flags & 1) {
-        for (uint32_t s = tid; s < len; s += kChunkThreads) dst[s] = 0.0;
+        if constexpr (kMode != kSumsOnly) {
+            for (uint32_t s = tid; s < len; s += kChunkThreads) {
+                if (kMode == kCodes)
+                    cdst[s] = 1u;
+                else
+                    dst[s] = 0.0;
+            }
+        }
         return;
     }
     const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
-    __shared__ uint32_t s_sign[kWordsPerChunk], s_zero[kWordsPerChunk], s_pre[kWordsPerChunk];
+    __shared__ uint32_t s_sign[kWordsPerChunk], s_nz[kWordsPerChunk], s_pre[kWordsPerChunk];
     __shared__ double s_red[3][4];
     {
         const uint32_t vm = word_mask(len, tid);
@@ -225,7 +312,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
             zw = d.ztag == 1 ? vm : (d.ztag == 2 ? load_u32_unaligned(blk.in + d.zero_off + 4 * tid) & vm : 0);
         }
         s_sign[tid] = sw;
-        s_zero[tid] = zw;
+        s_nz[tid] = ~zw & vm;
         using Scan = cub::BlockScan<uint32_t, kChunkThreads>;
         __shared__ typename Scan::TempStorage ss;
         uint32_t pre;
@@ -233,53 +320,43 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
         s_pre[tid] = pre;
     }
     __syncthreads();
-    const uint8_t* codes = blk.in + info.code_seg;
     const uint32_t width = info.width;
-    const uint32_t lt = (1u << lane) - 1;
+    // valid packed offsets: the idempotent window (codes) or the dequantisation table
+    const int64_t lo = (kMode == kCodes ? t.idem_lo : t.qlo) - t.qlo, hi = (kMode == kCodes ? t.idem_hi : t.qhi) - t.qlo;
+    const int64_t qbase = info.code_min - t.qlo;
+    const int64_t top = width >= 63 ? INT64_MAX : qbase + static_cast<int64_t>((1ull << width) - 1);
+    const bool check = qbase < lo || top > hi || top < qbase;
     double sq = 0.0, sre = 0.0, sim = 0.0;
-    const uint64_t half = info.count / 2, g0 = static_cast<uint64_t>(c) * kChunk;
     bool bad = false;
-#pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t k = 4 * j + w;
-        const uint32_t s = 32 * k + lane;
-        if (s >= len) continue;
-        const uint32_t vm = word_mask(len, k);
-        const uint32_t nzw = ~s_zero[k] & vm;
-        double v = 0.0;
-        if ((nzw >> lane) & 1u) {
-            const uint64_t rank = static_cast<uint64_t>(d.nz_prefix) + s_pre[k] + __popc(nzw & lt);
-            const uint64_t code = read_bits(codes, rank * width, width);
-            const int64_t q = info.code_min + static_cast<int64_t>(code);
-            if (q < t.qlo || q > t.qhi) {
-                bad = true;
-            } else {
-                const double m = __ldg(t.dequant + (q - t.qlo));
-                v = ((s_sign[k] >> lane) & 1u) ? -m : m;
-                sq += m * m;
-                if (g0 + s < half)
-                    sre += v;
-                else
-                    sim += v;
-            }
-        }
-        dst[s] = v;
-    }
+    const uint64_t half = info.count / 2, g0 = static_cast<uint64_t>(c) * kChunk;
+    const uint8_t* codes = blk.in + info.code_seg;
+    if (len == kChunk)
+        dec_scalars<kMode, true>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, check, t, dst,
+                                 cdst, half, g0, want_sums != 0, sq, sre, sim, bad);
+    else
+        dec_scalars<kMode, false>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, check, t, dst,
+                                  cdst, half, g0, want_sums != 0, sq, sre, sim, bad);
     if (bad) dev_fail(err, DE_CODE_WINDOW, bi);
-    if (want_sums) block_sums3(sq, sre, sim, s_red, &infos[bi].sumsq);
+    if (kMode == kSumsOnly || (kMode == kDoubles && want_sums)) block_sums3(sq, sre, sim, s_red, &infos[bi].sumsq);
 }
 
 }  // namespace
 
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
-                       uint64_t* launches) {
+                       uint64_t* launches, int mode) {
     if (nblk == 0) return;
     BMQ_CUDA(cudaMemsetAsync(d_info, 0, nblk * sizeof(DecInfo), st));
     k_dec_index<<<static_cast<uint32_t>(nblk), kIndexThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t,
                                                                         check_bound ? 1 : 0, d_err);
     const uint32_t grid = static_cast<uint32_t>(nblk * nch_max);
-    k_dec_chunk<<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, want_sums ? 1 : 0, d_err);
+    if (mode == 1)
+        k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err);
+    else if (mode == 2)
+        k_dec_chunk<kSumsOnly><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 1, d_err);
+    else
+        k_dec_chunk<kDoubles><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, want_sums ? 1 : 0,
+                                                              d_err);
     BMQ_CUDA(cudaGetLastError());
     if (launches) *launches += 2;
 }

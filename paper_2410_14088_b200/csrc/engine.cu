@@ -96,7 +96,7 @@ __global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t 
 __global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, const uint64_t* __restrict__ off,
                              const uint64_t* __restrict__ size, const uint8_t* pool, const uint8_t* host_pool,
                              const uint8_t* zero_hdr, double* work, uint32_t* pk, uint32_t b, DecBlock* dec,
-                             CmpBlock* cmp) {
+                             CmpBlock* cmp, int codes) {
     const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (i >= nblk) return;
     const uint64_t id = ids[i];
@@ -106,20 +106,10 @@ __global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, co
     DecBlock d;
     d.in = o == ~0ull ? zero_hdr : ((o & kHostTag) ? host_pool + (o & ~kHostTag) : pool + o);
     d.size = o == ~0ull ? kHeaderBytes : size[id];
-    d.out = slot;
+    d.out = codes ? reinterpret_cast<double*>(pk + i * count) : slot;  // codes: decode to packed words
     d.expect_count = count;
     dec[i] = d;
     cmp[i] = CmpBlock{slot, pk + i * count, count, id};
-}
-
-__global__ void k_store_cmp_sums(const BlockPlan* __restrict__ bp, const CmpBlock* __restrict__ cmp, uint64_t nblk,
-                                 double* sums) {
-    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (i >= nblk) return;
-    const uint64_t id = cmp[i].id;
-    sums[3 * id] = bp[i].sumsq;
-    sums[3 * id + 1] = bp[i].sum_re;
-    sums[3 * id + 2] = bp[i].sum_im;
 }
 
 __global__ void k_store_dec_sums(const DecInfo* __restrict__ di, const uint64_t* __restrict__ ids, uint64_t nblk,
@@ -548,8 +538,9 @@ void Engine::init_state() {
     BMQ_CUDA(cudaMemcpyAsync(cmp_.p, &blk, sizeof blk, cudaMemcpyHostToDevice, st_));
     launch_compress(st_, cmp_.p, 1, nch_, *tabs_, pool_[0].p, pool_cap_, cursor_.p, cursor_.p + 2, bplan_.p, cplan_.p,
                     off_.p, size_.p, true, false, err_.p, &counters_.kernel_launches);
-    k_store_cmp_sums<<<1, 32, 0, st_>>>(bplan_.p, cmp_.p, 1, sums_.p);
     check_device_error("init_state: ");
+    sums_ok_.assign(nid, 1);
+    sums_ok_[0] = 0;
     sync_meta_to_host();
     store_.put(0, h_size_[0]);
     if (nid > 1) store_.put_shared(1, nid, kHeaderBytes);  // one zero payload, counted once
@@ -654,8 +645,6 @@ void Engine::emit_batch(uint64_t nblk) {
         counters_.host_spill_bytes += total;
         ++counters_.host_spill_batches;
     }
-    k_store_cmp_sums<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, cmp_.p, nblk, sums_.p);
-    ++counters_.kernel_launches;
 }
 
 void Engine::ensure_host_pool() {
@@ -669,18 +658,27 @@ void Engine::ensure_host_pool() {
 void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk,
                            size_t bidx) {
     phase_event(4 * bidx);
+    // Code-domain stages (unit-entry monomial gates only) never leave the
+    // quantiser codes: decode to packed words, permute them, emit.
+    const bool codes = !d_vtab && sp.prog.mono && identity_ok_ && (cfg_.flags & BMQ_FLAG_CODE_DOMAIN);
     k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_.p, size_.p, pool_[cur_].p, host_pool_,
-                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p);
+                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, codes ? 1 : 0);
     ++counters_.kernel_launches;
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
-                      &counters_.kernel_launches);
+                      &counters_.kernel_launches, codes ? 1 : 0);
     phase_event(4 * bidx + 1);
     // the stage's last gate pass quantises straight into pk_ / cplan_
     BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
     const QuantOut qo{pk_.p, cplan_.p, nch_, *tabs_, err_.p};
     const uint64_t per = sp.gg.per_group();
-    const bool fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per,
-                                   &counters_.kernel_launches, &qo, d_vtab, nblk);
+    bool fused = true;
+    if (codes) {
+        run_mono_program(st_, sp.prog, pk_.p, L_.b, nblk / per, &counters_.kernel_launches, qo);
+        ++counters_.code_domain_batches;
+    } else {
+        fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per, &counters_.kernel_launches,
+                            &qo, d_vtab, nblk);
+    }
     phase_event(4 * bidx + 2);
     launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,
                          &counters_.kernel_launches);
@@ -757,12 +755,18 @@ void Engine::run_stage(uint64_t s) {
         rd += old_off[id] == ~0ull ? 0 : old_size[id];
         wr += h_off_[id] == ~0ull ? 0 : h_size_[id];
     }
-    const uint64_t half_dense = nwork * (16ull << L_.b);
+    // implementation bytes per phase: FP64 stages move 16 B per amplitude
+    // (8 B of packed codes out of the last pass), code-domain stages 8 B
+    const bool codes = !blockwise && sp.prog.mono && identity_ok_ && (cfg_.flags & BMQ_FLAG_CODE_DOMAIN);
+    const uint64_t half_dense = nwork * (16ull << L_.b), pk_bytes = nwork * (8ull << L_.b);
+    const uint64_t work_bytes = codes ? pk_bytes : half_dense;
     counters_.payload_bytes_read += rd;
     counters_.payload_bytes_written += wr;
-    counters_.decompress_bytes += rd + half_dense;
-    counters_.gate_bytes += 2 * half_dense * sp.prog.passes.size();
-    counters_.compress_bytes += half_dense + wr;
+    counters_.decompress_bytes += rd + work_bytes;
+    counters_.gate_bytes += codes ? 2 * pk_bytes * sp.prog.passes.size()
+                                  : 2 * half_dense * (sp.prog.passes.size() - 1) + half_dense + pk_bytes;
+    counters_.compress_bytes += pk_bytes + wr;
+    for (uint64_t id : work_ids) sums_ok_[id] = 0;
     counters_.groups_processed += groups_done;
     counters_.groups_skipped += groups_owned - groups_done;
     counters_.blocks_processed += nwork;
@@ -837,6 +841,7 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.compactions = counters_.compactions;
     r.host_spill_bytes = counters_.host_spill_bytes;
     r.host_spill_batches = counters_.host_spill_batches;
+    r.code_domain_batches = counters_.code_domain_batches;
     *rep = r;
 }
 
@@ -844,6 +849,7 @@ double Engine::state_norm() {
     BMQ_CUDA(cudaSetDevice(dev_));
     ensure_init();
     const uint64_t nid = L_.num_blocks();
+    if (cfg_.compress) ensure_sums();
     if (!cfg_.compress) {
         k_block_sums<<<static_cast<uint32_t>(nid), 256, 0, st_>>>(dense_.p, L_.b, sums_.p);
         BMQ_CUDA(cudaGetLastError());
@@ -862,9 +868,37 @@ void Engine::host_ids_to_device(const std::vector<uint64_t>& ids) {
 
 void Engine::decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums) {
     k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_.p, size_.p, pool_[cur_].p, host_pool_,
-                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p);
+                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0);
     launch_decompress(st_, dec_.p, nids, nch_, *tabs_, dinfo_.p, dchunk_.p, true, want_sums, err_.p,
                       &counters_.kernel_launches);
+}
+
+void Engine::ensure_sums(const uint64_t* ids, uint64_t n) {
+    if (!cfg_.compress || !initialized_) return;
+    std::vector<uint64_t> stale, zero;
+    const auto visit = [&](uint64_t id) {
+        if (sums_ok_[id]) return;
+        (h_off_[id] == ~0ull ? zero : stale).push_back(id);
+        sums_ok_[id] = 1;
+    };
+    if (ids) {
+        for (uint64_t i = 0; i < n; ++i) visit(ids[i]);
+    } else {
+        for (uint64_t id = 0; id < sums_ok_.size(); ++id) visit(id);
+    }
+    for (uint64_t id : zero) BMQ_CUDA(cudaMemsetAsync(sums_.p + 3 * id, 0, 3 * sizeof(double), st_));
+    for (uint64_t first = 0; first < stale.size(); first += max_blocks_) {
+        const uint64_t nb = std::min<uint64_t>(max_blocks_, stale.size() - first);
+        BMQ_CUDA(cudaMemcpyAsync(ids_.p, stale.data() + first, nb * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
+        k_build_desc<<<grid_for(nb), 256, 0, st_>>>(ids_.p, nb, off_.p, size_.p, pool_[cur_].p, host_pool_,
+                                                    zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0);
+        launch_decompress(st_, dec_.p, nb, nch_, *tabs_, dinfo_.p, dchunk_.p, true, true, err_.p,
+                          &counters_.kernel_launches, 2);
+        k_store_dec_sums<<<grid_for(nb), 256, 0, st_>>>(dinfo_.p, ids_.p, nb, sums_.p);
+        counters_.kernel_launches += 2;
+        BMQ_CUDA(cudaStreamSynchronize(st_));  // ids_ is reused by the next batch
+    }
+    if (!stale.empty()) check_device_error("sums: ");
 }
 
 void Engine::extract_state(double* amps, uint64_t namps) {
@@ -1043,6 +1077,7 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
     }
     h_off_[id] = used;
     h_size_[id] = size;
+    sums_ok_[id] = 1;
     store_.put(id, size);
 }
 
@@ -1085,6 +1120,7 @@ double Engine::fidelity_analytic(int kind) {
     ensure_init();
     if (kind == 0) {  // uniform 2^(-n/2): |<u|psi>| = 2^(-n/2) |sum psi_i|
         const uint64_t nid = L_.num_blocks();
+        if (cfg_.compress) ensure_sums();
         if (!cfg_.compress) {
             k_block_sums<<<static_cast<uint32_t>(nid), 256, 0, st_>>>(dense_.p, L_.b, sums_.p);
             BMQ_CUDA(cudaGetLastError());
@@ -1166,6 +1202,9 @@ void Engine::export_payloads(const uint64_t* ids, uint64_t n, uint64_t* meta, vo
     ensure_init();
     if (!cfg_.compress) raise(BMQ_ERR_INVALID_ARGUMENT, "payload export requires compression");
     const uint64_t nid = L_.num_blocks();
+    for (uint64_t i = 0; i < n; ++i)
+        if (ids[i] >= nid) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(ids[i]));
+    ensure_sums(ids, n);
     std::vector<double> sums(3 * nid);
     BMQ_CUDA(cudaMemcpyAsync(sums.data(), sums_.p, sums_.bytes(), cudaMemcpyDeviceToHost, st_));
     BMQ_CUDA(cudaStreamSynchronize(st_));
@@ -1249,6 +1288,7 @@ void Engine::import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* me
     for (const Xfer& x : xs) {
         h_off_[x.id] = x.size ? (x.dst | tag) : ~0ull;
         h_size_[x.id] = x.size ? x.size : kHeaderBytes;
+        sums_ok_[x.id] = 1;  // the sums travelled with the payload
     }
 }
 
@@ -1269,6 +1309,7 @@ void Engine::drop_payloads(const uint64_t* ids, uint64_t n) {
     for (uint64_t i = 0; i < n; ++i) {
         h_off_[ids[i]] = ~0ull;
         h_size_[ids[i]] = kHeaderBytes;
+        if (!sums_ok_.empty()) sums_ok_[ids[i]] = 1;
     }
 }
 
@@ -1300,6 +1341,7 @@ void Engine::partial_sums(double* out3) {
     BMQ_CUDA(cudaSetDevice(dev_));
     ensure_init();
     const uint64_t nid = L_.num_blocks();
+    if (cfg_.compress) ensure_sums();
     if (!cfg_.compress) {
         k_block_sums<<<static_cast<uint32_t>(nid), 256, 0, st_>>>(dense_.p, L_.b, sums_.p);
         BMQ_CUDA(cudaGetLastError());

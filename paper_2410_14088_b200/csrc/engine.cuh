@@ -113,6 +113,11 @@ private:
     void sync_meta_to_host();
     void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
     void host_ids_to_device(const std::vector<uint64_t>& ids);
+    // Per-id dequantised sums are computed lazily (the emit kernel does not
+    // produce them): ensure_sums decodes the payloads of stale ids, all ids
+    // or the n given ones.
+    void ensure_sums(const uint64_t* ids = nullptr, uint64_t n = 0);
+    std::vector<uint8_t> sums_ok_;
     uint64_t zero_payload(uint8_t* out, uint64_t cap) const;
     uint32_t peek_error();
     void check_device_error(const char* what);

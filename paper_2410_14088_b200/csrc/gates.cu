@@ -76,6 +76,7 @@ GateOp make_matrix_op(const Cx* u, bool two_qubit, uint32_t hi_bit, uint32_t lo_
 GateProgram::~GateProgram() {
     if (d_ops) dev_free(d_ops);
     if (d_chain_tab) dev_free(d_chain_tab);
+    if (d_perm_tab) dev_free(d_perm_tab);
 }
 
 namespace {
@@ -212,6 +213,158 @@ std::vector<FastOp> fuse_chains(const std::vector<GateOp>& ops, uint32_t begin, 
     return out;
 }
 
+// Unit index of an exact matrix entry: 1 -> 0, i -> 1, -1 -> 2, -i -> 3.
+int unit_of(double re, double im) {
+    if (im == 0.0 && re == 1.0) return 0;
+    if (re == 0.0 && im == 1.0) return 1;
+    if (im == 0.0 && re == -1.0) return 2;
+    if (re == 0.0 && im == -1.0) return 3;
+    return -1;
+}
+
+bool to_mono(const GateOp& g, MonoOp& o) {
+    o = MonoOp{};
+    o.hi = g.hi;
+    o.lo = g.lo;
+    const auto unit = [&](int e) { return unit_of(g.m[2 * e], g.m[2 * e + 1]); };
+    switch (g.type) {
+    case OP_DIAG: {
+        const int a = unit(0), b = unit(3);
+        if (a < 0 || b < 0) return false;
+        o.kind = MK_DIAG;
+        o.u0 = static_cast<uint8_t>(a);
+        o.u1 = static_cast<uint8_t>(b);
+        return true;
+    }
+    case OP_CDIAG: {
+        const int d = unit(15);
+        if (unit(0) != 0 || unit(5) != 0 || unit(10) != 0 || d < 0) return false;
+        o.kind = MK_CDIAG;
+        o.u1 = static_cast<uint8_t>(d);
+        return true;
+    }
+    case OP_CX:
+        o.kind = MK_MIX;
+        o.tp = g.tp_lo;
+        o.ctl = g.in_hi ? 1 : 2;
+        o.ctl_tp = g.tp_hi;
+        return true;
+    case OP_U2: {
+        if (g.et[0] != ET_ZERO || g.et[3] != ET_ZERO) return false;
+        const int a = unit(1), b = unit(2);
+        if (a < 0 || b < 0) return false;
+        o.kind = MK_MIX;
+        o.tp = g.tp_hi;
+        o.u0 = static_cast<uint8_t>(a);
+        o.u1 = static_cast<uint8_t>(b);
+        return true;
+    }
+    default: return false;
+    }
+}
+
+// A program is code-domain when every op is monomial with unit entries and
+// every pass tiles 2^12 amplitudes.
+void build_mono(GateProgram& prog) {
+    prog.mono = false;
+    if (prog.d_perm_tab) {
+        dev_free(prog.d_perm_tab);
+        prog.d_perm_tab = nullptr;
+    }
+    if (prog.ops.empty() || prog.total_bits < kMaxTileBits) return;
+    std::vector<std::shared_ptr<MonoPass>> mps;
+    const uint64_t all = prog.total_bits >= 64 ? ~0ull : (1ull << prog.total_bits) - 1;
+    for (const GatePass& p : prog.passes) {
+        if (p.tb != kMaxTileBits || p.count > static_cast<uint32_t>(kMaxMonoOps)) return;
+        auto mp = std::make_shared<MonoPass>();
+        std::memset(mp.get(), 0, sizeof(MonoPass));
+        mp->tile = make_runs(p.tile_mask, prog.total_bits, -1);
+        mp->base = make_runs(~p.tile_mask & all, prog.total_bits, static_cast<int>(prog.total_bits));
+        mp->nops = p.count;
+        for (uint32_t i = 0; i < p.count; ++i)
+            if (!to_mono(prog.ops[p.begin + i], mp->ops[i])) return;
+        mps.push_back(mp);
+    }
+    for (size_t i = 0; i < mps.size(); ++i) prog.passes[i].mp = mps[i];
+    prog.mono = true;
+    // Table form of each pass (composite signed permutation per pattern).
+    if (prog.total_bits + 1 > 32) return;  // planar tile offsets are 32-bit
+    std::vector<uint16_t> tabs;
+    std::vector<std::pair<size_t, std::shared_ptr<PermPass>>> pps;
+    for (size_t pi = 0; pi < prog.passes.size(); ++pi) {
+        const GatePass& p = prog.passes[pi];
+        const MonoPass& mp = *p.mp;
+        const auto in_tile = [&](uint32_t bit) { return ((p.tile_mask >> bit) & 1) != 0; };
+        std::vector<uint8_t> pat;
+        const auto need = [&](uint32_t bit) {
+            if (!in_tile(bit) && std::find(pat.begin(), pat.end(), bit) == pat.end()) pat.push_back(static_cast<uint8_t>(bit));
+        };
+        for (uint32_t i = 0; i < mp.nops; ++i) {
+            const MonoOp& o = mp.ops[i];
+            if (o.kind == MK_DIAG) need(o.hi);
+            if (o.kind == MK_CDIAG) {
+                need(o.hi);
+                need(o.lo);
+            }
+            if (o.kind == MK_MIX && o.ctl == 2) need(o.hi);
+        }
+        if (pat.size() > static_cast<size_t>(kMaxPatBits)) continue;
+        auto pp = std::make_shared<PermPass>();
+        std::memset(pp.get(), 0, sizeof(PermPass));
+        pp->tile = mp.tile;
+        pp->base = mp.base;
+        pp->npat_bits = static_cast<uint32_t>(pat.size());
+        for (size_t i = 0; i < pat.size(); ++i) pp->pat_bits[i] = pat[i];
+        const size_t off = tabs.size();
+        for (uint32_t P = 0; P < (1u << pat.size()); ++P) {
+            const auto bitval = [&](uint32_t bit, uint32_t k) -> uint32_t {
+                if (in_tile(bit)) return (k >> rank_in(p.tile_mask, bit)) & 1;
+                const size_t i = std::find(pat.begin(), pat.end(), bit) - pat.begin();
+                return (P >> i) & 1;
+            };
+            std::vector<uint16_t> src(4096);
+            std::vector<uint8_t> U(4096, 0);
+            for (uint32_t k = 0; k < 4096; ++k) src[k] = static_cast<uint16_t>(k);
+            for (uint32_t i = 0; i < mp.nops; ++i) {
+                const MonoOp& o = mp.ops[i];
+                if (o.kind == MK_DIAG) {
+                    for (uint32_t k = 0; k < 4096; ++k) U[k] = (U[k] + (bitval(o.hi, k) ? o.u1 : o.u0)) & 3;
+                } else if (o.kind == MK_CDIAG) {
+                    for (uint32_t k = 0; k < 4096; ++k)
+                        if (bitval(o.hi, k) && bitval(o.lo, k)) U[k] = (U[k] + o.u1) & 3;
+                } else {
+                    const uint32_t m = 1u << o.tp;
+                    for (uint32_t k = 0; k < 4096; ++k) {
+                        if (k & m) continue;
+                        const uint32_t i0 = k, i1 = k | m;
+                        const uint32_t ctl = o.ctl == 0 ? 1u : (o.ctl == 1 ? (i0 >> o.ctl_tp) & 1 : bitval(o.hi, k));
+                        if (!ctl) continue;
+                        const uint16_t s0 = src[i1], s1 = src[i0];
+                        const uint8_t v0 = (U[i1] + o.u0) & 3, v1 = (U[i0] + o.u1) & 3;
+                        src[i0] = s0;
+                        U[i0] = v0;
+                        src[i1] = s1;
+                        U[i1] = v1;
+                    }
+                }
+            }
+            for (uint32_t k = 0; k < 4096; ++k) {
+                const uint32_t u = U[k];
+                tabs.push_back(static_cast<uint16_t>(src[k] | (u & 1) << 12 | ((u ^ (u >> 1)) & 1) << 13 | (u >> 1) << 14));
+            }
+        }
+        pps.push_back({pi, pp});
+        pp->table = reinterpret_cast<const uint16_t*>(off);  // fixed up after upload
+    }
+    if (pps.empty()) return;
+    prog.d_perm_tab = static_cast<uint16_t*>(dev_alloc(tabs.size() * sizeof(uint16_t)));
+    BMQ_CUDA(cudaMemcpy(prog.d_perm_tab, tabs.data(), tabs.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    for (auto& [pi, pp] : pps) {
+        pp->table = prog.d_perm_tab + reinterpret_cast<uintptr_t>(pp->table);
+        prog.passes[pi].pp = pp;
+    }
+}
+
 }  // namespace
 
 void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bits) {
@@ -283,6 +436,7 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
     }
     if (begin < ops.size()) close(begin, static_cast<uint32_t>(ops.size()));
     prog.ops = std::move(ops);
+    build_mono(prog);
     if (prog.d_ops) {
         dev_free(prog.d_ops);
         prog.d_ops = nullptr;
@@ -759,7 +913,259 @@ __global__ void __launch_bounds__(kPassThreads) k_gate_pass(double* __restrict__
     }
 }
 
+// ------------------------------------------------- code-domain pass (mono)
+// Packed code words: (q - qlo) << 2 | negative << 1 | zero. Negation flips
+// the sign bit of a nonzero scalar; -0 is a zero with sign bit 0.
+__device__ __forceinline__ uint32_t code_neg(uint32_t c) { return (c & 1u) ? c : c ^ 2u; }
+
+// (re, im) * unit: 1 -> (re, im); i -> (-im, re); -1 -> (-re, -im); -i -> (im, -re)
+__device__ __forceinline__ uint2 code_unit(uint32_t u, uint2 a) {
+    switch (u & 3u) {
+    case 0: return a;
+    case 1: return make_uint2(code_neg(a.y), a.x);
+    case 2: return make_uint2(code_neg(a.x), code_neg(a.y));
+    default: return make_uint2(a.y, code_neg(a.x));
+    }
+}
+
+__global__ void __launch_bounds__(kFastThreads) k_code_pass(uint32_t* __restrict__ pk, uint32_t lb, uint64_t ntiles,
+                                                            const __grid_constant__ MonoPass pass,
+                                                            ChunkPlan* __restrict__ cps, uint32_t nch) {
+    __shared__ uint2 tile_s[1 << kMaxTileBits];
+    __shared__ uint64_t joff[kPer];
+    __shared__ MonoOp sops[kMaxMonoOps];
+    const uint32_t tid = threadIdx.x;
+    const uint64_t lmask = (1ull << lb) - 1;
+    const uint64_t im_off = 1ull << lb;
+    const uint64_t toff = runs_deposit(tid, pass.tile);
+    if (tid < kPer) joff[tid] = runs_deposit(static_cast<uint64_t>(tid) << 8, pass.tile);
+    for (uint32_t e = tid; e < pass.nops; e += kFastThreads) sops[e] = pass.ops[e];
+    __syncthreads();
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t base = runs_deposit(tile, pass.base);
+        __syncthreads();  // previous tile's stores have read tile_s
+        {
+            uint32_t re[kPer], im[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, 0);
+                re[j] = __ldcs(pk + a);
+                im[j] = __ldcs(pk + a + im_off);
+            }
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) tile_s[tid + 256 * j] = make_uint2(re[j], im[j]);
+        }
+        bool owners_only = true;
+        for (uint32_t i = 0; i < pass.nops; ++i) {
+            const MonoOp g = sops[i];
+            if (g.kind != MK_MIX) {
+                if (!owners_only) __syncthreads();
+                owners_only = true;
+#pragma unroll 4
+                for (int j = 0; j < kPer; ++j) {
+                    const uint64_t x = base | toff | joff[j];
+                    uint32_t u;
+                    if (g.kind == MK_DIAG) {
+                        u = ((x >> g.hi) & 1) ? g.u1 : g.u0;
+                    } else {
+                        if (!((x >> g.hi) & (x >> g.lo) & 1)) continue;
+                        u = g.u1;
+                    }
+                    if (u) {
+                        const uint32_t k = tid + 256u * j;
+                        tile_s[k] = code_unit(u, tile_s[k]);
+                    }
+                }
+                continue;
+            }
+            __syncthreads();
+            owners_only = false;
+            const uint32_t m = 1u << g.tp;
+            const uint32_t bctl = static_cast<uint32_t>((base >> g.hi) & 1);
+            for (uint32_t r = tid; r < 2048; r += kFastThreads) {
+                const uint32_t i0 = insert0(r, g.tp), i1 = i0 | m;
+                const uint32_t ctl = g.ctl == 0 ? 1u : (g.ctl == 1 ? (i0 >> g.ctl_tp) & 1 : bctl);
+                if (!ctl) continue;
+                const uint2 a0 = tile_s[i0], a1 = tile_s[i1];
+                tile_s[i0] = code_unit(g.u0, a1);
+                tile_s[i1] = code_unit(g.u1, a0);
+            }
+        }
+        if (!owners_only) __syncthreads();
+        if (cps) {  // last pass: codes + per-chunk counters (see quant_epilogue)
+            ChunkAcc acc_re, acc_im;
+            uint64_t key_re = ~0ull, key_im = ~0ull;
+            for (int j = 0; j < kPer; ++j) {
+                const uint2 v = tile_s[tid + 256 * j];
+                const uint64_t p = base | toff | joff[j];
+                const uint64_t slot = p >> lb, l = p & lmask;
+                const uint64_t s_im = im_off + l;
+                const uint64_t kre = slot * nch + (l >> 12), kim = slot * nch + (s_im >> 12);
+                if (kre != key_re) {  // warp-uniform
+                    if (key_re != ~0ull) flush_chunk(cps + key_re, acc_re);
+                    acc_re = ChunkAcc{};
+                    key_re = kre;
+                }
+                if (kim != key_im) {
+                    if (key_im != ~0ull) flush_chunk(cps + key_im, acc_im);
+                    acc_im = ChunkAcc{};
+                    key_im = kim;
+                }
+                uint32_t* dst = pk + (slot << (lb + 1));
+                __stcs(dst + l, v.x);
+                __stcs(dst + s_im, v.y);
+                acc_re.add(v.x);
+                acc_im.add(v.y);
+            }
+            flush_chunk(cps + key_re, acc_re);
+            flush_chunk(cps + key_im, acc_im);
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint2 v = tile_s[tid + 256 * j];
+            const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, 0);
+            __stcs(pk + a, v.x);
+            __stcs(pk + a + im_off, v.y);
+        }
+    }
+}
+
+// Table-driven code pass. Thread t owns tile positions 4t + e + 1024 g
+// (e, g in 0..3): positions 0..1 are buffer bits 0..1, so each (t, g) is four
+// consecutive code words of the real half and of the imaginary half (one
+// 16-byte load / store each). The tile is gathered once through the pass's
+// (src, unit) table. The last pass also accumulates per-chunk counters:
+// lanes are grouped by chunk (__match_any_sync) and reduced with REDUX.
+struct CodeAcc4 {
+    uint32_t mn = ~0u, mx = 0, nnz = 0, nneg = 0;  // min / max over nonzero packed words
+    __device__ __forceinline__ void add(uint32_t c) {
+        const uint32_t z = c & 1u;
+        mn = min(mn, z ? ~0u : c);
+        mx = max(mx, z ? 0u : c);
+        nnz += z ^ 1u;
+        nneg += (c >> 1) & 1u;
+    }
+    // all 32 lanes call; lanes with the same key reduce together
+    __device__ __forceinline__ void flush(ChunkPlan* cps, uint64_t key) {
+        const uint32_t grp = __match_any_sync(0xffffffffu, key);
+        const uint32_t a = __reduce_min_sync(grp, mn), b = __reduce_max_sync(grp, mx);
+        const uint32_t n = __reduce_add_sync(grp, nnz), g = __reduce_add_sync(grp, nneg);
+        if ((threadIdx.x & 31) == static_cast<uint32_t>(__ffs(grp) - 1)) {
+            ChunkPlan* cp = cps + key;
+            if (n) {
+                atomicMax(&cp->qmin_inv, kQOffMax - (a >> 2));
+                atomicMax(&cp->qmax_off, b >> 2);
+                atomicAdd(&cp->nnz, n);
+            }
+            if (g) atomicAdd(&cp->nneg, g);
+        }
+        *this = CodeAcc4{};
+    }
+};
+
+__device__ __forceinline__ uint32_t neg_if(uint32_t c, uint32_t n) { return c ^ ((~c & n & 1u) << 1); }
+
+__device__ __forceinline__ void apply_ent(uint32_t e, const uint2* tile_s, uint32_t& x, uint32_t& y) {
+    const uint2 a = tile_s[e & 0xfffu];
+    const bool sw = (e >> 12) & 1u;
+    x = neg_if(sw ? a.y : a.x, e >> 13);
+    y = neg_if(sw ? a.x : a.y, e >> 14);
+}
+
+constexpr int kPermGroups = 4;  // 4 x 4 positions per thread
+
+template <bool kLast>
+__global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict__ pk, uint32_t lb, uint64_t ntiles,
+                                                            const __grid_constant__ PermPass pass,
+                                                            ChunkPlan* __restrict__ cps) {
+    __shared__ __align__(16) uint2 tile_s[1 << kMaxTileBits];
+    const uint32_t tid = threadIdx.x;
+    const uint64_t lmask = (1ull << lb) - 1;
+    const uint64_t im_off = 1ull << lb;
+    uint32_t toffp[kPermGroups];
+#pragma unroll
+    for (int g = 0; g < kPermGroups; ++g) {
+        const uint64_t t = runs_deposit(4u * tid + 1024u * g, pass.tile);
+        toffp[g] = static_cast<uint32_t>(((t >> lb) << (lb + 1)) | (t & lmask));
+    }
+    const uint32_t kshift = lb >= 12 ? 12 : lb + 1;
+    const uint64_t kim = lb >= 12 ? (1ull << (lb - 12)) : 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t base = runs_deposit(tile, pass.base);
+        const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
+        uint4 re[kPermGroups], im[kPermGroups];
+#pragma unroll
+        for (int g = 0; g < kPermGroups; ++g) {
+            re[g] = __ldcs(reinterpret_cast<const uint4*>(pk + pb + toffp[g]));
+            im[g] = __ldcs(reinterpret_cast<const uint4*>(pk + pb + toffp[g] + im_off));
+        }
+        uint32_t pat = 0;
+        for (uint32_t i = 0; i < pass.npat_bits; ++i) pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
+        const uint16_t* tab = pass.table + (static_cast<uint64_t>(pat) << kMaxTileBits);
+        uint2 ent[kPermGroups];
+#pragma unroll
+        for (int g = 0; g < kPermGroups; ++g) ent[g] = __ldg(reinterpret_cast<const uint2*>(tab + 4u * tid + 1024u * g));
+        __syncthreads();  // previous tile's gathers are done
+#pragma unroll
+        for (int g = 0; g < kPermGroups; ++g) {
+            uint4* d = reinterpret_cast<uint4*>(tile_s + 4u * tid + 1024u * g);
+            d[0] = make_uint4(re[g].x, im[g].x, re[g].y, im[g].y);
+            d[1] = make_uint4(re[g].z, im[g].z, re[g].w, im[g].w);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int g = 0; g < kPermGroups; ++g) {
+            uint4 xo, yo;
+            apply_ent(ent[g].x & 0xffffu, tile_s, xo.x, yo.x);
+            apply_ent(ent[g].x >> 16, tile_s, xo.y, yo.y);
+            apply_ent(ent[g].y & 0xffffu, tile_s, xo.z, yo.z);
+            apply_ent(ent[g].y >> 16, tile_s, xo.w, yo.w);
+            const uint64_t addr = pb + toffp[g];
+            __stcs(reinterpret_cast<uint4*>(pk + addr), xo);
+            __stcs(reinterpret_cast<uint4*>(pk + addr + im_off), yo);
+            if (kLast) {
+                CodeAcc4 ar, ai;
+                ar.add(xo.x);
+                ar.add(xo.y);
+                ar.add(xo.z);
+                ar.add(xo.w);
+                ai.add(yo.x);
+                ai.add(yo.y);
+                ai.add(yo.z);
+                ai.add(yo.w);
+                const uint64_t key = addr >> kshift;  // chunk of the real half
+                ar.flush(cps, key);
+                ai.flush(cps, key + kim);
+            }
+        }
+    }
+}
+
 }  // namespace
+
+void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
+                      uint64_t* launches, const QuantOut& quant) {
+    if (!prog.mono) raise(BMQ_ERR_LOGIC, "stage is not a code-domain program");
+    for (size_t pi = 0; pi < prog.passes.size(); ++pi) {
+        const GatePass& p = prog.passes[pi];
+        const uint64_t tiles = nreps << (prog.total_bits - p.tb);
+        const uint64_t grid = std::min<uint64_t>(tiles, 148ull * 6 * 8);
+        const bool last = pi + 1 == prog.passes.size();
+        if (p.pp && lb >= 4) {  // 16-byte groups of four code words stay inside a block half
+            const uint64_t g2 = std::min<uint64_t>(tiles, 148ull * 4 * 16);
+            if (last)
+                k_perm_pass<true><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, quant.cps);
+            else
+                k_perm_pass<false><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, nullptr);
+        } else {
+            k_code_pass<<<static_cast<uint32_t>(grid), kFastThreads, 0, st>>>(pk, lb, tiles, *p.mp,
+                                                                              last ? quant.cps : nullptr, quant.nch);
+        }
+        BMQ_CUDA(cudaGetLastError());
+        if (launches) ++*launches;
+    }
+}
 
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant, const uint32_t* vtab,

@@ -58,12 +58,50 @@ struct FastPass {
     FastOp ops[kMaxFastOps];
 };
 
+// Code-domain ("monomial") ops. Every entry of X, Y, Z, S, Sdg, CX and CZ
+// is 0 or a unit in {1, i, -1, -i}, so the reference product u * a only moves
+// real / imaginary parts and flips signs (up to the sign of an exact zero).
+// A stage made only of such gates maps each decompressed scalar +-E[q] to
+// another +-E[q] of the same code, so it runs on the packed code words
+// (quantiser codes, sign and zero bits) with no floating point at all.
+// Units: 0 = 1, 1 = i, 2 = -1, 3 = -i.
+enum MonoKind : uint8_t { MK_DIAG = 0, MK_CDIAG = 1, MK_MIX = 2 };
+struct MonoOp {
+    uint8_t kind;
+    uint8_t tp;            // MIX: tile position of the mixing bit
+    uint8_t ctl;           // MIX: 0 none, 1 control bit in the tile (ctl_tp), 2 control bit in the base (hi)
+    uint8_t ctl_tp;
+    uint8_t hi, lo;        // buffer bits (DIAG: hi; CDIAG: hi and lo; MIX control: hi)
+    uint8_t u0, u1;        // DIAG: units of |0>, |1>; CDIAG: u1 on |11>; MIX: out0 = u0 a1, out1 = u1 a0
+};
+constexpr int kMaxMonoOps = 512;
+struct MonoPass {
+    BitRuns tile, base;
+    uint32_t nops;
+    MonoOp ops[kMaxMonoOps];
+};
+
+// The composite of a pass's monomial ops on one tile is a signed
+// permutation: out[k] = i^U(k) * in[src(k)], where (src, U) depends on the
+// tile position k and on the few base bits the ops test outside the tile
+// (their values form the "pattern"). Table entry per (pattern, k):
+//   src (12 bits) | swap re/im << 12 | negate re << 13 | negate im << 14
+constexpr int kMaxPatBits = 4;
+struct PermPass {
+    BitRuns tile, base;
+    uint32_t npat_bits;
+    uint8_t pat_bits[kMaxPatBits];  // buffer bits outside the tile, pattern bit i
+    const uint16_t* table;          // [1 << npat_bits][4096] (device)
+};
+
 struct GatePass {
     uint64_t tile_mask;   // buffer bits spanned by one CTA tile
     uint32_t tb;          // popcount(tile_mask)
     uint32_t begin, count;
     bool fast = false;
     std::shared_ptr<FastPass> fp;
+    std::shared_ptr<MonoPass> mp;  // set on every pass when GateProgram::mono
+    std::shared_ptr<PermPass> pp;  // table form of mp (when the pattern bits fit)
 };
 
 struct GateProgram {
@@ -72,8 +110,10 @@ struct GateProgram {
     GateOp* d_ops = nullptr;
     std::vector<double> chain_tab;   // host copy of the chain phase tables
     double* d_chain_tab = nullptr;
+    uint16_t* d_perm_tab = nullptr;  // PermPass tables of all passes
     uint32_t total_bits = 0;
     bool all_diagonal = true;     // no op mixes amplitudes
+    bool mono = false;            // every op is monomial with unit entries (code-domain stage)
     uint64_t diag_cond_mask = 0;  // bits whose values decide whether any op acts
     ~GateProgram();
     GateProgram() = default;
@@ -114,5 +154,11 @@ struct QuantOut {
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant = nullptr,
                  const uint32_t* vtab = nullptr, uint64_t nblocks = 0);
+
+// Code-domain program (prog.mono): the passes permute packed code words in
+// place (planar per block of 2^lb amplitudes, CmpBlock::pk layout); the last
+// pass also accumulates the per-chunk counters into quant->cps (zeroed).
+void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
+                      uint64_t* launches, const QuantOut& quant);
 
 }  // namespace bmq

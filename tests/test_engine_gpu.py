@@ -240,3 +240,48 @@ def test_ghz30_b20_block_sizes(gpu):
         assert sizes[1] == 26
         assert sim.fidelity_analytic("ghz") >= 0.99
         assert abs(rep.final_norm - 1) < 2e-3
+
+
+def monomial_circuit(gpu, rng, n, count):
+    """A dense complex state (H, T, RX layers) followed by `count` random
+    unit-entry monomial gates (X, Y, Z, S, Sdg, CX, CZ) and a closing RY
+    layer, so the plan holds code-domain stages between FP64 stages."""
+    gl = []
+    for q in range(n):
+        gl += [(0, q, 0, 0.0), (6, q, 0, 0.0), (8, q, 0, 0.1 + 0.05 * q)]
+    mono = [1, 2, 3, 4, 5, 12, 13]
+    for _ in range(count):
+        k = int(rng.choice(mono))
+        q0 = int(rng.integers(n))
+        q1 = int((q0 + 1 + rng.integers(n - 1)) % n)
+        gl.append((k, q0, q1 if k >= 12 else 0, 0.0))
+    gl += [(9, q, 0, 0.3) for q in range(0, n, 3)]
+    return gl, gpu.Circuit(n, [gpu.Gate(gpu.GateKind(k), a, b, ang) for k, a, b, ang in gl])
+
+
+@pytest.mark.parametrize("seed,n,b,inner,br", [(0, 16, 12, 2, 1e-3), (1, 17, 12, 3, 1e-4), (2, 16, 13, 1, 1e-2),
+                                               (3, 18, 12, 2, 1e-3)])
+def test_code_domain_stages_are_exact(gpu, port, seed, n, b, inner, br):
+    """Stages of X/Y/Z/S/Sdg/CX/CZ run on quantiser codes (BMQ_FLAG_CODE_DOMAIN):
+    payloads byte-identical to the oracle, with the path on and off."""
+    rng = np.random.default_rng(500 + seed)
+    gl, c = monomial_circuit(gpu, rng, n, 120)
+    want = port.simulate(n, gl, b, inner, br)
+    for on in (True, False):
+        with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=inner, error_bound=br, code_domain=on)) as sim:
+            rep = sim.run()
+            assert (rep.device["code_domain_batches"] > 0) == on
+            assert sim.payloads() == want.payloads
+            assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+            assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=NORM_RTOL)
+
+
+def test_code_domain_qft_swaps(gpu, port):
+    """QFT's closing bit-reversal (CX triples) runs in the code domain."""
+    c = gpu.generate_benchmark("qft", 18)
+    want = port.simulate(18, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=12, inner_size=2, identity_skip=True)) as sim:
+        rep = sim.run()
+        assert rep.device["code_domain_batches"] > 0
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
