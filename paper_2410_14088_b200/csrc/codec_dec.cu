@@ -208,7 +208,7 @@ enum DecMode : int { kDoubles = 0, kCodes = 1, kSumsOnly = 2 };
 // word hold consecutive ranks, so their codes are one contiguous bit range.
 // Each lane loads one aligned 32-bit word of that range; lane j's code is
 // then two shuffles and a funnel shift away (width <= 30). All 32 lanes call.
-__device__ __forceinline__ uint32_t warp_codes(const uint32_t* cs32, uint64_t a0, uint32_t cnt, uint32_t width,
+__device__ __forceinline__ uint32_t warp_codes(const uint32_t* __restrict__ cs32, uint64_t a0, uint32_t cnt, uint32_t width,
                                                uint32_t rank_in_word, uint32_t lane) {
     const uint32_t off0 = static_cast<uint32_t>(a0 & 31);
     const uint64_t w0 = a0 >> 5;
@@ -231,10 +231,14 @@ __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32
                                             double& sq, double& sre, double& sim, bool& bad) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uintptr_t cs = reinterpret_cast<uintptr_t>(codes);
-    const uint32_t* cs32 = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3));
-    const uint32_t bit0 = static_cast<uint32_t>(cs & 3) * 8;
     const bool coop = width <= 30;  // block-uniform
+    // this chunk's codes start at bit cb of the word-aligned segment base
+    const uint64_t cb = static_cast<uint64_t>(cs & 3) * 8 + static_cast<uint64_t>(nz_prefix) * width;
+    const uint32_t* __restrict__ cw = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3)) + (cb >> 5);
+    const uint32_t cb0 = static_cast<uint32_t>(cb & 31);
+    const uint32_t cmask = width >= 32 ? ~0u : (1u << width) - 1;
     const uint32_t lt = (1u << lane) - 1;
+    const uint32_t qb = static_cast<uint32_t>(qbase);  // packed offset of code 0 (window checked when !check)
 #pragma unroll 4
     for (int j = 0; j < 32; ++j) {
         const uint32_t k = 4 * j + w;
@@ -242,23 +246,30 @@ __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32
         const uint32_t s = 32 * k + lane;
         const uint32_t nzw = s_nz[k];
         const bool mine = (nzw >> lane) & 1u;
-        const uint32_t rw = __popc(nzw & lt);
         uint64_t code = 0;
         if (coop) {
-            const uint32_t cnt = __popc(nzw);
-            if (cnt) code = warp_codes(cs32, bit0 + (static_cast<uint64_t>(nz_prefix) + s_pre[k]) * width, cnt, width, rw, lane);
+            const uint32_t a0 = cb0 + s_pre[k] * width;  // chunk-relative bit of the word's first code
+            if (nzw == ~0u) {  // every scalar nonzero: rank = lane
+                const uint32_t a = a0 + lane * width;
+                const uint32_t wlo = __ldg(cw + (a >> 5)), whi = __ldg(cw + (a >> 5) + 1);
+                code = __funnelshift_r(wlo, whi, a & 31) & cmask;
+            } else if (nzw) {
+                code = warp_codes(cw, a0, __popc(nzw), width, __popc(nzw & lt), lane);
+            }
         } else if (mine) {
-            code = read_bits(codes, (static_cast<uint64_t>(nz_prefix) + s_pre[k] + rw) * width, width);
+            code = read_bits(codes, (static_cast<uint64_t>(nz_prefix) + s_pre[k] + __popc(nzw & lt)) * width, width);
         }
-        // packed word / table index of the code: q - qlo (qbase = code_min - qlo)
-        const int64_t qo = qbase + static_cast<int64_t>(code);
-        if (check && mine && (qo < lo || qo > hi)) bad = true;
-        const bool neg = (s_sign[k] >> lane) & 1u;
+        if (check && mine) {
+            const int64_t qo = qbase + static_cast<int64_t>(code);
+            if (qo < lo || qo > hi) bad = true;
+        }
+        const uint32_t neg = (s_sign[k] >> lane) & 1u;
         if constexpr (kMode == kCodes) {
-            const uint32_t pkw = mine ? pack_code(static_cast<uint32_t>(qo), neg, false) : 1u;
-            if (kFull || s < len) cdst[s] = pkw;
+            const uint32_t pkw = mine ? ((qb + static_cast<uint32_t>(code)) << 2) | (neg << 1) : 1u;
+            if (kFull || s < len) __stcs(cdst + s, pkw);
         } else {
             double v = 0.0;
+            const int64_t qo = qbase + static_cast<int64_t>(code);
             if (mine && !(check && (qo < lo || qo > hi))) {
                 const double m = __ldg(t.dequant + qo);
                 v = neg ? -m : m;
@@ -270,7 +281,7 @@ __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32
                         sim += v;
                 }
             }
-            if (kMode == kDoubles && (kFull || s < len)) dst[s] = v;
+            if (kMode == kDoubles && (kFull || s < len)) __stcs(dst + s, v);
         }
     }
 }

@@ -156,7 +156,7 @@ FastOp to_fast(const GateOp& g) {
 // complex entry) that share one bit and whose other bits are distinct and
 // monotone become one OP_CHAIN with a 64-entry phase table.
 std::vector<FastOp> fuse_chains(const std::vector<GateOp>& ops, uint32_t begin, uint32_t end,
-                                std::vector<double>& tab) {
+                                std::vector<double>& tab, uint64_t tile_mask) {
     std::vector<FastOp> out;
     const size_t pass_base = tab.size();  // chain offsets are relative to the pass
     const auto chainable = [](const GateOp& o) {
@@ -198,6 +198,8 @@ std::vector<FastOp> fuse_chains(const std::vector<GateOp>& ops, uint32_t begin, 
                     FastOp f{};
                     f.type = OP_CHAIN;
                     f.hi = static_cast<uint8_t>(c);
+                    f.in_hi = static_cast<uint8_t>((tile_mask >> c) & 1);
+                    f.tp_hi = f.in_hi ? rank_in(tile_mask, c) : 0;
                     f.et[0] = desc ? 1 : 0;
                     f.pad2 = static_cast<uint32_t>((off - pass_base) / 2);
                     std::memcpy(&f.m[0], &R, 8);
@@ -398,7 +400,7 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
         }
         if (fast) {
             const size_t tab_mark = prog.chain_tab.size();
-            std::vector<FastOp> fops = fuse_chains(ops, begin, end, prog.chain_tab);
+            std::vector<FastOp> fops = fuse_chains(ops, begin, end, prog.chain_tab, mask);
             if (fops.size() > static_cast<size_t>(kMaxFastOps) && end - begin > 1) {
                 prog.chain_tab.resize(tab_mark);
                 const uint32_t mid = begin + (end - begin) / 2;
@@ -568,50 +570,52 @@ __device__ __forceinline__ C2 chain_walk(uint32_t s, bool desc, const double2* t
     return a;
 }
 
+constexpr int kLanesPerStep = 8;
+
 template <bool kDesc>
 __device__ __forceinline__ int next_bit(uint32_t s) {
     return kDesc ? 31 - __clz(s) : __ffs(s) - 1;
 }
 
-// A lone phase chain over the thread's 16 amplitudes, eight at a time held
-// in registers. The chain's bits are visited once per thread in program
-// order (one bit scan and one phase load shared by eight amplitudes); each
-// amplitude multiplies when its own bit is set. The eight products of one
-// step are independent, so the FP64 pipeline stays busy.
-constexpr int kLanesPerStep = 8;
-
+// A lone phase chain (control c, other bits R, phases in program order).
+// Only amplitudes with bit c set are touched, so when c lies in the tile
+// the thread takes eight of the 2048 positions with that bit set (bit c
+// inserted into t + 256 i); when c is a base bit, the whole tile (or none of
+// it) qualifies.
 template <bool kDesc>
-__device__ __forceinline__ void chain_walks(double2* tile_s, const double2* tab, uint32_t tid, uint64_t xbase,
-                                            const uint64_t* joff, uint32_t c, uint32_t R) {
-    for (int h = 0; h < kPer / kLanesPerStep; ++h) {
-        uint32_t xs[kLanesPerStep];
-        uint32_t any = 0;
+__device__ __forceinline__ void chain_walk8(double2* tile_s, const double2* tab, uint32_t tid, uint32_t xlo,
+                                            const uint32_t* lut_lo, const uint32_t* lut_hi, int pc, uint32_t R,
+                                            uint32_t round) {
+    uint32_t pos[kLanesPerStep], sb[kLanesPerStep];
+    C2 a[kLanesPerStep];
+    uint32_t any = 0;
 #pragma unroll
-        for (int q = 0; q < kLanesPerStep; ++q) {
-            const uint64_t x = xbase | joff[h * kLanesPerStep + q];
-            xs[q] = ((x >> c) & 1) ? static_cast<uint32_t>(x) & R : 0u;
-            any |= xs[q];
-        }
-        if (!any) continue;
-        C2 a[kLanesPerStep];
+    for (int q = 0; q < kLanesPerStep; ++q) {
+        const uint32_t r = tid + 256u * (q + kLanesPerStep * round);
+        const uint32_t p = pc >= 0 ? (((r >> pc) << (pc + 1)) | (1u << pc) | (r & ((1u << pc) - 1))) : r;
+        pos[q] = p;
+        sb[q] = (xlo | lut_lo[p & 63] | lut_hi[p >> 6]) & R;
+        any |= sb[q];
+    }
 #pragma unroll
-        for (int q = 0; q < kLanesPerStep; ++q) {
-            const double2 v = tile_s[tid + 256u * (h * kLanesPerStep + q)];
-            a[q] = C2{v.x, v.y};
-        }
-        uint32_t rem = any;  // bits of R set in at least one of the eight
-        while (rem) {
-            const int r = next_bit<kDesc>(rem);
-            rem &= ~(1u << r);
-            const double2 u = tab[r];
-#pragma unroll
-            for (int q = 0; q < kLanesPerStep; ++q)
-                if ((xs[q] >> r) & 1u) a[q] = cmul(u.x, u.y, a[q]);
-        }
+    for (int q = 0; q < kLanesPerStep; ++q) {
+        const double2 v = tile_s[pos[q]];
+        a[q] = C2{v.x, v.y};
+    }
+    // walk the union of the eight masks (the eight positions differ only in
+    // the three tile bits taken from i); each amplitude multiplies when its
+    // own bit is set, so one bit scan and one phase load serve all eight
+    uint32_t rem = any;
+    while (rem) {
+        const int r = next_bit<kDesc>(rem);
+        rem &= ~(1u << r);
+        const double2 u = tab[r];
 #pragma unroll
         for (int q = 0; q < kLanesPerStep; ++q)
-            tile_s[tid + 256u * (h * kLanesPerStep + q)] = make_double2(a[q].re, a[q].im);
+            if ((sb[q] >> r) & 1u) a[q] = cmul(u.x, u.y, a[q]);
     }
+#pragma unroll
+    for (int q = 0; q < kLanesPerStep; ++q) tile_s[pos[q]] = make_double2(a[q].re, a[q].im);
 }
 
 __device__ __forceinline__ C2 apply_diag_run(const FastOp* ops, const double2* stab, uint32_t q0, uint32_t q1,
@@ -683,6 +687,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     // dynamic SMEM: 4096 amplitudes (tile position k) | chain tables | ops
     extern __shared__ double2 tile_s[];
     __shared__ uint64_t joff[kPer];
+    __shared__ uint32_t lut_lo[64], lut_hi[64];  // tile position -> buffer bits (low 32)
     double2* stab = tile_s + 4096;
     FastOp* sops = reinterpret_cast<FastOp*>(stab + pass.tab_entries);
     const uint32_t tid = threadIdx.x;
@@ -690,6 +695,8 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     const uint64_t im_off = interleaved ? 1 : (1ull << lb);
     const uint64_t toff = runs_deposit(tid, pass.tile);
     if (tid < kPer) joff[tid] = runs_deposit(static_cast<uint64_t>(tid) << 8, pass.tile);
+    if (tid < 64) lut_lo[tid] = static_cast<uint32_t>(runs_deposit(tid, pass.tile));
+    else if (tid < 128) lut_hi[tid - 64] = static_cast<uint32_t>(runs_deposit(static_cast<uint64_t>(tid - 64) << 6, pass.tile));
     for (uint32_t e = tid; e < pass.tab_entries; e += kFastThreads)
         stab[e] = __ldg(reinterpret_cast<const double2*>(pass.chain_tab) + pass.tab_base + e);
     {
@@ -726,15 +733,23 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 if (!owners_only) __syncthreads();
                 owners_only = true;
                 if (i2 == i + 1 && g.type == OP_CHAIN) {  // a lone phase chain: parameters in registers
-                    const uint32_t c = g.hi;
                     uint32_t R;
                     memcpy(&R, &g.m[0], 4);
                     const bool desc = g.et[0] != 0;
                     const double2* tab = stab + g.pad2;
-                    if (desc)
-                        chain_walks<true>(tile_s, tab, tid, xbase | toff, joff, c, R);
-                    else
-                        chain_walks<false>(tile_s, tab, tid, xbase | toff, joff, c, R);
+                    const int pc = g.in_hi ? g.tp_hi : -1;
+                    const uint32_t xlo = static_cast<uint32_t>(xbase);
+                    if (pc >= 0 || ((xbase >> g.hi) & 1)) {
+                        __syncthreads();  // positions cross thread ownership
+                        const uint32_t rounds = pc >= 0 ? 1 : 2;
+                        for (uint32_t rd = 0; rd < rounds; ++rd) {
+                            if (desc)
+                                chain_walk8<true>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, rd);
+                            else
+                                chain_walk8<false>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, rd);
+                        }
+                        owners_only = false;
+                    }
                 } else {
                     for (int j = 0; j < kPer; ++j) {
                         const uint32_t k = tid + 256u * j;
