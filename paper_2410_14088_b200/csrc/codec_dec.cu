@@ -223,12 +223,12 @@ __device__ __forceinline__ uint32_t warp_codes(const uint32_t* __restrict__ cs32
 // Per-scalar loop of one chunk. kFull: a whole 4096-scalar chunk (no
 // partial words). check: some code of the block may fall outside the window
 // (block-uniform; decided from code_min and the width).
-template <int kMode, bool kFull>
+template <int kMode, bool kFull, bool kCheck>
 __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32_t* s_nz, const uint32_t* s_pre,
                                             const uint8_t* codes, uint32_t width, uint32_t nz_prefix, uint32_t len,
-                                            int64_t qbase, int64_t lo, int64_t hi, bool check, const DevTables& t,
-                                            double* dst, uint32_t* cdst, uint64_t half, uint64_t g0, bool sums,
-                                            double& sq, double& sre, double& sim, bool& bad) {
+                                            int64_t qbase, int64_t lo, int64_t hi, const DevTables& t, double* dst,
+                                            uint32_t* cdst, uint64_t half, uint64_t g0, bool sums, double& sq,
+                                            double& sre, double& sim, bool& bad) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uintptr_t cs = reinterpret_cast<uintptr_t>(codes);
     const bool coop = width <= 30;  // block-uniform
@@ -238,40 +238,22 @@ __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32
     const uint32_t cb0 = static_cast<uint32_t>(cb & 31);
     const uint32_t cmask = width >= 32 ? ~0u : (1u << width) - 1;
     const uint32_t lt = (1u << lane) - 1;
-    const uint32_t qb = static_cast<uint32_t>(qbase);  // packed offset of code 0 (window checked when !check)
-#pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t k = 4 * j + w;
-        if (!kFull && k * 32 >= len) break;  // warp-uniform; later words are empty too
-        const uint32_t s = 32 * k + lane;
-        const uint32_t nzw = s_nz[k];
-        const bool mine = (nzw >> lane) & 1u;
-        uint64_t code = 0;
-        if (coop) {
-            const uint32_t a0 = cb0 + s_pre[k] * width;  // chunk-relative bit of the word's first code
-            if (nzw == ~0u) {  // every scalar nonzero: rank = lane
-                const uint32_t a = a0 + lane * width;
-                const uint32_t wlo = __ldg(cw + (a >> 5)), whi = __ldg(cw + (a >> 5) + 1);
-                code = __funnelshift_r(wlo, whi, a & 31) & cmask;
-            } else if (nzw) {
-                code = warp_codes(cw, a0, __popc(nzw), width, __popc(nzw & lt), lane);
-            }
-        } else if (mine) {
-            code = read_bits(codes, (static_cast<uint64_t>(nz_prefix) + s_pre[k] + __popc(nzw & lt)) * width, width);
-        }
-        if (check && mine) {
+    const uint32_t qb = static_cast<uint32_t>(qbase);  // packed offset of code 0 (in window when !kCheck)
+    const auto emit = [&](uint32_t s, bool mine, uint64_t code, uint32_t neg) {
+        if (kCheck && mine) {
             const int64_t qo = qbase + static_cast<int64_t>(code);
-            if (qo < lo || qo > hi) bad = true;
+            if (qo < lo || qo > hi) {
+                bad = true;
+                mine = false;
+            }
         }
-        const uint32_t neg = (s_sign[k] >> lane) & 1u;
         if constexpr (kMode == kCodes) {
             const uint32_t pkw = mine ? ((qb + static_cast<uint32_t>(code)) << 2) | (neg << 1) : 1u;
             if (kFull || s < len) __stcs(cdst + s, pkw);
         } else {
             double v = 0.0;
-            const int64_t qo = qbase + static_cast<int64_t>(code);
-            if (mine && !(check && (qo < lo || qo > hi))) {
-                const double m = __ldg(t.dequant + qo);
+            if (mine) {
+                const double m = __ldg(t.dequant + (qb + static_cast<uint32_t>(code)));
                 v = neg ? -m : m;
                 if (kMode == kSumsOnly || sums) {
                     sq += m * m;
@@ -283,6 +265,28 @@ __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32
             }
             if (kMode == kDoubles && (kFull || s < len)) __stcs(dst + s, v);
         }
+    };
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t k = 4 * j + w;
+        if (!kFull && k * 32 >= len) break;  // warp-uniform; later words are empty too
+        const uint32_t s = 32 * k + lane;
+        const uint32_t nzw = s_nz[k];
+        const uint32_t neg = (s_sign[k] >> lane) & 1u;
+        if (coop && nzw == ~0u) {  // every scalar nonzero: rank = lane
+            const uint32_t a = cb0 + s_pre[k] * width + lane * width;
+            const uint32_t wlo = __ldg(cw + (a >> 5)), whi = __ldg(cw + (a >> 5) + 1);
+            emit(s, true, __funnelshift_r(wlo, whi, a & 31) & cmask, neg);
+            continue;
+        }
+        const bool mine = (nzw >> lane) & 1u;
+        uint64_t code = 0;
+        if (coop) {
+            if (nzw) code = warp_codes(cw, cb0 + s_pre[k] * width, __popc(nzw), width, __popc(nzw & lt), lane);
+        } else if (mine) {
+            code = read_bits(codes, (static_cast<uint64_t>(nz_prefix) + s_pre[k] + __popc(nzw & lt)) * width, width);
+        }
+        emit(s, mine, code, neg);
     }
 }
 
@@ -341,12 +345,13 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     bool bad = false;
     const uint64_t half = info.count / 2, g0 = static_cast<uint64_t>(c) * kChunk;
     const uint8_t* codes = blk.in + info.code_seg;
-    if (len == kChunk)
-        dec_scalars<kMode, true>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, check, t, dst,
-                                 cdst, half, g0, want_sums != 0, sq, sre, sim, bad);
+    const bool sums = want_sums != 0;
+    if (len == kChunk && !check)
+        dec_scalars<kMode, true, false>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, t, dst,
+                                        cdst, half, g0, sums, sq, sre, sim, bad);
     else
-        dec_scalars<kMode, false>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, check, t, dst,
-                                  cdst, half, g0, want_sums != 0, sq, sre, sim, bad);
+        dec_scalars<kMode, false, true>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, t, dst,
+                                        cdst, half, g0, sums, sq, sre, sim, bad);
     if (bad) dev_fail(err, DE_CODE_WINDOW, bi);
     if (kMode == kSumsOnly || (kMode == kDoubles && want_sums)) block_sums3(sq, sre, sim, s_red, &infos[bi].sumsq);
 }
