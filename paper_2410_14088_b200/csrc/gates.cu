@@ -152,6 +152,36 @@ FastOp to_fast(const GateOp& g) {
     return f;
 }
 
+// Tile positions of a lone chain's walk (4 bits each, packed): five lane
+// positions (the lowest, so SMEM accesses stay dense), three warp positions,
+// three per-thread positions and (control outside the tile) one round
+// position. The per-thread positions prefer tile bits outside R, where the
+// thread's amplitudes have identical masks and every product is useful.
+uint64_t chain_positions(uint64_t tile_mask, int pc, uint64_t R) {
+    std::vector<int> rest, lanes;
+    for (int p = 0; p < static_cast<int>(kMaxTileBits); ++p)
+        if (p != pc) rest.push_back(p);
+    lanes.assign(rest.begin(), rest.begin() + 5);
+    rest.erase(rest.begin(), rest.begin() + 5);
+    const auto in_r = [&](int p) {
+        uint64_t m = tile_mask;
+        for (int k = 0; k < p; ++k) m &= m - 1;  // drop the p lowest set bits
+        const int bit = __builtin_ctzll(m);
+        return ((R >> bit) & 1) != 0;
+    };
+    std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return !in_r(a) && in_r(b); });
+    const int qb = kChainQBits;
+    std::vector<int> q(rest.begin(), rest.begin() + qb);     // per-thread
+    std::vector<int> other(rest.begin() + qb, rest.end());   // warps, then rounds
+    std::vector<int> order = lanes;                           // [0, 5): lanes
+    order.insert(order.end(), other.begin(), other.begin() + 3);  // [5, 8): warps
+    order.insert(order.end(), q.begin(), q.end());                // [8, 8 + qb): per thread
+    order.insert(order.end(), other.begin() + 3, other.end());    // rounds
+    uint64_t plan = 0;
+    for (size_t i = 0; i < order.size(); ++i) plan |= static_cast<uint64_t>(order[i]) << (4 * i);
+    return plan;
+}
+
 // Fast ops for [begin, end): consecutive CP-like ops (OP_CDIAG with a
 // complex entry) that share one bit and whose other bits are distinct and
 // monotone become one OP_CHAIN with a 64-entry phase table.
@@ -200,6 +230,8 @@ std::vector<FastOp> fuse_chains(const std::vector<GateOp>& ops, uint32_t begin, 
                     f.hi = static_cast<uint8_t>(c);
                     f.in_hi = static_cast<uint8_t>((tile_mask >> c) & 1);
                     f.tp_hi = f.in_hi ? rank_in(tile_mask, c) : 0;
+                    const uint64_t plan = chain_positions(tile_mask, f.in_hi ? f.tp_hi : -1, R);
+                    std::memcpy(&f.m[1], &plan, 8);
                     f.et[0] = desc ? 1 : 0;
                     f.pad2 = static_cast<uint32_t>((off - pass_base) / 2);
                     std::memcpy(&f.m[0], &R, 8);
@@ -570,7 +602,7 @@ __device__ __forceinline__ C2 chain_walk(uint32_t s, bool desc, const double2* t
     return a;
 }
 
-constexpr int kLanesPerStep = 8;
+constexpr int kLanesPerStep = 1 << kChainQBits;
 
 template <bool kDesc>
 __device__ __forceinline__ int next_bit(uint32_t s) {
@@ -585,34 +617,52 @@ __device__ __forceinline__ int next_bit(uint32_t s) {
 template <bool kDesc>
 __device__ __forceinline__ void chain_walk8(double2* tile_s, const double2* tab, uint32_t tid, uint32_t xlo,
                                             const uint32_t* lut_lo, const uint32_t* lut_hi, int pc, uint32_t R,
-                                            uint32_t round) {
+                                            uint64_t plan, uint32_t round) {
     uint32_t pos[kLanesPerStep], sb[kLanesPerStep];
     C2 a[kLanesPerStep];
-    uint32_t any = 0;
+    uint32_t tb = pc >= 0 ? (1u << pc) : 0u;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) tb |= ((tid >> b) & 1u) << ((plan >> (4 * b)) & 15);
+#pragma unroll
+    for (int b = 0; b < 4; ++b)  // round bits follow the per-thread bits
+        if (8 + kChainQBits + b < 12 - (pc >= 0 ? 1 : 0)) tb |= ((round >> b) & 1u) << ((plan >> (4 * (8 + kChainQBits + b))) & 15);
+    uint32_t qo[kChainQBits];
+#pragma unroll
+    for (int b = 0; b < kChainQBits; ++b) qo[b] = 1u << ((plan >> (4 * (8 + b))) & 15);
+    uint32_t any = 0, all = ~0u;
 #pragma unroll
     for (int q = 0; q < kLanesPerStep; ++q) {
-        const uint32_t r = tid + 256u * (q + kLanesPerStep * round);
-        const uint32_t p = pc >= 0 ? (((r >> pc) << (pc + 1)) | (1u << pc) | (r & ((1u << pc) - 1))) : r;
+        uint32_t p = tb;
+#pragma unroll
+        for (int b = 0; b < kChainQBits; ++b)
+            if ((q >> b) & 1) p |= qo[b];
         pos[q] = p;
         sb[q] = (xlo | lut_lo[p & 63] | lut_hi[p >> 6]) & R;
         any |= sb[q];
+        all &= sb[q];
     }
 #pragma unroll
     for (int q = 0; q < kLanesPerStep; ++q) {
         const double2 v = tile_s[pos[q]];
         a[q] = C2{v.x, v.y};
     }
-    // walk the union of the eight masks (the eight positions differ only in
-    // the three tile bits taken from i); each amplitude multiplies when its
-    // own bit is set, so one bit scan and one phase load serve all eight
+    // Walk the union of the eight masks in program order; bits set in all
+    // eight multiply unconditionally (independent products, full ILP), the
+    // others under each amplitude's own bit. One bit scan and one phase load
+    // serve all eight amplitudes.
     uint32_t rem = any;
     while (rem) {
         const int r = next_bit<kDesc>(rem);
         rem &= ~(1u << r);
         const double2 u = tab[r];
+        if ((all >> r) & 1u) {
 #pragma unroll
-        for (int q = 0; q < kLanesPerStep; ++q)
-            if ((sb[q] >> r) & 1u) a[q] = cmul(u.x, u.y, a[q]);
+            for (int q = 0; q < kLanesPerStep; ++q) a[q] = cmul(u.x, u.y, a[q]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kLanesPerStep; ++q)
+                if ((sb[q] >> r) & 1u) a[q] = cmul(u.x, u.y, a[q]);
+        }
     }
 #pragma unroll
     for (int q = 0; q < kLanesPerStep; ++q) tile_s[pos[q]] = make_double2(a[q].re, a[q].im);
@@ -734,19 +784,21 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 owners_only = true;
                 if (i2 == i + 1 && g.type == OP_CHAIN) {  // a lone phase chain: parameters in registers
                     uint32_t R;
+                    uint64_t plan;
                     memcpy(&R, &g.m[0], 4);
+                    memcpy(&plan, &g.m[1], 8);
                     const bool desc = g.et[0] != 0;
                     const double2* tab = stab + g.pad2;
                     const int pc = g.in_hi ? g.tp_hi : -1;
                     const uint32_t xlo = static_cast<uint32_t>(xbase);
                     if (pc >= 0 || ((xbase >> g.hi) & 1)) {
                         __syncthreads();  // positions cross thread ownership
-                        const uint32_t rounds = pc >= 0 ? 1 : 2;
+                        const uint32_t rounds = (pc >= 0 ? 2048u : 4096u) / (256u * kLanesPerStep);
                         for (uint32_t rd = 0; rd < rounds; ++rd) {
                             if (desc)
-                                chain_walk8<true>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, rd);
+                                chain_walk8<true>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, plan, rd);
                             else
-                                chain_walk8<false>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, rd);
+                                chain_walk8<false>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, plan, rd);
                         }
                         owners_only = false;
                     }

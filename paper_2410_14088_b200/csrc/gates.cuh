@@ -46,6 +46,7 @@ struct FastOp {
 };
 
 constexpr uint32_t kMaxTileBits = 12;  // 4096 amplitudes per tile
+constexpr int kChainQBits = 3;         // a lone chain walks 2^kChainQBits amplitudes per thread together
 constexpr int kMaxFastOps = 96;
 
 struct FastPass {
