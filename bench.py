@@ -194,6 +194,52 @@ def cpu_baseline(seconds_hint=20.0):
             "extrapolated_full_run_s": (1 << w["n"]) * len(plan) / value}
 
 
+def measure_e2e(cbq, circ, cfg, amp_stages, args, dist, world):
+    """The same simulation end to end through the C ABI, host buffers in and
+    out: gate list from pinned host memory -> bmq_simulator_create (H2D,
+    partition, allocation) -> run -> bmq_simulator_get_payloads into a pinned
+    host buffer (every final payload D2H) -> destroy."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2410_14088_b200 import _lib
+    lib = _lib.lib
+    gates = circ.c_array()
+    gate_bytes = C.sizeof(gates)
+    pinned_in = torch.empty(gate_bytes, dtype=torch.uint8, pin_memory=True)
+    C.memmove(pinned_in.data_ptr(), C.addressof(gates), gate_bytes)
+    gates_ptr = C.c_void_p(pinned_in.data_ptr())
+    ccfg = cfg.to_c()
+    pinned_out, sizes = None, None
+    times = []
+    h2d = d2h = 0
+    for step in range(max(1, min(args.steps, 3)) + 1):
+        barrier_sync(dist)
+        t0 = time.perf_counter()
+        h = C.c_void_p()
+        cbq._check(lib.bmq_simulator_create(circ.num_qubits, gates_ptr, len(gates), C.byref(ccfg), C.byref(h)))
+        rep = _lib.bmq_report()
+        cbq._check(lib.bmq_simulator_run(h, C.byref(rep), None, 0))
+        total = C.c_uint64()
+        if sizes is None:
+            nblk = 1 << (circ.num_qubits - cfg.block_bits)
+            sizes = np.zeros(nblk, dtype=np.uint64)
+        cbq._check(lib.bmq_simulator_get_payloads(h, None, 0, sizes.ctypes.data, C.byref(total)))
+        if pinned_out is None or pinned_out.numel() < total.value:
+            pinned_out = torch.empty(max(1, total.value), dtype=torch.uint8, pin_memory=True)
+        cbq._check(lib.bmq_simulator_get_payloads(h, C.c_void_p(pinned_out.data_ptr()), total.value,
+                                                  sizes.ctypes.data, C.byref(total)))
+        lib.bmq_simulator_destroy(h)
+        dt = time.perf_counter() - t0
+        if step > 0:  # first call is the warm-up (module load, table cache, pinned buffer)
+            times.append(dt)
+        h2d = gate_bytes
+        d2h = int(total.value) + 8 * len(sizes)
+    t_e2e = max_over_ranks(dist, statistics.median(times))
+    return {"value": world * amp_stages / t_e2e, "unit": "amp-stages/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "seconds": t_e2e}
+
+
 def phase_roofline(d, t_dev):
     """Dominant device phase: algorithmic bytes / CUDA-event time."""
     peak, peak_kind = load_peaks()
@@ -363,25 +409,7 @@ def main():
     # ---------------------------------------------------------------- e2e
     e2e = None
     if not args.no_e2e:
-        times = []
-        h2d = d2h = 0
-        gates_arr = circ.c_array()
-        for step in range(max(1, min(args.steps, 3)) + 1):
-            barrier_sync(dist)
-            t0 = time.perf_counter()
-            s2 = cbq.Simulator(circ, cfg)
-            s2.run()
-            pays = s2.payloads()
-            s2.close()
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
-            if step > 0:  # first call is the warm-up (CUDA module load, table cache)
-                times.append(dt)
-            h2d = len(bytes(gates_arr)) + 8
-            d2h = sum(len(p) for p in pays) + 8 * len(pays)
-        t_e2e = max_over_ranks(dist, statistics.median(times))
-        e2e = {"value": world * amp_stages / t_e2e, "unit": "amp-stages/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "seconds": t_e2e}
+        e2e = measure_e2e(cbq, circ, cfg, amp_stages, args, dist, world)
     roofline = phase_roofline(rep.device, t_dev)
     line = {
         "metric": "amp-stages/s (QFT-34, b=20, inner=2, b_r=1e-3)", "value": value, "unit": "amp-stages/s",
