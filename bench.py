@@ -34,7 +34,41 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(name="qft", n=34, b=20, inner=2, error_bound=1e-3)
+WORKLOAD = dict(name="qft", n=34, b=20, inner=2, error_bound=1e-3, layers=1)
+
+
+def metric_name(w):
+    label = {"qft": "QFT", "ghz": "GHZ", "qaoa3reg": "QAOA-3reg", "random": "random", "qaoa": "QAOA-ring",
+             "bv": "BV"}.get(w["name"], w["name"])
+    extra = f", p={w['layers']}" if w["name"] in ("qaoa", "qaoa3reg") else (
+        f", depth={w['layers']}" if w["name"] == "random" else "")
+    return f"amp-stages/s ({label}-{w['n']}{extra}, b={w['b']}, inner={w['inner']}, b_r={w['error_bound']:g})"
+
+
+def workload_tag(w):
+    lay = f"_l{w['layers']}" if w["name"] in ("qaoa", "qaoa3reg", "random") else ""
+    return f"{w['name']}{w['n']}{lay}_b{w['b']}_i{w['inner']}_br{w['error_bound']:g}"
+
+
+def data_desc(w):
+    what = {"qft": "QFT|0> circuit", "ghz": "GHZ circuit", "qaoa3reg": "QAOA MaxCut on a seeded random 3-regular graph",
+            "random": "seeded sqrt-X/Y/W + CZ grid random circuit"}.get(w["name"], w["name"] + " circuit")
+    return f"synthetic ({what} generated in-process; no datasets)"
+
+
+def fidelity_of(cbq, sim, circ, cfg, w):
+    """QFT|0> and GHZ have analytic ideal states; other circuits are compared
+    with an uncompressed FP64 device run when its dense state fits (n <= 32)."""
+    if w["name"] == "qft":
+        return sim.fidelity_analytic("uniform")
+    if w["name"] in ("ghz", "cat_state"):
+        return sim.fidelity_analytic("ghz")
+    if w["n"] > 32:
+        return None
+    import dataclasses
+    with cbq.Simulator(circ, dataclasses.replace(cfg, compress=False)) as exact:
+        exact.run()
+        return sim.fidelity_with(exact)
 
 
 def load_peaks():
@@ -281,7 +315,7 @@ def main_sharded(args, world, rank, local, dist):
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
     w = WORKLOAD
-    circ = cbq.generate_benchmark(w["name"], w["n"])
+    circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
     cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
                      identity_skip=not args.no_identity_skip)
     col = TorchCollective(torch.device("cuda", local))
@@ -332,11 +366,11 @@ def main_sharded(args, world, rank, local, dist):
         e2e = {"value": amp_stages / t_e2e, "unit": "amp-stages/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "seconds": t_e2e}
     line = {
-        "metric": "amp-stages/s (QFT-34, b=20, inner=2, b_r=1e-3)", "value": value, "unit": "amp-stages/s",
+        "metric": metric_name(w), "value": value, "unit": "amp-stages/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (QFT|0> circuit generated in-process; no datasets)",
-        "config": {"workload": f"qft{w['n']}_b{w['b']}_i{w['inner']}_br1e-3", "stages": stages,
+        "data": data_desc(w),
+        "config": {"workload": workload_tag(w), "stages": stages,
                    "parallelism": f"shard{world} (device qubits, NCCL payload remaps)",
                    "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
                    "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},
@@ -361,6 +395,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="bmq", choices=["bmq", "reference"])
+    ap.add_argument("--workload", default=WORKLOAD["name"], choices=["qft", "ghz", "qaoa3reg", "random", "qaoa", "bv"])
+    ap.add_argument("--layers", type=int, default=None, help="QAOA layers p / random-circuit depth")
+    ap.add_argument("--error-bound", type=float, default=None)
     ap.add_argument("--qubits", type=int, default=WORKLOAD["n"])
     ap.add_argument("--block-bits", type=int, default=WORKLOAD["b"])
     ap.add_argument("--inner-size", type=int, default=WORKLOAD["inner"])
@@ -374,7 +411,17 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    WORKLOAD.update(n=args.qubits, b=args.block_bits, inner=args.inner_size)
+    WORKLOAD.update(name=args.workload, n=args.qubits, b=args.block_bits, inner=args.inner_size)
+    if args.layers is not None:
+        WORKLOAD["layers"] = args.layers
+    elif args.workload in ("qaoa", "qaoa3reg"):
+        WORKLOAD["layers"] = 4
+    elif args.workload == "random":
+        WORKLOAD["layers"] = 40
+    if args.error_bound is not None:
+        WORKLOAD["error_bound"] = args.error_bound
+    if args.workload != "qft":
+        args.no_cpu_baseline = True  # the sampled CPU baseline is defined on the QFT plan
     world, rank, local, dist = dist_setup()
     import torch
     torch.cuda.set_device(local)
@@ -382,7 +429,7 @@ def main():
         return main_sharded(args, world, rank, local, dist)
     from paper_2410_14088_b200 import cbq
     w = WORKLOAD
-    circ = cbq.generate_benchmark(w["name"], w["n"])
+    circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
     cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
                      identity_skip=not args.no_identity_skip)
     sim = cbq.Simulator(circ, cfg)
@@ -403,7 +450,7 @@ def main():
     wall_ms = [r.wall_ms for r in reps]
     t_dev = max_over_ranks(dist, statistics.median(dev_ms))
     rep = reps[-1]
-    fidelity = sim.fidelity_analytic("uniform") if w["name"] == "qft" else None
+    fidelity = fidelity_of(cbq, sim, circ, cfg, w)
     sim.close()
     value = world * amp_stages / (t_dev / 1e3)
     # ---------------------------------------------------------------- e2e
@@ -412,11 +459,11 @@ def main():
         e2e = measure_e2e(cbq, circ, cfg, amp_stages, args, dist, world)
     roofline = phase_roofline(rep.device, t_dev)
     line = {
-        "metric": "amp-stages/s (QFT-34, b=20, inner=2, b_r=1e-3)", "value": value, "unit": "amp-stages/s",
+        "metric": metric_name(w), "value": value, "unit": "amp-stages/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (QFT|0> circuit generated in-process; no datasets)",
-        "config": {"workload": f"qft{w['n']}_b{w['b']}_i{w['inner']}_br1e-3", "stages": stages,
+        "data": data_desc(w),
+        "config": {"workload": workload_tag(w), "stages": stages,
                    "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
                    "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},

@@ -168,7 +168,10 @@ int bmq_gate_unitary(const bmq_gate* gate, double* out);
 int bmq_circuit_validate(uint32_t num_qubits, const bmq_gate* gates, uint64_t count);
 
 /* generate_benchmark (benchmarks.hpp:148-166); name in {ghz, cat_state, bv,
- * qft, qaoa}. *count receives the full gate count even when cap is short. */
+ * qft, qaoa}, plus the BASELINE.json workloads built from the reference gate
+ * set: "qaoa3reg" (QAOA MaxCut on a random 3-regular graph, `layers` = p) and
+ * "random" (sqrt-X/Y/W + CZ grid circuit, `layers` = cycles).
+ * *count receives the full gate count even when cap is short. */
 int bmq_generate_benchmark(const char* name, uint32_t num_qubits, uint32_t layers, uint64_t seed,
                            const char* secret, bmq_gate* out, uint64_t cap, uint64_t* count);
 

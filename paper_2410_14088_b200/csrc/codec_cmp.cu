@@ -367,6 +367,8 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
     uint32_t* stage = sm.stage;
     auto& s_cmp = sm.cmp;
     const uint32_t w_bits = bp.width;
+    // x / w_bits as a multiply-high: exact for x < 2^16 and w_bits <= 30
+    const uint32_t winv = w_bits > 1 ? 0xffffffffu / w_bits + 1 : 0;  // (w_bits == 1: x itself)
     const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
     const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
     const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
@@ -425,8 +427,9 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
         const uint32_t nwords = (off0 + cnt * w_bits + 31) >> 5;
         if (lane < nwords) {
             const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);  // word start, code-range relative
-            const uint32_t m_lo = wb > 0 ? static_cast<uint32_t>(wb) / w_bits : 0;
-            const uint32_t m_hi = min(cnt - 1, static_cast<uint32_t>(wb + 31) / w_bits);
+            const auto div_w = [&](uint32_t x) { return w_bits == 1 ? x : __umulhi(x, winv); };
+            const uint32_t m_lo = wb > 0 ? div_w(static_cast<uint32_t>(wb)) : 0;
+            const uint32_t m_hi = min(cnt - 1, div_w(static_cast<uint32_t>(wb + 31)));
             uint32_t v = 0;
             for (uint32_t m = m_lo; m <= m_hi; ++m) {
                 const int pos = static_cast<int>(m * w_bits) - wb;

@@ -689,6 +689,12 @@ __device__ __forceinline__ C2 apply_diag_run(const FastOp* ops, const double2* s
 
 __device__ __forceinline__ bool is_diag(uint8_t t) { return t == OP_DIAG || t == OP_CDIAG || t == OP_CHAIN; }
 
+__device__ __forceinline__ bool has_chain(const FastOp* ops, uint32_t q0, uint32_t q1) {
+    for (uint32_t q = q0; q < q1; ++q)
+        if (ops[q].type == OP_CHAIN) return true;
+    return false;
+}
+
 // Quantisation epilogue: amplitudes j of this thread -> packed words and
 // per-chunk counters. Lanes of a warp hold 32 consecutive locals (tile
 // positions 0..4 are buffer bits 0..4), so (block slot, chunk) is
@@ -801,6 +807,33 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                                 chain_walk8<false>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, plan, rd);
                         }
                         owners_only = false;
+                    }
+                } else if (!has_chain(sops, i, i2)) {
+                    // plain diagonal gates: op by op, each a branch-free
+                    // product with the entry its amplitude selects (an entry 1
+                    // multiplies exactly: 1*x - 0*y == x up to a zero's sign)
+                    for (int h = 0; h < kPer; h += 8) {  // eight amplitudes in registers at a time
+                        C2 a[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const double2 v = tile_s[tid + 256u * (h + j)];
+                            a[j] = C2{v.x, v.y};
+                        }
+                        for (uint32_t q = i; q < i2; ++q) {
+                            const FastOp& o = sops[q];
+                            const bool cd = o.type == OP_CDIAG;
+                            const double r0 = cd ? 1.0 : o.m[0], i0 = cd ? 0.0 : o.m[1];
+                            const double r1 = cd ? o.m[0] : o.m[2], i1 = cd ? o.m[1] : o.m[3];
+                            const uint32_t hi = o.hi, lo = cd ? o.lo : o.hi;
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const uint64_t x = xbase | toff | joff[h + j];
+                                const bool on = (x >> hi) & (x >> lo) & 1;
+                                a[j] = cmul(on ? r1 : r0, on ? i1 : i0, a[j]);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) tile_s[tid + 256u * (h + j)] = make_double2(a[j].re, a[j].im);
                     }
                 } else {
                     for (int j = 0; j < kPer; ++j) {

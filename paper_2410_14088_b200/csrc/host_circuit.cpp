@@ -90,9 +90,109 @@ int gate_matrix(const bmq_gate& g, Cx* u) {
 }
 
 // Benchmark generators (benchmarks.hpp:44-166).
+// ---- BASELINE.json workloads outside the reference's generator set. They
+// use only the reference gate set, so the reference consumes the same gate
+// lists (or their QASM text, bmq_emit_qasm -> parse_qasm) unchanged.
+
+// Random 3-regular graph on n nodes (n even, n >= 4) by the pairing model:
+// 3n points, Fisher-Yates shuffle driven by mt19937_64(seed), consecutive
+// points paired; a pairing with a loop or a repeated edge is redrawn.
+// Edges are returned sorted (i < j, lexicographic).
+std::vector<std::pair<uint32_t, uint32_t>> random_3regular(uint32_t n, uint64_t seed) {
+    if (n < 4 || n % 2) raise(BMQ_ERR_INVALID_ARGUMENT, "a 3-regular graph needs an even node count >= 4");
+    std::mt19937_64 rng(seed);
+    std::vector<uint32_t> pts(3 * n);
+    for (;;) {
+        for (uint32_t i = 0; i < 3 * n; ++i) pts[i] = i / 3;
+        for (uint32_t i = 3 * n - 1; i > 0; --i) std::swap(pts[i], pts[rng() % (i + 1)]);
+        std::vector<std::pair<uint32_t, uint32_t>> e;
+        bool ok = true;
+        for (uint32_t i = 0; i < 3 * n && ok; i += 2) {
+            const uint32_t a = std::min(pts[i], pts[i + 1]), b = std::max(pts[i], pts[i + 1]);
+            ok = a != b;
+            e.push_back({a, b});
+        }
+        if (!ok) continue;
+        std::sort(e.begin(), e.end());
+        if (std::adjacent_find(e.begin(), e.end()) != e.end()) continue;
+        return e;
+    }
+}
+
+// QAOA MaxCut: p layers of CX-RZ(gamma)-CX per
+// edge of a random 3-regular graph, then RX(beta) on every qubit; gamma and
+// beta drawn per layer exactly like make_qaoa (benchmarks.hpp:118-143); no
+// initial H layer, mirroring the reference's QAOA.
+std::vector<bmq_gate> make_qaoa_3regular(uint32_t n, uint32_t layers, uint64_t seed) {
+    if (layers < 1) raise(BMQ_ERR_INVALID_ARGUMENT, "qaoa requires at least one layer");
+    const auto edges = random_3regular(n, seed);
+    std::mt19937_64 rng(seed);
+    const double two_pi = 2.0 * std::numbers::pi;
+    std::vector<bmq_gate> c;
+    for (uint32_t l = 0; l < layers; ++l) {
+        const double gamma = static_cast<double>(rng() >> 11) * 0x1.0p-53 * two_pi;
+        const double beta = static_cast<double>(rng() >> 11) * 0x1.0p-53 * two_pi;
+        for (const auto& [i, j] : edges) {
+            c.push_back({BMQ_GATE_CX, i, j, 0, 0.0});
+            c.push_back({BMQ_GATE_RZ, j, 0, 0, gamma});
+            c.push_back({BMQ_GATE_CX, i, j, 0, 0.0});
+        }
+        for (uint32_t q = 0; q < n; ++q) c.push_back({BMQ_GATE_RX, q, 0, 0, beta});
+    }
+    return c;
+}
+
+// Random circuit on an r x c grid (r = largest
+// divisor of n not above sqrt(n)): per cycle a random sqrt(X) / sqrt(Y) /
+// sqrt(W) on every qubit, never the same gate twice in a row on one qubit,
+// then CZ on one of four nearest-neighbour patterns cycled A B C D
+// (horizontal even / odd columns, vertical even / odd rows). In the
+// reference gate set sqrt(X) = RX(pi/2), sqrt(Y) = RY(pi/2) and
+// sqrt(W) = RZ(-pi/4) RX(pi/2) RZ(pi/4) (up to a global phase).
+std::vector<bmq_gate> make_random_circuit(uint32_t n, uint32_t cycles, uint64_t seed) {
+    if (cycles < 1) raise(BMQ_ERR_INVALID_ARGUMENT, "random circuit requires at least one cycle");
+    uint32_t rows = 1;
+    for (uint32_t r = 1; r * r <= n; ++r)
+        if (n % r == 0) rows = r;
+    const uint32_t cols = n / rows;
+    std::mt19937_64 rng(seed);
+    const double h = std::numbers::pi / 2, qtr = std::numbers::pi / 4;
+    std::vector<bmq_gate> c;
+    std::vector<int> prev(n, -1);
+    for (uint32_t cy = 0; cy < cycles; ++cy) {
+        for (uint32_t q = 0; q < n; ++q) {
+            int g = static_cast<int>(rng() % 3);
+            if (prev[q] >= 0) {  // one of the two gates other than the previous one
+                const int k = static_cast<int>(rng() % 2);
+                g = (prev[q] + 1 + k) % 3;
+            }
+            prev[q] = g;
+            if (g == 0) {
+                c.push_back({BMQ_GATE_RX, q, 0, 0, h});
+            } else if (g == 1) {
+                c.push_back({BMQ_GATE_RY, q, 0, 0, h});
+            } else {
+                c.push_back({BMQ_GATE_RZ, q, 0, 0, -qtr});
+                c.push_back({BMQ_GATE_RX, q, 0, 0, h});
+                c.push_back({BMQ_GATE_RZ, q, 0, 0, qtr});
+            }
+        }
+        const uint32_t pat = cy % 4;
+        for (uint32_t r = 0; r < rows; ++r)
+            for (uint32_t k = 0; k < cols; ++k) {
+                const uint32_t q = r * cols + k;
+                if (pat < 2 && k % 2 == pat && k + 1 < cols) c.push_back({BMQ_GATE_CZ, q, q + 1, 0, 0.0});
+                if (pat >= 2 && r % 2 == pat - 2 && r + 1 < rows) c.push_back({BMQ_GATE_CZ, q, q + cols, 0, 0.0});
+            }
+    }
+    return c;
+}
+
 std::vector<bmq_gate> make_benchmark(const std::string& name, uint32_t n, uint32_t layers,
                                      uint64_t seed, const char* secret) {
     const bool ghz = name == "ghz" || name == "cat_state";
+    if (name == "qaoa3reg") return make_qaoa_3regular(n, layers, seed);
+    if (name == "random") return make_random_circuit(n, layers, seed);
     if (!ghz && name != "bv" && name != "qft" && name != "qaoa")
         raise(BMQ_ERR_INVALID_ARGUMENT, "unknown benchmark '" + name + "'");
     if (n < 2) raise(BMQ_ERR_INVALID_ARGUMENT, name + " requires at least 2 qubits");
