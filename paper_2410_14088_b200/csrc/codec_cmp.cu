@@ -369,6 +369,7 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
     const uint32_t w_bits = bp.width;
     // x / w_bits as a multiply-high: exact for x < 2^16 and w_bits <= 30
     const uint32_t winv = w_bits > 1 ? 0xffffffffu / w_bits + 1 : 0;  // (w_bits == 1: x itself)
+    const uint32_t kspan = w_bits ? (32 + w_bits - 1) / w_bits + 1 : 0;  // codes overlapping one 32-bit word
     const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
     const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
     const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
@@ -422,21 +423,37 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
             }
             continue;
         }
+        if (cnt == 32) {  // all nonzero: code m sits in lane m, no compaction
+            const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);
+            const uint32_t m_lo = wb > 0 ? __umulhi(static_cast<uint32_t>(wb), winv) : 0;
+            uint32_t v = 0;
+            for (uint32_t t = 0; t < kspan; ++t) {  // uniform trip count: every lane shuffles
+                const uint32_t m = m_lo + t;
+                const uint32_t cv = __shfl_sync(0xffffffffu, code, m & 31);
+                const int pos = static_cast<int>(m * w_bits) - wb;
+                if (m < 32 && pos < 32) v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
+            }
+            const uint32_t nwords = (off0 + 32 * w_bits + 31) >> 5;
+            if (lane < nwords && v) atomicOr(&stage[wbase + lane], v);
+            continue;
+        }
         if (mine) s_cmp[w][__popc(nzw & lt)] = code;
         __syncwarp();
-        const uint32_t nwords = (off0 + cnt * w_bits + 31) >> 5;
-        if (lane < nwords) {
+        {
             const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);  // word start, code-range relative
-            const auto div_w = [&](uint32_t x) { return w_bits == 1 ? x : __umulhi(x, winv); };
-            const uint32_t m_lo = wb > 0 ? div_w(static_cast<uint32_t>(wb)) : 0;
-            const uint32_t m_hi = min(cnt - 1, div_w(static_cast<uint32_t>(wb + 31)));
+            const uint32_t m_lo = wb <= 0 ? 0 : (w_bits == 1 ? static_cast<uint32_t>(wb)
+                                                              : __umulhi(static_cast<uint32_t>(wb), winv));
             uint32_t v = 0;
-            for (uint32_t m = m_lo; m <= m_hi; ++m) {
+            for (uint32_t t = 0; t < kspan; ++t) {  // uniform trip count, predicated
+                const uint32_t m = m_lo + t;
                 const int pos = static_cast<int>(m * w_bits) - wb;
-                const uint32_t cv = s_cmp[w][m];
-                v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
+                if (m < cnt && pos < 32) {
+                    const uint32_t cv = s_cmp[w][m];
+                    v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
+                }
             }
-            if (v) atomicOr(&stage[wbase + lane], v);
+            const uint32_t nwords = (off0 + cnt * w_bits + 31) >> 5;
+            if (lane < nwords && v) atomicOr(&stage[wbase + lane], v);
         }
         __syncwarp();
     }

@@ -85,4 +85,41 @@ __device__ __forceinline__ uint32_t quantize_pack(double v, const DevTables& t, 
     return pack_code(static_cast<uint32_t>(q - t.qlo), v < 0.0, false);
 }
 
+// quantize_pack for N scalars at once: every estimate first, then both
+// neighbouring thresholds of every estimate as independent loads (2N in
+// flight instead of a dependent chain per scalar), then the exact
+// settlement; an estimate off by more than one falls back to quantize().
+template <int N>
+__device__ __forceinline__ void quantize_pack_n(const double* v, uint32_t* pk, const DevTables& t, bool& bad,
+                                                bool& oow) {
+    uint64_t bits[N];
+    int64_t idx[N];
+    bool live[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        live[e] = isfinite(v[e]) && v[e] != 0.0;
+        if (!isfinite(v[e])) bad = true;
+        idx[e] = live[e] ? quantize_estimate(v[e], t, bits[e]) : 0;
+    }
+    uint64_t t0[N], t1[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        t0[e] = __ldg(t.thresh + idx[e]);
+        t1[e] = __ldg(t.thresh + idx[e] + 1);
+    }
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        if (!live[e]) {
+            pk[e] = 1u;
+            continue;
+        }
+        int64_t q;
+        if (bits[e] >= t0[e] && bits[e] < t1[e])
+            q = t.qlo + idx[e];
+        else
+            q = quantize(v[e], t, oow);
+        pk[e] = pack_code(static_cast<uint32_t>(q - t.qlo), v[e] < 0.0, false);
+    }
+}
+
 }  // namespace bmq

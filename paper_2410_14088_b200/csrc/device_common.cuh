@@ -102,6 +102,27 @@ __device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& 
     return t.qlo + i;
 }
 
+// The estimate of quantize() for finite v != 0 (table index, not clamped
+// against the exact thresholds yet) and |v|'s bit pattern.
+__device__ __forceinline__ int64_t quantize_estimate(double v, const DevTables& t, uint64_t& bits) {
+    bits = static_cast<uint64_t>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
+    const uint32_t ex = static_cast<uint32_t>(bits >> 52);
+    uint64_t man = bits & 0xfffffffffffffull;
+    int e2;
+    if (ex == 0) {
+        const int shift = __clzll(static_cast<long long>(man)) - 11;
+        man = (man << shift) & 0xfffffffffffffull;
+        e2 = -1022 - shift;
+    } else {
+        e2 = static_cast<int>(ex) - 1023;
+    }
+    const float m = static_cast<float>(__longlong_as_double(static_cast<long long>(man | 0x3ff0000000000000ull)));
+    const double x = (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
+    int64_t q = __double2ll_rn(x);
+    q = q < t.qlo ? t.qlo : (q > t.qhi ? t.qhi : q);
+    return q - t.qlo;
+}
+
 // Read `width` (<= 63) bits LSB-first starting at bit `bitpos` of the byte
 // stream at `base`. Reads aligned 32-bit words (buffers carry 16 B of slack).
 __device__ __forceinline__ uint64_t read_bits(const uint8_t* base, uint64_t bitpos, uint32_t width) {

@@ -399,6 +399,63 @@ void build_mono(GateProgram& prog) {
     }
 }
 
+// Lazy CX (see FastOp): fold every CX of a fast pass into the pass's GF(2)
+// map y = M x ^ c, annotate the other ops with the rows / columns of M they
+// need, and materialise the map before phase chains (which address
+// amplitudes by their full index).
+void lazify(std::vector<FastOp>& fops, FastPass& fp) {
+    uint16_t rows[kMaxTileBits], cols[kMaxTileBits];
+    const auto reset = [&]() {
+        for (uint32_t i = 0; i < kMaxTileBits; ++i) rows[i] = cols[i] = static_cast<uint16_t>(1u << i);
+    };
+    const auto identity = [&]() {
+        for (uint32_t i = 0; i < kMaxTileBits; ++i)
+            if (rows[i] != (1u << i)) return false;
+        return true;
+    };
+    reset();
+    bool affine = false;  // some CX has its control outside the tile: c may be nonzero
+    std::vector<FastOp> out;
+    for (FastOp f : fops) {
+        switch (f.type) {
+        case OP_CX:
+            if (f.in_hi) {
+                rows[f.tp_lo] ^= rows[f.tp_hi];
+                cols[f.tp_hi] ^= cols[f.tp_lo];
+            } else {
+                affine = true;
+            }
+            break;
+        case OP_U2:
+            f.mrow = rows[f.tp_hi];
+            f.dvec = cols[f.tp_hi];
+            break;
+        case OP_DIAG:
+            f.mrow = f.in_hi ? rows[f.tp_hi] : 0;
+            break;
+        case OP_CDIAG:
+            f.mrow = f.in_hi ? rows[f.tp_hi] : 0;
+            f.mrow2 = f.in_lo ? rows[f.tp_lo] : 0;
+            break;
+        case OP_CHAIN:
+            if (!identity() || affine) {
+                FastOp m{};
+                m.type = OP_PERM;
+                std::memcpy(&m.m[0], cols, sizeof cols);
+                out.push_back(m);
+                reset();
+                affine = false;
+            }
+            break;
+        default: break;
+        }
+        out.push_back(f);
+    }
+    std::memcpy(fp.minv, cols, sizeof cols);
+    fp.final_perm = (!identity() || affine) ? 1u : 0u;
+    fops = std::move(out);
+}
+
 }  // namespace
 
 void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bits) {
@@ -433,6 +490,8 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
         if (fast) {
             const size_t tab_mark = prog.chain_tab.size();
             std::vector<FastOp> fops = fuse_chains(ops, begin, end, prog.chain_tab, mask);
+            FastPass lazy{};
+            lazify(fops, lazy);
             if (fops.size() > static_cast<size_t>(kMaxFastOps) && end - begin > 1) {
                 prog.chain_tab.resize(tab_mark);
                 const uint32_t mid = begin + (end - begin) / 2;
@@ -446,6 +505,8 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
                 fp->tile = make_runs(mask, total_bits, -1);
                 fp->base = make_runs(~mask & all, total_bits, static_cast<int>(total_bits));
                 fp->nops = static_cast<uint32_t>(fops.size());
+                std::memcpy(fp->minv, lazy.minv, sizeof fp->minv);
+                fp->final_perm = lazy.final_perm;
                 fp->tab_base = tab_mark / 2;
                 fp->tab_entries = static_cast<uint32_t>((prog.chain_tab.size() - tab_mark) / 2);
                 std::copy(fops.begin(), fops.end(), fp->ops);
@@ -700,34 +761,47 @@ __device__ __forceinline__ bool has_chain(const FastOp* ops, uint32_t q0, uint32
 // positions 0..4 are buffer bits 0..4), so (block slot, chunk) is
 // warp-uniform and counters are reduced per warp before one set of atomics.
 __device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t base,
-                                               uint64_t toff, const uint64_t* joff, uint32_t lb) {
+                                               uint64_t toff, const uint64_t* joff, uint32_t lb, bool gather,
+                                               uint32_t cvec, const uint16_t* gat_lo, const uint16_t* gat_hi) {
     const uint64_t lmask = (1ull << lb) - 1;
     ChunkAcc acc_re, acc_im;
     uint64_t key_re = ~0ull, key_im = ~0ull;
     bool bad = false, oow = false;
-    for (int j = 0; j < kPer; ++j) {
-        const double2 v = tile_s[tid + 256 * j];
-        const uint64_t p = base | toff | joff[j];
-        const uint64_t slot = p >> lb, l = p & lmask;
-        const uint64_t s_im = (1ull << lb) + l;
-        const uint64_t kre = slot * q.nch + (l >> 12), kim = slot * q.nch + (s_im >> 12);
-        if (kre != key_re) {  // warp-uniform
-            if (key_re != ~0ull) flush_chunk(q.cps + key_re, acc_re);
-            acc_re = ChunkAcc{};
-            key_re = kre;
+    constexpr int kG = 2;  // amplitudes quantised together (2 kG probes in flight)
+    for (int g0 = 0; g0 < kPer; g0 += kG) {
+        double v[2 * kG];
+        uint32_t pk[2 * kG];
+#pragma unroll
+        for (int e = 0; e < kG; ++e) {
+            uint32_t y = tid + 256 * (g0 + e);
+            if (gather) y = gat_lo[(y ^ cvec) & 63] ^ gat_hi[(y ^ cvec) >> 6];
+            const double2 a = tile_s[y];
+            v[2 * e] = a.x;
+            v[2 * e + 1] = a.y;
         }
-        if (kim != key_im) {
-            if (key_im != ~0ull) flush_chunk(q.cps + key_im, acc_im);
-            acc_im = ChunkAcc{};
-            key_im = kim;
+        quantize_pack_n<2 * kG>(v, pk, q.t, bad, oow);
+#pragma unroll
+        for (int e = 0; e < kG; ++e) {
+            const uint64_t p = base | toff | joff[g0 + e];
+            const uint64_t slot = p >> lb, l = p & lmask;
+            const uint64_t s_im = (1ull << lb) + l;
+            const uint64_t kre = slot * q.nch + (l >> 12), kim = slot * q.nch + (s_im >> 12);
+            if (kre != key_re) {  // warp-uniform
+                if (key_re != ~0ull) flush_chunk(q.cps + key_re, acc_re);
+                acc_re = ChunkAcc{};
+                key_re = kre;
+            }
+            if (kim != key_im) {
+                if (key_im != ~0ull) flush_chunk(q.cps + key_im, acc_im);
+                acc_im = ChunkAcc{};
+                key_im = kim;
+            }
+            uint32_t* dst = q.pk + (slot << (lb + 1));
+            dst[l] = pk[2 * e];
+            dst[s_im] = pk[2 * e + 1];
+            acc_re.add(pk[2 * e]);
+            acc_im.add(pk[2 * e + 1]);
         }
-        const uint32_t pre = quantize_pack(v.x, q.t, bad, oow);
-        const uint32_t pim = quantize_pack(v.y, q.t, bad, oow);
-        uint32_t* dst = q.pk + (slot << (lb + 1));
-        dst[l] = pre;
-        dst[s_im] = pim;
-        acc_re.add(pre);
-        acc_im.add(pim);
     }
     flush_chunk(q.cps + key_re, acc_re);
     flush_chunk(q.cps + key_im, acc_im);
@@ -744,6 +818,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     extern __shared__ double2 tile_s[];
     __shared__ uint64_t joff[kPer];
     __shared__ uint32_t lut_lo[64], lut_hi[64];  // tile position -> buffer bits (low 32)
+    __shared__ uint16_t gat_lo[64], gat_hi[64];  // final M^-1 on a 12-bit tile index (lazy CX)
     double2* stab = tile_s + 4096;
     FastOp* sops = reinterpret_cast<FastOp*>(stab + pass.tab_entries);
     const uint32_t tid = threadIdx.x;
@@ -753,6 +828,13 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     if (tid < kPer) joff[tid] = runs_deposit(static_cast<uint64_t>(tid) << 8, pass.tile);
     if (tid < 64) lut_lo[tid] = static_cast<uint32_t>(runs_deposit(tid, pass.tile));
     else if (tid < 128) lut_hi[tid - 64] = static_cast<uint32_t>(runs_deposit(static_cast<uint64_t>(tid - 64) << 6, pass.tile));
+    else if (tid < 256) {
+        const uint32_t v = tid & 63, sh = tid < 192 ? 0 : 6;
+        uint32_t x = 0;
+        for (uint32_t b = 0; b < 6; ++b)
+            if ((v >> b) & 1) x ^= pass.minv[b + sh];
+        (tid < 192 ? gat_lo : gat_hi)[v] = static_cast<uint16_t>(x);
+    }
     for (uint32_t e = tid; e < pass.tab_entries; e += kFastThreads)
         stab[e] = __ldg(reinterpret_cast<const double2*>(pass.chain_tab) + pass.tab_base + e);
     {
@@ -781,8 +863,36 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             for (int j = 0; j < kPer; ++j) tile_s[tid + 256 * j] = make_double2(re[j], im[j]);
         }
         bool owners_only = true;
+        uint32_t cvec = 0;  // lazy CX: affine part of the tile's index map
         for (uint32_t i = 0; i < pass.nops;) {
             const FastOp& g = sops[i];
+            if (g.type == OP_CX) {  // no data moves: only the map changes
+                const uint32_t ctl = g.in_hi ? (cvec >> g.tp_hi) & 1u : static_cast<uint32_t>((base >> g.hi) & 1);
+                cvec ^= ctl << g.tp_lo;
+                ++i;
+                continue;
+            }
+            if (g.type == OP_PERM) {  // materialise: logical y takes the amplitude at M^-1 (y ^ c)
+                uint16_t cols[kMaxTileBits];
+                memcpy(cols, &g.m[0], sizeof cols);
+                __syncthreads();
+                double2 v[kPer];
+#pragma unroll
+                for (int j = 0; j < kPer; ++j) {
+                    const uint32_t y = (tid + 256u * j) ^ cvec;
+                    uint32_t x = 0;
+                    for (uint32_t b = 0; b < kMaxTileBits; ++b)
+                        if ((y >> b) & 1) x ^= cols[b];
+                    v[j] = tile_s[x];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < kPer; ++j) tile_s[tid + 256u * j] = v[j];
+                cvec = 0;
+                owners_only = true;
+                ++i;
+                continue;
+            }
             if (is_diag(g.type)) {
                 uint32_t i2 = i + 1;
                 while (i2 < pass.nops && is_diag(sops[i2].type)) ++i2;
@@ -824,11 +934,17 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                             const bool cd = o.type == OP_CDIAG;
                             const double r0 = cd ? 1.0 : o.m[0], i0 = cd ? 0.0 : o.m[1];
                             const double r1 = cd ? o.m[0] : o.m[2], i1 = cd ? o.m[1] : o.m[3];
-                            const uint32_t hi = o.hi, lo = cd ? o.lo : o.hi;
+                            // logical bit = parity(row of M & physical position) ^ c (in the
+                            // tile) or the base bit; a missing second bit reads as 1
+                            const uint32_t rh = o.in_hi ? o.mrow : 0u, rl = cd && o.in_lo ? o.mrow2 : 0u;
+                            const uint32_t ch = o.in_hi ? (cvec >> o.tp_hi) & 1u : static_cast<uint32_t>((xbase >> o.hi) & 1);
+                            const uint32_t cl = !cd ? 1u
+                                                    : (o.in_lo ? (cvec >> o.tp_lo) & 1u
+                                                               : static_cast<uint32_t>((xbase >> o.lo) & 1));
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const uint64_t x = xbase | toff | joff[h + j];
-                                const bool on = (x >> hi) & (x >> lo) & 1;
+                                const uint32_t k = tid + 256u * (h + j);
+                                const bool on = ((__popc(rh & k) ^ ch) & (__popc(rl & k) ^ cl) & 1u) != 0;
                                 a[j] = cmul(on ? r1 : r0, on ? i1 : i0, a[j]);
                             }
                         }
@@ -849,20 +965,14 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             ++i;
             __syncthreads();
             owners_only = false;
-            const bool cx = g.type == OP_CX;
-            const uint32_t tp = cx ? g.tp_lo : g.tp_hi;
-            const uint32_t m = 1u << tp;
-            const uint32_t bctl = static_cast<uint32_t>((base >> g.hi) & 1);
+            // U2 on logical tile bit t: physical pairs (x, x ^ dvec); x is
+            // the |0> side when parity(mrow & x) ^ c_t is 0
+            const uint32_t dv = g.dvec, piv = __ffs(dv) - 1, ct = (cvec >> g.tp_hi) & 1u;
             for (uint32_t r = tid; r < 2048; r += kFastThreads) {
-                const uint32_t i0 = insert0(r, tp), i1 = i0 | m;
-                if (cx) {
-                    const uint32_t ctl = g.in_hi ? (i0 >> g.tp_hi) & 1 : bctl;
-                    if (ctl) {
-                        const double2 t = tile_s[i0];
-                        tile_s[i0] = tile_s[i1];
-                        tile_s[i1] = t;
-                    }
-                } else {
+                const uint32_t x0 = insert0(r, piv), x1 = x0 ^ dv;
+                const bool sw = (__popc(g.mrow & x0) ^ ct) & 1u;
+                const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
+                {
                     const double2 v0 = tile_s[i0], v1 = tile_s[i1];
                     if (g.pad) {  // all entries real: u*a = (u*ar, u*ai) exactly
                         const double u00 = g.m[0], u01 = g.m[2], u10 = g.m[4], u11 = g.m[6];
@@ -879,16 +989,19 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 }
             }
         }
-        if (!owners_only) __syncthreads();
+        const bool gather = pass.final_perm || cvec;  // logical y lives at M^-1 (y ^ c)
+        if (!owners_only || gather) __syncthreads();
         if (quant.pk) {
-            quant_epilogue(quant, tile_s, tid, base, toff, joff, lb);
+            quant_epilogue(quant, tile_s, tid, base, toff, joff, lb, gather, cvec, gat_lo, gat_hi);
             continue;
         }
         {
             double re[kPer], im[kPer];
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
-                const double2 v = tile_s[tid + 256 * j];
+                uint32_t y = tid + 256 * j;
+                if (gather) y = gat_lo[(y ^ cvec) & 63] ^ gat_hi[(y ^ cvec) >> 6];
+                const double2 v = tile_s[y];
                 re[j] = v.x;
                 im[j] = v.y;
             }

@@ -13,7 +13,9 @@ namespace bmq {
 // bit c whose other bits are distinct and monotone in program order; an
 // amplitude with bit c set is multiplied, in program order, by the phase of
 // every set bit of (index & R), found by scanning set bits instead of ops.
-enum OpType : uint8_t { OP_U2 = 0, OP_DIAG = 1, OP_CX = 2, OP_CDIAG = 3, OP_U4 = 4, OP_CHAIN = 5 };
+// OP_PERM (fast kernel only): materialise the pass's pending CX permutation
+// (see FastOp::mrow) before an op that needs physical = logical positions.
+enum OpType : uint8_t { OP_U2 = 0, OP_DIAG = 1, OP_CX = 2, OP_CDIAG = 3, OP_U4 = 4, OP_CHAIN = 5, OP_PERM = 6 };
 // Matrix entry classes. Each class evaluates the reference product u * a
 // (libstdc++ (ur*ar - ui*ai, ur*ai + ui*ar), every product rounded) exactly,
 // up to the sign of an exact zero, which the codec maps to the same bytes.
@@ -37,12 +39,23 @@ struct BitRuns {
 };
 
 // Compact op for the register-tiled kernel (kernel parameter space).
+// Lazy CX: within a fast pass a CX moves no data. The tile keeps a GF(2)
+// affine map from physical tile position x to logical tile index
+// y = M x ^ c (M: pass-constant, tracked on the host; c: per tile, on the
+// device). Ops then address amplitudes through it:
+//   DIAG / CDIAG: logical bit at tile position p = parity(mrow & x) ^ c_p
+//                 (mrow = row p of M; mrow2 for CDIAG's second bit);
+//   U2 on tile position t: pairs (x, x ^ dvec) with dvec = M^-1 e_t, the
+//                 logical bit t of x being parity(mrow & x) ^ c_t.
+// The pass ends (and a phase chain starts) with a gather through M^-1.
 struct FastOp {
     uint8_t type, tp_hi, tp_lo, in_hi, in_lo, hi, lo, pad;
     uint8_t et[4];    // CHAIN: et[0] = 1 when the other bits descend in program order
     uint32_t pad2;    // CHAIN: offset of the 64-entry phase table (double2 units)
     double m[8];      // U2: u00 u01 u10 u11; DIAG: u00 u11; CDIAG: u33 (interleaved re/im)
                       // CHAIN: m[0] holds the mask R of other bits (bit pattern)
+                      // PERM: m[0..2] hold the 12 columns of M^-1 (uint16 each)
+    uint16_t mrow, mrow2, dvec, pad3;
 };
 
 constexpr uint32_t kMaxTileBits = 12;  // 4096 amplitudes per tile
@@ -53,6 +66,8 @@ struct FastPass {
     BitRuns tile;   // tile position k (12 bits) -> buffer offset
     BitRuns base;   // tile index -> buffer bits outside the tile
     uint32_t nops;
+    uint16_t minv[kMaxTileBits];  // columns of M^-1 at the end of the pass (lazy CX)
+    uint32_t final_perm;          // the pass ends with a non-identity M (gather on store)
     uint32_t tab_entries;     // phase-table entries (double2) of this pass's chains
     uint64_t tab_base;        // first entry of this pass in chain_tab
     const double* chain_tab;  // phase tables of OP_CHAIN ops (re, im pairs), 32 per chain
