@@ -106,6 +106,10 @@ typedef struct bmq_config {
  * lands on another scalar with the same code. Bit-exact under the same
  * idempotence check as BMQ_FLAG_IDENTITY_SKIP; default on. */
 #define BMQ_FLAG_CODE_DOMAIN 0x4u
+/* device_pool_bytes is only the initial arena size: arenas double when the
+ * live state fills more than half of one after a compaction (always the case
+ * for automatic sizing, device_pool_bytes == 0). */
+#define BMQ_FLAG_POOL_GROW 0x8u
 
 /* cbq::SimulationReport (engine.hpp:39-53) plus device-side counters. */
 typedef struct bmq_report {
@@ -148,6 +152,7 @@ typedef struct bmq_report {
     uint64_t host_spill_bytes;      /* payload bytes placed in the pinned host arena */
     uint64_t host_spill_batches;    /* batches whose payloads went to the host arena */
     uint64_t code_domain_batches;   /* batches run on quantiser codes (BMQ_FLAG_CODE_DOMAIN) */
+    uint64_t pool_growths;          /* automatic payload arenas doubled after a compaction */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

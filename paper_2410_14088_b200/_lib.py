@@ -28,6 +28,7 @@ BMQ_ERR_BUFFER_TOO_SMALL = 10
 BMQ_FLAG_ZERO_GROUP_SKIP = 0x1
 BMQ_FLAG_IDENTITY_SKIP = 0x2
 BMQ_FLAG_CODE_DOMAIN = 0x4
+BMQ_FLAG_POOL_GROW = 0x8
 
 
 class bmq_gate(C.Structure):
@@ -63,7 +64,7 @@ class bmq_report(C.Structure):
                 ("batches", C.c_uint64), ("decompress_bytes", C.c_uint64), ("gate_bytes", C.c_uint64),
                 ("compress_bytes", C.c_uint64), ("fused_batches", C.c_uint64), ("compactions", C.c_uint64),
                 ("host_spill_bytes", C.c_uint64), ("host_spill_batches", C.c_uint64),
-                ("code_domain_batches", C.c_uint64)]
+                ("code_domain_batches", C.c_uint64), ("pool_growths", C.c_uint64)]
 
 
 _P = C.c_void_p

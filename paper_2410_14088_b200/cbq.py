@@ -572,6 +572,7 @@ class Config:
     zero_group_skip: bool = True
     identity_skip: bool = False
     code_domain: bool = True
+    pool_grow: bool = False
     host_pool_bytes: int = 0
 
     def to_c(self) -> bmq_config:
@@ -584,7 +585,8 @@ class Config:
         c.host_pool_bytes = self.host_pool_bytes
         c.flags = (_lib.BMQ_FLAG_ZERO_GROUP_SKIP if self.zero_group_skip else 0) | \
                   (_lib.BMQ_FLAG_IDENTITY_SKIP if self.identity_skip else 0) | \
-                  (_lib.BMQ_FLAG_CODE_DOMAIN if self.code_domain else 0)
+                  (_lib.BMQ_FLAG_CODE_DOMAIN if self.code_domain else 0) | \
+                  (_lib.BMQ_FLAG_POOL_GROW if self.pool_grow else 0)
         return c
 
 
@@ -611,7 +613,7 @@ DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks
                       "payload_bytes_read", "payload_bytes_written", "dense_bytes", "kernel_launches",
                       "device_peak_bytes", "gate_passes", "decompress_ms", "gate_ms", "compress_ms", "batches",
                       "decompress_bytes", "gate_bytes", "compress_bytes", "fused_batches", "compactions",
-                      "host_spill_bytes", "host_spill_batches", "code_domain_batches")
+                      "host_spill_bytes", "host_spill_batches", "code_domain_batches", "pool_growths")
 
 
 def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:

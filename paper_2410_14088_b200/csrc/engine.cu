@@ -469,6 +469,8 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
         pool = std::min<uint64_t>({24ull << 30, total_b / 8, worst});
     }
     pool_cap_ = pool;
+    pool_auto_ = cfg.device_pool_bytes == 0 || (cfg.flags & BMQ_FLAG_POOL_GROW);
+    pool_worst_ = nid * (compress_bound(blk_scalars) + kArenaAlign);
     pool_[0].alloc(pool + 64);
     pool_[1].alloc(pool + 64);
     device_peak_ = 2 * (pool + 64) + work_.bytes() + pk_.bytes() + cplan_.bytes() + dchunk_.bytes();
@@ -528,6 +530,55 @@ void Engine::compact() {
     cur_ = nxt;
     sync_meta_to_host();
     ++counters_.compactions;
+    maybe_grow_pools();
+}
+
+// Automatic arenas grow when the live state fills more than half of one
+// after compaction (dense states at b_r = 1e-3 are ~1/4 of 2^(n+4) bytes:
+// compacting every batch would copy the whole state each time). The live
+// payloads move into a new, doubled arena; on allocation failure the
+// arenas stay as they are.
+void Engine::maybe_grow_pools() {
+    if (!pool_auto_ || growing_) return;
+    struct Guard {
+        bool& f;
+        explicit Guard(bool& g) : f(g) { f = true; }
+        ~Guard() { f = false; }
+    } guard(growing_);
+    uint64_t used = 0;
+    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    if (2 * used <= pool_cap_ || pool_cap_ >= pool_worst_) return;
+    size_t free_b = 0, total_b = 0;
+    BMQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t new_cap = std::min<uint64_t>(2 * pool_cap_, pool_worst_);
+    // the dead arena is released first; keep a margin of HBM for others
+    if (free_b + pool_cap_ < new_cap + (8ull << 30)) return;
+    const int dead = 1 - cur_;
+    pool_[dead].release();
+    try {
+        pool_[dead].alloc(new_cap + 64);
+    } catch (const Error&) {
+        cudaGetLastError();
+        pool_[dead].alloc(pool_cap_ + 64);
+        return;
+    }
+    const uint64_t old_cap = pool_cap_;
+    pool_cap_ = new_cap;
+    compact();  // live payloads -> the new arena (cur_ flips to it)
+    const int old = 1 - cur_;
+    pool_[old].release();
+    try {
+        pool_[old].alloc(new_cap + 64);
+    } catch (const Error&) {  // keep running on one large + one old-size arena
+        cudaGetLastError();
+        pool_[old].alloc(old_cap + 64);
+        pool_cap_ = old_cap;
+        compact();
+        return;
+    }
+    device_peak_ += 2 * (new_cap - old_cap);
+    ++counters_.pool_growths;
 }
 
 void Engine::init_state() {
@@ -867,6 +918,7 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.host_spill_bytes = counters_.host_spill_bytes;
     r.host_spill_batches = counters_.host_spill_batches;
     r.code_domain_batches = counters_.code_domain_batches;
+    r.pool_growths = counters_.pool_growths;
     *rep = r;
 }
 

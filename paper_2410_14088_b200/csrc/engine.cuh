@@ -110,6 +110,9 @@ private:
     void process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk, size_t bidx);
     void emit_batch(uint64_t nblk);
     void compact();
+    void maybe_grow_pools();
+    bool pool_auto_ = false, growing_ = false;
+    uint64_t pool_worst_ = 0;
     void sync_meta_to_host();
     void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
     void host_ids_to_device(const std::vector<uint64_t>& ids);

@@ -285,3 +285,18 @@ def test_code_domain_qft_swaps(gpu, port):
         assert rep.device["code_domain_batches"] > 0
         assert sim.payloads() == want.payloads
         assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+
+
+def test_pool_growth_is_exact(gpu, port):
+    """Arenas that start small double after compactions (BMQ_FLAG_POOL_GROW);
+    payloads stay byte-identical to the oracle."""
+    c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=2))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    biggest = max(len(p) for p in want.payloads)
+    pool = 8 * (biggest + 16)
+    with gpu.Simulator(c, gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, pool_grow=True,
+                                     work_bytes=4 * (16 << 12))) as sim:
+        rep = sim.run()
+        assert rep.device["pool_growths"] > 0
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
