@@ -352,42 +352,52 @@ constexpr int kStageWords = (kChunk * 30 + 31) / 32 + 2;  // codes are < 2^30 (k
 
 // The scalar part of emit for one chunk (kFull: all 4096 scalars valid).
 struct EmitSmem {
-    uint32_t sign[kWordsPerChunk], zero[kWordsPerChunk], pre[kWordsPerChunk];
+    uint32_t sign[kWordsPerChunk], zero[kWordsPerChunk], pre[kWordsPerChunk], bits[kWordsPerChunk];
     uint32_t stage[kStageWords];
-    uint32_t cmp[kChunkThreads / 32][32];
+    uint32_t cw[kChunk];  // nonzero codes of word k at cw[32 k + rank in word]
 };
 
-template <bool kFull>
+template <bool kFull, bool kW1>
 __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, const uint32_t* __restrict__ src,
                                            const BlockPlan& bp, uint8_t* pay, const DevTables& t, EmitSmem& sm) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    uint32_t* s_sign = sm.sign;
-    uint32_t* s_zero = sm.zero;
-    uint32_t* s_pre = sm.pre;
-    uint32_t* stage = sm.stage;
-    auto& s_cmp = sm.cmp;
     const uint32_t w_bits = bp.width;
     // x / w_bits as a multiply-high: exact for x < 2^16 and w_bits <= 30
-    const uint32_t winv = w_bits > 1 ? 0xffffffffu / w_bits + 1 : 0;  // (w_bits == 1: x itself)
+    const uint32_t winv = w_bits > 1 ? 0xffffffffu / w_bits + 1 : 0;
     const uint32_t kspan = w_bits ? (32 + w_bits - 1) / w_bits + 1 : 0;  // codes overlapping one 32-bit word
     const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
     const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
     const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
-    for (uint32_t i = tid; i < nstage; i += kChunkThreads) stage[i] = 0;
-    uint32_t pkv[32];
+    for (uint32_t i = tid; i < nstage; i += kChunkThreads) sm.stage[i] = 0;
+    const uint32_t lt = (1u << lane) - 1;
+    // A: all loads in flight; B: ballots -> bitmap words, width-1 code words,
+    // or (wider codes) the nonzero codes compacted per word into sm.cw
+    {
+        uint32_t pkv[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {  // all loads in flight before the first ballot
-        const uint32_t s = 128 * j + 32 * w + lane;
-        pkv[j] = (kFull || s < len) ? __ldcs(src + s) : 1u;
-    }
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t s = 128 * j + 32 * w + lane;
+            pkv[j] = (kFull || s < len) ? __ldcs(src + s) : 1u;
+        }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t pk = pkv[j];
-        const uint32_t sw = __ballot_sync(0xffffffffu, (pk >> 1) & 1u);
-        const uint32_t zw = __ballot_sync(0xffffffffu, pk & 1u) & (kFull ? ~0u : word_mask(len, 4 * j + w));
-        if (lane == 0) {
-            s_sign[4 * j + w] = sw;
-            s_zero[4 * j + w] = zw;
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t k = 4 * j + w;
+            const uint32_t pk = pkv[j];
+            const uint32_t code = (pk >> 2) - qmin_off;
+            const uint32_t sw = __ballot_sync(0xffffffffu, (pk >> 1) & 1u);
+            const uint32_t zw = __ballot_sync(0xffffffffu, pk & 1u) & (kFull ? ~0u : word_mask(len, k));
+            const uint32_t nzw = ~zw & (kFull ? ~0u : word_mask(len, k));
+            if constexpr (kW1) {
+                const uint32_t bw = __ballot_sync(0xffffffffu, !(pk & 1u) && (code & 1u));
+                if (nzw != ~0u && !(pk & 1u)) sm.cw[32 * k + __popc(nzw & lt)] = code;
+                if (lane == 0) sm.bits[k] = bw;
+            } else {
+                if (!(pk & 1u)) sm.cw[32 * k + __popc(nzw & lt)] = code;
+            }
+            if (lane == 0) {
+                sm.sign[k] = sw;
+                sm.zero[k] = zw;
+            }
         }
     }
     __syncthreads();
@@ -395,77 +405,53 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
     {
         using Scan = cub::BlockScan<uint32_t, kChunkThreads>;
         __shared__ typename Scan::TempStorage ss;
-        const uint32_t cnt = __popc(~s_zero[tid] & (kFull ? ~0u : word_mask(len, tid)));
+        const uint32_t cnt = __popc(~sm.zero[tid] & (kFull ? ~0u : word_mask(len, tid)));
         uint32_t pre;
         Scan(ss).ExclusiveSum(cnt, pre);
-        s_pre[tid] = pre;
+        sm.pre[tid] = pre;
     }
     __syncthreads();
-    // Warp-cooperative packing: the nonzero codes of one bitmap word are
-    // compacted by rank, then lane i assembles stage word i of the word's
-    // contiguous bit range; edge words are shared with neighbouring warps.
-    const uint32_t lt = (1u << lane) - 1;
-#pragma unroll
+    // C: each warp packs its words' codes LSB-first into the stage; lane i
+    // assembles stage word i of a word's contiguous bit range (edge words OR-ed)
+#pragma unroll 1
     for (int j = 0; j < 32; ++j) {
         const uint32_t k = 4 * j + w;
-        const uint32_t nzw = ~s_zero[k] & (kFull ? ~0u : word_mask(len, k));
+        const uint32_t nzw = ~sm.zero[k] & (kFull ? ~0u : word_mask(len, k));
         const uint32_t cnt = __popc(nzw);
         if (!cnt) continue;  // warp-uniform
-        const bool mine = (nzw >> lane) & 1u;
-        const uint32_t code = (pkv[j] >> 2) - qmin_off;
-        const uint32_t a0 = s_pre[k] * w_bits;  // chunk-relative bit of this word's first code
+        const uint32_t a0 = sm.pre[k] * w_bits;  // chunk-relative bit of this word's first code
         const uint32_t off0 = a0 & 31, wbase = a0 >> 5;
-        if (w_bits == 1 && cnt == 32) {
-            const uint32_t bits = __ballot_sync(0xffffffffu, code & 1u);
-            if (lane == 0 && bits) {
-                atomicOr(&stage[wbase], bits << off0);
-                if (off0) atomicOr(&stage[wbase + 1], bits >> (32 - off0));
+        if (kW1 && cnt == 32) {  // width 1, all nonzero: the word's code bits are one ballot
+            const uint32_t bw = sm.bits[k];
+            if (lane == 0 && bw) {
+                atomicOr(&sm.stage[wbase], bw << off0);
+                if (off0) atomicOr(&sm.stage[wbase + 1], bw >> (32 - off0));
             }
             continue;
         }
-        if (cnt == 32) {  // all nonzero: code m sits in lane m, no compaction
-            const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);
-            const uint32_t m_lo = wb > 0 ? __umulhi(static_cast<uint32_t>(wb), winv) : 0;
-            uint32_t v = 0;
-            for (uint32_t t = 0; t < kspan; ++t) {  // uniform trip count: every lane shuffles
-                const uint32_t m = m_lo + t;
-                const uint32_t cv = __shfl_sync(0xffffffffu, code, m & 31);
-                const int pos = static_cast<int>(m * w_bits) - wb;
-                if (m < 32 && pos < 32) v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
+        const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);  // word start, code-range relative
+        const uint32_t m_lo = wb <= 0 ? 0 : (w_bits == 1 ? static_cast<uint32_t>(wb)
+                                                          : __umulhi(static_cast<uint32_t>(wb), winv));
+        uint32_t v = 0;
+        for (uint32_t t = 0; t < kspan; ++t) {  // uniform trip count, predicated
+            const uint32_t m = m_lo + t;
+            const int pos = static_cast<int>(m * w_bits) - wb;
+            if (m < cnt && pos < 32) {
+                const uint32_t cv = sm.cw[32 * k + m];
+                v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
             }
-            const uint32_t nwords = (off0 + 32 * w_bits + 31) >> 5;
-            if (lane < nwords && v) atomicOr(&stage[wbase + lane], v);
-            continue;
         }
-        if (mine) s_cmp[w][__popc(nzw & lt)] = code;
-        __syncwarp();
-        {
-            const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);  // word start, code-range relative
-            const uint32_t m_lo = wb <= 0 ? 0 : (w_bits == 1 ? static_cast<uint32_t>(wb)
-                                                              : __umulhi(static_cast<uint32_t>(wb), winv));
-            uint32_t v = 0;
-            for (uint32_t t = 0; t < kspan; ++t) {  // uniform trip count, predicated
-                const uint32_t m = m_lo + t;
-                const int pos = static_cast<int>(m * w_bits) - wb;
-                if (m < cnt && pos < 32) {
-                    const uint32_t cv = s_cmp[w][m];
-                    v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
-                }
-            }
-            const uint32_t nwords = (off0 + cnt * w_bits + 31) >> 5;
-            if (lane < nwords && v) atomicOr(&stage[wbase + lane], v);
-        }
-        __syncwarp();
+        const uint32_t nwords = (off0 + cnt * w_bits + 31) >> 5;
+        if (lane < nwords && v) atomicOr(&sm.stage[wbase + lane], v);
     }
     __syncthreads();
     const uint32_t raw_bits = ((len + 7) / 8) * 8;
-    if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, s_sign, raw_bits, tid, kChunkThreads);
-    if (p.ztag == 2) write_bits_block(pay + p.zero_off, 0, s_zero, raw_bits, tid, kChunkThreads);
+    if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, sm.sign, raw_bits, tid, kChunkThreads);
+    if (p.ztag == 2) write_bits_block(pay + p.zero_off, 0, sm.zero, raw_bits, tid, kChunkThreads);
     const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix) * w_bits;
-    write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), stage, code_bits,
+    write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), sm.stage, code_bits,
                      tid, kChunkThreads);
 }
-
 
 __global__ void __launch_bounds__(kChunkThreads, 6) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
                                                             const ChunkPlan* __restrict__ cps,
@@ -508,10 +494,17 @@ __global__ void __launch_bounds__(kChunkThreads, 6) k_cmp_emit(const CmpBlock* _
     const ChunkPlan p = cp[c];
     const uint32_t len = chunk_len(blk.count, c);
     __shared__ EmitSmem sm;
-    if (len == kChunk)
-        emit_chunk<true>(p, len, blk.pk + static_cast<uint64_t>(c) * kChunk, bp, pay, t, sm);
-    else
-        emit_chunk<false>(p, len, blk.pk + static_cast<uint64_t>(c) * kChunk, bp, pay, t, sm);
+    const uint32_t* src = blk.pk + static_cast<uint64_t>(c) * kChunk;
+    if (bp.width == 1) {
+        if (len == kChunk)
+            emit_chunk<true, true>(p, len, src, bp, pay, t, sm);
+        else
+            emit_chunk<false, true>(p, len, src, bp, pay, t, sm);
+    } else if (len == kChunk) {
+        emit_chunk<true, false>(p, len, src, bp, pay, t, sm);
+    } else {
+        emit_chunk<false, false>(p, len, src, bp, pay, t, sm);
+    }
 }
 
 }  // namespace
