@@ -645,6 +645,7 @@ constexpr int kPer = 16;  // tile positions per thread: k = tid + 256 j
 // Walk the set bits of s in the chain's program order, multiplying by the
 // phase of each (exact reference product per phase).
 __device__ __forceinline__ C2 chain_walk(uint32_t s, bool desc, const double2* tab, C2 a) {
+    if (a.re == 0.0 && a.im == 0.0) return a;  // zero stays zero (see chain_walk8)
     if (desc) {
         while (s) {
             const int r = 31 - __clz(s);
@@ -706,6 +707,16 @@ __device__ __forceinline__ void chain_walk8(double2* tile_s, const double2* tab,
     for (int q = 0; q < kLanesPerStep; ++q) {
         const double2 v = tile_s[pos[q]];
         a[q] = C2{v.x, v.y};
+        // an exact zero stays zero under any phase (the product is +-0,
+        // which the codec stores as zero): no walk for it
+        if (v.x == 0.0 && v.y == 0.0) sb[q] = 0;
+    }
+    any = 0;
+    all = ~0u;
+#pragma unroll
+    for (int q = 0; q < kLanesPerStep; ++q) {
+        any |= sb[q];
+        all &= sb[q];
     }
     // Walk the union of the eight masks in program order; bits set in all
     // eight multiply unconditionally (independent products, full ILP), the
