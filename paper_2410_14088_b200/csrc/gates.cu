@@ -737,7 +737,8 @@ __device__ __forceinline__ void chain_walk8(double2* tile_s, const double2* tab,
         }
     }
 #pragma unroll
-    for (int q = 0; q < kLanesPerStep; ++q) tile_s[pos[q]] = make_double2(a[q].re, a[q].im);
+    for (int q = 0; q < kLanesPerStep; ++q)
+        if (sb[q]) tile_s[pos[q]] = make_double2(a[q].re, a[q].im);  // untouched amplitudes stay as they are
 }
 
 __device__ __forceinline__ C2 apply_diag_run(const FastOp* ops, const double2* stab, uint32_t q0, uint32_t q1,
@@ -985,6 +986,8 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
                 {
                     const double2 v0 = tile_s[i0], v1 = tile_s[i1];
+                    // a pair of exact zeros maps to zeros (+-0 for the codec)
+                    if (v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) continue;
                     if (g.pad) {  // all entries real: u*a = (u*ar, u*ai) exactly
                         const double u00 = g.m[0], u01 = g.m[2], u10 = g.m[4], u11 = g.m[6];
                         tile_s[i0] = make_double2(__dadd_rn(__dmul_rn(u00, v0.x), __dmul_rn(u01, v1.x)),
