@@ -153,6 +153,8 @@ typedef struct bmq_report {
     uint64_t host_spill_batches;    /* batches whose payloads went to the host arena */
     uint64_t code_domain_batches;   /* batches run on quantiser codes (BMQ_FLAG_CODE_DOMAIN) */
     uint64_t pool_growths;          /* automatic payload arenas doubled after a compaction */
+    uint64_t lazy_cx;               /* CX gates folded into a pass's index map (per batch) */
+    uint64_t perm_materialisations; /* index maps materialised before a phase chain (per batch) */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

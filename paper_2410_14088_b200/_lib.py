@@ -64,7 +64,8 @@ class bmq_report(C.Structure):
                 ("batches", C.c_uint64), ("decompress_bytes", C.c_uint64), ("gate_bytes", C.c_uint64),
                 ("compress_bytes", C.c_uint64), ("fused_batches", C.c_uint64), ("compactions", C.c_uint64),
                 ("host_spill_bytes", C.c_uint64), ("host_spill_batches", C.c_uint64),
-                ("code_domain_batches", C.c_uint64), ("pool_growths", C.c_uint64)]
+                ("code_domain_batches", C.c_uint64), ("pool_growths", C.c_uint64),
+                ("lazy_cx", C.c_uint64), ("perm_materialisations", C.c_uint64)]
 
 
 _P = C.c_void_p

@@ -613,7 +613,8 @@ DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks
                       "payload_bytes_read", "payload_bytes_written", "dense_bytes", "kernel_launches",
                       "device_peak_bytes", "gate_passes", "decompress_ms", "gate_ms", "compress_ms", "batches",
                       "decompress_bytes", "gate_bytes", "compress_bytes", "fused_batches", "compactions",
-                      "host_spill_bytes", "host_spill_batches", "code_domain_batches", "pool_growths")
+                      "host_spill_bytes", "host_spill_batches", "code_domain_batches", "pool_growths",
+                      "lazy_cx", "perm_materialisations")
 
 
 def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:

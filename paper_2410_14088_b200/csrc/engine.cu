@@ -758,6 +758,10 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     emit_batch(nblk);
     phase_event(4 * bidx + 3);
     if (fused) ++counters_.fused_batches;
+    if (!codes) {
+        counters_.lazy_cx += sp.prog.lazy_cx;
+        counters_.perm_materialisations += sp.prog.perms;
+    }
     counters_.gate_passes += sp.prog.passes.size();
 }
 
@@ -919,6 +923,8 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.host_spill_batches = counters_.host_spill_batches;
     r.code_domain_batches = counters_.code_domain_batches;
     r.pool_growths = counters_.pool_growths;
+    r.lazy_cx = counters_.lazy_cx;
+    r.perm_materialisations = counters_.perm_materialisations;
     *rep = r;
 }
 

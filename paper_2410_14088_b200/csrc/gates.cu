@@ -403,7 +403,7 @@ void build_mono(GateProgram& prog) {
 // map y = M x ^ c, annotate the other ops with the rows / columns of M they
 // need, and materialise the map before phase chains (which address
 // amplitudes by their full index).
-void lazify(std::vector<FastOp>& fops, FastPass& fp) {
+void lazify(std::vector<FastOp>& fops, FastPass& fp, uint32_t& ncx, uint32_t& nperm) {
     uint16_t rows[kMaxTileBits], cols[kMaxTileBits];
     const auto reset = [&]() {
         for (uint32_t i = 0; i < kMaxTileBits; ++i) rows[i] = cols[i] = static_cast<uint16_t>(1u << i);
@@ -419,6 +419,7 @@ void lazify(std::vector<FastOp>& fops, FastPass& fp) {
     for (FastOp f : fops) {
         switch (f.type) {
         case OP_CX:
+            ++ncx;
             if (f.in_hi) {
                 rows[f.tp_lo] ^= rows[f.tp_hi];
                 cols[f.tp_hi] ^= cols[f.tp_lo];
@@ -441,6 +442,7 @@ void lazify(std::vector<FastOp>& fops, FastPass& fp) {
             if (!identity() || affine) {
                 FastOp m{};
                 m.type = OP_PERM;
+                ++nperm;
                 std::memcpy(&m.m[0], cols, sizeof cols);
                 out.push_back(m);
                 reset();
@@ -461,6 +463,7 @@ void lazify(std::vector<FastOp>& fops, FastPass& fp) {
 void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bits) {
     prog.total_bits = total_bits;
     prog.passes.clear();
+    prog.lazy_cx = prog.perms = 0;
     const uint64_t all = total_bits >= 64 ? ~0ull : (1ull << total_bits) - 1;
     const uint32_t tb = std::min(total_bits, kMaxTileBits);
     const uint64_t coalesce = (1ull << std::min(5u, total_bits)) - 1;
@@ -491,7 +494,8 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
             const size_t tab_mark = prog.chain_tab.size();
             std::vector<FastOp> fops = fuse_chains(ops, begin, end, prog.chain_tab, mask);
             FastPass lazy{};
-            lazify(fops, lazy);
+            uint32_t ncx = 0, nperm = 0;
+            lazify(fops, lazy, ncx, nperm);
             if (fops.size() > static_cast<size_t>(kMaxFastOps) && end - begin > 1) {
                 prog.chain_tab.resize(tab_mark);
                 const uint32_t mid = begin + (end - begin) / 2;
@@ -506,6 +510,8 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
                 fp->base = make_runs(~mask & all, total_bits, static_cast<int>(total_bits));
                 fp->nops = static_cast<uint32_t>(fops.size());
                 std::memcpy(fp->minv, lazy.minv, sizeof fp->minv);
+                prog.lazy_cx += ncx;
+                prog.perms += nperm;
                 fp->final_perm = lazy.final_perm;
                 fp->tab_base = tab_mark / 2;
                 fp->tab_entries = static_cast<uint32_t>((prog.chain_tab.size() - tab_mark) / 2);

@@ -130,6 +130,7 @@ struct GateProgram {
     uint32_t total_bits = 0;
     bool all_diagonal = true;     // no op mixes amplitudes
     bool mono = false;            // every op is monomial with unit entries (code-domain stage)
+    uint32_t lazy_cx = 0, perms = 0;  // CX folded into index maps / materialisations (fast passes)
     uint64_t diag_cond_mask = 0;  // bits whose values decide whether any op acts
     ~GateProgram();
     GateProgram() = default;

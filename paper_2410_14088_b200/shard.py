@@ -253,7 +253,7 @@ class EngineShard:
 _SUMMED = ("groups_processed", "groups_skipped", "blocks_processed", "payload_bytes_read", "payload_bytes_written",
            "dense_bytes", "kernel_launches", "gate_passes", "batches", "decompress_bytes", "gate_bytes",
            "compress_bytes", "fused_batches", "compactions", "host_spill_bytes", "host_spill_batches",
-           "code_domain_batches", "pool_growths")
+           "code_domain_batches", "pool_growths", "lazy_cx", "perm_materialisations")
 
 
 class ShardedSimulator:

@@ -300,3 +300,52 @@ def test_pool_growth_is_exact(gpu, port):
         assert rep.device["pool_growths"] > 0
         assert sim.payloads() == want.payloads
         assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+
+
+def lazy_cx_circuit(gpu, rng, n, count):
+    """Dense start, then random CX (controls inside and outside the tile),
+    CP runs sharing a control (phase chains), H / RX / RZ / CZ: exercises the
+    lazy-CX index map, its materialisation before chains, and the gather on
+    store."""
+    gl = [(0, q, 0, 0.0) for q in range(n)] + [(10, q, 0, 0.3 + 0.1 * q) for q in range(n)]
+    for _ in range(count):
+        r = rng.random()
+        if r < 0.45:
+            a, b = rng.choice(n, 2, replace=False)
+            gl.append((12, int(a), int(b), 0.0))
+        elif r < 0.6:  # a phase chain: CP(j, c) for descending j
+            c = int(rng.integers(3, n))
+            for j in sorted(rng.choice(c, size=min(c, 4), replace=False), reverse=True):
+                gl.append((14, int(j), c, float(np.pi / 2 ** (c - j))))
+        elif r < 0.75:
+            gl.append((0, int(rng.integers(n)), 0, 0.0))
+        elif r < 0.9:
+            gl.append((8 + int(rng.integers(3)), int(rng.integers(n)), 0, float(rng.uniform(0, 6.28))))
+        else:
+            a, b = rng.choice(n, 2, replace=False)
+            gl.append((13, int(a), int(b), 0.0))
+    return gl, gpu.Circuit(n, [gpu.Gate(gpu.GateKind(k), a, b, ang) for k, a, b, ang in gl])
+
+
+@pytest.mark.parametrize("seed,n,b,inner", [(0, 16, 12, 2), (1, 17, 13, 3), (2, 16, 12, 4), (3, 18, 14, 2)])
+def test_lazy_cx_passes_are_exact(gpu, port, seed, n, b, inner):
+    rng = np.random.default_rng(900 + seed)
+    gl, c = lazy_cx_circuit(gpu, rng, n, 160)
+    want = port.simulate(n, gl, b, inner, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=inner, error_bound=1e-3)) as sim:
+        rep = sim.run()
+        assert rep.device["lazy_cx"] > 0 and rep.device["perm_materialisations"] > 0
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=NORM_RTOL)
+
+
+@pytest.mark.parametrize("n,b,inner", [(18, 12, 2), (19, 13, 3)])
+def test_qft_sparse_stages_are_exact(gpu, port, n, b, inner):
+    """QFT|0>: the phase chains act only on exact zeros (skipped walks) and
+    early H sweeps mostly on zero pairs; payloads stay byte-exact."""
+    c = gpu.generate_benchmark("qft", n)
+    want = port.simulate(n, [g.as_tuple() for g in c.gates], b, inner, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=inner, identity_skip=True)) as sim:
+        sim.run()
+        assert sim.payloads() == want.payloads
