@@ -672,6 +672,14 @@ __device__ __forceinline__ C2 chain_walk(uint32_t s, bool desc, const double2* t
 
 constexpr int kLanesPerStep = 1 << kChainQBits;
 
+// pdep over a <= 12-bit tile mask: the low bits of r into the set bits of m.
+__device__ __forceinline__ uint32_t deposit12(uint32_t r, uint32_t m) {
+    uint32_t out = 0;
+    for (; m; m &= m - 1, r >>= 1)
+        if (r & 1u) out |= m & (0u - m);
+    return out;
+}
+
 template <bool kDesc>
 __device__ __forceinline__ int next_bit(uint32_t s) {
     return kDesc ? 31 - __clz(s) : __ffs(s) - 1;
@@ -747,8 +755,15 @@ __device__ __forceinline__ void chain_walk8(double2* tile_s, const double2* tab,
         if (sb[q]) tile_s[pos[q]] = make_double2(a[q].re, a[q].im);  // untouched amplitudes stay as they are
 }
 
+// Diagonal ops [q0, q1) on the amplitude at physical tile position k (x:
+// its buffer index). DIAG / CDIAG read logical bits through the pass's lazy
+// CX map (FastOp::mrow, cvec); phase chains only run where the map is the
+// identity (lazify), so they use x directly.
 __device__ __forceinline__ C2 apply_diag_run(const FastOp* ops, const double2* stab, uint32_t q0, uint32_t q1,
-                                             uint64_t x, C2 a) {
+                                             uint64_t x, C2 a, uint32_t cvec, uint32_t k) {
+    const auto bit = [&](bool in, uint16_t row, uint8_t tp, uint8_t b) -> uint32_t {
+        return in ? ((__popc(row & k) ^ (cvec >> tp)) & 1u) : static_cast<uint32_t>((x >> b) & 1);
+    };
     for (uint32_t q = q0; q < q1; ++q) {
         const FastOp& o = ops[q];
         if (o.type == OP_CHAIN) {
@@ -757,9 +772,10 @@ __device__ __forceinline__ C2 apply_diag_run(const FastOp* ops, const double2* s
             memcpy(&R, &o.m[0], 4);
             a = chain_walk(static_cast<uint32_t>(x) & R, o.et[0] != 0, stab + o.pad2, a);
         } else if (o.type == OP_CDIAG) {
-            if (((x >> o.hi) & (x >> o.lo) & 1) && o.et[0] != ET_ONE) a = entry_mul(o.et[0], o.m[0], o.m[1], a);
+            if (bit(o.in_hi, o.mrow, o.tp_hi, o.hi) & bit(o.in_lo, o.mrow2, o.tp_lo, o.lo) && o.et[0] != ET_ONE)
+                a = entry_mul(o.et[0], o.m[0], o.m[1], a);
         } else {  // OP_DIAG
-            const int e = static_cast<int>((x >> o.hi) & 1);
+            const int e = static_cast<int>(bit(o.in_hi, o.mrow, o.tp_hi, o.hi));
             if (o.et[e] != ET_ONE) a = entry_mul(o.et[e], o.m[2 * e], o.m[2 * e + 1], a);
         }
     }
@@ -831,7 +847,8 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                                                                  int interleaved, uint64_t ntiles,
                                                                  const __grid_constant__ FastPass pass,
                                                                  const __grid_constant__ QuantOut quant,
-                                                                 const uint32_t* __restrict__ vtab) {
+                                                                 const uint32_t* __restrict__ vtab,
+                                                                 int dbg_full_support) {
     // dynamic SMEM: 4096 amplitudes (tile position k) | chain tables | ops
     extern __shared__ double2 tile_s[];
     __shared__ uint64_t joff[kPer];
@@ -861,16 +878,21 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         const uint32_t words = pass.nops * static_cast<uint32_t>(sizeof(FastOp) / 4);
         for (uint32_t e = tid; e < words; e += kFastThreads) dst[e] = src[e];
     }
+    __shared__ uint32_t s_supp[2];
+    if (tid < 2) s_supp[tid] = 0;
     __syncthreads();
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t parity = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, parity ^= 1) {
         const uint64_t base = runs_deposit(tile, pass.base);
         // Index used by diagonal conditions. Block-wise batches (vtab) hold
         // single blocks of a diagonal stage: the bits above lb are the
         // block's inner value, not its slot in the batch.
         const uint64_t xbase = vtab ? ((static_cast<uint64_t>(vtab[base >> lb]) << lb) | (base & lmask)) : base;
         __syncthreads();  // previous tile's stores have read tile_s
+        if (tid == 0) s_supp[parity ^ 1] = 0;  // the next tile's slot (last read two tiles ago)
         {
             double re[kPer], im[kPer];
+            uint32_t nzpos = 0;
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
@@ -878,8 +900,19 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 im[j] = buf[a + im_off];
             }
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) tile_s[tid + 256 * j] = make_double2(re[j], im[j]);
+            for (int j = 0; j < kPer; ++j) {
+                tile_s[tid + 256 * j] = make_double2(re[j], im[j]);
+                if (re[j] != 0.0 || im[j] != 0.0) nzpos |= 0x80000000u | (tid + 256u * j);  // bit 31: some nonzero
+            }
+            nzpos = __reduce_or_sync(0xffffffffu, nzpos);
+            if ((tid & 31) == 0 && nzpos) atomicOr(&s_supp[parity], nzpos);
         }
+        __syncthreads();
+        // Support: every nonzero amplitude of the tile sits at a position
+        // inside S (x & ~S == 0). Diagonal gates keep S, a mixing gate adds
+        // its partner offset; ops below only visit positions inside S (a zero
+        // stays zero under every gate, up to the sign the codec ignores).
+        uint32_t S = dbg_full_support ? 0x80000fffu : s_supp[parity];  // bit 31 set unless the tile is all zero
         bool owners_only = true;
         uint32_t cvec = 0;  // lazy CX: affine part of the tile's index map
         for (uint32_t i = 0; i < pass.nops;) {
@@ -907,6 +940,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
 #pragma unroll
                 for (int j = 0; j < kPer; ++j) tile_s[tid + 256u * j] = v[j];
                 cvec = 0;
+                if (S) S = 0x80000fffu;  // (conservative: the map moved the support)
                 owners_only = true;
                 ++i;
                 continue;
@@ -916,6 +950,25 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 while (i2 < pass.nops && is_diag(sops[i2].type)) ++i2;
                 if (!owners_only) __syncthreads();
                 owners_only = true;
+                if (S == 0) {  // an all-zero tile: nothing to do
+                    i = i2;
+                    continue;
+                }
+                const uint32_t Sp = S & 0xfffu;  // positions
+                if (__popc(Sp) < 11) {  // sparse tile: only the 2^|S| positions of the support
+                    __syncthreads();
+                    const uint32_t np = 1u << __popc(Sp);
+                    for (uint32_t r = tid; r < np; r += kFastThreads) {
+                        const uint32_t k = deposit12(r, Sp);
+                        const double2 v = tile_s[k];
+                        const uint64_t xb = xbase | lut_lo[k & 63] | lut_hi[k >> 6];
+                        const C2 o = apply_diag_run(sops, stab, i, i2, xb, C2{v.x, v.y}, cvec, k);
+                        tile_s[k] = make_double2(o.re, o.im);
+                    }
+                    owners_only = false;
+                    i = i2;
+                    continue;
+                }
                 if (i2 == i + 1 && g.type == OP_CHAIN) {  // a lone phase chain: parameters in registers
                     uint32_t R;
                     uint64_t plan;
@@ -925,7 +978,27 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                     const double2* tab = stab + g.pad2;
                     const int pc = g.in_hi ? g.tp_hi : -1;
                     const uint32_t xlo = static_cast<uint32_t>(xbase);
-                    if (pc >= 0 || ((xbase >> g.hi) & 1)) {
+                    // support: no nonzero amplitude with bit c, or none with a bit of R
+                    uint32_t rs = xlo & R;
+                    for (uint32_t m = S & 0xfffu; m; m &= m - 1) {
+                        const uint32_t p = __ffs(m) - 1;
+                        rs |= (p < 6 ? lut_lo[1u << p] : lut_hi[1u << (p - 6)]) & R;
+                    }
+                    const bool active = rs && (pc >= 0 ? ((S >> pc) & 1) : ((xbase >> g.hi) & 1));
+                    if (active && __popc(S & 0xfffu) < 11) {  // sparse tile: the support positions with bit c
+                        __syncthreads();
+                        const uint32_t Sp = S & 0xfffu;
+                        const uint32_t cm = pc >= 0 ? (Sp & ~(1u << pc)) : Sp, cb = pc >= 0 ? (1u << pc) : 0u;
+                        const uint32_t np = 1u << __popc(cm);
+                        for (uint32_t r = tid; r < np; r += kFastThreads) {
+                            const uint32_t k = deposit12(r, cm) | cb;
+                            const double2 v = tile_s[k];
+                            const uint32_t x = xlo | lut_lo[k & 63] | lut_hi[k >> 6];
+                            const C2 o = chain_walk(x & R, desc, tab, C2{v.x, v.y});
+                            tile_s[k] = make_double2(o.re, o.im);
+                        }
+                        owners_only = false;
+                    } else if (active) {
                         __syncthreads();  // positions cross thread ownership
                         const uint32_t rounds = (pc >= 0 ? 2048u : 4096u) / (256u * kLanesPerStep);
                         for (uint32_t rd = 0; rd < rounds; ++rd) {
@@ -973,7 +1046,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                     for (int j = 0; j < kPer; ++j) {
                         const uint32_t k = tid + 256u * j;
                         const double2 v = tile_s[k];
-                        const C2 r = apply_diag_run(sops, stab, i, i2, xbase | toff | joff[j], C2{v.x, v.y});
+                        const C2 r = apply_diag_run(sops, stab, i, i2, xbase | toff | joff[j], C2{v.x, v.y}, cvec, k);
                         tile_s[k] = make_double2(r.re, r.im);
                     }
                 }
@@ -986,8 +1059,13 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             // U2 on logical tile bit t: physical pairs (x, x ^ dvec); x is
             // the |0> side when parity(mrow & x) ^ c_t is 0
             const uint32_t dv = g.dvec, piv = __ffs(dv) - 1, ct = (cvec >> g.tp_hi) & 1u;
-            for (uint32_t r = tid; r < 2048; r += kFastThreads) {
-                const uint32_t x0 = insert0(r, piv), x1 = x0 ^ dv;
+            if (S == 0) continue;  // zeros map to zeros
+            const uint32_t S2 = (S | dv) & 0xfffu;
+            const bool dense = __popc(S2) >= 11;
+            const uint32_t npairs = dense ? 2048u : (1u << (__popc(S2) - 1)), pm = S2 & ~(1u << piv);
+            S = S2 | 0x80000000u;
+            for (uint32_t r = tid; r < npairs; r += kFastThreads) {
+                const uint32_t x0 = dense ? insert0(r, piv) : deposit12(r, pm), x1 = x0 ^ dv;
                 const bool sw = (__popc(g.mrow & x0) ^ ct) & 1u;
                 const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
                 {
@@ -1400,6 +1478,13 @@ void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, ui
     }
 }
 
+// BMQ_DBG_FULL_SUPPORT=1 disables tile support tracking (every position is
+// visited), for bisecting; read once.
+bool full_support_debug() {
+    static const bool on = getenv("BMQ_DBG_FULL_SUPPORT") != nullptr;
+    return on;
+}
+
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant, const uint32_t* vtab,
                  uint64_t nblocks) {
@@ -1428,7 +1513,8 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
             const uint64_t grid = std::min<uint64_t>(tiles, 148ull * per_sm * 8);
             const bool last = pi + 1 == prog.passes.size();
             k_gate_pass_fast<<<static_cast<uint32_t>(grid), kFastThreads, smem, st>>>(
-                buf, lb, interleaved ? 1 : 0, tiles, *p.fp, (fuse && last) ? *quant : none, vtab);
+                buf, lb, interleaved ? 1 : 0, tiles, *p.fp, (fuse && last) ? *quant : none, vtab,
+                full_support_debug() ? 1 : 0);
         } else {
             const uint32_t nth = std::min<uint32_t>(kPassThreads, 1u << p.tb);
             const size_t smem = 2 * (size_t(1) << p.tb) * sizeof(double);

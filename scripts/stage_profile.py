@@ -8,7 +8,7 @@ b = int(sys.argv[3]) if len(sys.argv) > 3 else 20
 inner = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 br = float(sys.argv[5]) if len(sys.argv) > 5 else 1e-3
 c = cbq.generate_benchmark(name, n, cbq.BenchmarkParams(layers=4))
-cfg = cbq.Config(block_bits=b, inner_size=inner, error_bound=br)
+cfg = cbq.Config(block_bits=b, inner_size=inner, error_bound=br, identity_skip=True)
 sim = cbq.Simulator(c, cfg)
 rep = sim.run(); sim.reset(); rep = sim.run()
 plan = sim.plan()
@@ -17,6 +17,6 @@ rows = []
 for i, (st, ms) in enumerate(zip(plan.stages, rep.stage_ms)):
     kinds = collections.Counter(cbq.gate_name(c.gates[g].kind) for g in range(st.gate_begin, st.gate_end))
     rows.append((ms, i, st.inner, dict(kinds)))
-for ms, i, inn, k in sorted(rows, reverse=True)[:30]:
+for ms, i, inn, k in sorted(rows, reverse=True)[:40]:
     print(f"stage {i:3d} {ms:9.2f} ms inner={inn} {k}")
 print("sum stage ms", sum(r[0] for r in rows))

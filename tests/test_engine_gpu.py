@@ -349,3 +349,21 @@ def test_qft_sparse_stages_are_exact(gpu, port, n, b, inner):
     with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=inner, identity_skip=True)) as sim:
         sim.run()
         assert sim.payloads() == want.payloads
+
+
+def test_support_tracking_matches_full_sweeps(gpu):
+    """Tile support tracking (ops visit only positions that can be nonzero)
+    against full sweeps (BMQ_DBG_FULL_SUPPORT=1 in a child process): same bytes."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); from paper_2410_14088_b200 import cbq; import hashlib\n"
+            "for name, n, b in (('qft', 18, 12), ('ghz', 18, 12), ('bv', 17, 12)):\n"
+            "    c = cbq.generate_benchmark(name, n)\n"
+            "    with cbq.Simulator(c, cbq.Config(block_bits=b, inner_size=2)) as s:\n"
+            "        s.run(); print(hashlib.sha256(b''.join(s.payloads())).hexdigest())\n") % os.path.dirname(GOLDEN + "/../..")
+    outs = []
+    for env in ({}, {"BMQ_DBG_FULL_SUPPORT": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env={**os.environ, **env})
+        assert r.returncode == 0, r.stderr
+        outs.append(r.stdout)
+    assert outs[0] == outs[1] and outs[0].count("\n") == 3
