@@ -360,7 +360,7 @@ def test_support_tracking_matches_full_sweeps(gpu):
             "for name, n, b in (('qft', 18, 12), ('ghz', 18, 12), ('bv', 17, 12)):\n"
             "    c = cbq.generate_benchmark(name, n)\n"
             "    with cbq.Simulator(c, cbq.Config(block_bits=b, inner_size=2)) as s:\n"
-            "        s.run(); print(hashlib.sha256(b''.join(s.payloads())).hexdigest())\n") % os.path.dirname(GOLDEN + "/../..")
+            "        s.run(); print(hashlib.sha256(b''.join(s.payloads())).hexdigest())\n") % os.path.dirname(os.path.dirname(GOLDEN))
     outs = []
     for env in ({}, {"BMQ_DBG_FULL_SUPPORT": "1"}):
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env={**os.environ, **env})
