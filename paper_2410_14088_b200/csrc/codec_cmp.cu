@@ -411,6 +411,14 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
         sm.pre[tid] = pre;
     }
     __syncthreads();
+    if (kW1 && kFull && p.nnz == kChunk) {  // every code one bit, no zeros: the stream is the ballot words
+        const uint32_t raw_bits = kChunk;
+        if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, sm.sign, raw_bits, tid, kChunkThreads);
+        const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix);
+        write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), sm.bits,
+                         kChunk, tid, kChunkThreads);
+        return;
+    }
     // C: each warp packs its words' codes LSB-first into the stage; lane i
     // assembles stage word i of a word's contiguous bit range (edge words OR-ed)
 #pragma unroll 1
