@@ -955,7 +955,8 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                     continue;
                 }
                 const uint32_t Sp = S & 0xfffu;  // positions
-                if (__popc(Sp) < 11) {  // sparse tile: only the 2^|S| positions of the support
+                const bool lone_chain = i2 == i + 1 && g.type == OP_CHAIN;
+                if (!lone_chain && __popc(Sp) < 11) {  // sparse tile: only the 2^|S| positions of the support
                     __syncthreads();
                     const uint32_t np = 1u << __popc(Sp);
                     for (uint32_t r = tid; r < np; r += kFastThreads) {
@@ -969,7 +970,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                     i = i2;
                     continue;
                 }
-                if (i2 == i + 1 && g.type == OP_CHAIN) {  // a lone phase chain: parameters in registers
+                if (lone_chain) {  // a lone phase chain: parameters in registers
                     uint32_t R;
                     uint64_t plan;
                     memcpy(&R, &g.m[0], 4);
