@@ -346,7 +346,53 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     const uint64_t half = info.count / 2, g0 = static_cast<uint64_t>(c) * kChunk;
     const uint8_t* codes = blk.in + info.code_seg;
     const bool sums = want_sums != 0;
-    if (len == kChunk && !check)
+    const uint32_t nnz_chunk = s_pre[kWordsPerChunk - 1] + __popc(s_nz[kWordsPerChunk - 1]);
+    if (kMode != kSumsOnly && len == kChunk && !check && width <= 16 && nnz_chunk == kChunk) {
+        // No zero in the chunk and narrow codes: scalar s has rank s, so each
+        // thread decodes four consecutive scalars from one 64-bit window and
+        // writes them with 16-byte stores.
+        const uintptr_t cs = reinterpret_cast<uintptr_t>(codes);
+        const uint64_t cb = static_cast<uint64_t>(cs & 3) * 8 + static_cast<uint64_t>(d.nz_prefix) * width;
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3)) + (cb >> 5);
+        const uint32_t cb0 = static_cast<uint32_t>(cb & 31), cmask = (1u << width) - 1;
+        const uint32_t qb = static_cast<uint32_t>(qbase);
+#pragma unroll 4
+        for (int i = 0; i < kChunk / (4 * kChunkThreads); ++i) {
+            const uint32_t s0 = 4 * tid + 4 * kChunkThreads * i;
+            const uint32_t a = cb0 + s0 * width;
+            const uint32_t w0 = __ldg(cw + (a >> 5)), w1 = __ldg(cw + (a >> 5) + 1), w2 = __ldg(cw + (a >> 5) + 2);
+            const uint64_t win = ((static_cast<uint64_t>(__funnelshift_r(w1, w2, a & 31)) << 32) |
+                                  __funnelshift_r(w0, w1, a & 31));
+            const uint32_t sg = (s_sign[s0 >> 5] >> (s0 & 31)) & 15u;
+            uint32_t c[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) c[e] = static_cast<uint32_t>(win >> (e * width)) & cmask;
+            if constexpr (kMode == kCodes) {
+                uint4 o;
+                o.x = ((qb + c[0]) << 2) | ((sg & 1u) << 1);
+                o.y = ((qb + c[1]) << 2) | (sg & 2u);
+                o.z = ((qb + c[2]) << 2) | ((sg >> 1) & 2u);
+                o.w = ((qb + c[3]) << 2) | ((sg >> 2) & 2u);
+                __stcs(reinterpret_cast<uint4*>(cdst + s0), o);
+            } else {
+                double v[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double m = __ldg(t.dequant + (qb + c[e]));
+                    v[e] = ((sg >> e) & 1u) ? -m : m;
+                    if (sums) {
+                        sq += m * m;
+                        if (g0 + s0 + e < half)
+                            sre += v[e];
+                        else
+                            sim += v[e];
+                    }
+                }
+                __stcs(reinterpret_cast<double2*>(dst + s0), make_double2(v[0], v[1]));
+                __stcs(reinterpret_cast<double2*>(dst + s0 + 2), make_double2(v[2], v[3]));
+            }
+        }
+    } else if (len == kChunk && !check)
         dec_scalars<kMode, true, false>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, t, dst,
                                         cdst, half, g0, sums, sq, sre, sim, bad);
     else
