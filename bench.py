@@ -130,6 +130,9 @@ class ClockSampler:
 
 
 def dist_setup():
+    # the driver reads one JSON line from rank 0: keep NCCL's banner off stdout
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
