@@ -33,7 +33,7 @@ namespace bmq {
 const char* dev_error_message(uint32_t code) {
     switch (code) {
     case DE_NONFINITE: return "input scalars must be finite";
-    case DE_WINDOW: return "scalar magnitude below the quantiser table window of this error bound";
+    case DE_WINDOW: return "scalar magnitude outside the quantiser table window of this error bound";
     case DE_HDR_TRUNC: return "header truncated";
     case DE_HDR_BOUND: return "header: invalid relative error bound";
     case DE_HDR_TRAIL: return "header: trailing bytes after payload";
@@ -117,6 +117,7 @@ const DevTables& device_tables(double b_r) {
     t.idem_hi = h.idem_hi;
     t.b_r = h.b_r;
     t.inv_ba = 1.0 / h.b_a;
+    t.est_eps = 1e-6 * t.inv_ba + 1e-6;
     return cache.emplace(std::make_pair(dev, key), t).first->second;
 }
 
@@ -141,7 +142,9 @@ __global__ void __launch_bounds__(kChunkThreads) k_cmp_stats(const CmpBlock* __r
     for (int j = 0; j < 32; ++j) {
         const uint32_t s = 128 * j + 32 * w + lane;
         if (s < len) {
-            const uint32_t pk = quantize_pack(__ldg(src + s), t, bad, oow);
+            const double v = __ldg(src + s);
+            uint32_t pk;
+            quantize_pack_n<1>(&v, &pk, t, bad, oow);
             dst[s] = pk;
             acc.add(pk);
         }

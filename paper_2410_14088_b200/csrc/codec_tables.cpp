@@ -87,11 +87,19 @@ std::unique_ptr<CodecTables> build(double b_r) {
     t->b_a = std::log2(1.0 + b_r);
     const Quantiser f{t->b_a};
     const uint64_t max_bits = to_bits(DBL_MAX);
-    t->qhi = f(max_bits);
+    const int64_t qtop = f(max_bits);
+    t->qhi = qtop;
     t->qlo = f(1);  // DBL_TRUE_MIN
-    if (static_cast<uint64_t>(t->qhi - t->qlo) + 2 > kMaxEntries) t->qlo = t->qhi - static_cast<int64_t>(kMaxEntries) + 2;
+    if (static_cast<uint64_t>(t->qhi - t->qlo) + 2 > kMaxEntries) {
+        // Tiny bounds: keep a window of kMaxEntries codes for magnitudes up
+        // to 2^32 and down from there (amplitudes are at most 1); scalars
+        // outside it are rejected as out of window.
+        t->qhi = std::min(qtop, f(to_bits(0x1p32)));
+        t->qlo = t->qhi - static_cast<int64_t>(kMaxEntries) + 2;
+    }
     const uint64_t count = static_cast<uint64_t>(t->qhi - t->qlo) + 1;
     t->thresh.assign(count + 1, kInfBits);
+    if (t->qhi < qtop) t->thresh[count] = threshold(f, t->qhi + 1, max_bits);  // top of the window
     t->dequant.assign(count, 0.0);
     unsigned nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;

@@ -94,18 +94,24 @@ __device__ __forceinline__ void quantize_pack_n(const double* v, uint32_t* pk, c
                                                 bool& oow) {
     uint64_t bits[N];
     int64_t idx[N];
-    bool live[N];
+    bool live[N], sure[N];
 #pragma unroll
     for (int e = 0; e < N; ++e) {
         live[e] = isfinite(v[e]) && v[e] != 0.0;
         if (!isfinite(v[e])) bad = true;
-        idx[e] = live[e] ? quantize_estimate(v[e], t, bits[e]) : 0;
+        const double x = live[e] ? quantize_estimate_x(v[e], t, bits[e]) : 0.0;
+        const double r = rint(x);
+        int64_t q = static_cast<int64_t>(r);
+        // the rounding is settled unless x lies within est_eps of a half-integer
+        sure[e] = 0.5 - fabs(x - r) > t.est_eps && q >= t.qlo && q <= t.qhi;
+        q = q < t.qlo ? t.qlo : (q > t.qhi ? t.qhi : q);
+        idx[e] = q - t.qlo;
     }
     uint64_t t0[N], t1[N];
 #pragma unroll
-    for (int e = 0; e < N; ++e) {
-        t0[e] = __ldg(t.thresh + idx[e]);
-        t1[e] = __ldg(t.thresh + idx[e] + 1);
+    for (int e = 0; e < N; ++e) {  // threshold probes only near a tie
+        t0[e] = (live[e] && !sure[e]) ? __ldg(t.thresh + idx[e]) : 0;
+        t1[e] = (live[e] && !sure[e]) ? __ldg(t.thresh + idx[e] + 1) : ~0ull;
     }
 #pragma unroll
     for (int e = 0; e < N; ++e) {
@@ -114,7 +120,7 @@ __device__ __forceinline__ void quantize_pack_n(const double* v, uint32_t* pk, c
             continue;
         }
         int64_t q;
-        if (bits[e] >= t0[e] && bits[e] < t1[e])
+        if (sure[e] || (bits[e] >= t0[e] && bits[e] < t1[e]))
             q = t.qlo + idx[e];
         else
             q = quantize(v[e], t, oow);

@@ -60,6 +60,7 @@ struct DevTables {
     int64_t idem_lo, idem_hi;
     double b_r;               // relative bound written into headers
     double inv_ba;            // 1 / b_a, estimate only
+    double est_eps;           // bound on |estimate - log2(v)/b_a| (see quantize_estimate_x)
 };
 
 // Device copy of host_tables(b_r) on the current device (cached).
@@ -98,8 +99,37 @@ __device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& 
         }
         --i;
     }
-    while (bits >= __ldg(T + i + 1)) ++i;
+    const int64_t last = t.qhi - t.qlo;  // T[last + 1] bounds the window from above
+    while (bits >= __ldg(T + i + 1)) {
+        if (i == last) {
+            out_of_window = true;
+            return t.qhi;
+        }
+        ++i;
+    }
     return t.qlo + i;
+}
+
+// x ~ log2|v| / b_a for finite v != 0 from a float log2 of the mantissa.
+// __log2f on [1, 2) is within 2^-22.5 of log2, the float rounding of the
+// mantissa adds at most 2^-24 / ln 2, the double arithmetic a few ulp: the
+// estimate is within est_eps = 1e-6 / b_a + 1e-6 of the reference's
+// log2(v) / b_a (glibc log2 is within an ulp). Away from a half-integer by
+// more than that, llround of the reference value is round(x) itself.
+__device__ __forceinline__ double quantize_estimate_x(double v, const DevTables& t, uint64_t& bits) {
+    bits = static_cast<uint64_t>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
+    const uint32_t ex = static_cast<uint32_t>(bits >> 52);
+    uint64_t man = bits & 0xfffffffffffffull;
+    int e2;
+    if (ex == 0) {
+        const int shift = __clzll(static_cast<long long>(man)) - 11;
+        man = (man << shift) & 0xfffffffffffffull;
+        e2 = -1022 - shift;
+    } else {
+        e2 = static_cast<int>(ex) - 1023;
+    }
+    const float m = static_cast<float>(__longlong_as_double(static_cast<long long>(man | 0x3ff0000000000000ull)));
+    return (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
 }
 
 // The estimate of quantize() for finite v != 0 (table index, not clamped

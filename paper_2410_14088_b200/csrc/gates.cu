@@ -801,7 +801,7 @@ __device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2*
     ChunkAcc acc_re, acc_im;
     uint64_t key_re = ~0ull, key_im = ~0ull;
     bool bad = false, oow = false;
-    constexpr int kG = 2;  // amplitudes quantised together (2 kG probes in flight)
+    constexpr int kG = 1;  // amplitudes quantised together (2 kG probes in flight)
     for (int g0 = 0; g0 < kPer; g0 += kG) {
         double v[2 * kG];
         uint32_t pk[2 * kG];

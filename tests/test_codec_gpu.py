@@ -118,3 +118,21 @@ def test_corrupt_payload_messages(gpu, port):
         with pytest.raises(gpu.CodecError) as got:
             gpu.decompress_block(bad)
         assert str(got.value) == str(want.value)
+
+
+@pytest.mark.parametrize("br", [1e-2, 1e-3, 1e-4, 1e-5, 3.0])
+def test_quantiser_near_rounding_ties(gpu, port, br):
+    """Scalars a few ulps around the rounding boundaries exp2((q + 1/2) b_a)
+    of the reference quantiser: the device settles them through the
+    threshold table, everything else through the estimate's error margin;
+    both must give the reference's codes."""
+    rng = np.random.default_rng(int(1 / br) % 1000 + 7)
+    ba = math.log2(1.0 + br)
+    depth = 40 if br >= 1e-4 else 12  # stay inside the 1e-5 table window (codec_tables.cpp kMaxEntries)
+    q = rng.integers(-int(depth / ba), 2, 6000)
+    mid = np.exp2((q + 0.5) * ba)
+    ulp = np.spacing(mid)
+    x = mid + ulp * rng.integers(-4, 5, q.size)
+    x *= np.where(rng.random(q.size) < 0.5, -1.0, 1.0)
+    x = np.concatenate([x, np.exp2(q * ba), rng.standard_normal(2192) * 1e-3])
+    assert gpu.compress_block(x, br) == port.compress_block(x, br)
