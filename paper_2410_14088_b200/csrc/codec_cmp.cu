@@ -504,6 +504,8 @@ __global__ void __launch_bounds__(kChunkThreads, 6) k_cmp_emit(const CmpBlock* _
     }
     const ChunkPlan p = cp[c];
     const uint32_t len = chunk_len(blk.count, c);
+    // a full chunk of zeros is tags only (sign tag 0, zero tag 1): no bytes
+    if (p.nnz == 0 && len == kChunk) return;
     __shared__ EmitSmem sm;
     const uint32_t* src = blk.pk + static_cast<uint64_t>(c) * kChunk;
     if (bp.width == 1) {
