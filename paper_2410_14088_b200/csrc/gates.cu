@@ -755,6 +755,12 @@ __device__ __forceinline__ void chain_walk8(double2* tile_s, const double2* tab,
         if (sb[q]) tile_s[pos[q]] = make_double2(a[q].re, a[q].im);  // untouched amplitudes stay as they are
 }
 
+// Lazy CX on the affine part of a tile's index map (see FastOp).
+__device__ __forceinline__ uint32_t cx_update(const FastOp& g, uint32_t cvec, uint64_t base) {
+    const uint32_t ctl = g.in_hi ? (cvec >> g.tp_hi) & 1u : static_cast<uint32_t>((base >> g.hi) & 1);
+    return cvec ^ (ctl << g.tp_lo);
+}
+
 // Diagonal ops [q0, q1) on the amplitude at physical tile position k (x:
 // its buffer index). DIAG / CDIAG read logical bits through the pass's lazy
 // CX map (FastOp::mrow, cvec); phase chains only run where the map is the
@@ -766,6 +772,10 @@ __device__ __forceinline__ C2 apply_diag_run(const FastOp* ops, const double2* s
     };
     for (uint32_t q = q0; q < q1; ++q) {
         const FastOp& o = ops[q];
+        if (o.type == OP_CX) {  // (chain-free runs only: the map's affine part moves on)
+            cvec = cx_update(o, cvec, x);
+            continue;
+        }
         if (o.type == OP_CHAIN) {
             if (!((x >> o.hi) & 1)) continue;
             uint32_t R;
@@ -918,8 +928,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         for (uint32_t i = 0; i < pass.nops;) {
             const FastOp& g = sops[i];
             if (g.type == OP_CX) {  // no data moves: only the map changes
-                const uint32_t ctl = g.in_hi ? (cvec >> g.tp_hi) & 1u : static_cast<uint32_t>((base >> g.hi) & 1);
-                cvec ^= ctl << g.tp_lo;
+                cvec = cx_update(g, cvec, base);
                 ++i;
                 continue;
             }
@@ -948,6 +957,15 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             if (is_diag(g.type)) {
                 uint32_t i2 = i + 1;
                 while (i2 < pass.nops && is_diag(sops[i2].type)) ++i2;
+                // a chain-free run also absorbs CX ops (lazy: they only change
+                // the index map), so CX-RZ-CX sequences are one sweep
+                if (!has_chain(sops, i, i2))
+                    while (i2 < pass.nops && (sops[i2].type == OP_CX || sops[i2].type == OP_DIAG ||
+                                              sops[i2].type == OP_CDIAG))
+                        ++i2;
+                const uint32_t cvec_in = cvec;  // the map's affine part at the start of the run
+                for (uint32_t q = i; q < i2; ++q)
+                    if (sops[q].type == OP_CX) cvec = cx_update(sops[q], cvec, base);
                 if (!owners_only) __syncthreads();
                 owners_only = true;
                 if (S == 0) {  // an all-zero tile: nothing to do
@@ -963,7 +981,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                         const uint32_t k = deposit12(r, Sp);
                         const double2 v = tile_s[k];
                         const uint64_t xb = xbase | lut_lo[k & 63] | lut_hi[k >> 6];
-                        const C2 o = apply_diag_run(sops, stab, i, i2, xb, C2{v.x, v.y}, cvec, k);
+                        const C2 o = apply_diag_run(sops, stab, i, i2, xb, C2{v.x, v.y}, cvec_in, k);
                         tile_s[k] = make_double2(o.re, o.im);
                     }
                     owners_only = false;
@@ -1021,17 +1039,22 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                             const double2 v = tile_s[tid + 256u * (h + j)];
                             a[j] = C2{v.x, v.y};
                         }
+                        uint32_t cv = cvec_in;
                         for (uint32_t q = i; q < i2; ++q) {
                             const FastOp& o = sops[q];
+                            if (o.type == OP_CX) {
+                                cv = cx_update(o, cv, base);
+                                continue;
+                            }
                             const bool cd = o.type == OP_CDIAG;
                             const double r0 = cd ? 1.0 : o.m[0], i0 = cd ? 0.0 : o.m[1];
                             const double r1 = cd ? o.m[0] : o.m[2], i1 = cd ? o.m[1] : o.m[3];
                             // logical bit = parity(row of M & physical position) ^ c (in the
                             // tile) or the base bit; a missing second bit reads as 1
                             const uint32_t rh = o.in_hi ? o.mrow : 0u, rl = cd && o.in_lo ? o.mrow2 : 0u;
-                            const uint32_t ch = o.in_hi ? (cvec >> o.tp_hi) & 1u : static_cast<uint32_t>((xbase >> o.hi) & 1);
+                            const uint32_t ch = o.in_hi ? (cv >> o.tp_hi) & 1u : static_cast<uint32_t>((xbase >> o.hi) & 1);
                             const uint32_t cl = !cd ? 1u
-                                                    : (o.in_lo ? (cvec >> o.tp_lo) & 1u
+                                                    : (o.in_lo ? (cv >> o.tp_lo) & 1u
                                                                : static_cast<uint32_t>((xbase >> o.lo) & 1));
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
@@ -1047,7 +1070,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                     for (int j = 0; j < kPer; ++j) {
                         const uint32_t k = tid + 256u * j;
                         const double2 v = tile_s[k];
-                        const C2 r = apply_diag_run(sops, stab, i, i2, xbase | toff | joff[j], C2{v.x, v.y}, cvec, k);
+                        const C2 r = apply_diag_run(sops, stab, i, i2, xbase | toff | joff[j], C2{v.x, v.y}, cvec_in, k);
                         tile_s[k] = make_double2(r.re, r.im);
                     }
                 }
