@@ -365,9 +365,6 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
                                            const BlockPlan& bp, uint8_t* pay, const DevTables& t, EmitSmem& sm) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t w_bits = bp.width;
-    // x / w_bits as a multiply-high: exact for x < 2^16 and w_bits <= 30
-    const uint32_t winv = w_bits > 1 ? 0xffffffffu / w_bits + 1 : 0;
-    const uint32_t kspan = w_bits ? (32 + w_bits - 1) / w_bits + 1 : 0;  // codes overlapping one 32-bit word
     const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
     const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
     const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
@@ -422,8 +419,8 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
                          kChunk, tid, kChunkThreads);
         return;
     }
-    // C: each warp packs its words' codes LSB-first into the stage; lane i
-    // assembles stage word i of a word's contiguous bit range (edge words OR-ed)
+    // C: each warp packs its words' codes LSB-first into the stage (shared
+    // OR: a code spans at most two stage words, edge words are shared)
 #pragma unroll 1
     for (int j = 0; j < 32; ++j) {
         const uint32_t k = 4 * j + w;
@@ -440,20 +437,16 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
             }
             continue;
         }
-        const int wb = static_cast<int>(32 * lane) - static_cast<int>(off0);  // word start, code-range relative
-        const uint32_t m_lo = wb <= 0 ? 0 : (w_bits == 1 ? static_cast<uint32_t>(wb)
-                                                          : __umulhi(static_cast<uint32_t>(wb), winv));
-        uint32_t v = 0;
-        for (uint32_t t = 0; t < kspan; ++t) {  // uniform trip count, predicated
-            const uint32_t m = m_lo + t;
-            const int pos = static_cast<int>(m * w_bits) - wb;
-            if (m < cnt && pos < 32) {
-                const uint32_t cv = sm.cw[32 * k + m];
-                v |= pos >= 0 ? (cv << pos) : (cv >> -pos);
+        // scatter: the word's code of rank r (in lane r of sm.cw) goes to bits
+        // [a0 + r w, a0 + (r + 1) w) of the stage, touching at most two words
+        if (lane < cnt) {
+            const uint32_t cv = sm.cw[32 * k + lane];
+            const uint32_t pbit = a0 + lane * w_bits, wi = pbit >> 5, sh = pbit & 31;
+            if (cv) {
+                atomicOr(&sm.stage[wi], cv << sh);
+                if (sh + w_bits > 32) atomicOr(&sm.stage[wi + 1], cv >> (32 - sh));
             }
         }
-        const uint32_t nwords = (off0 + cnt * w_bits + 31) >> 5;
-        if (lane < nwords && v) atomicOr(&sm.stage[wbase + lane], v);
     }
     __syncthreads();
     const uint32_t raw_bits = ((len + 7) / 8) * 8;
