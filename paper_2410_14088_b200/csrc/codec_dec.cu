@@ -317,6 +317,17 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
         return;
     }
     const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
+    {
+        // Warm L1 with the chunk's code bytes (at most len codes from its
+        // first rank on): the per-word code fetches below then hit L1 instead
+        // of each paying a DRAM round trip.
+        const uint8_t* c0 = blk.in + info.code_seg + ((static_cast<uint64_t>(d.nz_prefix) * info.width) >> 3);
+        const uint32_t span = (len * info.width + 7) / 8 + 8;
+        const uintptr_t line0 = reinterpret_cast<uintptr_t>(c0) & ~uintptr_t(127);
+        const uint32_t nlines = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(c0) + span - line0 + 127) >> 7);
+        for (uint32_t l = tid; l < nlines; l += kChunkThreads)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(line0 + 128ull * l));
+    }
     __shared__ uint32_t s_sign[kWordsPerChunk], s_nz[kWordsPerChunk], s_pre[kWordsPerChunk];
     __shared__ double s_red[3][4];
     {
