@@ -32,9 +32,12 @@ __device__ __forceinline__ bool tag_error(uint32_t tag, uint32_t len, uint32_t& 
 
 constexpr int kIndexThreads = 256;
 
+// zflag (optional): one byte per (block, chunk), 1 when every scalar of the
+// chunk is zero (an ALL_ZERO block, or a full chunk with zero tag 1).
 __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __restrict__ blks, uint32_t nch_max,
                                                              DecInfo* __restrict__ infos, DecChunk* __restrict__ dcs,
-                                                             DevTables t, int check_bound, DevError* err) {
+                                                             DevTables t, int check_bound, DevError* err,
+                                                             uint8_t* __restrict__ zflag) {
     const uint32_t bi = blockIdx.x;
     const DecBlock blk = blks[bi];
     const uint8_t* p = blk.in;
@@ -96,6 +99,8 @@ __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __r
             info.flags = 2;
         }
         if (tid == 0) infos[bi] = info;
+        if (zflag)
+            for (uint32_t c = tid; c < nch_max; c += kIndexThreads) zflag[static_cast<uint64_t>(bi) * nch_max + c] = 1;
         return;
     }
     // Both bitmaps: tags, raw offsets; the first bad chunk (in order) reports.
@@ -125,6 +130,7 @@ __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __r
                 } else {
                     dc[c].ztag = static_cast<uint8_t>(tag);
                     dc[c].zero_off = static_cast<uint32_t>(raw0 + carry);
+                    if (zflag) zflag[static_cast<uint64_t>(bi) * nch_max + c] = (tag == 1 && len == kChunk) ? 1 : 0;
                 }
             }
             unsigned long long pre, tot;
@@ -305,7 +311,11 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     double* dst = blk.out + static_cast<uint64_t>(c) * kChunk;
     uint32_t* cdst = reinterpret_cast<uint32_t*>(blk.out) + static_cast<uint64_t>(c) * kChunk;
     const int tid = threadIdx.x;
+    // codes mode with want_sums set: chunks flagged all-zero (zflag) are
+    // left unwritten; the permutation pass reads them as zero words
+    const bool skip_zero = kMode == kCodes && want_sums;
     if (info.flags & 1) {
+        if (skip_zero) return;
         if constexpr (kMode != kSumsOnly) {
             for (uint32_t s = tid; s < len; s += kChunkThreads) {
                 if (kMode == kCodes)
@@ -317,6 +327,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
         return;
     }
     const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
+    if (skip_zero && d.ztag == 1 && len == kChunk) return;
     {
         // Warm L1 with the chunk's code bytes (at most len codes from its
         // first rank on): the per-word code fetches below then hit L1 instead
@@ -417,14 +428,14 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
 
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
-                       uint64_t* launches, int mode) {
+                       uint64_t* launches, int mode, uint8_t* zflag) {
     if (nblk == 0) return;
     BMQ_CUDA(cudaMemsetAsync(d_info, 0, nblk * sizeof(DecInfo), st));
     k_dec_index<<<static_cast<uint32_t>(nblk), kIndexThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t,
-                                                                        check_bound ? 1 : 0, d_err);
+                                                                        check_bound ? 1 : 0, d_err, zflag);
     const uint32_t grid = static_cast<uint32_t>(nblk * nch_max);
     if (mode == 1)
-        k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err);
+        k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, zflag ? 1 : 0, d_err);
     else if (mode == 2)
         k_dec_chunk<kSumsOnly><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 1, d_err);
     else

@@ -451,6 +451,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     bplan_.alloc(max_blocks_);
     dinfo_.alloc(max_blocks_);
     dchunk_.alloc(max_blocks_ * nch_);
+    zflag_.alloc(max_blocks_ * nch_);
     ids_.alloc(std::max<uint64_t>(nid, max_blocks_));
     vtab_.alloc(std::max<uint64_t>(nid, max_blocks_));
     new_off_.alloc(nid);
@@ -737,8 +738,11 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_.p, size_.p, pool_[cur_].p, host_pool_,
                                                   zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, codes ? 1 : 0);
     ++counters_.kernel_launches;
+    // code-domain stages: all-zero chunks stay unwritten; the first
+    // permutation pass reads them as zero words
+    uint8_t* zf = codes && mono_zero_skip(sp.prog, L_.b) ? zflag_.p : nullptr;
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
-                      &counters_.kernel_launches, codes ? 1 : 0);
+                      &counters_.kernel_launches, codes ? 1 : 0, zf);
     phase_event(4 * bidx + 1);
     // the stage's last gate pass quantises straight into pk_ / cplan_
     BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
@@ -746,7 +750,7 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     const uint64_t per = sp.gg.per_group();
     bool fused = true;
     if (codes) {
-        run_mono_program(st_, sp.prog, pk_.p, L_.b, nblk / per, &counters_.kernel_launches, qo);
+        run_mono_program(st_, sp.prog, pk_.p, L_.b, nblk / per, &counters_.kernel_launches, qo, zf);
         ++counters_.code_domain_batches;
     } else {
         fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per, &counters_.kernel_launches,

@@ -169,6 +169,7 @@ private:
     DevArray<BlockPlan> bplan_;
     DevArray<DecInfo> dinfo_;
     DevArray<DecChunk> dchunk_;
+    DevArray<uint8_t> zflag_;  // per (batch slot, chunk): all-zero input chunk (code-domain stages)
     DevArray<uint64_t> ids_;
     DevArray<uint32_t> vtab_;
     DevArray<DevError> err_;

@@ -1413,7 +1413,8 @@ constexpr int kPermGroups = 4;  // 4 x 4 positions per thread
 template <bool kLast>
 __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict__ pk, uint32_t lb, uint64_t ntiles,
                                                             const __grid_constant__ PermPass pass,
-                                                            ChunkPlan* __restrict__ cps) {
+                                                            ChunkPlan* __restrict__ cps, const uint8_t* __restrict__ zf,
+                                                            uint32_t nch) {
     __shared__ __align__(16) uint2 tile_s[1 << kMaxTileBits];
     const uint32_t tid = threadIdx.x;
     const uint64_t lmask = (1ull << lb) - 1;
@@ -1432,8 +1433,17 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
         uint4 re[kPermGroups], im[kPermGroups];
 #pragma unroll
         for (int g = 0; g < kPermGroups; ++g) {
-            re[g] = __ldcs(reinterpret_cast<const uint4*>(pk + pb + toffp[g]));
-            im[g] = __ldcs(reinterpret_cast<const uint4*>(pk + pb + toffp[g] + im_off));
+            const uint64_t addr = pb + toffp[g];
+            if (zf) {  // all-zero input chunks were not written: read them as zero words
+                const uint64_t slot = addr >> (lb + 1), off = addr & ((2ull << lb) - 1);
+                const uint8_t* zs = zf + slot * nch;
+                re[g] = zs[off >> 12] ? make_uint4(1u, 1u, 1u, 1u) : __ldcs(reinterpret_cast<const uint4*>(pk + addr));
+                im[g] = zs[(off + im_off) >> 12] ? make_uint4(1u, 1u, 1u, 1u)
+                                                  : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
+                continue;
+            }
+            re[g] = __ldcs(reinterpret_cast<const uint4*>(pk + addr));
+            im[g] = __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
         }
         uint32_t pat = 0;
         for (uint32_t i = 0; i < pass.npat_bits; ++i) pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
@@ -1479,8 +1489,13 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
 
 }  // namespace
 
+bool mono_zero_skip(const GateProgram& prog, uint32_t lb) {
+    return prog.mono && !prog.passes.empty() && prog.passes[0].pp && lb >= 12;
+}
+
 void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
-                      uint64_t* launches, const QuantOut& quant) {
+                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag) {
+    if (zflag && !mono_zero_skip(prog, lb)) raise(BMQ_ERR_LOGIC, "zero-chunk skipping needs a table first pass");
     if (!prog.mono) raise(BMQ_ERR_LOGIC, "stage is not a code-domain program");
     for (size_t pi = 0; pi < prog.passes.size(); ++pi) {
         const GatePass& p = prog.passes[pi];
@@ -1489,10 +1504,13 @@ void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, ui
         const bool last = pi + 1 == prog.passes.size();
         if (p.pp && lb >= 4) {  // 16-byte groups of four code words stay inside a block half
             const uint64_t g2 = std::min<uint64_t>(tiles, 148ull * 4 * 16);
+            const uint8_t* zf = pi == 0 ? zflag : nullptr;
             if (last)
-                k_perm_pass<true><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, quant.cps);
+                k_perm_pass<true><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, quant.cps,
+                                                                                     zf, quant.nch);
             else
-                k_perm_pass<false><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, nullptr);
+                k_perm_pass<false><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, nullptr,
+                                                                                      zf, quant.nch);
         } else {
             k_code_pass<<<static_cast<uint32_t>(grid), kFastThreads, 0, st>>>(pk, lb, tiles, *p.mp,
                                                                               last ? quant.cps : nullptr, quant.nch);

@@ -175,7 +175,10 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
 // Code-domain program (prog.mono): the passes permute packed code words in
 // place (planar per block of 2^lb amplitudes, CmpBlock::pk layout); the last
 // pass also accumulates the per-chunk counters into quant->cps (zeroed).
+// zflag (optional; needs mono_zero_skip): all-zero input chunks (launch_decompress)
+// that the decoder left unwritten; the first pass reads them as zero words.
+bool mono_zero_skip(const GateProgram& prog, uint32_t lb);
 void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
-                      uint64_t* launches, const QuantOut& quant);
+                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag = nullptr);
 
 }  // namespace bmq
