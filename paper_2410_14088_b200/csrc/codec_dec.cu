@@ -300,7 +300,7 @@ template <int kMode>
 __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __restrict__ blks, uint32_t nch_max,
                                                              DecInfo* __restrict__ infos,
                                                              const DecChunk* __restrict__ dcs, DevTables t,
-                                                             int want_sums, DevError* err) {
+                                                             int want_sums, DevError* err, int skip_zero_chunks) {
     const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
     const DecInfo info = infos[bi];
     if (info.flags & 2) return;
@@ -311,9 +311,9 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     double* dst = blk.out + static_cast<uint64_t>(c) * kChunk;
     uint32_t* cdst = reinterpret_cast<uint32_t*>(blk.out) + static_cast<uint64_t>(c) * kChunk;
     const int tid = threadIdx.x;
-    // codes mode with want_sums set: chunks flagged all-zero (zflag) are
-    // left unwritten; the permutation pass reads them as zero words
-    const bool skip_zero = kMode == kCodes && want_sums;
+    // chunks flagged all-zero (zflag) are left unwritten; the first gate /
+    // permutation pass of the stage reads them as zeros
+    const bool skip_zero = kMode != kSumsOnly && skip_zero_chunks;
     if (info.flags & 1) {
         if (skip_zero) return;
         if constexpr (kMode != kSumsOnly) {
@@ -434,13 +434,14 @@ void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, u
     k_dec_index<<<static_cast<uint32_t>(nblk), kIndexThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t,
                                                                         check_bound ? 1 : 0, d_err, zflag);
     const uint32_t grid = static_cast<uint32_t>(nblk * nch_max);
+    const int skip = zflag ? 1 : 0;
     if (mode == 1)
-        k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, zflag ? 1 : 0, d_err);
+        k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err, skip);
     else if (mode == 2)
-        k_dec_chunk<kSumsOnly><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 1, d_err);
+        k_dec_chunk<kSumsOnly><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 1, d_err, 0);
     else
         k_dec_chunk<kDoubles><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, want_sums ? 1 : 0,
-                                                              d_err);
+                                                              d_err, skip);
     BMQ_CUDA(cudaGetLastError());
     if (launches) *launches += 2;
 }

@@ -740,7 +740,8 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     ++counters_.kernel_launches;
     // code-domain stages: all-zero chunks stay unwritten; the first
     // permutation pass reads them as zero words
-    uint8_t* zf = codes && mono_zero_skip(sp.prog, L_.b) ? zflag_.p : nullptr;
+    uint8_t* zf = (codes ? mono_zero_skip(sp.prog, L_.b) : program_zero_skip(sp.prog, L_.b, false)) ? zflag_.p
+                                                                                                    : nullptr;
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
                       &counters_.kernel_launches, codes ? 1 : 0, zf);
     phase_event(4 * bidx + 1);
@@ -754,7 +755,7 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
         ++counters_.code_domain_batches;
     } else {
         fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per, &counters_.kernel_launches,
-                            &qo, d_vtab, nblk);
+                            &qo, d_vtab, nblk, zf, nch_);
     }
     phase_event(4 * bidx + 2);
     launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,

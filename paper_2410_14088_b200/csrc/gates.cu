@@ -858,7 +858,8 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                                                                  const __grid_constant__ FastPass pass,
                                                                  const __grid_constant__ QuantOut quant,
                                                                  const uint32_t* __restrict__ vtab,
-                                                                 int dbg_full_support) {
+                                                                 int dbg_full_support,
+                                                                 const uint8_t* __restrict__ zf, uint32_t nch) {
     // dynamic SMEM: 4096 amplitudes (tile position k) | chain tables | ops
     extern __shared__ double2 tile_s[];
     __shared__ uint64_t joff[kPer];
@@ -906,6 +907,13 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
+                if (zf) {  // all-zero input chunks were not written (warp-uniform test)
+                    const uint8_t* zs = zf + (a >> (lb + 1)) * nch;
+                    const uint64_t off = a & ((2ull << lb) - 1);
+                    re[j] = zs[off >> 12] ? 0.0 : buf[a];
+                    im[j] = zs[(off + im_off) >> 12] ? 0.0 : buf[a + im_off];
+                    continue;
+                }
                 re[j] = buf[a];
                 im[j] = buf[a + im_off];
             }
@@ -1527,9 +1535,15 @@ bool full_support_debug() {
     return on;
 }
 
+bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved) {
+    return !interleaved && lb >= 12 && !prog.passes.empty() && prog.passes[0].fast;
+}
+
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant, const uint32_t* vtab,
-                 uint64_t nblocks) {
+                 uint64_t nblocks, const uint8_t* zflag, uint32_t nch) {
+    if (zflag && !program_zero_skip(prog, lb, interleaved))
+        raise(BMQ_ERR_LOGIC, "zero-chunk skipping needs a fast first pass");
     const bool fuse = quant && !interleaved && lb >= 12 && !prog.passes.empty() && prog.passes.back().fast;
     if (vtab) {  // block-wise batch: every pass must be fast and its tile local
         for (const GatePass& p : prog.passes)
@@ -1556,7 +1570,7 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
             const bool last = pi + 1 == prog.passes.size();
             k_gate_pass_fast<<<static_cast<uint32_t>(grid), kFastThreads, smem, st>>>(
                 buf, lb, interleaved ? 1 : 0, tiles, *p.fp, (fuse && last) ? *quant : none, vtab,
-                full_support_debug() ? 1 : 0);
+                full_support_debug() ? 1 : 0, pi == 0 ? zflag : nullptr, nch);
         } else {
             const uint32_t nth = std::min<uint32_t>(kPassThreads, 1u << p.tb);
             const size_t smem = 2 * (size_t(1) << p.tb) * sizeof(double);

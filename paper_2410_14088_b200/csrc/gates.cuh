@@ -168,9 +168,14 @@ struct QuantOut {
 // With vtab (block-wise batches of a diagonal-only stage) the buffer holds
 // nblocks independent blocks; vtab[slot] is the inner value of the block in
 // that slot, used for the ops' inner-bit conditions.
+// zflag (optional; needs program_zero_skip): the decoder left all-zero input
+// chunks unwritten (one byte per (block slot, chunk), nch chunks per block);
+// the first pass reads them as zeros.
+bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved);
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant = nullptr,
-                 const uint32_t* vtab = nullptr, uint64_t nblocks = 0);
+                 const uint32_t* vtab = nullptr, uint64_t nblocks = 0, const uint8_t* zflag = nullptr,
+                 uint32_t nch = 0);
 
 // Code-domain program (prog.mono): the passes permute packed code words in
 // place (planar per block of 2^lb amplitudes, CmpBlock::pk layout); the last
