@@ -33,7 +33,8 @@ void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
                        uint64_t* launches, int mode = 0, uint8_t* zflag = nullptr);
-// (zflag, modes 0 and 1: one byte per (block, chunk) marking all-zero
-// chunks, which are then not written; see k_dec_index.)
+// (zflag, mode 1: one byte per (block, chunk) marking all-zero chunks, which
+// are then not written (k_dec_index); mode 0: one byte per 32-scalar group of
+// the output, 0 for an all-zero group that was not stored.)
 
 }  // namespace bmq

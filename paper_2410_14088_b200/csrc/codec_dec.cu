@@ -234,7 +234,7 @@ __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32
                                             const uint8_t* codes, uint32_t width, uint32_t nz_prefix, uint32_t len,
                                             int64_t qbase, int64_t lo, int64_t hi, const DevTables& t, double* dst,
                                             uint32_t* cdst, uint64_t half, uint64_t g0, bool sums, double& sq,
-                                            double& sre, double& sim, bool& bad) {
+                                            double& sre, double& sim, bool& bad, uint8_t* gflag) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uintptr_t cs = reinterpret_cast<uintptr_t>(codes);
     const bool coop = width <= 30;  // block-uniform
@@ -279,6 +279,10 @@ __device__ __forceinline__ void dec_scalars(const uint32_t* s_sign, const uint32
         const uint32_t s = 32 * k + lane;
         const uint32_t nzw = s_nz[k];
         const uint32_t neg = (s_sign[k] >> lane) & 1u;
+        if (kMode == kDoubles && gflag) {  // 32-scalar group flags: zero groups are not stored
+            if (lane == 0) gflag[k] = nzw ? 1 : 0;
+            if (!nzw) continue;
+        }
         if (coop && nzw == ~0u) {  // every scalar nonzero: rank = lane
             const uint32_t a = cb0 + s_pre[k] * width + lane * width;
             const uint32_t wlo = __ldg(cw + (a >> 5)), whi = __ldg(cw + (a >> 5) + 1);
@@ -300,7 +304,8 @@ template <int kMode>
 __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __restrict__ blks, uint32_t nch_max,
                                                              DecInfo* __restrict__ infos,
                                                              const DecChunk* __restrict__ dcs, DevTables t,
-                                                             int want_sums, DevError* err, int skip_zero_chunks) {
+                                                             int want_sums, DevError* err, int skip_zero_chunks,
+                                                             uint8_t* __restrict__ wflag) {
     const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
     const DecInfo info = infos[bi];
     if (info.flags & 2) return;
@@ -311,10 +316,13 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     double* dst = blk.out + static_cast<uint64_t>(c) * kChunk;
     uint32_t* cdst = reinterpret_cast<uint32_t*>(blk.out) + static_cast<uint64_t>(c) * kChunk;
     const int tid = threadIdx.x;
-    // chunks flagged all-zero (zflag) are left unwritten; the first gate /
-    // permutation pass of the stage reads them as zeros
-    const bool skip_zero = kMode != kSumsOnly && skip_zero_chunks;
+    // codes: chunks flagged all-zero (zflag) are left unwritten and the first
+    // permutation pass reads them as zeros; doubles with wflag: one flag per
+    // 32-scalar group (1 = stored, 0 = all zero and not stored)
+    uint8_t* gflag = (kMode == kDoubles && wflag) ? wflag + (static_cast<uint64_t>(bi) * nch_max + c) * 128 : nullptr;
+    const bool skip_zero = (kMode == kCodes && skip_zero_chunks) || gflag;
     if (info.flags & 1) {
+        if (gflag && tid < 128) gflag[tid] = 0;
         if (skip_zero) return;
         if constexpr (kMode != kSumsOnly) {
             for (uint32_t s = tid; s < len; s += kChunkThreads) {
@@ -327,7 +335,10 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
         return;
     }
     const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
-    if (skip_zero && d.ztag == 1 && len == kChunk) return;
+    if (skip_zero && d.ztag == 1 && len == kChunk) {
+        if (gflag && tid < 128) gflag[tid] = 0;
+        return;
+    }
     {
         // Warm L1 with the chunk's code bytes (at most len codes from its
         // first rank on): the per-word code fetches below then hit L1 instead
@@ -378,6 +389,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
         const uint32_t* cw = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3)) + (cb >> 5);
         const uint32_t cb0 = static_cast<uint32_t>(cb & 31), cmask = (1u << width) - 1;
         const uint32_t qb = static_cast<uint32_t>(qbase);
+        if (gflag && tid < 128) gflag[tid] = 1;  // zero-free chunk
 #pragma unroll 4
         for (int i = 0; i < kChunk / (4 * kChunkThreads); ++i) {
             const uint32_t s0 = 4 * tid + 4 * kChunkThreads * i;
@@ -416,10 +428,10 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
         }
     } else if (len == kChunk && !check)
         dec_scalars<kMode, true, false>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, t, dst,
-                                        cdst, half, g0, sums, sq, sre, sim, bad);
+                                        cdst, half, g0, sums, sq, sre, sim, bad, gflag);
     else
         dec_scalars<kMode, false, true>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, t, dst,
-                                        cdst, half, g0, sums, sq, sre, sim, bad);
+                                        cdst, half, g0, sums, sq, sre, sim, bad, gflag);
     if (bad) dev_fail(err, DE_CODE_WINDOW, bi);
     if (kMode == kSumsOnly || (kMode == kDoubles && want_sums)) block_sums3(sq, sre, sim, s_red, &infos[bi].sumsq);
 }
@@ -431,17 +443,21 @@ void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, u
                        uint64_t* launches, int mode, uint8_t* zflag) {
     if (nblk == 0) return;
     BMQ_CUDA(cudaMemsetAsync(d_info, 0, nblk * sizeof(DecInfo), st));
+    // mode 1: zflag = per-chunk zero flags (index kernel); mode 0: zflag =
+    // per-32-scalar group flags (decode kernel)
     k_dec_index<<<static_cast<uint32_t>(nblk), kIndexThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t,
-                                                                        check_bound ? 1 : 0, d_err, zflag);
+                                                                        check_bound ? 1 : 0, d_err,
+                                                                        mode == 1 ? zflag : nullptr);
     const uint32_t grid = static_cast<uint32_t>(nblk * nch_max);
-    const int skip = zflag ? 1 : 0;
     if (mode == 1)
-        k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err, skip);
+        k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err,
+                                                             zflag ? 1 : 0, nullptr);
     else if (mode == 2)
-        k_dec_chunk<kSumsOnly><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 1, d_err, 0);
+        k_dec_chunk<kSumsOnly><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 1, d_err, 0,
+                                                               nullptr);
     else
         k_dec_chunk<kDoubles><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, want_sums ? 1 : 0,
-                                                              d_err, skip);
+                                                              d_err, 0, zflag);
     BMQ_CUDA(cudaGetLastError());
     if (launches) *launches += 2;
 }

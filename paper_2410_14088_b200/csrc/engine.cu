@@ -452,6 +452,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     dinfo_.alloc(max_blocks_);
     dchunk_.alloc(max_blocks_ * nch_);
     zflag_.alloc(max_blocks_ * nch_);
+    wflag_.alloc(work_scalars_ / 32);
     ids_.alloc(std::max<uint64_t>(nid, max_blocks_));
     vtab_.alloc(std::max<uint64_t>(nid, max_blocks_));
     new_off_.alloc(nid);
@@ -740,8 +741,10 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     ++counters_.kernel_launches;
     // code-domain stages: all-zero chunks stay unwritten; the first
     // permutation pass reads them as zero words
-    uint8_t* zf = (codes ? mono_zero_skip(sp.prog, L_.b) : program_zero_skip(sp.prog, L_.b, false)) ? zflag_.p
-                                                                                                    : nullptr;
+    // zero skipping: code-domain stages flag all-zero chunks (zflag_), FP
+    // stages all-zero 32-scalar groups (wflag_); neither is stored
+    uint8_t* zf = codes ? (mono_zero_skip(sp.prog, L_.b) ? zflag_.p : nullptr)
+                        : (program_zero_skip(sp.prog, L_.b, false) ? wflag_.p : nullptr);
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
                       &counters_.kernel_launches, codes ? 1 : 0, zf);
     phase_event(4 * bidx + 1);

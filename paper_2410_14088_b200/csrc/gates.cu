@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                                                                  const __grid_constant__ QuantOut quant,
                                                                  const uint32_t* __restrict__ vtab,
                                                                  int dbg_full_support,
-                                                                 const uint8_t* __restrict__ zf, uint32_t nch) {
+                                                                 uint8_t* __restrict__ wf) {
     // dynamic SMEM: 4096 amplitudes (tile position k) | chain tables | ops
     extern __shared__ double2 tile_s[];
     __shared__ uint64_t joff[kPer];
@@ -907,11 +907,9 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
-                if (zf) {  // all-zero input chunks were not written (warp-uniform test)
-                    const uint8_t* zs = zf + (a >> (lb + 1)) * nch;
-                    const uint64_t off = a & ((2ull << lb) - 1);
-                    re[j] = zs[off >> 12] ? 0.0 : buf[a];
-                    im[j] = zs[(off + im_off) >> 12] ? 0.0 : buf[a + im_off];
+                if (wf) {  // 32-scalar groups flagged zero were not stored (warp-uniform test)
+                    re[j] = wf[a >> 5] ? buf[a] : 0.0;
+                    im[j] = wf[(a + im_off) >> 5] ? buf[a + im_off] : 0.0;
                     continue;
                 }
                 re[j] = buf[a];
@@ -931,6 +929,17 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         // its partner offset; ops below only visit positions inside S (a zero
         // stays zero under every gate, up to the sign the codec ignores).
         uint32_t S = dbg_full_support ? 0x80000fffu : s_supp[parity];  // bit 31 set unless the tile is all zero
+        if (S == 0 && wf && !quant.pk) {  // an all-zero tile stays zero: flag its groups, store nothing
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
+                if ((tid & 31) == 0) {
+                    wf[a >> 5] = 0;
+                    wf[(a + im_off) >> 5] = 0;
+                }
+            }
+            continue;
+        }
         bool owners_only = true;
         uint32_t cvec = 0;  // lazy CX: affine part of the tile's index map
         for (uint32_t i = 0; i < pass.nops;) {
@@ -1086,6 +1095,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 continue;
             }
             ++i;
+            if (S == 0) continue;  // zeros map to zeros (tile-uniform)
             __syncthreads();
             owners_only = false;
             // U2 on logical tile bit t: physical pairs (x, x ^ dvec); x is
@@ -1138,6 +1148,16 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
+                if (wf) {  // an all-zero 32-scalar group is flagged instead of stored
+                    const bool nr = __any_sync(0xffffffffu, re[j] != 0.0), ni = __any_sync(0xffffffffu, im[j] != 0.0);
+                    if ((threadIdx.x & 31) == 0) {
+                        wf[a >> 5] = nr;
+                        wf[(a + im_off) >> 5] = ni;
+                    }
+                    if (nr) buf[a] = re[j];
+                    if (ni) buf[a + im_off] = im[j];
+                    continue;
+                }
                 buf[a] = re[j];
                 buf[a + im_off] = im[j];
             }
@@ -1536,14 +1556,17 @@ bool full_support_debug() {
 }
 
 bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved) {
-    return !interleaved && lb >= 12 && !prog.passes.empty() && prog.passes[0].fast;
+    if (interleaved || lb < 12 || prog.passes.empty()) return false;
+    for (const GatePass& p : prog.passes)
+        if (!p.fast) return false;
+    return true;
 }
 
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant, const uint32_t* vtab,
                  uint64_t nblocks, const uint8_t* zflag, uint32_t nch) {
     if (zflag && !program_zero_skip(prog, lb, interleaved))
-        raise(BMQ_ERR_LOGIC, "zero-chunk skipping needs a fast first pass");
+        raise(BMQ_ERR_LOGIC, "zero-group skipping needs fast passes only");
     const bool fuse = quant && !interleaved && lb >= 12 && !prog.passes.empty() && prog.passes.back().fast;
     if (vtab) {  // block-wise batch: every pass must be fast and its tile local
         for (const GatePass& p : prog.passes)
@@ -1570,7 +1593,7 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
             const bool last = pi + 1 == prog.passes.size();
             k_gate_pass_fast<<<static_cast<uint32_t>(grid), kFastThreads, smem, st>>>(
                 buf, lb, interleaved ? 1 : 0, tiles, *p.fp, (fuse && last) ? *quant : none, vtab,
-                full_support_debug() ? 1 : 0, pi == 0 ? zflag : nullptr, nch);
+                full_support_debug() ? 1 : 0, const_cast<uint8_t*>(zflag));
         } else {
             const uint32_t nth = std::min<uint32_t>(kPassThreads, 1u << p.tb);
             const size_t smem = 2 * (size_t(1) << p.tb) * sizeof(double);

@@ -168,9 +168,10 @@ struct QuantOut {
 // With vtab (block-wise batches of a diagonal-only stage) the buffer holds
 // nblocks independent blocks; vtab[slot] is the inner value of the block in
 // that slot, used for the ops' inner-bit conditions.
-// zflag (optional; needs program_zero_skip): the decoder left all-zero input
-// chunks unwritten (one byte per (block slot, chunk), nch chunks per block);
-// the first pass reads them as zeros.
+// zflag (optional; needs program_zero_skip): one flag byte per 32-scalar
+// group of buf (index = planar address / 32), 0 for an all-zero group that
+// was not stored; every pass reads and (except the quantising last pass)
+// maintains them. nch is unused.
 bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved);
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant = nullptr,
