@@ -899,8 +899,18 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         // single blocks of a diagonal stage: the bits above lb are the
         // block's inner value, not its slot in the batch.
         const uint64_t xbase = vtab ? ((static_cast<uint64_t>(vtab[base >> lb]) << lb) | (base & lmask)) : base;
-        __syncthreads();  // previous tile's stores have read tile_s
+        // Group flags of the warp's 32 groups (lane 2j + c: scalar c of row j).
+        uint32_t fl = 1;
+        if (wf) {
+            const uint32_t lane = tid & 31;
+            const uint64_t a = planar_addr(base | toff | joff[lane >> 1], lb, lmask, interleaved);
+            fl = wf[(a + ((lane & 1) ? im_off : 0)) >> 5];
+        }
+        // Barrier: the previous tile's stores have read tile_s.
+        const int any_group = __syncthreads_or(fl);
         if (tid == 0) s_supp[parity ^ 1] = 0;  // the next tile's slot (last read two tiles ago)
+        // All groups flagged zero: the tile stays zero in place (flags stay 0).
+        if (!any_group && !quant.pk) continue;
         {
             double re[kPer], im[kPer];
             uint32_t nzpos = 0;
@@ -908,8 +918,8 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             for (int j = 0; j < kPer; ++j) {
                 const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
                 if (wf) {  // 32-scalar groups flagged zero were not stored (warp-uniform test)
-                    re[j] = wf[a >> 5] ? buf[a] : 0.0;
-                    im[j] = wf[(a + im_off) >> 5] ? buf[a + im_off] : 0.0;
+                    re[j] = __shfl_sync(0xffffffffu, fl, 2 * j) ? buf[a] : 0.0;
+                    im[j] = __shfl_sync(0xffffffffu, fl, 2 * j + 1) ? buf[a + im_off] : 0.0;
                     continue;
                 }
                 re[j] = buf[a];
