@@ -93,19 +93,18 @@ template <int N>
 __device__ __forceinline__ void quantize_pack_n(const double* v, uint32_t* pk, const DevTables& t, bool& bad,
                                                 bool& oow) {
     uint64_t bits[N];
-    int64_t idx[N];
+    int idx[N];  // table index (< 2^25 entries)
     bool live[N], sure[N];
+    const double qlo = static_cast<double>(t.qlo), qhi = static_cast<double>(t.qhi);
 #pragma unroll
     for (int e = 0; e < N; ++e) {
         live[e] = isfinite(v[e]) && v[e] != 0.0;
         if (!isfinite(v[e])) bad = true;
         const double x = live[e] ? quantize_estimate_x(v[e], t, bits[e]) : 0.0;
         const double r = rint(x);
-        int64_t q = static_cast<int64_t>(r);
         // the rounding is settled unless x lies within est_eps of a half-integer
-        sure[e] = 0.5 - fabs(x - r) > t.est_eps && q >= t.qlo && q <= t.qhi;
-        q = q < t.qlo ? t.qlo : (q > t.qhi ? t.qhi : q);
-        idx[e] = q - t.qlo;
+        sure[e] = 0.5 - fabs(x - r) > t.est_eps && r >= qlo && r <= qhi;
+        idx[e] = __double2int_rz(fmin(fmax(r, qlo), qhi) - qlo);
     }
     uint64_t t0[N], t1[N];
 #pragma unroll
@@ -119,12 +118,12 @@ __device__ __forceinline__ void quantize_pack_n(const double* v, uint32_t* pk, c
             pk[e] = 1u;
             continue;
         }
-        int64_t q;
+        uint32_t qoff;
         if (sure[e] || (bits[e] >= t0[e] && bits[e] < t1[e]))
-            q = t.qlo + idx[e];
+            qoff = static_cast<uint32_t>(idx[e]);
         else
-            q = quantize(v[e], t, oow);
-        pk[e] = pack_code(static_cast<uint32_t>(q - t.qlo), v[e] < 0.0, false);
+            qoff = static_cast<uint32_t>(quantize(v[e], t, oow) - t.qlo);
+        pk[e] = pack_code(qoff, v[e] < 0.0, false);
     }
 }
 

@@ -86,7 +86,7 @@ __device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& 
     } else {
         e2 = static_cast<int>(ex) - 1023;
     }
-    const float m = static_cast<float>(__longlong_as_double(static_cast<long long>(man | 0x3ff0000000000000ull)));
+    const float m = __int_as_float(0x3f800000 | static_cast<int>(man >> 29));  // mantissa truncated to float
     const double x = (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
     int64_t q = __double2ll_rn(x);
     q = q < t.qlo ? t.qlo : (q > t.qhi ? t.qhi : q);
@@ -111,8 +111,8 @@ __device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& 
 }
 
 // x ~ log2|v| / b_a for finite v != 0 from a float log2 of the mantissa.
-// __log2f on [1, 2) is within 2^-22.5 of log2, the float rounding of the
-// mantissa adds at most 2^-24 / ln 2, the double arithmetic a few ulp: the
+// __log2f on [1, 2) is within 2^-22.5 of log2, truncating the mantissa
+// to float adds at most 2^-23 / ln 2, the double arithmetic a few ulp: the
 // estimate is within est_eps = 1e-6 / b_a + 1e-6 of the reference's
 // log2(v) / b_a (glibc log2 is within an ulp). Away from a half-integer by
 // more than that, llround of the reference value is round(x) itself.
@@ -128,7 +128,7 @@ __device__ __forceinline__ double quantize_estimate_x(double v, const DevTables&
     } else {
         e2 = static_cast<int>(ex) - 1023;
     }
-    const float m = static_cast<float>(__longlong_as_double(static_cast<long long>(man | 0x3ff0000000000000ull)));
+    const float m = __int_as_float(0x3f800000 | static_cast<int>(man >> 29));  // mantissa truncated to float
     return (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
 }
 
@@ -146,7 +146,7 @@ __device__ __forceinline__ int64_t quantize_estimate(double v, const DevTables& 
     } else {
         e2 = static_cast<int>(ex) - 1023;
     }
-    const float m = static_cast<float>(__longlong_as_double(static_cast<long long>(man | 0x3ff0000000000000ull)));
+    const float m = __int_as_float(0x3f800000 | static_cast<int>(man >> 29));  // mantissa truncated to float
     const double x = (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
     int64_t q = __double2ll_rn(x);
     q = q < t.qlo ? t.qlo : (q > t.qhi ? t.qhi : q);

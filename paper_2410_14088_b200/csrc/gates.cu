@@ -674,6 +674,10 @@ constexpr int kLanesPerStep = 1 << kChainQBits;
 
 // pdep over a <= 12-bit tile mask: the low bits of r into the set bits of m.
 __device__ __forceinline__ uint32_t deposit12(uint32_t r, uint32_t m) {
+    if (__popc(m) > 6) {  // dense mask: insert a zero at each hole, lowest first
+        for (uint32_t h = ~m & 0xfffu; h; h &= h - 1) r = insert0(r, __ffs(h) - 1);
+        return r;
+    }
     uint32_t out = 0;
     for (; m; m &= m - 1, r >>= 1)
         if (r & 1u) out |= m & (0u - m);
@@ -826,10 +830,11 @@ __device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2*
         quantize_pack_n<2 * kG>(v, pk, q.t, bad, oow);
 #pragma unroll
         for (int e = 0; e < kG; ++e) {
-            const uint64_t p = base | toff | joff[g0 + e];
-            const uint64_t slot = p >> lb, l = p & lmask;
-            const uint64_t s_im = (1ull << lb) + l;
-            const uint64_t kre = slot * q.nch + (l >> 12), kim = slot * q.nch + (s_im >> 12);
+            // planar scalar index; chunks are 4096 scalars and 2^(lb+1) / 4096
+            // = nch per block (lb >= 12), so the chunk key is index >> 12
+            const uint64_t a_re = planar_addr(base | toff | joff[g0 + e], lb, lmask, false);
+            const uint64_t a_im = a_re + (1ull << lb);
+            const uint64_t kre = a_re >> 12, kim = a_im >> 12;
             if (kre != key_re) {  // warp-uniform
                 if (key_re != ~0ull) flush_chunk(q.cps + key_re, acc_re);
                 acc_re = ChunkAcc{};
@@ -840,9 +845,8 @@ __device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2*
                 acc_im = ChunkAcc{};
                 key_im = kim;
             }
-            uint32_t* dst = q.pk + (slot << (lb + 1));
-            dst[l] = pk[2 * e];
-            dst[s_im] = pk[2 * e + 1];
+            q.pk[a_re] = pk[2 * e];
+            q.pk[a_im] = pk[2 * e + 1];
             acc_re.add(pk[2 * e]);
             acc_im.add(pk[2 * e + 1]);
         }
@@ -1025,11 +1029,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                     const int pc = g.in_hi ? g.tp_hi : -1;
                     const uint32_t xlo = static_cast<uint32_t>(xbase);
                     // support: no nonzero amplitude with bit c, or none with a bit of R
-                    uint32_t rs = xlo & R;
-                    for (uint32_t m = S & 0xfffu; m; m &= m - 1) {
-                        const uint32_t p = __ffs(m) - 1;
-                        rs |= (p < 6 ? lut_lo[1u << p] : lut_hi[1u << (p - 6)]) & R;
-                    }
+                    const uint32_t rs = (xlo | lut_lo[S & 63u] | lut_hi[(S >> 6) & 63u]) & R;
                     const bool active = rs && (pc >= 0 ? ((S >> pc) & 1) : ((xbase >> g.hi) & 1));
                     if (active && __popc(S & 0xfffu) < 11) {  // sparse tile: the support positions with bit c
                         __syncthreads();
