@@ -95,16 +95,18 @@ __device__ __forceinline__ void quantize_pack_n(const double* v, uint32_t* pk, c
     uint64_t bits[N];
     int idx[N];  // table index (< 2^25 entries)
     bool live[N], sure[N];
-    const double qlo = static_cast<double>(t.qlo), qhi = static_cast<double>(t.qhi);
+    const double qlo = static_cast<double>(t.qlo);
+    const int span = static_cast<int>(t.qhi - t.qlo);
 #pragma unroll
     for (int e = 0; e < N; ++e) {
         live[e] = isfinite(v[e]) && v[e] != 0.0;
         if (!isfinite(v[e])) bad = true;
         const double x = live[e] ? quantize_estimate_x(v[e], t, bits[e]) : 0.0;
         const double r = rint(x);
+        const int i = __double2int_rz(r - qlo);  // exact (integers below 2^53); saturates
         // the rounding is settled unless x lies within est_eps of a half-integer
-        sure[e] = 0.5 - fabs(x - r) > t.est_eps && r >= qlo && r <= qhi;
-        idx[e] = __double2int_rz(fmin(fmax(r, qlo), qhi) - qlo);
+        sure[e] = 0.5 - fabs(x - r) > t.est_eps && i >= 0 && i <= span;
+        idx[e] = min(max(i, 0), span);
     }
     uint64_t t0[N], t1[N];
 #pragma unroll

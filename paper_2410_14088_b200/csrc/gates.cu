@@ -896,6 +896,18 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     __shared__ uint32_t s_supp[2];
     if (tid < 2) s_supp[tid] = 0;
     __syncthreads();
+    // Sweeps are the same for every tile: a run of diagonal ops, extended
+    // over CX / DIAG / CDIAG when it holds no phase chain (lazy CX).
+    if (tid < pass.nops && is_diag(sops[tid].type)) {
+        uint32_t i2 = tid + 1;
+        while (i2 < pass.nops && is_diag(sops[i2].type)) ++i2;
+        const bool chain = has_chain(sops, tid, i2);
+        if (!chain)
+            while (i2 < pass.nops && (sops[i2].type == OP_CX || sops[i2].type == OP_DIAG || sops[i2].type == OP_CDIAG))
+                ++i2;
+        sops[tid].run = static_cast<uint16_t>(i2 | (chain ? 0x8000u : 0u));
+    }
+    __syncthreads();
     uint32_t parity = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, parity ^= 1) {
         const uint64_t base = runs_deposit(tile, pass.base);
@@ -986,14 +998,10 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 continue;
             }
             if (is_diag(g.type)) {
-                uint32_t i2 = i + 1;
-                while (i2 < pass.nops && is_diag(sops[i2].type)) ++i2;
                 // a chain-free run also absorbs CX ops (lazy: they only change
                 // the index map), so CX-RZ-CX sequences are one sweep
-                if (!has_chain(sops, i, i2))
-                    while (i2 < pass.nops && (sops[i2].type == OP_CX || sops[i2].type == OP_DIAG ||
-                                              sops[i2].type == OP_CDIAG))
-                        ++i2;
+                const uint32_t i2 = g.run & 0x7fffu;
+                const bool run_chain = (g.run & 0x8000u) != 0;
                 const uint32_t cvec_in = cvec;  // the map's affine part at the start of the run
                 for (uint32_t q = i; q < i2; ++q)
                     if (sops[q].type == OP_CX) cvec = cx_update(sops[q], cvec, base);
@@ -1055,7 +1063,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                         }
                         owners_only = false;
                     }
-                } else if (!has_chain(sops, i, i2)) {
+                } else if (!run_chain) {
                     // plain diagonal gates: op by op, each a branch-free
                     // product with the entry its amplitude selects (an entry 1
                     // multiplies exactly: 1*x - 0*y == x up to a zero's sign)

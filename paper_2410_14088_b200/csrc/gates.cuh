@@ -55,7 +55,8 @@ struct FastOp {
     double m[8];      // U2: u00 u01 u10 u11; DIAG: u00 u11; CDIAG: u33 (interleaved re/im)
                       // CHAIN: m[0] holds the mask R of other bits (bit pattern)
                       // PERM: m[0..2] hold the 12 columns of M^-1 (uint16 each)
-    uint16_t mrow, mrow2, dvec, pad3;
+    uint16_t mrow, mrow2, dvec;
+    uint16_t run;     // diagonal ops (set on device): end of the sweep starting here | has-chain << 15
 };
 
 constexpr uint32_t kMaxTileBits = 12;  // 4096 amplitudes per tile
