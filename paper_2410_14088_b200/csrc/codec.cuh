@@ -32,9 +32,11 @@ void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk
 // uint32_t*; 2: no output, dequantised sums only (DecInfo::sumsq, ...).
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
-                       uint64_t* launches, int mode = 0, uint8_t* zflag = nullptr);
+                       uint64_t* launches, int mode = 0, uint8_t* zflag = nullptr, uint32_t* imnz = nullptr);
 // (zflag, mode 1: one byte per (block, chunk) marking all-zero chunks, which
 // are then not written (k_dec_index); mode 0: one byte per 32-scalar group of
 // the output, 0 for an all-zero group that was not stored.)
+// (imnz, mode 1 with zflag: set to 1 when a chunk of some block's imaginary
+// half is not all zero; the caller zeroes it first.)
 
 }  // namespace bmq

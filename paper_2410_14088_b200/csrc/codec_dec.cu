@@ -37,7 +37,7 @@ constexpr int kIndexThreads = 256;
 __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __restrict__ blks, uint32_t nch_max,
                                                              DecInfo* __restrict__ infos, DecChunk* __restrict__ dcs,
                                                              DevTables t, int check_bound, DevError* err,
-                                                             uint8_t* __restrict__ zflag) {
+                                                             uint8_t* __restrict__ zflag, uint32_t* imnz) {
     const uint32_t bi = blockIdx.x;
     const DecBlock blk = blks[bi];
     const uint8_t* p = blk.in;
@@ -130,7 +130,9 @@ __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __r
                 } else {
                     dc[c].ztag = static_cast<uint8_t>(tag);
                     dc[c].zero_off = static_cast<uint32_t>(raw0 + carry);
-                    if (zflag) zflag[static_cast<uint64_t>(bi) * nch_max + c] = (tag == 1 && len == kChunk) ? 1 : 0;
+                    const bool zc = tag == 1 && len == kChunk;
+                    if (zflag) zflag[static_cast<uint64_t>(bi) * nch_max + c] = zc ? 1 : 0;
+                    if (imnz && !zc && 2 * c >= nch) *imnz = 1;  // imaginary half (chunks nch/2.. of 2^(lb+1) scalars)
                 }
             }
             unsigned long long pre, tot;
@@ -440,14 +442,15 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
 
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
-                       uint64_t* launches, int mode, uint8_t* zflag) {
+                       uint64_t* launches, int mode, uint8_t* zflag, uint32_t* imnz) {
     if (nblk == 0) return;
     BMQ_CUDA(cudaMemsetAsync(d_info, 0, nblk * sizeof(DecInfo), st));
     // mode 1: zflag = per-chunk zero flags (index kernel); mode 0: zflag =
     // per-32-scalar group flags (decode kernel)
     k_dec_index<<<static_cast<uint32_t>(nblk), kIndexThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t,
                                                                         check_bound ? 1 : 0, d_err,
-                                                                        mode == 1 ? zflag : nullptr);
+                                                                        mode == 1 ? zflag : nullptr,
+                                                                        mode == 1 && zflag ? imnz : nullptr);
     const uint32_t grid = static_cast<uint32_t>(nblk * nch_max);
     if (mode == 1)
         k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err,

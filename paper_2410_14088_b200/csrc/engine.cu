@@ -452,6 +452,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     dinfo_.alloc(max_blocks_);
     dchunk_.alloc(max_blocks_ * nch_);
     zflag_.alloc(max_blocks_ * nch_);
+    imnz_.alloc(1);
     wflag_.alloc(work_scalars_ / 32);
     ids_.alloc(std::max<uint64_t>(nid, max_blocks_));
     vtab_.alloc(std::max<uint64_t>(nid, max_blocks_));
@@ -745,8 +746,9 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     // stages all-zero 32-scalar groups (wflag_); neither is stored
     uint8_t* zf = codes ? (mono_zero_skip(sp.prog, L_.b) ? zflag_.p : nullptr)
                         : (program_zero_skip(sp.prog, L_.b, false) ? wflag_.p : nullptr);
+    if (codes && zf) BMQ_CUDA(cudaMemsetAsync(imnz_.p, 0, sizeof(uint32_t), st_));
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
-                      &counters_.kernel_launches, codes ? 1 : 0, zf);
+                      &counters_.kernel_launches, codes ? 1 : 0, zf, codes && zf ? imnz_.p : nullptr);
     phase_event(4 * bidx + 1);
     // the stage's last gate pass quantises straight into pk_ / cplan_
     BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
@@ -754,7 +756,8 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     const uint64_t per = sp.gg.per_group();
     bool fused = true;
     if (codes) {
-        run_mono_program(st_, sp.prog, pk_.p, L_.b, nblk / per, &counters_.kernel_launches, qo, zf);
+        run_mono_program(st_, sp.prog, pk_.p, L_.b, nblk / per, &counters_.kernel_launches, qo, zf,
+                         zf ? imnz_.p : nullptr);
         ++counters_.code_domain_batches;
     } else {
         fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per, &counters_.kernel_launches,

@@ -384,6 +384,7 @@ void build_mono(GateProgram& prog) {
             }
             for (uint32_t k = 0; k < 4096; ++k) {
                 const uint32_t u = U[k];
+                if (u & 1) pp->reim_swap = 1;
                 tabs.push_back(static_cast<uint16_t>(src[k] | (u & 1) << 12 | ((u ^ (u >> 1)) & 1) << 13 | (u >> 1) << 14));
             }
         }
@@ -1460,7 +1461,7 @@ template <bool kLast>
 __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict__ pk, uint32_t lb, uint64_t ntiles,
                                                             const __grid_constant__ PermPass pass,
                                                             ChunkPlan* __restrict__ cps, const uint8_t* __restrict__ zf,
-                                                            uint32_t nch) {
+                                                            uint32_t nch, const uint32_t* __restrict__ imnz) {
     __shared__ __align__(16) uint2 tile_s[1 << kMaxTileBits];
     const uint32_t tid = threadIdx.x;
     const uint64_t lmask = (1ull << lb) - 1;
@@ -1473,6 +1474,56 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
     }
     const uint32_t kshift = lb >= 12 ? 12 : lb + 1;
     const uint64_t kim = lb >= 12 ? (1ull << (lb - 12)) : 0;
+    // imaginary halves all zero (and no pass swaps re / im): they stay zero,
+    // and the real halves permute alone (no entry has the swap bit)
+    const bool im_zero = imnz && *imnz == 0;
+    if (im_zero) {
+        uint32_t* tile_w = reinterpret_cast<uint32_t*>(tile_s);
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const uint64_t base = runs_deposit(tile, pass.base);
+            const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
+            uint4 re[kPermGroups];
+#pragma unroll
+            for (int g = 0; g < kPermGroups; ++g) {
+                const uint64_t addr = pb + toffp[g];
+                const uint64_t slot = addr >> (lb + 1), off = addr & ((2ull << lb) - 1);
+                re[g] = zf && zf[slot * nch + (off >> 12)] ? make_uint4(1u, 1u, 1u, 1u)
+                                                      : __ldcs(reinterpret_cast<const uint4*>(pk + addr));
+            }
+            uint32_t pat = 0;
+            for (uint32_t i = 0; i < pass.npat_bits; ++i)
+                pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
+            const uint16_t* tab = pass.table + (static_cast<uint64_t>(pat) << kMaxTileBits);
+            uint2 ent[kPermGroups];
+#pragma unroll
+            for (int g = 0; g < kPermGroups; ++g)
+                ent[g] = __ldg(reinterpret_cast<const uint2*>(tab + 4u * tid + 1024u * g));
+            __syncthreads();  // previous tile's gathers are done
+#pragma unroll
+            for (int g = 0; g < kPermGroups; ++g) *reinterpret_cast<uint4*>(tile_w + 4u * tid + 1024u * g) = re[g];
+            __syncthreads();
+#pragma unroll
+            for (int g = 0; g < kPermGroups; ++g) {
+                uint4 xo;
+                const uint32_t e0 = ent[g].x & 0xffffu, e1 = ent[g].x >> 16, e2 = ent[g].y & 0xffffu, e3 = ent[g].y >> 16;
+                xo.x = neg_if(tile_w[e0 & 0xfffu], e0 >> 13);
+                xo.y = neg_if(tile_w[e1 & 0xfffu], e1 >> 13);
+                xo.z = neg_if(tile_w[e2 & 0xfffu], e2 >> 13);
+                xo.w = neg_if(tile_w[e3 & 0xfffu], e3 >> 13);
+                const uint64_t addr = pb + toffp[g];
+                __stcs(reinterpret_cast<uint4*>(pk + addr), xo);
+                if (kLast) {
+                    CodeAcc4 ar;
+                    ar.add(xo.x);
+                    ar.add(xo.y);
+                    ar.add(xo.z);
+                    ar.add(xo.w);
+                    ar.flush(cps, addr >> kshift);
+                }
+            }
+        }
+        return;
+    }
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t base = runs_deposit(tile, pass.base);
         const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
@@ -1484,12 +1535,12 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
                 const uint64_t slot = addr >> (lb + 1), off = addr & ((2ull << lb) - 1);
                 const uint8_t* zs = zf + slot * nch;
                 re[g] = zs[off >> 12] ? make_uint4(1u, 1u, 1u, 1u) : __ldcs(reinterpret_cast<const uint4*>(pk + addr));
-                im[g] = zs[(off + im_off) >> 12] ? make_uint4(1u, 1u, 1u, 1u)
-                                                  : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
+                im[g] = im_zero || zs[(off + im_off) >> 12] ? make_uint4(1u, 1u, 1u, 1u)
+                                                             : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
                 continue;
             }
             re[g] = __ldcs(reinterpret_cast<const uint4*>(pk + addr));
-            im[g] = __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
+            im[g] = im_zero ? make_uint4(1u, 1u, 1u, 1u) : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
         }
         uint32_t pat = 0;
         for (uint32_t i = 0; i < pass.npat_bits; ++i) pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
@@ -1514,20 +1565,23 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
             apply_ent(ent[g].y >> 16, tile_s, xo.w, yo.w);
             const uint64_t addr = pb + toffp[g];
             __stcs(reinterpret_cast<uint4*>(pk + addr), xo);
-            __stcs(reinterpret_cast<uint4*>(pk + addr + im_off), yo);
+            if (!im_zero) __stcs(reinterpret_cast<uint4*>(pk + addr + im_off), yo);
             if (kLast) {
-                CodeAcc4 ar, ai;
+                CodeAcc4 ar;
                 ar.add(xo.x);
                 ar.add(xo.y);
                 ar.add(xo.z);
                 ar.add(xo.w);
-                ai.add(yo.x);
-                ai.add(yo.y);
-                ai.add(yo.z);
-                ai.add(yo.w);
                 const uint64_t key = addr >> kshift;  // chunk of the real half
                 ar.flush(cps, key);
-                ai.flush(cps, key + kim);
+                if (!im_zero) {  // (zero codes add nothing to the counters)
+                    CodeAcc4 ai;
+                    ai.add(yo.x);
+                    ai.add(yo.y);
+                    ai.add(yo.z);
+                    ai.add(yo.w);
+                    ai.flush(cps, key + kim);
+                }
             }
         }
     }
@@ -1540,9 +1594,13 @@ bool mono_zero_skip(const GateProgram& prog, uint32_t lb) {
 }
 
 void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
-                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag) {
+                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag, const uint32_t* imnz) {
     if (zflag && !mono_zero_skip(prog, lb)) raise(BMQ_ERR_LOGIC, "zero-chunk skipping needs a table first pass");
     if (!prog.mono) raise(BMQ_ERR_LOGIC, "stage is not a code-domain program");
+    // imaginary halves can stay untouched only if every pass is a table pass that never swaps re / im
+    if (!zflag) imnz = nullptr;
+    for (const GatePass& p : prog.passes)
+        if (!p.pp || p.pp->reim_swap) imnz = nullptr;
     for (size_t pi = 0; pi < prog.passes.size(); ++pi) {
         const GatePass& p = prog.passes[pi];
         const uint64_t tiles = nreps << (prog.total_bits - p.tb);
@@ -1553,10 +1611,10 @@ void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, ui
             const uint8_t* zf = pi == 0 ? zflag : nullptr;
             if (last)
                 k_perm_pass<true><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, quant.cps,
-                                                                                     zf, quant.nch);
+                                                                                     zf, quant.nch, imnz);
             else
                 k_perm_pass<false><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, nullptr,
-                                                                                      zf, quant.nch);
+                                                                                      zf, quant.nch, imnz);
         } else {
             k_code_pass<<<static_cast<uint32_t>(grid), kFastThreads, 0, st>>>(pk, lb, tiles, *p.mp,
                                                                               last ? quant.cps : nullptr, quant.nch);

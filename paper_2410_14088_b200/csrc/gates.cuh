@@ -107,6 +107,7 @@ constexpr int kMaxPatBits = 4;
 struct PermPass {
     BitRuns tile, base;
     uint32_t npat_bits;
+    uint32_t reim_swap;             // some entry swaps re / im (an odd unit)
     uint8_t pat_bits[kMaxPatBits];  // buffer bits outside the tile, pattern bit i
     const uint16_t* table;          // [1 << npat_bits][4096] (device)
 };
@@ -184,8 +185,12 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
 // pass also accumulates the per-chunk counters into quant->cps (zeroed).
 // zflag (optional; needs mono_zero_skip): all-zero input chunks (launch_decompress)
 // that the decoder left unwritten; the first pass reads them as zero words.
+// imnz (optional, with zflag): device word, 0 when every imaginary-half chunk
+// of the input is all zero (launch_decompress); if no pass swaps re / im the
+// imaginary halves then stay zero and are neither read nor written.
 bool mono_zero_skip(const GateProgram& prog, uint32_t lb);
 void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
-                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag = nullptr);
+                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag = nullptr,
+                      const uint32_t* imnz = nullptr);
 
 }  // namespace bmq

@@ -276,6 +276,29 @@ def test_code_domain_stages_are_exact(gpu, port, seed, n, b, inner, br):
             assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=NORM_RTOL)
 
 
+@pytest.mark.parametrize("seed,kinds", [(0, (1, 3, 12, 13)), (1, (1, 3, 12, 13, 4)), (2, (12,)), (3, (2, 12, 13))])
+def test_code_domain_real_states_are_exact(gpu, port, seed, kinds):
+    """A real state (H, RY) under X/Z/CX/CZ keeps its imaginary halves zero:
+    the code-domain passes leave them untouched. With S or Y in the stage the
+    halves mix and are processed; payloads byte-identical to the oracle."""
+    rng = np.random.default_rng(700 + seed)
+    n, b = 17, 12
+    gl = [(0, q, 0, 0.0) for q in range(n)] + [(9, q, 0, 0.2 + 0.1 * q) for q in range(n)]
+    for _ in range(60):
+        k = int(rng.choice(kinds))
+        q0 = int(rng.integers(n))
+        q1 = int((q0 + 1 + rng.integers(n - 1)) % n)
+        gl.append((k, q0, q1 if k >= 12 else 0, 0.0))
+    gl += [(9, q, 0, 0.3) for q in range(0, n, 4)]
+    c = gpu.Circuit(n, [gpu.Gate(gpu.GateKind(k), a, bb, ang) for k, a, bb, ang in gl])
+    want = port.simulate(n, gl, b, 2, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=2, error_bound=1e-3)) as sim:
+        rep = sim.run()
+        assert rep.device["code_domain_batches"] > 0
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+
+
 def test_code_domain_qft_swaps(gpu, port):
     """QFT's closing bit-reversal (CX triples) runs in the code domain."""
     c = gpu.generate_benchmark("qft", 18)
