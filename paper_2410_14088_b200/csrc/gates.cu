@@ -1446,6 +1446,16 @@ struct CodeAcc4 {
     }
 };
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ uint32_t neg_if(uint32_t c, uint32_t n) { return c ^ ((~c & n & 1u) << 1); }
 
 __device__ __forceinline__ void apply_ent(uint32_t e, const uint2* tile_s, uint32_t& x, uint32_t& y) {
@@ -1478,18 +1488,33 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
     // and the real halves permute alone (no entry has the swap bit)
     const bool im_zero = imnz && *imnz == 0;
     if (im_zero) {
-        uint32_t* tile_w = reinterpret_cast<uint32_t*>(tile_s);
-        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // Real halves only, double-buffered: the next tile's words stream
+        // into SMEM (cp.async) while this tile is gathered and stored.
+        uint32_t* tile_w = reinterpret_cast<uint32_t*>(tile_s);  // two 4096-word buffers
+        const auto issue = [&](uint64_t tile, uint32_t* dst) {
             const uint64_t base = runs_deposit(tile, pass.base);
             const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
-            uint4 re[kPermGroups];
 #pragma unroll
             for (int g = 0; g < kPermGroups; ++g) {
                 const uint64_t addr = pb + toffp[g];
-                const uint64_t slot = addr >> (lb + 1), off = addr & ((2ull << lb) - 1);
-                re[g] = zf && zf[slot * nch + (off >> 12)] ? make_uint4(1u, 1u, 1u, 1u)
-                                                      : __ldcs(reinterpret_cast<const uint4*>(pk + addr));
+                uint32_t* d = dst + 4u * tid + 1024u * g;
+                if (zf && zf[(addr >> (lb + 1)) * nch + ((addr & ((2ull << lb) - 1)) >> 12)])
+                    *reinterpret_cast<uint4*>(d) = make_uint4(1u, 1u, 1u, 1u);  // unwritten all-zero chunk
+                else
+                    cp_async16(d, pk + addr);
             }
+            cp_async_commit();
+        };
+        uint64_t tile = blockIdx.x;
+        if (tile < ntiles) issue(tile, tile_w);
+        for (uint32_t k = 0; tile < ntiles; tile += gridDim.x, ++k) {
+            const uint32_t* cur = tile_w + ((k & 1u) << kMaxTileBits);
+            if (tile + gridDim.x < ntiles)
+                issue(tile + gridDim.x, tile_w + (((k + 1) & 1u) << kMaxTileBits));
+            else
+                cp_async_commit();  // (an empty group keeps the wait count uniform)
+            const uint64_t base = runs_deposit(tile, pass.base);
+            const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
             uint32_t pat = 0;
             for (uint32_t i = 0; i < pass.npat_bits; ++i)
                 pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
@@ -1498,18 +1523,16 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
 #pragma unroll
             for (int g = 0; g < kPermGroups; ++g)
                 ent[g] = __ldg(reinterpret_cast<const uint2*>(tab + 4u * tid + 1024u * g));
-            __syncthreads();  // previous tile's gathers are done
-#pragma unroll
-            for (int g = 0; g < kPermGroups; ++g) *reinterpret_cast<uint4*>(tile_w + 4u * tid + 1024u * g) = re[g];
+            cp_async_wait<1>();  // this tile's group has landed
             __syncthreads();
 #pragma unroll
             for (int g = 0; g < kPermGroups; ++g) {
                 uint4 xo;
                 const uint32_t e0 = ent[g].x & 0xffffu, e1 = ent[g].x >> 16, e2 = ent[g].y & 0xffffu, e3 = ent[g].y >> 16;
-                xo.x = neg_if(tile_w[e0 & 0xfffu], e0 >> 13);
-                xo.y = neg_if(tile_w[e1 & 0xfffu], e1 >> 13);
-                xo.z = neg_if(tile_w[e2 & 0xfffu], e2 >> 13);
-                xo.w = neg_if(tile_w[e3 & 0xfffu], e3 >> 13);
+                xo.x = neg_if(cur[e0 & 0xfffu], e0 >> 13);
+                xo.y = neg_if(cur[e1 & 0xfffu], e1 >> 13);
+                xo.z = neg_if(cur[e2 & 0xfffu], e2 >> 13);
+                xo.w = neg_if(cur[e3 & 0xfffu], e3 >> 13);
                 const uint64_t addr = pb + toffp[g];
                 __stcs(reinterpret_cast<uint4*>(pk + addr), xo);
                 if (kLast) {
@@ -1521,6 +1544,7 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
                     ar.flush(cps, addr >> kshift);
                 }
             }
+            __syncthreads();  // this buffer is refilled two tiles on
         }
         return;
     }
