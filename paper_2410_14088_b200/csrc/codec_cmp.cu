@@ -368,8 +368,31 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
     const uint32_t qmin_off = static_cast<uint32_t>(bp.code_min - t.qlo);
     const uint64_t code_bits = static_cast<uint64_t>(p.nnz) * w_bits;
     const uint32_t nstage = static_cast<uint32_t>((code_bits + 31) / 32);
-    for (uint32_t i = tid; i < nstage; i += kChunkThreads) sm.stage[i] = 0;
     const uint32_t lt = (1u << lane) - 1;
+    if (kW1 && kFull && p.nnz == kChunk) {
+        // every code one bit, no zeros: the sign bitmap and the code stream
+        // are two ballots per word (no zero bitmap, no prefix)
+        uint32_t pkv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pkv[j] = __ldcs(src + 128 * j + 32 * w + lane);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t k = 4 * j + w;
+            const uint32_t sw = __ballot_sync(0xffffffffu, (pkv[j] >> 1) & 1u);
+            const uint32_t bw = __ballot_sync(0xffffffffu, (((pkv[j] >> 2) - qmin_off) & 1u) != 0);
+            if (lane == 0) {
+                sm.sign[k] = sw;
+                sm.bits[k] = bw;
+            }
+        }
+        __syncthreads();
+        if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, sm.sign, kChunk, tid, kChunkThreads);
+        const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix);
+        write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), sm.bits,
+                         kChunk, tid, kChunkThreads);
+        return;
+    }
+    for (uint32_t i = tid; i < nstage; i += kChunkThreads) sm.stage[i] = 0;
     // A: all loads in flight; B: ballots -> bitmap words, width-1 code words,
     // or (wider codes) the nonzero codes compacted per word into sm.cw
     {
@@ -411,14 +434,6 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
         sm.pre[tid] = pre;
     }
     __syncthreads();
-    if (kW1 && kFull && p.nnz == kChunk) {  // every code one bit, no zeros: the stream is the ballot words
-        const uint32_t raw_bits = kChunk;
-        if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, sm.sign, raw_bits, tid, kChunkThreads);
-        const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix);
-        write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), sm.bits,
-                         kChunk, tid, kChunkThreads);
-        return;
-    }
     // C: each warp packs its words' codes LSB-first into the stage (shared
     // OR: a code spans at most two stage words, edge words are shared)
 #pragma unroll 1
