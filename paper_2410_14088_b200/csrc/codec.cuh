@@ -37,6 +37,7 @@ void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, u
 // are then not written (k_dec_index); mode 0: one byte per 32-scalar group of
 // the output, 0 for an all-zero group that was not stored.)
 // (imnz, mode 1 with zflag: set to 1 when a chunk of some block's imaginary
-// half is not all zero; the caller zeroes it first.)
+// half is not all zero; mode 0 with zflag: set to 1 when some group flag is
+// 0. The caller zeroes it first.)
 
 }  // namespace bmq

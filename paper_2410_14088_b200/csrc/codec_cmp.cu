@@ -138,13 +138,13 @@ __global__ void __launch_bounds__(kChunkThreads) k_cmp_stats(const CmpBlock* __r
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     ChunkAcc acc;
     bool bad = false, oow = false;
+    const double qlo_d = static_cast<double>(t.qlo);
+    const int span = static_cast<int>(t.qhi - t.qlo);
 #pragma unroll 4
     for (int j = 0; j < 32; ++j) {
         const uint32_t s = 128 * j + 32 * w + lane;
         if (s < len) {
-            const double v = __ldg(src + s);
-            uint32_t pk;
-            quantize_pack_n<1>(&v, &pk, t, bad, oow);
+            const uint32_t pk = quantize_pack_fast(__ldg(src + s), t, qlo_d, span, bad, oow);
             dst[s] = pk;
             acc.add(pk);
         }

@@ -37,7 +37,8 @@ constexpr int kIndexThreads = 256;
 __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __restrict__ blks, uint32_t nch_max,
                                                              DecInfo* __restrict__ infos, DecChunk* __restrict__ dcs,
                                                              DevTables t, int check_bound, DevError* err,
-                                                             uint8_t* __restrict__ zflag, uint32_t* imnz) {
+                                                             uint8_t* __restrict__ zflag, uint32_t* imnz,
+                                                             uint32_t* wz) {
     const uint32_t bi = blockIdx.x;
     const DecBlock blk = blks[bi];
     const uint8_t* p = blk.in;
@@ -99,12 +100,14 @@ __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __r
             info.flags = 2;
         }
         if (tid == 0) infos[bi] = info;
+        if (wz && tid == 0) *wz = 1;  // an ALL_ZERO block: its groups are flagged zero
         if (zflag)
             for (uint32_t c = tid; c < nch_max; c += kIndexThreads) zflag[static_cast<uint64_t>(bi) * nch_max + c] = 1;
         return;
     }
     // Both bitmaps: tags, raw offsets; the first bad chunk (in order) reports.
     uint64_t seg = kHeaderBytes;
+    bool any_zero = false;
     for (int bm = 0; bm < 2 && !fail; ++bm) {
         const uint32_t trunc = bm == 0 ? DE_SIGN_TRUNC : DE_ZERO_TRUNC;
         if (blk.size - seg < ntag) {
@@ -133,6 +136,7 @@ __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __r
                     const bool zc = tag == 1 && len == kChunk;
                     if (zflag) zflag[static_cast<uint64_t>(bi) * nch_max + c] = zc ? 1 : 0;
                     if (imnz && !zc && 2 * c >= nch) *imnz = 1;  // imaginary half (chunks nch/2.. of 2^(lb+1) scalars)
+                    if (tag != 0) any_zero = true;  // the chunk has zero scalars (maybe whole zero groups)
                 }
             }
             unsigned long long pre, tot;
@@ -160,6 +164,8 @@ __global__ void __launch_bounds__(kIndexThreads) k_dec_index(const DecBlock* __r
         }
         seg = raw0 + carry;
     }
+    // wz: some block may hold an all-zero 32-scalar group (one store per block)
+    if (__syncthreads_or(any_zero) && wz && tid == 0) *wz = 1;
     // nonzero scalars per chunk -> prefix
     unsigned long long nnz_total = 0;
     if (!fail) {
@@ -450,7 +456,8 @@ void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, u
     k_dec_index<<<static_cast<uint32_t>(nblk), kIndexThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t,
                                                                         check_bound ? 1 : 0, d_err,
                                                                         mode == 1 ? zflag : nullptr,
-                                                                        mode == 1 && zflag ? imnz : nullptr);
+                                                                        mode == 1 && zflag ? imnz : nullptr,
+                                                                        mode == 0 && zflag ? imnz : nullptr);
     const uint32_t grid = static_cast<uint32_t>(nblk * nch_max);
     if (mode == 1)
         k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err,

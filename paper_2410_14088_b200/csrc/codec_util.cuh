@@ -85,48 +85,43 @@ __device__ __forceinline__ uint32_t quantize_pack(double v, const DevTables& t, 
     return pack_code(static_cast<uint32_t>(q - t.qlo), v < 0.0, false);
 }
 
-// quantize_pack for N scalars at once: every estimate first, then both
-// neighbouring thresholds of every estimate as independent loads (2N in
-// flight instead of a dependent chain per scalar), then the exact
-// settlement; an estimate off by more than one falls back to quantize().
-template <int N>
-__device__ __forceinline__ void quantize_pack_n(const double* v, uint32_t* pk, const DevTables& t, bool& bad,
-                                                bool& oow) {
-    uint64_t bits[N];
-    int idx[N];  // table index (< 2^25 entries)
-    bool live[N], sure[N];
-    const double qlo = static_cast<double>(t.qlo);
-    const int span = static_cast<int>(t.qhi - t.qlo);
-#pragma unroll
-    for (int e = 0; e < N; ++e) {
-        live[e] = isfinite(v[e]) && v[e] != 0.0;
-        if (!isfinite(v[e])) bad = true;
-        const double x = live[e] ? quantize_estimate_x(v[e], t, bits[e]) : 0.0;
-        const double r = rint(x);
-        const int i = __double2int_rz(r - qlo);  // exact (integers below 2^53); saturates
-        // the rounding is settled unless x lies within est_eps of a half-integer
-        sure[e] = 0.5 - fabs(x - r) > t.est_eps && i >= 0 && i <= span;
-        idx[e] = min(max(i, 0), span);
+// The estimate of quantize_pack in registers: x ~ log2|v| / b_a from the bit
+// pattern (finite, nonzero), see quantize_estimate_x.
+__device__ __forceinline__ double quant_estimate_bits(uint64_t bits, const DevTables& t) {
+    const uint32_t ex = static_cast<uint32_t>(bits >> 52);
+    uint64_t man = bits & 0xfffffffffffffull;
+    int e2 = static_cast<int>(ex) - 1023;
+    if (ex == 0) {  // subnormal: normalise the mantissa
+        const int shift = __clzll(static_cast<long long>(man)) - 11;
+        man = (man << shift) & 0xfffffffffffffull;
+        e2 = -1022 - shift;
     }
-    uint64_t t0[N], t1[N];
-#pragma unroll
-    for (int e = 0; e < N; ++e) {  // threshold probes only near a tie
-        t0[e] = (live[e] && !sure[e]) ? __ldg(t.thresh + idx[e]) : 0;
-        t1[e] = (live[e] && !sure[e]) ? __ldg(t.thresh + idx[e] + 1) : ~0ull;
+    const float m = __int_as_float(0x3f800000 | static_cast<int>(man >> 29));  // mantissa truncated to float
+    return (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
+}
+
+// quantize_pack with every step in registers: a scalar whose estimate x
+// lies farther than est_eps from a half-integer (inside the table window)
+// takes round(x) directly; the others (about 2 est_eps of them) probe both
+// neighbouring thresholds and settle exactly, and an estimate off by more
+// than one falls back to quantize(). qlo_d = (double) t.qlo, span = qhi - qlo.
+__device__ __forceinline__ uint32_t quantize_pack_fast(double v, const DevTables& t, double qlo_d, int span,
+                                                       bool& bad, bool& oow) {
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
+    if (bits == 0) return 1u;  // +-0
+    if (bits >= 0x7ff0000000000000ull) {
+        bad = true;
+        return 1u;
     }
-#pragma unroll
-    for (int e = 0; e < N; ++e) {
-        if (!live[e]) {
-            pk[e] = 1u;
-            continue;
-        }
-        uint32_t qoff;
-        if (sure[e] || (bits[e] >= t0[e] && bits[e] < t1[e]))
-            qoff = static_cast<uint32_t>(idx[e]);
-        else
-            qoff = static_cast<uint32_t>(quantize(v[e], t, oow) - t.qlo);
-        pk[e] = pack_code(qoff, v[e] < 0.0, false);
+    const double x = quant_estimate_bits(bits, t);
+    const double r = rint(x);
+    const int i = __double2int_rz(r - qlo_d);  // exact (integers below 2^53); saturates
+    uint32_t qoff = static_cast<uint32_t>(min(max(i, 0), span));
+    if (!(0.5 - fabs(x - r) > t.est_eps && static_cast<unsigned>(i) <= static_cast<unsigned>(span))) {
+        const uint64_t lo = __ldg(t.thresh + qoff), hi = __ldg(t.thresh + qoff + 1);
+        if (!(bits >= lo && bits < hi)) qoff = static_cast<uint32_t>(quantize(v, t, oow) - t.qlo);
     }
+    return pack_code(qoff, v < 0.0, false);
 }
 
 }  // namespace bmq

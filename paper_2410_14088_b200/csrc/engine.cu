@@ -746,9 +746,10 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     // stages all-zero 32-scalar groups (wflag_); neither is stored
     uint8_t* zf = codes ? (mono_zero_skip(sp.prog, L_.b) ? zflag_.p : nullptr)
                         : (program_zero_skip(sp.prog, L_.b, false) ? wflag_.p : nullptr);
-    if (codes && zf) BMQ_CUDA(cudaMemsetAsync(imnz_.p, 0, sizeof(uint32_t), st_));
+    // imnz_: code domain, some imaginary-half chunk nonzero; FP: some group flag 0
+    if (zf) BMQ_CUDA(cudaMemsetAsync(imnz_.p, 0, sizeof(uint32_t), st_));
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
-                      &counters_.kernel_launches, codes ? 1 : 0, zf, codes && zf ? imnz_.p : nullptr);
+                      &counters_.kernel_launches, codes ? 1 : 0, zf, zf ? imnz_.p : nullptr);
     phase_event(4 * bidx + 1);
     // the stage's last gate pass quantises straight into pk_ / cplan_
     BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
@@ -761,7 +762,7 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
         ++counters_.code_domain_batches;
     } else {
         fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per, &counters_.kernel_launches,
-                            &qo, d_vtab, nblk, zf, nch_);
+                            &qo, d_vtab, nblk, zf, nch_, zf ? imnz_.p : nullptr);
     }
     phase_event(4 * bidx + 2);
     launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,

@@ -16,6 +16,7 @@
 // and multiplies by each bit's phase, so the cost is the number of phases
 // that actually apply, not the number of gates.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 
@@ -517,6 +518,12 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
                 fp->tab_base = tab_mark / 2;
                 fp->tab_entries = static_cast<uint32_t>((prog.chain_tab.size() - tab_mark) / 2);
                 std::copy(fops.begin(), fops.end(), fp->ops);
+                if (getenv("BMQ_DBG_PASSES")) {  // development aid: the pass's ops
+                    fprintf(stderr, "pass %zu mask %llx ops %zu:", prog.passes.size(),
+                            static_cast<unsigned long long>(mask), fops.size());
+                    for (const FastOp& o : fops) fprintf(stderr, " %u/%u", o.type, o.tp_hi);
+                    fprintf(stderr, "\n");
+                }
                 p.fast = true;
                 p.fp = fp;
             }
@@ -809,51 +816,43 @@ __device__ __forceinline__ bool has_chain(const FastOp* ops, uint32_t q0, uint32
 // per-chunk counters. Lanes of a warp hold 32 consecutive locals (tile
 // positions 0..4 are buffer bits 0..4), so (block slot, chunk) is
 // warp-uniform and counters are reduced per warp before one set of atomics.
-__device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t base,
-                                               uint64_t toff, const uint64_t* joff, uint32_t lb, bool gather,
-                                               uint32_t cvec, const uint16_t* gat_lo, const uint16_t* gat_hi) {
-    const uint64_t lmask = (1ull << lb) - 1;
+__device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t pbt,
+                                               const uint64_t* pjoff, uint32_t lb, bool gather, uint32_t cvec,
+                                               const uint16_t* gat_lo, const uint16_t* gat_hi) {
+    // pbt: planar index of (tile base | thread offset); pjoff[j]: of row j
+    const uint64_t im_off = 1ull << lb;
+    const double qlo_d = static_cast<double>(q.t.qlo);
+    const int span = static_cast<int>(q.t.qhi - q.t.qlo);
     ChunkAcc acc_re, acc_im;
-    uint64_t key_re = ~0ull, key_im = ~0ull;
+    uint64_t key = ~0ull;  // chunk of the real scalar (the imaginary one is key + nch / 2)
+    const uint64_t kim = im_off >> 12;
     bool bad = false, oow = false;
-    constexpr int kG = 1;  // amplitudes quantised together (2 kG probes in flight)
-    for (int g0 = 0; g0 < kPer; g0 += kG) {
-        double v[2 * kG];
-        uint32_t pk[2 * kG];
-#pragma unroll
-        for (int e = 0; e < kG; ++e) {
-            uint32_t y = tid + 256 * (g0 + e);
-            if (gather) y = gat_lo[(y ^ cvec) & 63] ^ gat_hi[(y ^ cvec) >> 6];
-            const double2 a = tile_s[y];
-            v[2 * e] = a.x;
-            v[2 * e + 1] = a.y;
-        }
-        quantize_pack_n<2 * kG>(v, pk, q.t, bad, oow);
-#pragma unroll
-        for (int e = 0; e < kG; ++e) {
-            // planar scalar index; chunks are 4096 scalars and 2^(lb+1) / 4096
-            // = nch per block (lb >= 12), so the chunk key is index >> 12
-            const uint64_t a_re = planar_addr(base | toff | joff[g0 + e], lb, lmask, false);
-            const uint64_t a_im = a_re + (1ull << lb);
-            const uint64_t kre = a_re >> 12, kim = a_im >> 12;
-            if (kre != key_re) {  // warp-uniform
-                if (key_re != ~0ull) flush_chunk(q.cps + key_re, acc_re);
-                acc_re = ChunkAcc{};
-                key_re = kre;
+    for (int j = 0; j < kPer; ++j) {
+        uint32_t y = tid + 256 * j;
+        if (gather) y = gat_lo[(y ^ cvec) & 63] ^ gat_hi[(y ^ cvec) >> 6];
+        const double2 a = tile_s[y];
+        const uint32_t pr = quantize_pack_fast(a.x, q.t, qlo_d, span, bad, oow);
+        const uint32_t pi = quantize_pack_fast(a.y, q.t, qlo_d, span, bad, oow);
+        // chunks are 4096 scalars and 2^(lb+1) / 4096 = nch per block (lb >= 12),
+        // so the chunk key is the planar index >> 12
+        const uint64_t a_re = pbt + pjoff[j];
+        const uint64_t k = a_re >> 12;
+        if (k != key) {  // warp-uniform
+            if (key != ~0ull) {
+                flush_chunk(q.cps + key, acc_re);
+                flush_chunk(q.cps + key + kim, acc_im);
             }
-            if (kim != key_im) {
-                if (key_im != ~0ull) flush_chunk(q.cps + key_im, acc_im);
-                acc_im = ChunkAcc{};
-                key_im = kim;
-            }
-            q.pk[a_re] = pk[2 * e];
-            q.pk[a_im] = pk[2 * e + 1];
-            acc_re.add(pk[2 * e]);
-            acc_im.add(pk[2 * e + 1]);
+            acc_re = ChunkAcc{};
+            acc_im = ChunkAcc{};
+            key = k;
         }
+        q.pk[a_re] = pr;
+        q.pk[a_re + im_off] = pi;
+        acc_re.add(pr);
+        acc_im.add(pi);
     }
-    flush_chunk(q.cps + key_re, acc_re);
-    flush_chunk(q.cps + key_im, acc_im);
+    flush_chunk(q.cps + key, acc_re);
+    flush_chunk(q.cps + key + kim, acc_im);
     if (bad) dev_fail(q.err, DE_NONFINITE, 0);
     if (oow) dev_fail(q.err, DE_WINDOW, 0);
 }
@@ -864,10 +863,11 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                                                                  const __grid_constant__ QuantOut quant,
                                                                  const uint32_t* __restrict__ vtab,
                                                                  int dbg_full_support,
-                                                                 uint8_t* __restrict__ wf) {
+                                                                 uint8_t* __restrict__ wf, uint32_t* wz) {
     // dynamic SMEM: 4096 amplitudes (tile position k) | chain tables | ops
     extern __shared__ double2 tile_s[];
     __shared__ uint64_t joff[kPer];
+    __shared__ uint64_t pjoff[kPer];             // planar index of joff[j] (planar_addr is OR-linear)
     __shared__ uint32_t lut_lo[64], lut_hi[64];  // tile position -> buffer bits (low 32)
     __shared__ uint16_t gat_lo[64], gat_hi[64];  // final M^-1 on a 12-bit tile index (lazy CX)
     double2* stab = tile_s + 4096;
@@ -876,7 +876,11 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     const uint64_t lmask = (1ull << lb) - 1;
     const uint64_t im_off = interleaved ? 1 : (1ull << lb);
     const uint64_t toff = runs_deposit(tid, pass.tile);
-    if (tid < kPer) joff[tid] = runs_deposit(static_cast<uint64_t>(tid) << 8, pass.tile);
+    const uint64_t ptoff = planar_addr(toff, lb, lmask, interleaved);
+    if (tid < kPer) {
+        joff[tid] = runs_deposit(static_cast<uint64_t>(tid) << 8, pass.tile);
+        pjoff[tid] = planar_addr(joff[tid], lb, lmask, interleaved);
+    }
     if (tid < 64) lut_lo[tid] = static_cast<uint32_t>(runs_deposit(tid, pass.tile));
     else if (tid < 128) lut_hi[tid - 64] = static_cast<uint32_t>(runs_deposit(static_cast<uint64_t>(tid - 64) << 6, pass.tile));
     else if (tid < 256) {
@@ -896,6 +900,10 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     }
     __shared__ uint32_t s_supp[2];
     if (tid < 2) s_supp[tid] = 0;
+    // *wz == 0: no group of the buffer is flagged zero (every flag is 1), so
+    // loads need not test flags; a pass that flags a group zero sets it
+    const bool wf_read = wf && *reinterpret_cast<volatile uint32_t*>(wz) != 0;
+    bool set_wz = false;  // this thread flagged a group zero (one store per CTA at the end)
     __syncthreads();
     // Sweeps are the same for every tile: a run of diagonal ops, extended
     // over CX / DIAG / CDIAG when it holds no phase chain (lazy CX).
@@ -912,15 +920,16 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     uint32_t parity = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, parity ^= 1) {
         const uint64_t base = runs_deposit(tile, pass.base);
+        const uint64_t pbt = planar_addr(base, lb, lmask, interleaved) + ptoff;  // planar index of base | toff
         // Index used by diagonal conditions. Block-wise batches (vtab) hold
         // single blocks of a diagonal stage: the bits above lb are the
         // block's inner value, not its slot in the batch.
         const uint64_t xbase = vtab ? ((static_cast<uint64_t>(vtab[base >> lb]) << lb) | (base & lmask)) : base;
         // Group flags of the warp's 32 groups (lane 2j + c: scalar c of row j).
         uint32_t fl = 1;
-        if (wf) {
+        if (wf_read) {
             const uint32_t lane = tid & 31;
-            const uint64_t a = planar_addr(base | toff | joff[lane >> 1], lb, lmask, interleaved);
+            const uint64_t a = pbt + pjoff[lane >> 1];
             fl = wf[(a + ((lane & 1) ? im_off : 0)) >> 5];
         }
         // Barrier: the previous tile's stores have read tile_s.
@@ -933,8 +942,8 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             uint32_t nzpos = 0;
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
-                const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
-                if (wf) {  // 32-scalar groups flagged zero were not stored (warp-uniform test)
+                const uint64_t a = pbt + pjoff[j];
+                if (wf_read) {  // 32-scalar groups flagged zero were not stored (warp-uniform test)
                     re[j] = __shfl_sync(0xffffffffu, fl, 2 * j) ? buf[a] : 0.0;
                     im[j] = __shfl_sync(0xffffffffu, fl, 2 * j + 1) ? buf[a + im_off] : 0.0;
                     continue;
@@ -959,10 +968,11 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         if (S == 0 && wf && !quant.pk) {  // an all-zero tile stays zero: flag its groups, store nothing
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
-                const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
+                const uint64_t a = pbt + pjoff[j];
                 if ((tid & 31) == 0) {
                     wf[a >> 5] = 0;
                     wf[(a + im_off) >> 5] = 0;
+                    set_wz = true;
                 }
             }
             continue;
@@ -1151,7 +1161,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         const bool gather = pass.final_perm || cvec;  // logical y lives at M^-1 (y ^ c)
         if (!owners_only || gather) __syncthreads();
         if (quant.pk) {
-            quant_epilogue(quant, tile_s, tid, base, toff, joff, lb, gather, cvec, gat_lo, gat_hi);
+            quant_epilogue(quant, tile_s, tid, pbt, pjoff, lb, gather, cvec, gat_lo, gat_hi);
             continue;
         }
         {
@@ -1166,12 +1176,13 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             }
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
-                const uint64_t a = planar_addr(base | toff | joff[j], lb, lmask, interleaved);
+                const uint64_t a = pbt + pjoff[j];
                 if (wf) {  // an all-zero 32-scalar group is flagged instead of stored
                     const bool nr = __any_sync(0xffffffffu, re[j] != 0.0), ni = __any_sync(0xffffffffu, im[j] != 0.0);
                     if ((threadIdx.x & 31) == 0) {
                         wf[a >> 5] = nr;
                         wf[(a + im_off) >> 5] = ni;
+                        if (!(nr && ni)) set_wz = true;
                     }
                     if (nr) buf[a] = re[j];
                     if (ni) buf[a + im_off] = im[j];
@@ -1182,6 +1193,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             }
         }
     }
+    if (wf && __syncthreads_or(set_wz) && tid == 0) *wz = 1;
 }
 
 // ------------------------------------------------------ general pass (SMEM)
@@ -1664,7 +1676,8 @@ bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved) {
 
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant, const uint32_t* vtab,
-                 uint64_t nblocks, const uint8_t* zflag, uint32_t nch) {
+                 uint64_t nblocks, const uint8_t* zflag, uint32_t nch, uint32_t* wz) {
+    if (zflag && !wz) raise(BMQ_ERR_LOGIC, "zero-group flags need their summary word");
     if (zflag && !program_zero_skip(prog, lb, interleaved))
         raise(BMQ_ERR_LOGIC, "zero-group skipping needs fast passes only");
     const bool fuse = quant && !interleaved && lb >= 12 && !prog.passes.empty() && prog.passes.back().fast;
@@ -1693,7 +1706,7 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
             const bool last = pi + 1 == prog.passes.size();
             k_gate_pass_fast<<<static_cast<uint32_t>(grid), kFastThreads, smem, st>>>(
                 buf, lb, interleaved ? 1 : 0, tiles, *p.fp, (fuse && last) ? *quant : none, vtab,
-                full_support_debug() ? 1 : 0, const_cast<uint8_t*>(zflag));
+                full_support_debug() ? 1 : 0, const_cast<uint8_t*>(zflag), wz);
         } else {
             const uint32_t nth = std::min<uint32_t>(kPassThreads, 1u << p.tb);
             const size_t smem = 2 * (size_t(1) << p.tb) * sizeof(double);

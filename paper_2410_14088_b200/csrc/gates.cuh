@@ -173,12 +173,13 @@ struct QuantOut {
 // zflag (optional; needs program_zero_skip): one flag byte per 32-scalar
 // group of buf (index = planar address / 32), 0 for an all-zero group that
 // was not stored; every pass reads and (except the quantising last pass)
-// maintains them. nch is unused.
+// maintains them. nch is unused. wz (with zflag): device word, nonzero when
+// some flag may be 0; launch_decompress and the passes set it.
 bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved);
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant = nullptr,
                  const uint32_t* vtab = nullptr, uint64_t nblocks = 0, const uint8_t* zflag = nullptr,
-                 uint32_t nch = 0);
+                 uint32_t nch = 0, uint32_t* wz = nullptr);
 
 // Code-domain program (prog.mono): the passes permute packed code words in
 // place (planar per block of 2^lb amplitudes, CmpBlock::pk layout); the last
