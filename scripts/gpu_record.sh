@@ -11,7 +11,8 @@ bash scripts/gpu_workloads.sh > /dev/null 2>&1
 Q=30 THR=1e18 bash scripts/gpu_launches.sh > /dev/null 2>&1
 W=qaoa3reg Q=28 A="--error-bound 1e-4" bash scripts/gpu_launches_w.sh > /dev/null 2>&1
 B="python bench.py --qubits 30 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gate_pass_fast -s 16 -c 1 -o gpurun_out/rec_chain $B > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gate_pass_fast -s 18 -c 1 -o gpurun_out/rec_chain $B > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gate_pass_fast -s 16 -c 1 -o gpurun_out/rec_chain0 $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_perm_pass -s 0 -c 1 -o gpurun_out/rec_perm $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dec_chunk -s 17 -c 1 -o gpurun_out/rec_dec $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cmp_emit -s 18 -c 1 -o gpurun_out/rec_emit $B > /dev/null 2>&1

@@ -98,6 +98,27 @@ def test_zero_group_skip_is_exact(gpu):
     assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_cancellation_inside_stage_is_exact(gpu, port, seed):
+    """A dense state whose stage undoes itself (RY layer, then H twice on every
+    qubit, then RY back): later passes of the stage see groups the earlier
+    passes zeroed although the decoded batch had none (zero-group summary)."""
+    n, b = 17, 12
+    rng = np.random.default_rng(900 + seed)
+    ang = [float(a) for a in rng.uniform(0.2, 1.2, n)]
+    gl = [(0, q, 0, 0.0) for q in range(n)]
+    gl += [(9, q, 0, ang[q]) for q in range(n)]
+    gl += [(0, q, 0, 0.0) for q in range(n)] * 2
+    gl += [(9, q, 0, -ang[q]) for q in range(n)]
+    gl += [(0, q, 0, 0.0) for q in range(n)]
+    c = gpu.Circuit(n, [gpu.Gate(gpu.GateKind(k), a, bb, t) for k, a, bb, t in gl])
+    want = port.simulate(n, gl, b, 2, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=2, error_bound=1e-3)) as sim:
+        rep = sim.run()
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+
+
 @pytest.mark.parametrize("name,n,b,inner,layers", [("qft", 18, 12, 2, 1), ("qft", 17, 12, 4, 1),
                                                    ("qaoa", 16, 12, 2, 2), ("bv", 16, 13, 2, 1)])
 def test_identity_skip_is_exact(gpu, port, name, n, b, inner, layers):
