@@ -476,10 +476,13 @@ __global__ void __launch_bounds__(kChunkThreads, 6) k_cmp_emit(const CmpBlock* _
                                                             const ChunkPlan* __restrict__ cps,
                                                             BlockPlan* __restrict__ bps, uint8_t* __restrict__ out,
                                                             DevTables t, const DevError* err) {
-    if (err->code) return;
+    // every record this CTA needs, loaded together (one memory round trip)
     const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
+    const uint32_t failed = err->code;
     const CmpBlock blk = blks[bi];
     const BlockPlan bp = bps[bi];
+    const ChunkPlan p = cps[static_cast<uint64_t>(bi) * nch_max + c];
+    if (failed) return;
     if (c > 0 && c >= bp.nch) return;  // (an empty block still gets its header from chunk 0)
     if (bp.out_off == ~0ull) return;   // virtual ALL_ZERO
     uint8_t* pay = out + bp.out_off;
@@ -510,7 +513,6 @@ __global__ void __launch_bounds__(kChunkThreads, 6) k_cmp_emit(const CmpBlock* _
             pay[bp.ztag_off + k] = static_cast<uint8_t>(zb);
         }
     }
-    const ChunkPlan p = cp[c];
     const uint32_t len = chunk_len(blk.count, c);
     // a full chunk of zeros is tags only (sign tag 0, zero tag 1): no bytes
     if (p.nnz == 0 && len == kChunk) return;

@@ -314,12 +314,14 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
                                                              const DecChunk* __restrict__ dcs, DevTables t,
                                                              int want_sums, DevError* err, int skip_zero_chunks,
                                                              uint8_t* __restrict__ wflag) {
+    // the CTA's records, loaded together (one memory round trip)
     const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
     const DecInfo info = infos[bi];
+    const DecBlock blk = blks[bi];
+    const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
     if (info.flags & 2) return;
     const uint64_t nch = (info.count + kChunk - 1) / kChunk;
     if (c >= nch) return;
-    const DecBlock blk = blks[bi];
     const uint32_t len = chunk_len(info.count, c);
     double* dst = blk.out + static_cast<uint64_t>(c) * kChunk;
     uint32_t* cdst = reinterpret_cast<uint32_t*>(blk.out) + static_cast<uint64_t>(c) * kChunk;
@@ -342,7 +344,6 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
         }
         return;
     }
-    const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
     if (skip_zero && d.ztag == 1 && len == kChunk) {
         if (gflag && tid < 128) gflag[tid] = 0;
         return;
