@@ -389,7 +389,27 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     const uint8_t* codes = blk.in + info.code_seg;
     const bool sums = want_sums != 0;
     const uint32_t nnz_chunk = s_pre[kWordsPerChunk - 1] + __popc(s_nz[kWordsPerChunk - 1]);
-    if (kMode != kSumsOnly && len == kChunk && !check && width <= 16 && nnz_chunk == kChunk) {
+    if (kMode == kSumsOnly && len == kChunk && !check && width == 1 && nnz_chunk == kChunk &&
+        (half & (kChunk - 1)) == 0) {
+        // sums of a zero-free chunk of one-bit codes: every scalar is +-E[qb]
+        // or +-E[qb + 1], so each thread counts its 32 codes and signs
+        const uintptr_t cs = reinterpret_cast<uintptr_t>(codes);
+        const uint64_t cb = static_cast<uint64_t>(cs & 3) * 8 + d.nz_prefix;
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3)) + (cb >> 5);
+        const uint32_t a = static_cast<uint32_t>(cb & 31) + 32u * tid;
+        const uint32_t code = __funnelshift_r(__ldg(cw + (a >> 5)), __ldg(cw + (a >> 5) + 1), a & 31);
+        const uint32_t sg = s_sign[tid];
+        const uint32_t qb = static_cast<uint32_t>(qbase);
+        const double m0 = __ldg(t.dequant + qb), m1 = __ldg(t.dequant + qb + 1);
+        const int n1 = __popc(code), n0 = 32 - n1;
+        const int neg1 = __popc(code & sg), neg0 = __popc(~code & sg);
+        sq = n0 * (m0 * m0) + n1 * (m1 * m1);
+        const double vs = m0 * (n0 - 2 * neg0) + m1 * (n1 - 2 * neg1);
+        if (g0 < half)  // (the chunk lies in one half)
+            sre = vs;
+        else
+            sim = vs;
+    } else if (kMode != kSumsOnly && len == kChunk && !check && width <= 16 && nnz_chunk == kChunk) {
         // No zero in the chunk and narrow codes: scalar s has rank s, so each
         // thread decodes four consecutive scalars from one 64-bit window and
         // writes them with 16-byte stores.

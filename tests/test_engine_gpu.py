@@ -329,6 +329,10 @@ def test_code_domain_qft_swaps(gpu, port):
         assert rep.device["code_domain_batches"] > 0
         assert sim.payloads() == want.payloads
         assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        # final sums (one-bit-code chunks are counted, not decoded)
+        assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=NORM_RTOL)
+        amps = sim.extract_state()
+        assert sim.fidelity_analytic("uniform") == pytest.approx(abs(amps.sum()) / np.sqrt(len(amps)), rel=1e-9)
 
 
 def test_pool_growth_is_exact(gpu, port):
