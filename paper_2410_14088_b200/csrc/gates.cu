@@ -817,34 +817,34 @@ __device__ __forceinline__ bool has_chain(const FastOp* ops, uint32_t q0, uint32
 // positions 0..4 are buffer bits 0..4), so (block slot, chunk) is
 // warp-uniform and counters are reduced per warp before one set of atomics.
 __device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t pbt,
-                                               const uint64_t* pjoff, uint32_t lb, bool gather, uint32_t cvec,
-                                               const uint16_t* gat_lo, const uint16_t* gat_hi) {
+                                               const uint64_t* pjoff, uint32_t jnew, uint32_t lb, bool gather,
+                                               uint32_t cvec, const uint16_t* gat_lo, const uint16_t* gat_hi) {
     // pbt: planar index of (tile base | thread offset); pjoff[j]: of row j
     const uint64_t im_off = 1ull << lb;
     const double qlo_d = static_cast<double>(q.t.qlo);
     const int span = static_cast<int>(q.t.qhi - q.t.qlo);
     ChunkAcc acc_re, acc_im;
-    uint64_t key = ~0ull;  // chunk of the real scalar (the imaginary one is key + nch / 2)
-    const uint64_t kim = im_off >> 12;
+    // chunks are 4096 scalars and 2^(lb+1) / 4096 = nch per block (lb >= 12),
+    // so the chunk of a scalar is its planar index >> 12; the bits of pbt and
+    // pjoff[j] are disjoint, so row j's chunk is (pbt >> 12) | (pjoff[j] >> 12)
+    // and it changes only at the rows set in jnew (the same for every tile)
+    const uint64_t kb = pbt >> 12, kim = im_off >> 12;
+    uint64_t key = kb | (pjoff[0] >> 12);
     bool bad = false, oow = false;
+#pragma unroll 1
     for (int j = 0; j < kPer; ++j) {
         uint32_t y = tid + 256 * j;
         if (gather) y = gat_lo[(y ^ cvec) & 63] ^ gat_hi[(y ^ cvec) >> 6];
         const double2 a = tile_s[y];
         const uint32_t pr = quantize_pack_fast(a.x, q.t, qlo_d, span, bad, oow);
         const uint32_t pi = quantize_pack_fast(a.y, q.t, qlo_d, span, bad, oow);
-        // chunks are 4096 scalars and 2^(lb+1) / 4096 = nch per block (lb >= 12),
-        // so the chunk key is the planar index >> 12
         const uint64_t a_re = pbt + pjoff[j];
-        const uint64_t k = a_re >> 12;
-        if (k != key) {  // warp-uniform
-            if (key != ~0ull) {
-                flush_chunk(q.cps + key, acc_re);
-                flush_chunk(q.cps + key + kim, acc_im);
-            }
+        if ((jnew >> j) & 1u) {  // warp-uniform
+            flush_chunk(q.cps + key, acc_re);
+            flush_chunk(q.cps + key + kim, acc_im);
             acc_re = ChunkAcc{};
             acc_im = ChunkAcc{};
-            key = k;
+            key = kb | (pjoff[j] >> 12);
         }
         q.pk[a_re] = pr;
         q.pk[a_re + im_off] = pi;
@@ -904,6 +904,11 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
     // loads need not test flags; a pass that flags a group zero sets it
     const bool wf_read = wf && *reinterpret_cast<volatile uint32_t*>(wz) != 0;
     bool set_wz = false;  // this thread flagged a group zero (one store per CTA at the end)
+    __syncthreads();
+    // rows j > 0 whose chunk differs from row j - 1's (quant epilogue)
+    uint32_t jnew = 0;
+    for (int j = 1; j < kPer; ++j)
+        if ((pjoff[j] >> 12) != (pjoff[j - 1] >> 12)) jnew |= 1u << j;
     __syncthreads();
     // Sweeps are the same for every tile: a run of diagonal ops, extended
     // over CX / DIAG / CDIAG when it holds no phase chain (lazy CX).
@@ -1161,7 +1166,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         const bool gather = pass.final_perm || cvec;  // logical y lives at M^-1 (y ^ c)
         if (!owners_only || gather) __syncthreads();
         if (quant.pk) {
-            quant_epilogue(quant, tile_s, tid, pbt, pjoff, lb, gather, cvec, gat_lo, gat_hi);
+            quant_epilogue(quant, tile_s, tid, pbt, pjoff, jnew, lb, gather, cvec, gat_lo, gat_hi);
             continue;
         }
         {
