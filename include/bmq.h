@@ -317,6 +317,17 @@ int bmq_simulator_partial_sums(bmq_simulator* sim, double* sums3);
 /* Report of the stages run so far (final_norm, wall_ms, device_ms = 0). */
 int bmq_simulator_report(bmq_simulator* sim, bmq_report* report);
 
+/* ---- checkpoint / resume (the reference keeps no persisted
+ * index, store.hpp:36-46) ----
+ * save: every payload (exact bytes, codec.hpp:33-54) with its block sums,
+ * the BlockStore accounting replay and the stage cursor, to one file.
+ * load: into a simulator of the same circuit, layout, plan and error bound
+ * (validated); *next_stage = the first stage still to run (continue with
+ * bmq_simulator_run_stages / bmq_simulator_run). Payloads, max_footprint and
+ * the final state equal those of an uninterrupted run. */
+int bmq_simulator_save(bmq_simulator* sim, const char* path);
+int bmq_simulator_load(bmq_simulator* sim, const char* path, uint64_t* next_stage);
+
 #ifdef __cplusplus
 }
 #endif

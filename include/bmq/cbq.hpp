@@ -337,6 +337,18 @@ public:
         detail::check(bmq_simulator_put_payload(sim_, id, p.data(), p.size()));
     }
 
+    // Stage-level driving and checkpoint / resume (new: the reference keeps
+    // no persisted index, store.hpp:36-46).
+    void run_stages(std::uint64_t first, std::uint64_t last) {
+        detail::check(bmq_simulator_run_stages(sim_, first, last));
+    }
+    void save(const std::string& path) const { detail::check(bmq_simulator_save(sim_, path.c_str())); }
+    std::uint64_t load(const std::string& path) {  // returns the next stage to run
+        std::uint64_t next = 0;
+        detail::check(bmq_simulator_load(sim_, path.c_str(), &next));
+        return next;
+    }
+
     Layout layout() const { return make_layout(circuit_.num_qubits, config_.block_bits); }
     PartitionPlan plan() const { return partition_circuit(circuit_, config_.block_bits, config_.inner_size); }
 

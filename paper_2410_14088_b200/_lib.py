@@ -120,6 +120,8 @@ SIGNATURES = {
     "bmq_simulator_account_stage": (C.c_int, [_P, _U64, C.POINTER(_U64)]),
     "bmq_simulator_partial_sums": (C.c_int, [_P, C.POINTER(_D)]),
     "bmq_simulator_report": (C.c_int, [_P, C.POINTER(bmq_report)]),
+    "bmq_simulator_save": (C.c_int, [_P, C.c_char_p]),
+    "bmq_simulator_load": (C.c_int, [_P, C.c_char_p, C.POINTER(_U64)]),
 }
 
 

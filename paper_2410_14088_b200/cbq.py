@@ -30,6 +30,7 @@ EngineError / QasmError     (a ValueError), std::logic_error -> ``LogicError``
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 import math
 from dataclasses import dataclass, field
@@ -680,6 +681,23 @@ class Simulator:
 
     def run_stages(self, first: int, last: int) -> None:
         _check(lib.bmq_simulator_run_stages(self._h, first, last))
+
+    def report(self) -> SimulationReport:
+        """Report of the stages run so far (final_norm taken now; wall/device time 0)."""
+        r = bmq_report()
+        _check(lib.bmq_simulator_report(self._h, C.byref(r)))
+        r.final_norm = self.state_norm()
+        return report_from_c(r, [])
+
+    def save(self, path: str) -> None:
+        """Checkpoint: payloads, block sums, store accounting and the stage cursor."""
+        _check(lib.bmq_simulator_save(self._h, os.fsencode(path)))
+
+    def load(self, path: str) -> int:
+        """Resume from save(); returns the next stage to run."""
+        nxt = C.c_uint64()
+        _check(lib.bmq_simulator_load(self._h, os.fsencode(path), C.byref(nxt)))
+        return nxt.value
 
     def state_norm(self) -> float:
         out = C.c_double()

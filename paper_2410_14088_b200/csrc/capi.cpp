@@ -400,4 +400,21 @@ int bmq_simulator_report(bmq_simulator* sim, bmq_report* report) {
     });
 }
 
+int bmq_simulator_save(bmq_simulator* sim, const char* path) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        null_check(path, "path");
+        sim->engine->save_checkpoint(path);
+    });
+}
+
+int bmq_simulator_load(bmq_simulator* sim, const char* path, uint64_t* next_stage) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        null_check(path, "path");
+        const uint64_t next = sim->engine->load_checkpoint(path);
+        if (next_stage) *next_stage = next;
+    });
+}
+
 }  // extern "C"

@@ -22,7 +22,9 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <string>
 
 #include "engine.cuh"
 
@@ -77,6 +79,35 @@ void StoreModel::put_shared(uint64_t first, uint64_t last, uint64_t size) {  // 
         size_[id] = size;
     }
     peak_ = std::max(peak_, resident_ + spilled_live_);
+}
+
+void StoreModel::serialize(std::vector<uint8_t>& out) const {
+    const uint64_t n = size_.size();
+    const uint64_t head[9] = {n, budget_, resident_, spilled_live_, peak_, spilled_blocks_, shared_refs_,
+                              shared_size_, shared_spilled_ ? 1ull : 0ull};
+    const size_t at = out.size();
+    out.resize(at + sizeof head + n * 8 + n);
+    std::memcpy(out.data() + at, head, sizeof head);
+    std::memcpy(out.data() + at + sizeof head, size_.data(), n * 8);
+    std::memcpy(out.data() + at + sizeof head + n * 8, flags_.data(), n);
+}
+
+void StoreModel::deserialize(const uint8_t* p, uint64_t nbytes) {
+    uint64_t head[9];
+    if (nbytes < sizeof head) raise(BMQ_ERR_STORE, "checkpoint: truncated store accounting");
+    std::memcpy(head, p, sizeof head);
+    const uint64_t n = head[0];
+    if (n != size_.size() || nbytes != sizeof head + n * 9) raise(BMQ_ERR_STORE, "checkpoint: store accounting does not match the layout");
+    budget_ = head[1];
+    resident_ = head[2];
+    spilled_live_ = head[3];
+    peak_ = head[4];
+    spilled_blocks_ = head[5];
+    shared_refs_ = head[6];
+    shared_size_ = head[7];
+    shared_spilled_ = head[8] != 0;
+    std::memcpy(size_.data(), p + sizeof head, n * 8);
+    std::memcpy(flags_.data(), p + sizeof head + n * 8, n);
 }
 
 // ---------------------------------------------------------------- kernels
@@ -1454,4 +1485,116 @@ void Engine::partial_sums(double* out3) {
         for (int k = 0; k < 3; ++k) out3[k] += h[3 * id + k];
 }
 
+// ------------------------------------------------------- checkpoint / resume
+// File: "BMQCKPT1" | u32 n, b, version, pad | f64 b_r | u64 fnv(gates),
+// fnv(plan), next_stage, stage_compress_calls, stage_decompress_calls,
+// store-accounting bytes A, payload bytes P | accounting[A] |
+// meta[4 * 2^c] (size, sumsq, sum_re, sum_im as bits) | payloads[P] packed
+// 16-byte aligned in id order (bmq_simulator_export layout).
+namespace {
+constexpr char kCkptMagic[8] = {'B', 'M', 'Q', 'C', 'K', 'P', 'T', '1'};
+uint64_t fnv1a(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+    const uint8_t* p = static_cast<const uint8_t*>(data);
+    for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
+    return h;
+}
+struct PinnedBuf {
+    void* p = nullptr;
+    explicit PinnedBuf(uint64_t n) { BMQ_CUDA(cudaMallocHost(&p, std::max<uint64_t>(n, 16))); }
+    ~PinnedBuf() { cudaFreeHost(p); }
+};
+struct File {
+    FILE* f;
+    File(const char* path, const char* mode) : f(std::fopen(path, mode)) {
+        if (!f) raise(BMQ_ERR_STORE, std::string("checkpoint: cannot open ") + path);
+    }
+    ~File() { if (f) std::fclose(f); }
+    void write(const void* p, size_t n) {
+        if (n && std::fwrite(p, 1, n, f) != n) raise(BMQ_ERR_STORE, "checkpoint: write failed");
+    }
+    void read(void* p, size_t n) {
+        if (n && std::fread(p, 1, n, f) != n) raise(BMQ_ERR_STORE, "checkpoint: truncated file");
+    }
+};
+}  // namespace
+
+void Engine::save_checkpoint(const char* path) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    ensure_init();
+    if (sharded()) raise(BMQ_ERR_ENGINE, "checkpoint: save each rank's payloads through export instead");
+    if (!cfg_.compress) raise(BMQ_ERR_INVALID_ARGUMENT, "checkpoint requires compression");
+    const uint64_t nid = L_.num_blocks();
+    std::vector<uint64_t> ids(nid), meta(4 * nid);
+    for (uint64_t i = 0; i < nid; ++i) ids[i] = i;
+    export_payloads(ids.data(), nid, meta.data(), nullptr, 0);  // sizes and sums first
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < nid; ++i) total += (meta[4 * i] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+    PinnedBuf buf(total);
+    export_payloads(ids.data(), nid, meta.data(), buf.p, std::max<uint64_t>(total, 16));
+    std::vector<uint8_t> acct;
+    store_.serialize(acct);
+    const uint32_t head32[4] = {L_.n, L_.b, 1u, 0u};
+    const double br = cfg_.error_bound;
+    const uint64_t head64[7] = {fnv1a(gates_.data(), gates_.size() * sizeof(bmq_gate)),
+                                fnv1a(plan_.data(), plan_.size() * sizeof(bmq_stage)),
+                                next_stage_, stage_compress_calls_, stage_decompress_calls_, acct.size(), total};
+    File f(path, "wb");
+    f.write(kCkptMagic, 8);
+    f.write(head32, sizeof head32);
+    f.write(&br, 8);
+    f.write(head64, sizeof head64);
+    f.write(acct.data(), acct.size());
+    f.write(meta.data(), meta.size() * 8);
+    f.write(buf.p, total);
+}
+
+uint64_t Engine::load_checkpoint(const char* path) {
+    BMQ_CUDA(cudaSetDevice(dev_));
+    if (sharded()) raise(BMQ_ERR_ENGINE, "checkpoint: load each rank's payloads through import instead");
+    if (!cfg_.compress) raise(BMQ_ERR_INVALID_ARGUMENT, "checkpoint requires compression");
+    File f(path, "rb");
+    char magic[8];
+    f.read(magic, 8);
+    if (std::memcmp(magic, kCkptMagic, 8)) raise(BMQ_ERR_STORE, "checkpoint: not a checkpoint file");
+    uint32_t head32[4];
+    double br;
+    uint64_t head64[7];
+    f.read(head32, sizeof head32);
+    f.read(&br, 8);
+    f.read(head64, sizeof head64);
+    if (head32[2] != 1u) raise(BMQ_ERR_STORE, "checkpoint: unsupported version");
+    if (head32[0] != L_.n || head32[1] != L_.b || br != cfg_.error_bound)
+        raise(BMQ_ERR_STORE, "checkpoint: qubits, block bits or error bound differ from this simulator");
+    if (head64[0] != fnv1a(gates_.data(), gates_.size() * sizeof(bmq_gate)) ||
+        head64[1] != fnv1a(plan_.data(), plan_.size() * sizeof(bmq_stage)))
+        raise(BMQ_ERR_STORE, "checkpoint: circuit or stage plan differs from this simulator");
+    const uint64_t next = head64[2];
+    if (next > plan_.size()) raise(BMQ_ERR_STORE, "checkpoint: stage cursor out of range");
+    const uint64_t nid = L_.num_blocks();
+    std::vector<uint8_t> acct(head64[5]);
+    f.read(acct.data(), acct.size());
+    std::vector<uint64_t> ids(nid), meta(4 * nid);
+    f.read(meta.data(), meta.size() * 8);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < nid; ++i) {
+        ids[i] = i;
+        total += (meta[4 * i] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+    }
+    if (total != head64[6]) raise(BMQ_ERR_STORE, "checkpoint: payload index does not match the payload bytes");
+    PinnedBuf buf(total);
+    f.read(buf.p, total);
+    // fresh arena: the previous payloads are dropped, then every id imported
+    reset();
+    init_state();
+    StoreModel model = store_;
+    model.deserialize(acct.data(), acct.size());
+    import_payloads(ids.data(), nid, meta.data(), buf.p);
+    store_ = model;
+    next_stage_ = next;
+    stage_compress_calls_ = head64[3];
+    stage_decompress_calls_ = head64[4];
+    return next;
+}
+
 }  // namespace bmq
+

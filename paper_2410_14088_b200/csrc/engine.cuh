@@ -40,6 +40,9 @@ public:
     void put_shared(uint64_t first_id, uint64_t last_id, uint64_t size);  // ids [first, last)
     uint64_t peak() const { return peak_; }
     uint64_t spilled_blocks() const { return spilled_blocks_; }
+    // checkpoint image of the whole accounting state
+    void serialize(std::vector<uint8_t>& out) const;
+    void deserialize(const uint8_t* p, uint64_t n);
 
 private:
     void detach(uint64_t id);
@@ -92,6 +95,13 @@ public:
     void account_stage(uint64_t s, const uint64_t* sizes);
     void partial_sums(double* out3);
     void report(bmq_report* rep, double device_ms);
+
+    // Checkpoint / resume: every payload with its sums, the
+    // store accounting and the stage cursor, in one file. load_checkpoint
+    // needs an engine of the same circuit, layout, plan and bound and returns
+    // the next stage to run.
+    void save_checkpoint(const char* path);
+    uint64_t load_checkpoint(const char* path);
 
     const Layout& layout() const { return L_; }
     const std::vector<bmq_stage>& plan() const { return plan_; }

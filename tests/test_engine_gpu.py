@@ -415,3 +415,40 @@ def test_support_tracking_matches_full_sweeps(gpu):
         assert r.returncode == 0, r.stderr
         outs.append(r.stdout)
     assert outs[0] == outs[1] and outs[0].count("\n") == 3
+
+
+@pytest.mark.parametrize("name,n,b,cut", [("qft", 18, 12, 7), ("qaoa", 16, 12, 5)])
+def test_checkpoint_resume_is_exact(gpu, tmp_path, name, n, b, cut):
+    """save() after `cut` stages, load() into a fresh simulator, run the rest:
+    payloads, max_footprint and norm equal the uninterrupted run."""
+    c = gpu.generate_benchmark(name, n, gpu.BenchmarkParams(layers=2)) if name == "qaoa" \
+        else gpu.generate_benchmark(name, n)
+    cfg = gpu.Config(block_bits=b, inner_size=2, error_bound=1e-3)
+    with gpu.Simulator(c, cfg) as full:
+        rep_full = full.run()
+        want = full.payloads()
+        nstages = len(full.plan().stages)
+    path = str(tmp_path / "state.bmqckpt")
+    with gpu.Simulator(c, cfg) as a:
+        a.run_stages(0, cut)
+        a.save(path)
+    with gpu.Simulator(c, cfg) as b2:
+        assert b2.load(path) == cut
+        b2.run_stages(cut, nstages)
+        rep = b2.report()
+        assert b2.payloads() == want
+        assert rep.max_footprint_bytes == rep_full.max_footprint_bytes
+        assert rep.stage_compress_calls == rep_full.stage_compress_calls
+        assert rep.final_norm == pytest.approx(rep_full.final_norm, rel=1e-12)
+    # a simulator of another bound, or a damaged file, is refused
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=2, error_bound=1e-4)) as other:
+        with pytest.raises(Exception, match="checkpoint"):
+            other.load(path)
+    with open(path, "rb") as f:
+        data = f.read()
+    bad = str(tmp_path / "short.bmqckpt")
+    with open(bad, "wb") as f:
+        f.write(data[: len(data) // 2])
+    with gpu.Simulator(c, cfg) as other:
+        with pytest.raises(Exception, match="checkpoint"):
+            other.load(bad)
