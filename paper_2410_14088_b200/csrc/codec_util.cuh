@@ -85,21 +85,6 @@ __device__ __forceinline__ uint32_t quantize_pack(double v, const DevTables& t, 
     return pack_code(static_cast<uint32_t>(q - t.qlo), v < 0.0, false);
 }
 
-// The estimate of quantize_pack in registers: x ~ log2|v| / b_a from the bit
-// pattern (finite, nonzero), see quantize_estimate_x.
-__device__ __forceinline__ double quant_estimate_bits(uint64_t bits, const DevTables& t) {
-    const uint32_t ex = static_cast<uint32_t>(bits >> 52);
-    uint64_t man = bits & 0xfffffffffffffull;
-    int e2 = static_cast<int>(ex) - 1023;
-    if (ex == 0) {  // subnormal: normalise the mantissa
-        const int shift = __clzll(static_cast<long long>(man)) - 11;
-        man = (man << shift) & 0xfffffffffffffull;
-        e2 = -1022 - shift;
-    }
-    const float m = __int_as_float(0x3f800000 | static_cast<int>(man >> 29));  // mantissa truncated to float
-    return (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
-}
-
 // quantize_pack with every step in registers: a scalar whose estimate x
 // lies farther than est_eps from a half-integer (inside the table window)
 // takes round(x) directly; the others (about 2 est_eps of them) probe both
@@ -108,16 +93,18 @@ __device__ __forceinline__ double quant_estimate_bits(uint64_t bits, const DevTa
 __device__ __forceinline__ uint32_t quantize_pack_fast(double v, const DevTables& t, double qlo_d, int span,
                                                        bool& bad, bool& oow) {
     const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
-    if (bits == 0) return 1u;  // +-0
-    if (bits >= 0x7ff0000000000000ull) {
-        bad = true;
+    if (bits - 1 >= 0x7fefffffffffffffull) {  // +-0 (wraps), inf or NaN
+        if (bits) bad = true;
         return 1u;
     }
-    const double x = quant_estimate_bits(bits, t);
+    // normal numbers here; a subnormal (ex == 0) is settled by the exact search
+    const uint32_t ex = static_cast<uint32_t>(bits >> 52);
+    const float m = __int_as_float(0x3f800000 | static_cast<int>((bits >> 29) & 0x7fffffu));  // (see quantize_estimate_x)
+    const double x = (static_cast<double>(static_cast<int>(ex) - 1023) + static_cast<double>(__log2f(m))) * t.inv_ba;
     const double r = rint(x);
     const int i = __double2int_rz(r - qlo_d);  // exact (integers below 2^53); saturates
     uint32_t qoff = static_cast<uint32_t>(min(max(i, 0), span));
-    if (!(0.5 - fabs(x - r) > t.est_eps && static_cast<unsigned>(i) <= static_cast<unsigned>(span))) {
+    if (!(ex != 0 && 0.5 - fabs(x - r) > t.est_eps && static_cast<unsigned>(i) <= static_cast<unsigned>(span))) {
         const uint64_t lo = __ldg(t.thresh + qoff), hi = __ldg(t.thresh + qoff + 1);
         if (!(bits >= lo && bits < hi)) qoff = static_cast<uint32_t>(quantize(v, t, oow) - t.qlo);
     }
