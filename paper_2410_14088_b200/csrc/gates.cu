@@ -349,6 +349,12 @@ void build_mono(GateProgram& prog) {
         pp->tile = mp.tile;
         pp->base = mp.base;
         pp->npat_bits = static_cast<uint32_t>(pat.size());
+        for (uint32_t b = 0, k = 0; b < 64; ++b) {  // buffer bits of tile positions 2..6 and 10..11
+            if (!((p.tile_mask >> b) & 1)) continue;
+            if (k >= 2 && k <= 6) pp->lane_bits |= 1ull << b;
+            if (k >= 10) pp->group_bits |= 1ull << b;
+            ++k;
+        }
         for (size_t i = 0; i < pat.size(); ++i) pp->pat_bits[i] = pat[i];
         const size_t off = tabs.size();
         for (uint32_t P = 0; P < (1u << pat.size()); ++P) {
@@ -1461,6 +1467,21 @@ struct CodeAcc4 {
         }
         *this = CodeAcc4{};
     }
+    // all 32 lanes call with the same key
+    __device__ __forceinline__ void flush_uniform(ChunkPlan* cps, uint64_t key) {
+        const uint32_t a = __reduce_min_sync(0xffffffffu, mn), b = __reduce_max_sync(0xffffffffu, mx);
+        const uint32_t n = __reduce_add_sync(0xffffffffu, nnz), g = __reduce_add_sync(0xffffffffu, nneg);
+        if ((threadIdx.x & 31) == 0) {
+            ChunkPlan* cp = cps + key;
+            if (n) {
+                atomicMax(&cp->qmin_inv, kQOffMax - (a >> 2));
+                atomicMax(&cp->qmax_off, b >> 2);
+                atomicAdd(&cp->nnz, n);
+            }
+            if (g) atomicAdd(&cp->nneg, g);
+        }
+        *this = CodeAcc4{};
+    }
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1524,6 +1545,7 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
         };
         uint64_t tile = blockIdx.x;
         if (tile < ntiles) issue(tile, tile_w);
+        CodeAcc4 acc;  // last pass: counters of the real halves (see PermPass::chunk_mode)
         for (uint32_t k = 0; tile < ntiles; tile += gridDim.x, ++k) {
             const uint32_t* cur = tile_w + ((k & 1u) << kMaxTileBits);
             if (tile + gridDim.x < ntiles)
@@ -1553,12 +1575,14 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
                 const uint64_t addr = pb + toffp[g];
                 __stcs(reinterpret_cast<uint4*>(pk + addr), xo);
                 if (kLast) {
-                    CodeAcc4 ar;
-                    ar.add(xo.x);
-                    ar.add(xo.y);
-                    ar.add(xo.z);
-                    ar.add(xo.w);
-                    ar.flush(cps, addr >> kshift);
+                    acc.add(xo.x);
+                    acc.add(xo.y);
+                    acc.add(xo.z);
+                    acc.add(xo.w);
+                    if (pass.chunk_mode == 0)
+                        acc.flush(cps, addr >> kshift);
+                    else if (pass.chunk_mode == 1 || g == kPermGroups - 1)
+                        acc.flush_uniform(cps, addr >> kshift);
                 }
             }
             __syncthreads();  // this buffer is refilled two tiles on
@@ -1650,11 +1674,14 @@ void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, ui
         if (p.pp && lb >= 4) {  // 16-byte groups of four code words stay inside a block half
             const uint64_t g2 = std::min<uint64_t>(tiles, 148ull * 4 * 16);
             const uint8_t* zf = pi == 0 ? zflag : nullptr;
+            PermPass pp = *p.pp;
+            pp.chunk_mode = 0;
+            if (lb >= 12 && !(pp.lane_bits >> 12)) pp.chunk_mode = (pp.group_bits >> 12) ? 1u : 2u;
             if (last)
-                k_perm_pass<true><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, quant.cps,
+                k_perm_pass<true><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, pp, quant.cps,
                                                                                      zf, quant.nch, imnz);
             else
-                k_perm_pass<false><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, *p.pp, nullptr,
+                k_perm_pass<false><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, pp, nullptr,
                                                                                       zf, quant.nch, imnz);
         } else {
             k_code_pass<<<static_cast<uint32_t>(grid), kFastThreads, 0, st>>>(pk, lb, tiles, *p.mp,

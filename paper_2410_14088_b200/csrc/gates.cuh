@@ -108,6 +108,12 @@ struct PermPass {
     BitRuns tile, base;
     uint32_t npat_bits;
     uint32_t reim_swap;             // some entry swaps re / im (an odd unit)
+    // buffer bits of tile positions 2..6 (a warp's lanes) and 10..11 (a
+    // thread's four groups): below bit 12 (and lb >= 12) the chunk of a
+    // lane's words is warp-uniform / also group-uniform, so the last pass's
+    // counters reduce without matching (run_mono_program sets chunk_mode)
+    uint64_t lane_bits, group_bits;
+    uint32_t chunk_mode;            // 0: match lanes by chunk, 1: warp-uniform, 2: tile-uniform per warp
     uint8_t pat_bits[kMaxPatBits];  // buffer bits outside the tile, pattern bit i
     const uint16_t* table;          // [1 << npat_bits][4096] (device)
 };
