@@ -1146,26 +1146,37 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             const bool dense = __popc(S2) >= 11;
             const uint32_t npairs = dense ? 2048u : (1u << (__popc(S2) - 1)), pm = S2 & ~(1u << piv);
             S = S2 | 0x80000000u;
-            for (uint32_t r = tid; r < npairs; r += kFastThreads) {
-                const uint32_t x0 = dense ? insert0(r, piv) : deposit12(r, pm), x1 = x0 ^ dv;
-                const bool sw = (__popc(g.mrow & x0) ^ ct) & 1u;
-                const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
-                {
+            // (op fields are read into registers once: tile_s stores could alias sops)
+            const uint32_t mrow = g.mrow;
+            if (g.pad) {  // all entries real: u*a = (u*ar, u*ai) exactly
+                const double u00 = g.m[0], u01 = g.m[2], u10 = g.m[4], u11 = g.m[6];
+                for (uint32_t r = tid; r < npairs; r += kFastThreads) {
+                    const uint32_t x0 = dense ? insert0(r, piv) : deposit12(r, pm), x1 = x0 ^ dv;
+                    const bool sw = (__popc(mrow & x0) ^ ct) & 1u;
+                    const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
                     const double2 v0 = tile_s[i0], v1 = tile_s[i1];
                     // a pair of exact zeros maps to zeros (+-0 for the codec)
                     if (v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) continue;
-                    if (g.pad) {  // all entries real: u*a = (u*ar, u*ai) exactly
-                        const double u00 = g.m[0], u01 = g.m[2], u10 = g.m[4], u11 = g.m[6];
-                        tile_s[i0] = make_double2(__dadd_rn(__dmul_rn(u00, v0.x), __dmul_rn(u01, v1.x)),
-                                                  __dadd_rn(__dmul_rn(u00, v0.y), __dmul_rn(u01, v1.y)));
-                        tile_s[i1] = make_double2(__dadd_rn(__dmul_rn(u10, v0.x), __dmul_rn(u11, v1.x)),
-                                                  __dadd_rn(__dmul_rn(u10, v0.y), __dmul_rn(u11, v1.y)));
-                    } else {
-                        const C2 a0{v0.x, v0.y}, a1{v1.x, v1.y};
-                        const C2 o0 = row2(g.et, g.m, 0, a0, a1), o1 = row2(g.et, g.m, 1, a0, a1);
-                        tile_s[i0] = make_double2(o0.re, o0.im);
-                        tile_s[i1] = make_double2(o1.re, o1.im);
-                    }
+                    tile_s[i0] = make_double2(__dadd_rn(__dmul_rn(u00, v0.x), __dmul_rn(u01, v1.x)),
+                                              __dadd_rn(__dmul_rn(u00, v0.y), __dmul_rn(u01, v1.y)));
+                    tile_s[i1] = make_double2(__dadd_rn(__dmul_rn(u10, v0.x), __dmul_rn(u11, v1.x)),
+                                              __dadd_rn(__dmul_rn(u10, v0.y), __dmul_rn(u11, v1.y)));
+                }
+            } else {
+                uint8_t et[4];
+                double m[8];
+                memcpy(et, g.et, sizeof et);
+                memcpy(m, g.m, sizeof m);
+                for (uint32_t r = tid; r < npairs; r += kFastThreads) {
+                    const uint32_t x0 = dense ? insert0(r, piv) : deposit12(r, pm), x1 = x0 ^ dv;
+                    const bool sw = (__popc(mrow & x0) ^ ct) & 1u;
+                    const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
+                    const double2 v0 = tile_s[i0], v1 = tile_s[i1];
+                    if (v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) continue;
+                    const C2 a0{v0.x, v0.y}, a1{v1.x, v1.y};
+                    const C2 o0 = row2(et, m, 0, a0, a1), o1 = row2(et, m, 1, a0, a1);
+                    tile_s[i0] = make_double2(o0.re, o0.im);
+                    tile_s[i1] = make_double2(o1.re, o1.im);
                 }
             }
         }
