@@ -356,8 +356,10 @@ constexpr int kStageWords = (kChunk * 30 + 31) / 32 + 2;  // codes are < 2^30 (k
 // The scalar part of emit for one chunk (kFull: all 4096 scalars valid).
 struct EmitSmem {
     uint32_t sign[kWordsPerChunk], zero[kWordsPerChunk], pre[kWordsPerChunk], bits[kWordsPerChunk];
-    uint32_t stage[kStageWords];
-    uint32_t cw[kChunk];  // nonzero codes of word k at cw[32 k + rank in word]
+    union {                      // cw is read into registers before stage is zeroed and packed
+        uint32_t cw[kChunk];     // nonzero codes of word k at cw[32 k + rank in word]
+        uint32_t stage[kStageWords];
+    };
 };
 
 template <bool kFull, bool kW1>
@@ -392,7 +394,6 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
                          kChunk, tid, kChunkThreads);
         return;
     }
-    for (uint32_t i = tid; i < nstage; i += kChunkThreads) sm.stage[i] = 0;
     // A: all loads in flight; B: ballots -> bitmap words, width-1 code words,
     // or (wider codes) the nonzero codes compacted per word into sm.cw
     {
@@ -435,8 +436,19 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
     }
     __syncthreads();
     // C: each warp packs its words' codes LSB-first into the stage (shared
-    // OR: a code spans at most two stage words, edge words are shared)
-#pragma unroll 1
+    // OR: a code spans at most two stage words, edge words are shared). The
+    // stage overlays cw: every warp first takes its codes into registers.
+    uint32_t cv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t k = 4 * j + w;
+        const uint32_t cnt = __popc(~sm.zero[k] & (kFull ? ~0u : word_mask(len, k)));
+        cv[j] = lane < cnt ? sm.cw[32 * k + lane] : 0u;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < nstage; i += kChunkThreads) sm.stage[i] = 0;
+    __syncthreads();
+#pragma unroll
     for (int j = 0; j < 32; ++j) {
         const uint32_t k = 4 * j + w;
         const uint32_t nzw = ~sm.zero[k] & (kFull ? ~0u : word_mask(len, k));
@@ -452,15 +464,12 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
             }
             continue;
         }
-        // scatter: the word's code of rank r (in lane r of sm.cw) goes to bits
+        // scatter: the word's code of rank r (lane r) goes to bits
         // [a0 + r w, a0 + (r + 1) w) of the stage, touching at most two words
-        if (lane < cnt) {
-            const uint32_t cv = sm.cw[32 * k + lane];
+        if (lane < cnt && cv[j]) {
             const uint32_t pbit = a0 + lane * w_bits, wi = pbit >> 5, sh = pbit & 31;
-            if (cv) {
-                atomicOr(&sm.stage[wi], cv << sh);
-                if (sh + w_bits > 32) atomicOr(&sm.stage[wi + 1], cv >> (32 - sh));
-            }
+            atomicOr(&sm.stage[wi], cv[j] << sh);
+            if (sh + w_bits > 32) atomicOr(&sm.stage[wi + 1], cv[j] >> (32 - sh));
         }
     }
     __syncthreads();
@@ -472,7 +481,7 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
                      tid, kChunkThreads);
 }
 
-__global__ void __launch_bounds__(kChunkThreads, 6) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
+__global__ void __launch_bounds__(kChunkThreads, 8) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
                                                             const ChunkPlan* __restrict__ cps,
                                                             BlockPlan* __restrict__ bps, uint8_t* __restrict__ out,
                                                             DevTables t, const DevError* err) {
