@@ -481,7 +481,7 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
                      tid, kChunkThreads);
 }
 
-__global__ void __launch_bounds__(kChunkThreads, 8) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
+__global__ void __launch_bounds__(kChunkThreads, 9) k_cmp_emit(const CmpBlock* __restrict__ blks, uint32_t nch_max,
                                                             const ChunkPlan* __restrict__ cps,
                                                             BlockPlan* __restrict__ bps, uint8_t* __restrict__ out,
                                                             DevTables t, const DevError* err) {
