@@ -951,12 +951,13 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         {
             double re[kPer], im[kPer];
             uint32_t nzpos = 0;
+            const uint32_t fmask = __ballot_sync(0xffffffffu, fl != 0);  // bit 2j + c: group (row j, part c) stored
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const uint64_t a = pbt + pjoff[j];
                 if (wf_read) {  // 32-scalar groups flagged zero were not stored (warp-uniform test)
-                    re[j] = __shfl_sync(0xffffffffu, fl, 2 * j) ? buf[a] : 0.0;
-                    im[j] = __shfl_sync(0xffffffffu, fl, 2 * j + 1) ? buf[a + im_off] : 0.0;
+                    re[j] = ((fmask >> (2 * j)) & 1u) ? buf[a] : 0.0;
+                    im[j] = ((fmask >> (2 * j + 1)) & 1u) ? buf[a + im_off] : 0.0;
                     continue;
                 }
                 re[j] = buf[a];
