@@ -1144,7 +1144,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             const uint32_t dv = g.dvec, piv = __ffs(dv) - 1, ct = (cvec >> g.tp_hi) & 1u;
             if (S == 0) continue;  // zeros map to zeros
             const uint32_t S2 = (S | dv) & 0xfffu;
-            const bool dense = __popc(S2) >= 11;
+            const bool dense = __popc(S2) == 12;  // (11 support bits: 1024 pairs, none all-zero by construction)
             const uint32_t npairs = dense ? 2048u : (1u << (__popc(S2) - 1)), pm = S2 & ~(1u << piv);
             S = S2 | 0x80000000u;
             // (op fields are read into registers once: tile_s stores could alias sops)
