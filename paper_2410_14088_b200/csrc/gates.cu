@@ -1028,6 +1028,36 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 const uint32_t cvec_in = cvec;  // the map's affine part at the start of the run
                 for (uint32_t q = i; q < i2; ++q)
                     if (sops[q].type == OP_CX) cvec = cx_update(sops[q], cvec, base);
+                if (!run_chain && S != 0) {
+                    // a chain-free run is the identity on this tile when each op's
+                    // entry is 1 for every value its condition bits take on the
+                    // support (an in-tile logical bit is constant when its row of
+                    // M misses S; an outer bit is the tile base's)
+                    const uint32_t Sp = S & 0xfffu;
+                    bool act = false;
+                    uint32_t cv = cvec_in;
+                    const auto vals = [&](uint8_t in, uint16_t row, uint8_t tp, uint8_t b) -> uint32_t {
+                        if (!in) return ((xbase >> b) & 1) ? 2u : 1u;  // bit 0: can be 0, bit 1: can be 1
+                        if (row & Sp) return 3u;
+                        return ((cv >> tp) & 1u) ? 2u : 1u;
+                    };
+                    for (uint32_t q = i; q < i2 && !act; ++q) {
+                        const FastOp& o = sops[q];
+                        if (o.type == OP_CX) {
+                            cv = cx_update(o, cv, base);
+                            continue;
+                        }
+                        const uint32_t vh = vals(o.in_hi, o.mrow, o.tp_hi, o.hi);
+                        if (o.type == OP_DIAG)
+                            act = ((vh & 1u) && o.et[0] != ET_ONE) || ((vh & 2u) && o.et[1] != ET_ONE);
+                        else
+                            act = (vh & 2u) && (vals(o.in_lo, o.mrow2, o.tp_lo, o.lo) & 2u) && o.et[0] != ET_ONE;
+                    }
+                    if (!act) {
+                        i = i2;
+                        continue;
+                    }
+                }
                 if (!owners_only) __syncthreads();
                 owners_only = true;
                 if (S == 0) {  // an all-zero tile: nothing to do
