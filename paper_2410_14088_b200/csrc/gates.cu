@@ -1058,6 +1058,16 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                         continue;
                     }
                 }
+                if (run_chain && i2 == i + 1 && g.type == OP_CHAIN && S != 0) {
+                    // a lone chain with nothing to act on (see below): no sweep, no barrier
+                    uint32_t R;
+                    memcpy(&R, &g.m[0], 4);
+                    const uint32_t rs = (static_cast<uint32_t>(xbase) | lut_lo[S & 63u] | lut_hi[(S >> 6) & 63u]) & R;
+                    if (!(rs && (g.in_hi ? ((S >> g.tp_hi) & 1) : ((xbase >> g.hi) & 1)))) {
+                        i = i2;
+                        continue;
+                    }
+                }
                 if (!owners_only) __syncthreads();
                 owners_only = true;
                 if (S == 0) {  // an all-zero tile: nothing to do
