@@ -1586,27 +1586,31 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
         // Real halves only, double-buffered: the next tile's words stream
         // into SMEM (cp.async) while this tile is gathered and stored.
         uint32_t* tile_w = reinterpret_cast<uint32_t*>(tile_s);  // two 4096-word buffers
-        const auto issue = [&](uint64_t tile, uint32_t* dst) {
+        // The copies are issued unconditionally (an all-zero chunk the decoder
+        // left unwritten is read stale); its flag, loaded with the copies and
+        // used one tile later, has the thread overwrite its own slots with
+        // zero words once they have landed.
+        const auto issue = [&](uint64_t tile, uint32_t* dst) -> uint32_t {
             const uint64_t base = runs_deposit(tile, pass.base);
             const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
+            uint32_t zm = 0;
 #pragma unroll
             for (int g = 0; g < kPermGroups; ++g) {
                 const uint64_t addr = pb + toffp[g];
-                uint32_t* d = dst + 4u * tid + 1024u * g;
-                if (zf && zf[(addr >> (lb + 1)) * nch + ((addr & ((2ull << lb) - 1)) >> 12)])
-                    *reinterpret_cast<uint4*>(d) = make_uint4(1u, 1u, 1u, 1u);  // unwritten all-zero chunk
-                else
-                    cp_async16(d, pk + addr);
+                cp_async16(dst + 4u * tid + 1024u * g, pk + addr);
+                if (zf && zf[(addr >> (lb + 1)) * nch + ((addr & ((2ull << lb) - 1)) >> 12)]) zm |= 1u << g;
             }
             cp_async_commit();
+            return zm;
         };
         uint64_t tile = blockIdx.x;
-        if (tile < ntiles) issue(tile, tile_w);
+        uint32_t zcur = tile < ntiles ? issue(tile, tile_w) : 0u;
         CodeAcc4 acc;  // last pass: counters of the real halves (see PermPass::chunk_mode)
         for (uint32_t k = 0; tile < ntiles; tile += gridDim.x, ++k) {
-            const uint32_t* cur = tile_w + ((k & 1u) << kMaxTileBits);
+            uint32_t* cur = tile_w + ((k & 1u) << kMaxTileBits);
+            uint32_t znext = 0;
             if (tile + gridDim.x < ntiles)
-                issue(tile + gridDim.x, tile_w + (((k + 1) & 1u) << kMaxTileBits));
+                znext = issue(tile + gridDim.x, tile_w + (((k + 1) & 1u) << kMaxTileBits));
             else
                 cp_async_commit();  // (an empty group keeps the wait count uniform)
             const uint64_t base = runs_deposit(tile, pass.base);
@@ -1620,6 +1624,12 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
             for (int g = 0; g < kPermGroups; ++g)
                 ent[g] = __ldg(reinterpret_cast<const uint2*>(tab + 4u * tid + 1024u * g));
             cp_async_wait<1>();  // this tile's group has landed
+            if (zcur) {
+#pragma unroll
+                for (int g = 0; g < kPermGroups; ++g)
+                    if ((zcur >> g) & 1u) *reinterpret_cast<uint4*>(cur + 4u * tid + 1024u * g) = make_uint4(1u, 1u, 1u, 1u);
+            }
+            zcur = znext;
             __syncthreads();
 #pragma unroll
             for (int g = 0; g < kPermGroups; ++g) {
