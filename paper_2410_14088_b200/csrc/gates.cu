@@ -1590,8 +1590,7 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
         // left unwritten is read stale); its flag, loaded with the copies and
         // used one tile later, has the thread overwrite its own slots with
         // zero words once they have landed.
-        const auto issue = [&](uint64_t tile, uint32_t* dst) -> uint32_t {
-            const uint64_t base = runs_deposit(tile, pass.base);
+        const auto issue = [&](uint64_t base, uint32_t* dst) -> uint32_t {
             const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
             uint32_t zm = 0;
 #pragma unroll
@@ -1604,16 +1603,19 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
             return zm;
         };
         uint64_t tile = blockIdx.x;
-        uint32_t zcur = tile < ntiles ? issue(tile, tile_w) : 0u;
+        uint64_t base_next = tile < ntiles ? runs_deposit(tile, pass.base) : 0;
+        uint32_t zcur = tile < ntiles ? issue(base_next, tile_w) : 0u;
         CodeAcc4 acc;  // last pass: counters of the real halves (see PermPass::chunk_mode)
         for (uint32_t k = 0; tile < ntiles; tile += gridDim.x, ++k) {
             uint32_t* cur = tile_w + ((k & 1u) << kMaxTileBits);
+            const uint64_t base = base_next;
             uint32_t znext = 0;
-            if (tile + gridDim.x < ntiles)
-                znext = issue(tile + gridDim.x, tile_w + (((k + 1) & 1u) << kMaxTileBits));
-            else
+            if (tile + gridDim.x < ntiles) {
+                base_next = runs_deposit(tile + gridDim.x, pass.base);
+                znext = issue(base_next, tile_w + (((k + 1) & 1u) << kMaxTileBits));
+            } else {
                 cp_async_commit();  // (an empty group keeps the wait count uniform)
-            const uint64_t base = runs_deposit(tile, pass.base);
+            }
             const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
             uint32_t pat = 0;
             for (uint32_t i = 0; i < pass.npat_bits; ++i)
