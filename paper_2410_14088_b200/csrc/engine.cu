@@ -446,6 +446,15 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     BMQ_CUDA(cudaMemset(cursor_.p, 0, 4 * sizeof(uint64_t)));
     h_off_.assign(nid, ~0ull);
     h_size_.assign(nid, 0);
+    // pinned in place (the vectors are never resized): the per-stage metadata
+    // copies run at full PCIe speed instead of through pageable staging
+    if (cudaHostRegister(h_off_.data(), nid * sizeof(uint64_t), cudaHostRegisterDefault) == cudaSuccess)
+        meta_pinned_ = true;
+    if (meta_pinned_ && cudaHostRegister(h_size_.data(), nid * sizeof(uint64_t), cudaHostRegisterDefault) != cudaSuccess) {
+        cudaHostUnregister(h_off_.data());
+        meta_pinned_ = false;
+    }
+    cudaGetLastError();  // (registration is an optimisation; a failure is not an error)
     if (raw) {
         dense_.alloc(nid * blk_scalars);
         work_scalars_ = 0;
@@ -520,6 +529,10 @@ Engine::~Engine() {
     if (ev1_) cudaEventDestroy(ev1_);
     for (cudaEvent_t e : phase_ev_) cudaEventDestroy(e);
     if (host_pool_) cudaFreeHost(host_pool_);
+    if (meta_pinned_) {
+        cudaHostUnregister(h_off_.data());
+        cudaHostUnregister(h_size_.data());
+    }
 }
 
 uint32_t Engine::peek_error() {
@@ -851,6 +864,8 @@ void Engine::run_stage(uint64_t s) {
         o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
     }
     const uint64_t nwork = work_ids.size();
+    uint64_t rd = 0;  // payload bytes this stage reads (sizes before it runs)
+    for (uint64_t id : work_ids) rd += h_off_[id] == ~0ull ? 0 : h_size_[id];
     size_t nbatches = 0;
     if (nwork) {
         BMQ_CUDA(cudaMemcpyAsync(ids_.p, work_ids.data(), nwork * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
@@ -862,19 +877,14 @@ void Engine::run_stage(uint64_t s) {
             process_batch(sp, ids_.p + first, blockwise ? vtab_.p + first : nullptr, nblk, nbatches);
         }
     }
-    const std::vector<uint64_t> old_size = h_size_;
-    const std::vector<uint64_t> old_off = h_off_;
     check_device_error(("stage " + std::to_string(s) + ": ").c_str());
     sync_meta_to_host();
     collect_phase_times(nbatches);
     // accounting replay in the reference put order (groups ascending); a
     // sharded run replays the gathered global sizes in account_stage()
     if (!sharded()) account_stage(s, h_size_.data());
-    uint64_t rd = 0, wr = 0;
-    for (uint64_t id : work_ids) {
-        rd += old_off[id] == ~0ull ? 0 : old_size[id];
-        wr += h_off_[id] == ~0ull ? 0 : h_size_[id];
-    }
+    uint64_t wr = 0;
+    for (uint64_t id : work_ids) wr += h_off_[id] == ~0ull ? 0 : h_size_[id];
     // implementation bytes per phase: FP64 stages move 16 B per amplitude
     // (8 B of packed codes out of the last pass), code-domain stages 8 B
     const bool codes = !blockwise && sp.prog.mono && identity_ok_ && (cfg_.flags & BMQ_FLAG_CODE_DOMAIN);

@@ -189,6 +189,7 @@ private:
 
     // host mirrors
     std::vector<uint64_t> h_off_, h_size_;
+    bool meta_pinned_ = false;  // h_off_ / h_size_ registered with cudaHostRegister
     StoreModel store_;
     uint64_t stage_compress_calls_ = 0, stage_decompress_calls_ = 0;
     bmq_report counters_{};
