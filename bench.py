@@ -161,52 +161,93 @@ def max_over_ranks(dist, value):
     return float(t.item())
 
 
-def reference_sample_groups(ref, gl, plan, b, groups):
-    """A dense stage of the QFT-34 plan: the first bit-reversal swap stage
-    (CX triples), whose input blocks are the uniform real QFT|0> state."""
+def qft_stage_sample(ref, w):
+    """Stratified sample of the QFT|0> run for the reference CPU pipeline.
+
+    Before stage s the QFT|0> state is exactly |+> on the qubits whose H gate
+    precedes the stage and |0> on the rest (make_qft, benchmarks.hpp:97-114:
+    every CP's control j < i is still |0> when it is applied), so per stage the
+    number of groups holding a nonzero block is 2^(#H'd outer qubits) and the
+    rest are ALL_ZERO groups, which the reference processes too (it has no
+    zero skipping: engine.hpp:109-120). The sample takes, per stage, one
+    nonzero group (outer value 0, its blocks built from that state) and, when
+    the stage has any, one ALL_ZERO group; each group runs the reference
+    pipeline with the stage's real gates. Returns (plan, samples, counts)."""
     import numpy as np
-    first_cx = next(i for i, g in enumerate(gl) if g[0] == 12)
-    s = next(k for k, st in enumerate(plan) if st[0] <= first_cx < st[1])
-    stage = plan[s]
-    ids = ref.enumerate_groups(34, b, stage)[:groups]
-    blk = np.zeros(2 << b)
-    blk[: 1 << b] = 2.0 ** -17
-    payload = ref.compress_block(blk, WORKLOAD["error_bound"])
-    return s, stage, ids, [payload] * ids.size
+    n, b = w["n"], w["b"]
+    gl = ref.generate_benchmark("qft", n)
+    plan = ref.partition(n, gl, b, w["inner"])
+    h_at = {g[1]: i for i, g in enumerate(gl) if g[0] == 0}  # GateKind::H
+    cache = {}
+
+    def payload(hset, nonzero):
+        key = (frozenset(q for q in hset if q < b), nonzero)
+        if key not in cache:
+            blk = np.zeros(2 << b)
+            if nonzero:
+                lmask = sum(1 << q for q in range(b) if q not in hset)
+                loc = np.arange(1 << b, dtype=np.int64)
+                blk[: 1 << b][(loc & lmask) == 0] = 2.0 ** (-len(hset) / 2)
+            cache[key] = ref.compress_block(blk, w["error_bound"])
+        return cache[key]
+
+    samples, counts = [], []
+    for s, (gb, ge, inner) in enumerate(plan):
+        hset = {q for q, i in h_at.items() if i < gb}
+        outer = [q for q in range(b, n) if q not in inner]
+        groups = ref.enumerate_groups(n, b, (gb, ge, inner))
+        nz = 1 << sum(1 for q in outer if q in hset)
+        zero = groups.shape[0] - nz
+        gmask = sum(1 << (q - b) for q in range(b, n) if q not in hset)
+        ids = groups[0]
+        samples.append((s, ids, [payload(hset, (int(g) & gmask) == 0) for g in ids]))
+        counts.append(nz)
+        if zero:
+            j = next(k for k, q in enumerate(outer) if q not in hset)  # an outer |0> qubit set to 1
+            samples.append((s, groups[1 << j], [payload(hset, False)] * groups.shape[1]))
+            counts.append(zero)
+    return gl, plan, samples, counts
+
+
+def reference_qft_rate(ref, w, gl, plan, samples, counts, cores):
+    """One pass of the stratified sample on `cores` threads; the full-run time
+    is the measured per-group times weighted by each stage's group counts,
+    divided over the threads (perfect scaling assumed: favourable to the CPU)."""
+    gms, wall = ref.stage_groups(w["n"], gl, plan, w["b"], w["error_bound"], cores, samples)
+    full_s = float(sum(c * t for c, t in zip(counts, gms))) / 1e3 / cores
+    return (1 << w["n"]) * len(plan) / full_s, full_s, wall
 
 
 def run_reference(args):
     """--impl reference: the reference CPU pipeline (oracle/_ref, unmodified
-    headers) on bounded samples of the same workload, all host threads."""
+    headers) on a stratified sample of the same workload, all host threads."""
     world, rank, local, dist = dist_setup()
     if rank != 0:
         return 0
     from oracle import oracle
     ref = oracle.ref()
     w = WORKLOAD
-    gl = ref.generate_benchmark(w["name"], w["n"])
-    plan = ref.partition(w["n"], gl, w["b"], w["inner"])
     cores = os.cpu_count() or 1
-    groups = max(cores, 2 * cores)
-    s, stage, ids, pays = reference_sample_groups(ref, gl, plan, w["b"], groups)
-    amps = ids.size << w["b"]
-    rates = []
+    gl, plan, samples, counts = qft_stage_sample(ref, w)
+    rates, walls, fulls = [], [], []
     for step in range(args.warmup + args.steps):
-        ms, _ = ref.group_pipeline(w["n"], gl, stage, w["b"], w["error_bound"], cores, ids, pays)
+        rate, full_s, wall = reference_qft_rate(ref, w, gl, plan, samples, counts, cores)
         if step >= args.warmup:
-            rates.append(amps / (ms / 1e3))
+            rates.append(rate)
+            walls.append(wall)
+            fulls.append(full_s)
     value = statistics.median(rates)
-    total = (1 << w["n"]) * len(plan)
-    sample = (f"{ids.shape[0]} groups x {ids.shape[1]} blocks of stage {s} (first bit-reversal swap stage, "
-              f"dense uniform input) of QFT-34 b=20 inner=2 per step, through the reference per-group pipeline "
-              f"(engine.hpp:203-225) with parallel_for on {cores} threads")
+    sample = (f"{len(samples)} groups per step (x{1 << w['inner']} blocks of 2^{w['b']} amps): one nonzero and one "
+              f"ALL_ZERO group of each of the {len(plan)} stages of {workload_tag(w)}, with QFT|0>'s exact input "
+              f"state, through the reference per-group pipeline (engine.hpp:203-225) on {cores} threads; full-run "
+              f"time = per-group times x the stage's group counts / threads (extrapolated)")
     line = {
-        "impl": "reference", "metric": "amp-stages/s (QFT-34, b=20, inner=2, b_r=1e-3)", "value": value,
+        "impl": "reference", "metric": metric_name(w), "value": value,
         "unit": "amp-stages/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ids.size * (1 << w["b"]) / value * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (QFT|0> circuit; sampled dense stage)",
-        "config": {"workload": "qft34_b20_i2_br1e-3", "stages": len(plan), "sample_groups": int(ids.shape[0])},
-        "extrapolated_full_run_s": total / value,
+        "ms_per_step": statistics.median(walls), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (QFT|0> circuit; stratified per-stage sample)",
+        "config": {"workload": workload_tag(w), "stages": len(plan), "sample_groups": len(samples)},
+        "extrapolated_full_run_s": statistics.median(fulls),
         "cpu_baseline": {"value": value, "unit": "amp-stages/s", "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "amp-stages/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -215,20 +256,33 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline(seconds_hint=20.0):
+def cpu_baseline(full_runs=True):
+    """The reference CPU path on this host: the stratified QFT-34 sample
+    (extrapolated, labelled) plus complete Simulator::run calls of smaller
+    QFT configurations (measured, engine.hpp:97-134)."""
     from oracle import oracle
     ref = oracle.ref()
     w = WORKLOAD
-    gl = ref.generate_benchmark(w["name"], w["n"])
-    plan = ref.partition(w["n"], gl, w["b"], w["inner"])
     cores = os.cpu_count() or 1
-    s, stage, ids, pays = reference_sample_groups(ref, gl, plan, w["b"], 2 * cores)
-    ms, _ = ref.group_pipeline(w["n"], gl, stage, w["b"], w["error_bound"], cores, ids, pays)
-    value = ids.size * (1 << w["b"]) / (ms / 1e3)
-    return {"value": value, "unit": "amp-stages/s", "cores": cores, "kind": "reference",
-            "sample": f"{ids.shape[0]} groups (x{ids.shape[1]} blocks of 2^20 amps) of QFT-34 b=20 inner=2 "
-                      f"stage {s} through the unmodified reference pipeline, {ms / 1e3:.1f} s on {cores} threads",
-            "extrapolated_full_run_s": (1 << w["n"]) * len(plan) / value}
+    gl, plan, samples, counts = qft_stage_sample(ref, w)
+    rate, full_s, wall = reference_qft_rate(ref, w, gl, plan, samples, counts, cores)
+    out = {"value": rate, "unit": "amp-stages/s", "cores": cores, "kind": "reference",
+           "sample": f"{len(samples)} groups (one nonzero + one ALL_ZERO group per stage of {workload_tag(w)}) "
+                     f"through the unmodified reference pipeline in {wall / 1e3:.1f} s on {cores} threads; "
+                     f"full run extrapolated from per-stage group counts",
+           "extrapolated_full_run_s": full_s}
+    if full_runs:
+        runs = []
+        for n, b in ((20, 14), (24, 20)):
+            g = ref.generate_benchmark("qft", n)
+            res = ref.simulate(n, g, b, w["inner"], w["error_bound"], workers=cores, want_payloads=False)
+            r = res.report
+            runs.append({"workload": f"qft{n}_b{b}_i{w['inner']}", "wall_s": r["wall_ms"] / 1e3,
+                         "stages": r["stage_count"],
+                         "amp_stages_per_s": (1 << n) * r["stage_count"] / (r["wall_ms"] / 1e3),
+                         "measured": "complete Simulator::run (init + stages + final state_norm)"})
+        out["full_runs"] = runs
+    return out
 
 
 def measure_e2e(cbq, circ, cfg, amp_stages, args, dist, world):
@@ -277,15 +331,48 @@ def measure_e2e(cbq, circ, cfg, amp_stages, args, dist, world):
             "d2h_bytes_per_step": d2h, "seconds": t_e2e}
 
 
-def phase_roofline(d, t_dev):
-    """Dominant device phase: algorithmic bytes / CUDA-event time."""
+def measure_link():
+    """Pinned host <-> device copy bandwidth (GB/s) of this GPU: 1 GiB each way,
+    CUDA events on the copy stream, best of 3 (north_star's BW_link)."""
+    import torch
+    n = 1 << 30
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    dev = torch.empty(n, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, dst, src in (("h2d", dev, host), ("d2h", host, dev)):
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        out[name + "_gbs"] = best
+    del host, dev
+    torch.cuda.empty_cache()
+    return out
+
+
+def roofline(d, t_dev, link):
+    """t_roof = max(B_HBM / BW_HBM, B_link / BW_link) with B_HBM the
+    model bytes (reference-exact payload bytes of every block of every group
+    holding a nonzero block, read + written, plus 32 B per amplitude of those
+    groups) and B_link the host-tier payload bytes; frac = t_roof / t_sim.
+    Beside it, each device phase's own bytes over its CUDA-event time and the
+    dominant kernel's ncu DRAM traffic (profiles/traffic.json)."""
     peak, peak_kind = load_peaks()
+    t = t_dev / 1e3
+    b_hbm = d["model_bytes"]
+    b_link = d["link_h2d_bytes"] + d["link_d2h_bytes"]
+    bw_link = min(link["h2d_gbs"], link["d2h_gbs"]) if link else None
+    t_hbm = b_hbm / (peak * 1e9)
+    t_link = b_link / (bw_link * 1e9) if (bw_link and b_link) else 0.0
+    bound = "hbm" if t_hbm >= t_link else "link"
     phases = {"decompress": (d["decompress_ms"], d["decompress_bytes"]),
               "gate": (d["gate_ms"], d["gate_bytes"]),
               "compress": (d["compress_ms"], d["compress_bytes"])}
     dom = max(phases, key=lambda k: phases[k][0])
-    ms, nbytes = phases[dom]
-    achieved = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -294,14 +381,18 @@ def phase_roofline(d, t_dev):
                 traffic = json.load(f).get(dom)
         except Exception:
             traffic = None
-    model_bytes = d["payload_bytes_read"] + d["payload_bytes_written"] + d["dense_bytes"]
-    return {"bound": "hbm", "kernel": f"{dom} phase", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_source": peak_kind, "traffic": traffic,
-            "stage_loop": {"model_bytes": model_bytes,
-                           "achieved_gbs": model_bytes / (t_dev / 1e3) / 1e9,
-                           "frac": model_bytes / (t_dev / 1e3) / 1e9 / peak},
-            "phase_ms": {k: v[0] for k, v in phases.items()},
-            "phase_bytes": {k: v[1] for k, v in phases.items()}}
+    achieved = (b_hbm if bound == "hbm" else b_link) / t / 1e9
+    ref_bw = peak if bound == "hbm" else bw_link
+    return {"bound": bound, "kernel": "stage loop (SURVEY 8(d) model bytes / device-timed simulation)",
+            "achieved": achieved, "peak": ref_bw, "unit": "GB/s", "frac": max(t_hbm, t_link) / t,
+            "peak_source": peak_kind if bound == "hbm" else "measured pinned copy (bench.py measure_link)",
+            "traffic": traffic, "model_bytes": b_hbm, "model_groups": d["model_groups"],
+            "link": dict(link or {}, bytes=b_link, h2d_bytes=d["link_h2d_bytes"], d2h_bytes=d["link_d2h_bytes"],
+                         copy_ms=d["link_ms"]),
+            "phases": {k: {"ms": v[0], "bytes": v[1], "gbs": v[1] / (v[0] / 1e3) / 1e9 if v[0] > 0 else None,
+                           "frac": v[1] / (v[0] / 1e3) / 1e9 / peak if v[0] > 0 else None}
+                       for k, v in phases.items()},
+            "dominant_phase": dom}
 
 
 def main_sharded(args, world, rank, local, dist):
@@ -382,7 +473,7 @@ def main_sharded(args, world, rank, local, dist):
         "gpu_launches": int(rep.device["kernel_launches"]),
         "groups_processed": rep.device["groups_processed"], "groups_skipped": rep.device["groups_skipped"],
         "remaps": ssim.remaps, "exchange_ms_rank0": ssim.exchange_ms, "account_ms_rank0": ssim.account_ms,
-        "roofline": dict(phase_roofline(local_rep.device, t_dev), scope="rank 0"),
+        "roofline": dict(roofline(local_rep.device, t_dev, None), scope="rank 0"),
         "clocks": clocks.summary(), "e2e": e2e,
     }
     dist.barrier()
@@ -390,6 +481,59 @@ def main_sharded(args, world, rank, local, dist):
     if rank == 0:
         print(json.dumps(line))
     return 0
+
+
+def e2e_once(args):
+    """--e2e-once (internal): ONE create -> run -> get_payloads -> destroy through
+    the C ABI in a fresh process, timed from before create (CUDA context,
+    codec-table build and allocation included): a one-shot caller's cost."""
+    import ctypes as C
+    import numpy as np
+    from paper_2410_14088_b200 import _lib, cbq
+    w = WORKLOAD
+    circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
+    cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"])
+    gates = circ.c_array()
+    ccfg = cfg.to_c()
+    lib = _lib.lib
+    t0 = time.perf_counter()
+    h = C.c_void_p()
+    cbq._check(lib.bmq_simulator_create(circ.num_qubits, gates, len(gates), C.byref(ccfg), C.byref(h)))
+    rep = _lib.bmq_report()
+    cbq._check(lib.bmq_simulator_run(h, C.byref(rep), None, 0))
+    sizes = np.zeros(1 << (circ.num_qubits - cfg.block_bits), dtype=np.uint64)
+    total = C.c_uint64()
+    cbq._check(lib.bmq_simulator_get_payloads(h, None, 0, sizes.ctypes.data, C.byref(total)))
+    out = np.empty(max(1, total.value), dtype=np.uint8)
+    cbq._check(lib.bmq_simulator_get_payloads(h, out.ctypes.data, total.value, sizes.ctypes.data, C.byref(total)))
+    lib.bmq_simulator_destroy(h)
+    print(json.dumps({"seconds": time.perf_counter() - t0, "payload_bytes": int(total.value)}))
+    return 0
+
+
+def cold_first_call(args):
+    cmd = [sys.executable, os.path.abspath(__file__), "--e2e-once", "--workload", WORKLOAD["name"],
+           "--qubits", str(WORKLOAD["n"]), "--block-bits", str(WORKLOAD["b"]), "--inner-size",
+           str(WORKLOAD["inner"]), "--error-bound", repr(WORKLOAD["error_bound"]), "--layers",
+           str(WORKLOAD["layers"])]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0")))
+        return json.loads(r.stdout.strip().splitlines()[-1])["seconds"]
+    except Exception:
+        return None
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec the same
+    command as N ranks (one per GPU) on this node."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -411,7 +555,15 @@ def main():
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: N independent full simulations instead of one sharded simulation")
     ap.add_argument("--sharded", action="store_true", help="use the sharded driver even at N=1")
+    ap.add_argument("--no-link", action="store_true", help="skip the pinned host-link bandwidth measurement")
+    ap.add_argument("--e2e-once", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        return relaunch_under_torchrun(args)
+    if env_world is not None and int(env_world) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={env_world}"}))
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     WORKLOAD.update(name=args.workload, n=args.qubits, b=args.block_bits, inner=args.inner_size)
@@ -423,6 +575,8 @@ def main():
         WORKLOAD["layers"] = 40
     if args.error_bound is not None:
         WORKLOAD["error_bound"] = args.error_bound
+    if args.e2e_once:
+        return e2e_once(args)
     if args.workload != "qft":
         args.no_cpu_baseline = True  # the sampled CPU baseline is defined on the QFT plan
     world, rank, local, dist = dist_setup()
@@ -460,7 +614,13 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(cbq, circ, cfg, amp_stages, args, dist, world)
-    roofline = phase_roofline(rep.device, t_dev)
+        if rank == 0:
+            cold = cold_first_call(args)
+            e2e["cold_first_call_s"] = cold
+            e2e["cold_first_call_note"] = ("one create->run->get_payloads->destroy in a fresh process, timed from "
+                                           "before create: CUDA context, codec tables, allocation included")
+    link = measure_link() if not args.no_link else None
+    roof = roofline(rep.device, t_dev, link)
     line = {
         "metric": metric_name(w), "value": value, "unit": "amp-stages/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev,
@@ -475,7 +635,8 @@ def main():
         "fidelity": fidelity, "final_norm": rep.final_norm,
         "gpu_launches": int(rep.device["kernel_launches"]),
         "groups_processed": rep.device["groups_processed"], "groups_skipped": rep.device["groups_skipped"],
-        "roofline": roofline, "clocks": clocks.summary(), "e2e": e2e,
+        "device_peak_bytes": int(rep.device["device_peak_bytes"]),
+        "roofline": roof, "clocks": clocks.summary(), "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -155,6 +155,15 @@ typedef struct bmq_report {
     uint64_t pool_growths;          /* automatic payload arenas doubled after a compaction */
     uint64_t lazy_cx;               /* CX gates folded into a pass's index map (per batch) */
     uint64_t perm_materialisations; /* index maps materialised before a phase chain (per batch) */
+    /* SURVEY 8(d) roofline numerator: for every group with at least one
+     * non-ALL_ZERO input block, the reference-exact payload bytes of ALL its
+     * blocks read and written (identity-skipped blocks included, ALL_ZERO
+     * blocks as their 26-byte header) plus 32 B per amplitude of the group */
+    uint64_t model_bytes;
+    uint64_t model_groups;          /* the groups model_bytes counts */
+    uint64_t link_h2d_bytes;        /* host-tier payload bytes moved host -> device */
+    uint64_t link_d2h_bytes;        /* host-tier payload bytes moved device -> host */
+    double link_ms;                 /* CUDA-event time of the host-tier copies (copy streams) */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only
@@ -238,6 +247,10 @@ int bmq_apply_stage(double* amps, uint64_t namps, uint32_t num_qubits, const bmq
 int bmq_dense_reference(uint32_t num_qubits, const bmq_gate* gates, uint64_t ngates,
                         double* state, uint32_t verify_cap_qubits);
 
+/* fidelity (engine.hpp:299-308): |sum_i conj(a_i) b_i| of two interleaved
+ * complex host states of namps amplitudes, reduced on the device. */
+int bmq_fidelity(const double* a, const double* b, uint64_t namps, double* fidelity);
+
 /* ------------------------------------------------------------ simulator
  * cbq::Simulator (engine.hpp:58-250). */
 
@@ -314,6 +327,10 @@ int bmq_simulator_stage_sizes(bmq_simulator* sim, uint64_t stage, uint64_t* size
 int bmq_simulator_account_stage(bmq_simulator* sim, uint64_t stage, const uint64_t* sizes);
 /* {sum |a|^2, sum re, sum im} over the blocks this rank holds. */
 int bmq_simulator_partial_sums(bmq_simulator* sim, double* sums3);
+/* store().footprint() (store.hpp:30-35): the replayed BlockStore accounting
+ * of the reference's sequential put order. Any pointer may be NULL. */
+int bmq_simulator_footprint(bmq_simulator* sim, uint64_t* resident_bytes, uint64_t* spilled_live_bytes,
+                            uint64_t* peak_bytes);
 /* Report of the stages run so far (final_norm, wall_ms, device_ms = 0). */
 int bmq_simulator_report(bmq_simulator* sim, bmq_report* report);
 

@@ -11,14 +11,17 @@
 
 #include <algorithm>
 #include <array>
+#include <bit>
 #include <complex>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -47,6 +50,19 @@ class DeviceError : public std::runtime_error {  // CUDA / no device (new)
 public:
     using std::runtime_error::runtime_error;
 };
+class QasmError : public std::runtime_error {  // qasm.hpp:17-31
+public:
+    QasmError(int line, int col, const std::string& msg)
+        : std::runtime_error("line " + std::to_string(line) + ", col " + std::to_string(col) + ": " + msg),
+          line_(line),
+          col_(col) {}
+    int line() const { return line_; }
+    int col() const { return col_; }
+
+private:
+    int line_;
+    int col_;
+};
 
 namespace detail {
 [[noreturn]] inline void rethrow(int rc) {
@@ -57,6 +73,12 @@ namespace detail {
     case BMQ_ERR_CODEC: throw CodecError(msg);
     case BMQ_ERR_STORE: throw StoreError(msg);
     case BMQ_ERR_ENGINE: throw EngineError(msg);
+    case BMQ_ERR_QASM: {  // "line L, col C: what" (qasm.hpp:20-22)
+        int line = 0, col = 0, used = 0;
+        if (std::sscanf(msg.c_str(), "line %d, col %d: %n", &line, &col, &used) == 2 && used > 0)
+            throw QasmError(line, col, msg.substr(static_cast<std::size_t>(used)));
+        throw QasmError(0, 0, msg);
+    }
     default: throw DeviceError(msg);
     }
 }
@@ -140,6 +162,46 @@ inline Circuit generate_benchmark(Benchmark b, std::uint32_t n, const BenchmarkP
     return c;
 }
 
+// -------------------------------------------------------------------- qasm
+// parse_qasm (qasm.hpp:387-389): OPENQASM 2.0 subset; warnings (ignored
+// measure) are appended to *warnings. Errors throw QasmError(line, col).
+inline Circuit parse_qasm(std::string_view text, std::vector<std::string>* warnings = nullptr) {
+    const std::string t(text);
+    std::uint32_t n = 0;
+    std::uint64_t count = 0, nw = 0;
+    int rc = bmq_parse_qasm(t.c_str(), &n, nullptr, 0, &count, nullptr, 0, &nw);
+    if (rc != BMQ_OK && rc != BMQ_ERR_BUFFER_TOO_SMALL) detail::rethrow(rc);
+    std::vector<bmq_gate> v(std::max<std::uint64_t>(count, 1));
+    std::string w(4096 + 256 * nw, '\0');
+    detail::check(bmq_parse_qasm(t.c_str(), &n, v.data(), v.size(), &count, w.data(), w.size(), &nw));
+    Circuit c(n);
+    for (std::uint64_t i = 0; i < count; ++i)
+        c.gates.push_back(Gate{static_cast<GateKind>(v[i].kind), v[i].q0, v[i].q1, v[i].angle});
+    if (warnings && nw) {
+        w.resize(std::strlen(w.c_str()));
+        std::size_t pos = 0;
+        for (std::uint64_t k = 0; k < nw; ++k) {
+            const std::size_t e = w.find('\n', pos);
+            warnings->push_back(w.substr(pos, e == std::string::npos ? std::string::npos : e - pos));
+            if (e == std::string::npos) break;
+            pos = e + 1;
+        }
+    }
+    return c;
+}
+
+// emit_qasm (qasm.hpp:392-411): parse_qasm(emit_qasm(c)) == c.
+inline std::string emit_qasm(const Circuit& circuit) {
+    const auto g = circuit.c_gates();
+    std::uint64_t size = 0;
+    int rc = bmq_emit_qasm(circuit.num_qubits, g.data(), g.size(), nullptr, 0, &size);
+    if (rc != BMQ_OK && rc != BMQ_ERR_BUFFER_TOO_SMALL) detail::rethrow(rc);
+    std::string out(size + 1, '\0');
+    detail::check(bmq_emit_qasm(circuit.num_qubits, g.data(), g.size(), out.data(), out.size(), &size));
+    out.resize(size);
+    return out;
+}
+
 // --------------------------------------------------------------- partition
 struct Layout {  // partition.hpp:14-21
     std::uint32_t n = 1, b = 1, c = 0;
@@ -210,6 +272,77 @@ inline std::uint32_t buffer_bit_of_qubit(const Stage& stage, const Layout& layou
     return bit;
 }
 
+// ------------------------------------------------------------------ kernel
+// kernel.hpp:14-122. Gate application runs on the B200 (bmq_apply_gate /
+// bmq_apply_stage copy the caller's buffer to the device and back) with the
+// reference's arithmetic, so results are bit-identical to the CPU kernels.
+using SVBlock = std::vector<Complex>;
+
+struct GroupBuffer {  // kernel.hpp:16-19
+    SVGroup group;
+    std::vector<Complex> amps;
+};
+
+inline void apply_unitary2(std::span<Complex> amps, std::uint32_t bit, const Mat2& u) {  // kernel.hpp:24-38
+    double m[8];
+    for (int i = 0; i < 4; ++i) {
+        m[2 * i] = u[i].real();
+        m[2 * i + 1] = u[i].imag();
+    }
+    detail::check(bmq_apply_gate(reinterpret_cast<double*>(amps.data()), amps.size(), m, 0, bit, 0));
+}
+
+inline void apply_unitary4(std::span<Complex> amps, std::uint32_t hi_bit, std::uint32_t lo_bit,
+                           const Mat4& u) {  // kernel.hpp:42-64
+    double m[32];
+    for (int i = 0; i < 16; ++i) {
+        m[2 * i] = u[i].real();
+        m[2 * i + 1] = u[i].imag();
+    }
+    detail::check(bmq_apply_gate(reinterpret_cast<double*>(amps.data()), amps.size(), m, 1, hi_bit, lo_bit));
+}
+
+inline GroupBuffer assemble_group_buffer(SVGroup group, const std::vector<SVBlock>& blocks) {  // kernel.hpp:66-84
+    if (blocks.empty() || !std::has_single_bit(blocks.size()))
+        throw std::invalid_argument("group block count must be a nonzero power of two");
+    if (blocks.size() != group.block_ids.size()) throw std::invalid_argument("block list does not match the group");
+    const std::size_t block_size = blocks.front().size();
+    GroupBuffer buf;
+    buf.amps.reserve(block_size * blocks.size());
+    for (const SVBlock& blk : blocks) {
+        if (blk.size() != block_size) throw std::invalid_argument("group blocks must have equal length");
+        buf.amps.insert(buf.amps.end(), blk.begin(), blk.end());
+    }
+    buf.group = std::move(group);
+    return buf;
+}
+
+inline std::vector<SVBlock> split_buffer(const GroupBuffer& buf, std::uint32_t block_bits) {  // kernel.hpp:87-98
+    const std::uint64_t block_size = 1ull << block_bits;
+    if (buf.amps.size() % block_size != 0)
+        throw std::invalid_argument("buffer length not divisible by the block size");
+    std::vector<SVBlock> blocks;
+    blocks.reserve(buf.amps.size() / block_size);
+    for (std::size_t off = 0; off < buf.amps.size(); off += block_size)
+        blocks.emplace_back(buf.amps.begin() + static_cast<std::ptrdiff_t>(off),
+                            buf.amps.begin() + static_cast<std::ptrdiff_t>(off + block_size));
+    return blocks;
+}
+
+inline void apply_gate(GroupBuffer& buf, const Mat2& u, std::uint32_t bit) { apply_unitary2(buf.amps, bit, u); }
+inline void apply_gate(GroupBuffer& buf, const Mat4& u, std::uint32_t hi_bit, std::uint32_t lo_bit) {
+    apply_unitary4(buf.amps, hi_bit, lo_bit, u);
+}
+
+// apply_stage (kernel.hpp:111-122): the stage's gates in program order, outer
+// operands refused with the reference's logic_error.
+inline void apply_stage(GroupBuffer& buf, const Stage& stage, const Circuit& circuit, const Layout& layout) {
+    const auto g = circuit.c_gates();
+    const bmq_stage s = stage.c();
+    detail::check(bmq_apply_stage(reinterpret_cast<double*>(buf.amps.data()), buf.amps.size(), circuit.num_qubits,
+                                  g.data(), g.size(), &s, layout.b));
+}
+
 // ------------------------------------------------------------------- codec
 struct ErrorBound {  // codec.hpp:19-29
     double relative;
@@ -248,7 +381,38 @@ struct Config {  // engine.hpp:23-37 (+ device knobs)
     bool compress = true;
     std::uint32_t verify_cap_qubits = 24;
     int device = 0;
+    // device-side knobs (bmq_config)
     bool identity_skip = false;
+    bool zero_group_skip = true;
+    bool code_domain = true;
+    bool pool_grow = false;
+    std::uint64_t device_pool_bytes = 0;  // 0 = automatic
+    std::uint64_t work_bytes = 0;         // 0 = automatic
+    std::uint64_t host_pool_bytes = 0;    // pinned host level of the store; 0 = none
+    bmq_config c() const {
+        bmq_config k;
+        bmq_config_default(&k);
+        k.block_bits = block_bits;
+        k.inner_size = inner_size;
+        k.error_bound = error_bound;
+        k.memory_budget = memory_budget;
+        k.workers = workers;
+        k.compress = compress ? 1u : 0u;
+        k.verify_cap_qubits = verify_cap_qubits;
+        k.device = device;
+        k.device_pool_bytes = device_pool_bytes;
+        k.work_bytes = work_bytes;
+        k.host_pool_bytes = host_pool_bytes;
+        k.flags = (zero_group_skip ? BMQ_FLAG_ZERO_GROUP_SKIP : 0u) | (identity_skip ? BMQ_FLAG_IDENTITY_SKIP : 0u) |
+                  (code_domain ? BMQ_FLAG_CODE_DOMAIN : 0u) | (pool_grow ? BMQ_FLAG_POOL_GROW : 0u);
+        return k;
+    }
+};
+
+struct Footprint {  // store.hpp:30-35
+    std::uint64_t resident_bytes = 0;
+    std::uint64_t spilled_live_bytes = 0;
+    std::uint64_t peak_bytes = 0;
 };
 
 struct SimulationReport {  // engine.hpp:39-53
@@ -265,18 +429,30 @@ struct SimulationReport {  // engine.hpp:39-53
 
 class Simulator {  // engine.hpp:58-250
 public:
+    // BlockStore view (store.hpp:47-300): exact payload bytes per id and the
+    // replayed footprint; the payloads themselves live in the device pool.
+    class StoreView {
+    public:
+        explicit StoreView(bmq_simulator* s) : s_(s) {}
+        std::vector<std::uint8_t> get(std::uint64_t id) const {
+            std::uint64_t size = 0;
+            detail::check(bmq_simulator_get_payload(s_, id, nullptr, 0, &size));
+            std::vector<std::uint8_t> out(size);
+            detail::check(bmq_simulator_get_payload(s_, id, out.data(), out.size(), &size));
+            return out;
+        }
+        Footprint footprint() const {
+            Footprint f;
+            detail::check(bmq_simulator_footprint(s_, &f.resident_bytes, &f.spilled_live_bytes, &f.peak_bytes));
+            return f;
+        }
+
+    private:
+        bmq_simulator* s_;
+    };
+
     Simulator(Circuit circuit, Config config) : circuit_(std::move(circuit)), config_(config) {
-        bmq_config c;
-        bmq_config_default(&c);
-        c.block_bits = config_.block_bits;
-        c.inner_size = config_.inner_size;
-        c.error_bound = config_.error_bound;
-        c.memory_budget = config_.memory_budget;
-        c.workers = config_.workers;
-        c.compress = config_.compress ? 1u : 0u;
-        c.verify_cap_qubits = config_.verify_cap_qubits;
-        c.device = config_.device;
-        if (config_.identity_skip) c.flags |= BMQ_FLAG_IDENTITY_SKIP;
+        const bmq_config c = config_.c();
         const auto g = circuit_.c_gates();
         detail::check(bmq_simulator_create(circuit_.num_qubits, g.data(), g.size(), &c, &sim_));
     }
@@ -349,6 +525,7 @@ public:
         return next;
     }
 
+    StoreView store() const { return StoreView(sim_); }
     Layout layout() const { return make_layout(circuit_.num_qubits, config_.block_bits); }
     PartitionPlan plan() const { return partition_circuit(circuit_, config_.block_bits, config_.inner_size); }
 
@@ -367,6 +544,15 @@ inline std::vector<Complex> dense_reference(const Circuit& c, std::uint32_t veri
     detail::check(bmq_dense_reference(c.num_qubits, g.data(), g.size(), reinterpret_cast<double*>(st.data()),
                                       verify_cap_qubits));
     return st;
+}
+
+// fidelity (engine.hpp:299-308): |<a|b>|, conjugate-linear in a.
+inline double fidelity(std::span<const Complex> a, std::span<const Complex> b) {
+    if (a.size() != b.size()) throw std::invalid_argument("fidelity requires equal-length states");
+    double f = 0.0;
+    detail::check(bmq_fidelity(reinterpret_cast<const double*>(a.data()), reinterpret_cast<const double*>(b.data()),
+                               a.size(), &f));
+    return f;
 }
 
 }  // namespace cbq

@@ -323,6 +323,31 @@ class Ref(_Lib):
             C.byref(wall), C.byref(outb)))
         return wall.value, outb.value
 
+    def stage_groups(self, n, gates, stages, block_bits, error_bound, workers, samples):
+        """Time the reference per-group pipeline on groups of several stages at
+        once. samples: list of (stage index, block ids of one group, payloads).
+        Returns (per-group thread ms, wall ms of the parallel region)."""
+        arr = gates_array(gates)
+        st = (Stage * len(stages))(*[stage_struct(*x) for x in stages])
+        gstage = np.array([s for s, _, _ in samples], dtype=np.uint64)
+        ids = np.concatenate([np.asarray(i, dtype=np.uint64).reshape(-1) for _, i, _ in samples])
+        first = np.zeros(len(samples), dtype=np.uint64)
+        first[1:] = np.cumsum([len(i) for _, i, _ in samples])[:-1]
+        pays = [p for _, _, ps in samples for p in ps]
+        sizes = np.array([len(p) for p in pays], dtype=np.uint64)
+        offs = np.zeros_like(sizes)
+        offs[1:] = np.cumsum(sizes)[:-1]
+        blob = b"".join(pays)
+        buf = (C.c_uint8 * max(1, len(blob))).from_buffer_copy(blob or b"\0")
+        gms = np.zeros(len(samples))
+        wall = C.c_double()
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self._f("stage_groups")(
+            C.c_uint32(n), arr, C.c_uint64(len(gates)), st, C.c_uint64(len(stages)), C.c_uint32(block_bits),
+            C.c_double(error_bound), C.c_uint32(workers), vp(gstage), vp(first), C.c_uint64(len(samples)),
+            vp(ids), buf, vp(offs), vp(sizes), vp(gms), C.byref(wall)))
+        return gms, wall.value
+
 
 _port = None
 _ref = None

@@ -440,4 +440,68 @@ int cbqref_group_pipeline(uint32_t n, const cbqref_gate* gates, uint64_t ngates,
     });
 }
 
+
+// Stratified CPU-baseline sample across a whole plan: group gi runs the
+// reference per-group pipeline (as cbqref_group_pipeline) for stage
+// stages[group_stage[gi]], on `workers` threads of the reference's own
+// parallel_for. group_ids / payloads are row-major over the sampled groups,
+// each group holding 2^|inner| ids of its own stage (offsets in id_first).
+// group_ms[gi] receives the thread time of group gi, *wall_ms the wall time
+// of the whole parallel region.
+int cbqref_stage_groups(uint32_t n, const cbqref_gate* gates, uint64_t ngates, const cbqref_stage* stages,
+                        uint64_t nstages, uint32_t block_bits, double error_bound, uint32_t workers,
+                        const uint64_t* group_stage, const uint64_t* id_first, uint64_t ngroups,
+                        const uint64_t* group_ids, const uint8_t* payloads, const uint64_t* pay_offsets,
+                        const uint64_t* pay_sizes, double* group_ms, double* wall_ms) {
+    return guarded([&] {
+        const cbq::Circuit c = to_circuit(n, gates, ngates);
+        const cbq::Layout layout = cbq::make_layout(n, block_bits);
+        const cbq::ErrorBound bound(error_bound);
+        std::vector<cbq::Stage> st(nstages);
+        for (uint64_t s = 0; s < nstages; ++s) st[s] = to_stage(stages[s]);
+        // one store per group: sampled groups of different stages may share ids
+        std::vector<cbq::BlockStore> stores(ngroups);
+        for (uint64_t g = 0; g < ngroups; ++g) {
+            const uint64_t per = 1ull << st[group_stage[g]].inner.size();
+            for (uint64_t v = 0; v < per; ++v) {
+                const uint64_t k = id_first[g] + v;
+                stores[g].put(group_ids[k], std::vector<uint8_t>(payloads + pay_offsets[k],
+                                                                 payloads + pay_offsets[k] + pay_sizes[k]));
+            }
+        }
+        const uint64_t bs = layout.block_size();
+        const auto t0 = std::chrono::steady_clock::now();
+        cbq::parallel_for(workers, ngroups, [&](std::size_t gi) {
+            const auto g0 = std::chrono::steady_clock::now();
+            const cbq::Stage& stage = st[group_stage[gi]];
+            const uint64_t per = 1ull << stage.inner.size();
+            cbq::BlockStore& store = stores[gi];
+            cbq::SVGroup grp;
+            grp.outer_value = gi;
+            std::vector<cbq::SVBlock> blocks;
+            for (uint64_t v = 0; v < per; ++v) {
+                const uint64_t id = group_ids[id_first[gi] + v];
+                grp.block_ids.push_back(id);
+                const auto scal = cbq::decompress_block(store.get(id));
+                cbq::SVBlock b(bs);
+                for (uint64_t i = 0; i < bs; ++i) b[i] = cbq::Complex(scal[i], scal[bs + i]);
+                blocks.push_back(std::move(b));
+            }
+            cbq::GroupBuffer buf = cbq::assemble_group_buffer(grp, blocks);
+            cbq::apply_stage(buf, stage, c, layout);
+            const auto out = cbq::split_buffer(buf, layout.b);
+            for (std::size_t j = 0; j < out.size(); ++j) {
+                std::vector<double> scal(2 * bs);
+                for (uint64_t i = 0; i < bs; ++i) {
+                    scal[i] = out[j][i].real();
+                    scal[bs + i] = out[j][i].imag();
+                }
+                store.put(grp.block_ids[j], cbq::compress_block(scal, bound));
+            }
+            group_ms[gi] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - g0).count();
+        });
+        *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
 }  // extern "C"

@@ -65,7 +65,9 @@ class bmq_report(C.Structure):
                 ("compress_bytes", C.c_uint64), ("fused_batches", C.c_uint64), ("compactions", C.c_uint64),
                 ("host_spill_bytes", C.c_uint64), ("host_spill_batches", C.c_uint64),
                 ("code_domain_batches", C.c_uint64), ("pool_growths", C.c_uint64),
-                ("lazy_cx", C.c_uint64), ("perm_materialisations", C.c_uint64)]
+                ("lazy_cx", C.c_uint64), ("perm_materialisations", C.c_uint64),
+                ("model_bytes", C.c_uint64), ("model_groups", C.c_uint64), ("link_h2d_bytes", C.c_uint64),
+                ("link_d2h_bytes", C.c_uint64), ("link_ms", C.c_double)]
 
 
 _P = C.c_void_p

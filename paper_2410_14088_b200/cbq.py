@@ -615,7 +615,8 @@ DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks
                       "device_peak_bytes", "gate_passes", "decompress_ms", "gate_ms", "compress_ms", "batches",
                       "decompress_bytes", "gate_bytes", "compress_bytes", "fused_batches", "compactions",
                       "host_spill_bytes", "host_spill_batches", "code_domain_batches", "pool_growths",
-                      "lazy_cx", "perm_materialisations")
+                      "lazy_cx", "perm_materialisations",
+                      "model_bytes", "model_groups", "link_h2d_bytes", "link_d2h_bytes", "link_ms")
 
 
 def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:

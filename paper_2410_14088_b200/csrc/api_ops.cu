@@ -27,6 +27,28 @@ uint32_t log2_exact(uint64_t n) {
 
 __global__ void k_set_one(double* p) { p[0] = 1.0; }
 
+// per-CTA partial sums of conj(a_i) * b_i over interleaved complex buffers
+__global__ void k_cdot(const double2* __restrict__ a, const double2* __restrict__ b, uint64_t n, double2* partial) {
+    double re = 0.0, im = 0.0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const double2 x = a[i], y = b[i];
+        re += x.x * y.x + x.y * y.y;
+        im += x.x * y.y - x.y * y.x;
+    }
+    __shared__ double s[2][256];
+    s[0][threadIdx.x] = re;
+    s[1][threadIdx.x] = im;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            s[0][threadIdx.x] += s[0][threadIdx.x + o];
+            s[1][threadIdx.x] += s[1][threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(s[0][0], s[1][0]);
+}
+
 }  // namespace
 
 void api_compress_blocks(const double* scalars, uint64_t nblocks, uint64_t n, double b_r, uint8_t* out,
@@ -229,6 +251,35 @@ void api_dense_reference(uint32_t n, const bmq_gate* gates, uint64_t ngates, dou
     run_program(st, prog, d.p, 0, true, 1, nullptr);
     BMQ_CUDA(cudaMemcpyAsync(state, d.p, 16 * N, cudaMemcpyDeviceToHost, st));
     BMQ_CUDA(cudaStreamSynchronize(st));
+}
+
+// fidelity (engine.hpp:299-308): |sum conj(a_i) b_i| of two host states,
+// reduced on the device (a different summation order than the reference's
+// left-to-right loop: equal within rounding).
+double api_fidelity(const double* a, const double* b, uint64_t namps) {
+    require_device();
+    if (namps == 0) return 0.0;
+    cudaStream_t st = cudaStreamPerThread;
+    DevArray<double> da, db;
+    da.alloc(2 * namps);
+    db.alloc(2 * namps);
+    BMQ_CUDA(cudaMemcpyAsync(da.p, a, 16 * namps, cudaMemcpyHostToDevice, st));
+    BMQ_CUDA(cudaMemcpyAsync(db.p, b, 16 * namps, cudaMemcpyHostToDevice, st));
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((namps + 255) / 256, 148 * 8));
+    DevArray<double2> part;
+    part.alloc(grid);
+    k_cdot<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(da.p), reinterpret_cast<const double2*>(db.p),
+                                 namps, part.p);
+    BMQ_CUDA(cudaGetLastError());
+    std::vector<double2> h(grid);
+    BMQ_CUDA(cudaMemcpyAsync(h.data(), part.p, grid * sizeof(double2), cudaMemcpyDeviceToHost, st));
+    BMQ_CUDA(cudaStreamSynchronize(st));
+    double re = 0.0, im = 0.0;
+    for (const double2& x : h) {
+        re += x.x;
+        im += x.y;
+    }
+    return std::hypot(re, im);
 }
 
 }  // namespace bmq

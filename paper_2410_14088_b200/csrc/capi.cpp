@@ -191,6 +191,25 @@ int bmq_dense_reference(uint32_t num_qubits, const bmq_gate* gates, uint64_t nga
     return guarded([&] { bmq::api_dense_reference(num_qubits, gates, ngates, state, verify_cap_qubits); });
 }
 
+int bmq_fidelity(const double* a, const double* b, uint64_t namps, double* fidelity) {
+    return guarded([&] {
+        null_check(fidelity, "fidelity");
+        if (namps) {
+            null_check(a, "state a");
+            null_check(b, "state b");
+        }
+        *fidelity = bmq::api_fidelity(a, b, namps);
+    });
+}
+
+int bmq_simulator_footprint(bmq_simulator* sim, uint64_t* resident_bytes, uint64_t* spilled_live_bytes,
+                            uint64_t* peak_bytes) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        sim->engine->footprint(resident_bytes, spilled_live_bytes, peak_bytes);
+    });
+}
+
 void bmq_config_default(bmq_config* cfg) {
     if (!cfg) return;
     std::memset(cfg, 0, sizeof *cfg);

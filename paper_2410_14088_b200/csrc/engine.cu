@@ -444,17 +444,10 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     red_.alloc(2 * 148 * 64);
     BMQ_CUDA(cudaMemset(err_.p, 0, sizeof(DevError)));
     BMQ_CUDA(cudaMemset(cursor_.p, 0, 4 * sizeof(uint64_t)));
+    // pinned host mirrors: the per-stage metadata copies run at full link
+    // speed instead of through pageable staging
     h_off_.assign(nid, ~0ull);
     h_size_.assign(nid, 0);
-    // pinned in place (the vectors are never resized): the per-stage metadata
-    // copies run at full PCIe speed instead of through pageable staging
-    if (cudaHostRegister(h_off_.data(), nid * sizeof(uint64_t), cudaHostRegisterDefault) == cudaSuccess)
-        meta_pinned_ = true;
-    if (meta_pinned_ && cudaHostRegister(h_size_.data(), nid * sizeof(uint64_t), cudaHostRegisterDefault) != cudaSuccess) {
-        cudaHostUnregister(h_off_.data());
-        meta_pinned_ = false;
-    }
-    cudaGetLastError();  // (registration is an optimisation; a failure is not an error)
     if (raw) {
         dense_.alloc(nid * blk_scalars);
         work_scalars_ = 0;
@@ -529,10 +522,6 @@ Engine::~Engine() {
     if (ev1_) cudaEventDestroy(ev1_);
     for (cudaEvent_t e : phase_ev_) cudaEventDestroy(e);
     if (host_pool_) cudaFreeHost(host_pool_);
-    if (meta_pinned_) {
-        cudaHostUnregister(h_off_.data());
-        cudaHostUnregister(h_size_.data());
-    }
 }
 
 uint32_t Engine::peek_error() {
@@ -724,6 +713,8 @@ void Engine::raw_run_stage(uint64_t s) {
     counters_.groups_processed += gg.groups();
     counters_.blocks_processed += L_.num_blocks();
     counters_.dense_bytes += 32ull << L_.n;
+    counters_.model_bytes += 32ull << L_.n;
+    counters_.model_groups += gg.groups();
     stage_compress_calls_ += L_.num_blocks();
     stage_decompress_calls_ += L_.num_blocks();
 }
@@ -834,6 +825,7 @@ void Engine::run_stage(uint64_t s) {
     // the blocks to process, in the reference's group order
     std::vector<uint64_t> work_ids;
     std::vector<uint32_t> work_v;
+    std::vector<uint64_t> model_ids;
     work_ids.reserve(nid);
     uint64_t o = 0, groups_done = 0, groups_owned = 0;
     for (uint64_t g = 0; g < ngroups; ++g) {
@@ -842,6 +834,12 @@ void Engine::run_stage(uint64_t s) {
             continue;
         }
         ++groups_owned;
+        {  // SURVEY 8(d) model: every block of a group with a non-ALL_ZERO input
+            bool nz = false;
+            for (uint64_t v = 0; v < per && !nz; ++v) nz = h_off_[o | inner[v]] != ~0ull;
+            if (nz)
+                for (uint64_t v = 0; v < per; ++v) model_ids.push_back(o | inner[v]);
+        }
         if (blockwise) {
             bool any = false;
             for (uint64_t v = 0; v < per; ++v) {
@@ -866,6 +864,8 @@ void Engine::run_stage(uint64_t s) {
     const uint64_t nwork = work_ids.size();
     uint64_t rd = 0;  // payload bytes this stage reads (sizes before it runs)
     for (uint64_t id : work_ids) rd += h_off_[id] == ~0ull ? 0 : h_size_[id];
+    uint64_t model_in = 0;
+    for (uint64_t id : model_ids) model_in += h_size_[id];
     size_t nbatches = 0;
     if (nwork) {
         BMQ_CUDA(cudaMemcpyAsync(ids_.p, work_ids.data(), nwork * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
@@ -885,6 +885,10 @@ void Engine::run_stage(uint64_t s) {
     if (!sharded()) account_stage(s, h_size_.data());
     uint64_t wr = 0;
     for (uint64_t id : work_ids) wr += h_off_[id] == ~0ull ? 0 : h_size_[id];
+    uint64_t model_out = 0;
+    for (uint64_t id : model_ids) model_out += h_size_[id];
+    counters_.model_bytes += model_in + model_out + model_ids.size() * (32ull << L_.b);
+    counters_.model_groups += model_ids.size() / per;
     // implementation bytes per phase: FP64 stages move 16 B per amplitude
     // (8 B of packed codes out of the last pass), code-domain stages 8 B
     const bool codes = !blockwise && sp.prog.mono && identity_ok_ && (cfg_.flags & BMQ_FLAG_CODE_DOMAIN);
@@ -978,6 +982,11 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.pool_growths = counters_.pool_growths;
     r.lazy_cx = counters_.lazy_cx;
     r.perm_materialisations = counters_.perm_materialisations;
+    r.model_bytes = counters_.model_bytes;
+    r.model_groups = counters_.model_groups;
+    r.link_h2d_bytes = counters_.link_h2d_bytes;
+    r.link_d2h_bytes = counters_.link_d2h_bytes;
+    r.link_ms = counters_.link_ms;
     *rep = r;
 }
 

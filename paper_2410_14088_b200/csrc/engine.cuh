@@ -30,6 +30,48 @@ struct DevArray {
     size_t bytes() const { return n * sizeof(T); }
 };
 
+// Page-locked host array (cudaMallocHost), owned RAII: the engine's host
+// mirrors of per-id metadata are copied every stage.
+template <class T>
+class PinnedVec {
+public:
+    PinnedVec() = default;
+    PinnedVec(const PinnedVec&) = delete;
+    PinnedVec& operator=(const PinnedVec&) = delete;
+    ~PinnedVec() { release(); }
+    void assign(size_t count, T value) {
+        if (count != n_) {
+            release();
+            if (count) {
+                void* q = nullptr;
+                if (cudaMallocHost(&q, count * sizeof(T)) != cudaSuccess) {
+                    cudaGetLastError();
+                    raise(BMQ_ERR_CUDA, "cudaMallocHost failed for host metadata");
+                }
+                p_ = static_cast<T*>(q);
+            }
+            n_ = count;
+        }
+        for (size_t i = 0; i < n_; ++i) p_[i] = value;
+    }
+    T* data() { return p_; }
+    const T* data() const { return p_; }
+    size_t size() const { return n_; }
+    T& operator[](size_t i) { return p_[i]; }
+    const T& operator[](size_t i) const { return p_[i]; }
+    T* begin() { return p_; }
+    T* end() { return p_ + n_; }
+
+private:
+    void release() {
+        if (p_) cudaFreeHost(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
 // Host replay of BlockStore's accounting (store.hpp:64-117,188-232) in the
 // reference's sequential put order, so max_footprint_bytes and
 // spilled_blocks match the reference run with one worker.
@@ -39,6 +81,8 @@ public:
     void put(uint64_t id, uint64_t size);
     void put_shared(uint64_t first_id, uint64_t last_id, uint64_t size);  // ids [first, last)
     uint64_t peak() const { return peak_; }
+    uint64_t resident() const { return resident_; }
+    uint64_t spilled_live() const { return spilled_live_; }
     uint64_t spilled_blocks() const { return spilled_blocks_; }
     // checkpoint image of the whole accounting state
     void serialize(std::vector<uint8_t>& out) const;
@@ -95,6 +139,12 @@ public:
     void account_stage(uint64_t s, const uint64_t* sizes);
     void partial_sums(double* out3);
     void report(bmq_report* rep, double device_ms);
+    // BlockStore::footprint() (store.hpp:30-35,138-142) of the replayed accounting
+    void footprint(uint64_t* resident, uint64_t* spilled_live, uint64_t* peak) const {
+        if (resident) *resident = store_.resident();
+        if (spilled_live) *spilled_live = store_.spilled_live();
+        if (peak) *peak = store_.peak();
+    }
 
     // Checkpoint / resume: every payload with its sums, the
     // store accounting and the stage cursor, in one file. load_checkpoint
@@ -188,8 +238,7 @@ private:
     DevArray<double> red_;
 
     // host mirrors
-    std::vector<uint64_t> h_off_, h_size_;
-    bool meta_pinned_ = false;  // h_off_ / h_size_ registered with cudaHostRegister
+    PinnedVec<uint64_t> h_off_, h_size_;
     StoreModel store_;
     uint64_t stage_compress_calls_ = 0, stage_decompress_calls_ = 0;
     bmq_report counters_{};

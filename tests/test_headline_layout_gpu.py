@@ -1,0 +1,96 @@
+"""Parity at the headline layout, b = 20 (2^20 amplitudes per block, 512
+4096-scalar chunks per block, 2^21 scalars per block slot), against runs of
+the UNMODIFIED reference (tests/golden/sim_golden_b20.json, made by
+tests/golden/make_golden_b20.py from oracle/_ref: Simulator::run,
+engine.hpp:97-134, workers = 1).
+
+Checked per case: final payloads byte-identical (FNV-1a-64 in id order plus
+the leading sizes), peak footprint replayed in put order, compression ratio,
+stage / call counts, norm (1e-10 relative) and fidelity against the dense
+FP64 reference within 1e-6 of the reference's (north_star).
+
+Also at full scale, where the oracle cannot follow: batches larger than 2^31
+and 2^32 scalars must give the same bytes as small batches (32-bit index
+paths in the decoder, gate passes, quantiser epilogue and emit)."""
+import ctypes as C
+import json
+import os
+
+import pytest
+
+from test_engine_gpu import FIDELITY_ATOL, NORM_RTOL, fnv
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sim_golden_b20.json")
+
+
+def cases():
+    with open(GOLDEN) as f:
+        return json.load(f)["simulations"]
+
+
+def circuit_of(gpu, case):
+    gates = [gpu.Gate(gpu.GateKind(k), a, b, float.fromhex(x)) for k, a, b, x in case["gates"]]
+    c = gpu.Circuit(case["n"], gates)
+    if case["name"] in ("qaoa3reg", "random"):  # the repo's generator must still produce the pinned gates
+        mine = gpu.generate_benchmark(case["name"], case["n"], gpu.BenchmarkParams(layers=case["layers"], seed=1))
+        assert mine == c
+    return c
+
+
+@pytest.mark.parametrize("case", cases(), ids=lambda c: f"{c['name']}{c['n']}-b{c['b']}-i{c['inner']}-{c['error_bound']}")
+@pytest.mark.parametrize("identity_skip", [True, False], ids=["skip", "noskip"])
+def test_b20_matches_reference(gpu, port, case, identity_skip):
+    c = circuit_of(gpu, case)
+    cfg = gpu.Config(block_bits=case["b"], inner_size=case["inner"], error_bound=case["error_bound"],
+                     identity_skip=identity_skip)
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run()
+        want = case["report"]
+        assert rep.stage_count == want["stage_count"]
+        pays = sim.payloads()
+        assert [len(p) for p in pays[:16]] == case["payload_sizes_head"]
+        assert sum(len(p) for p in pays) == case["payload_total"]
+        assert f"{fnv(port, pays):016x}" == case["payload_fnv"]
+        assert rep.max_footprint_bytes == want["max_footprint_bytes"]
+        assert rep.compression_ratio == want["compression_ratio"]
+        assert rep.spilled_blocks == want["spilled_blocks"]
+        assert rep.stage_compress_calls == want["stage_compress_calls"]
+        assert rep.stage_decompress_calls == want["stage_decompress_calls"]
+        assert rep.final_norm == pytest.approx(want["final_norm"], rel=NORM_RTOL)
+        if want.get("has_fidelity"):
+            f = sim.fidelity_dense(gpu.dense_reference(c))
+            assert abs(f - want["fidelity"]) <= FIDELITY_ATOL
+            assert f >= 0.99
+
+
+def run_fnv(gpu, port, circ, b, inner, br, work_bytes):
+    cfg = gpu.Config(block_bits=b, inner_size=inner, error_bound=br, work_bytes=work_bytes)
+    with gpu.Simulator(circ, cfg) as sim:
+        rep = sim.run()
+        pays = sim.payloads()
+        fid = sim.fidelity_analytic("uniform") if circ.gates and circ.gates[0].kind == 0 else None
+        return f"{fnv(port, pays):016x}", rep, fid
+
+
+@pytest.mark.parametrize("n,work_gib", [(32, 32), (33, 40)])
+def test_batches_beyond_2p31_scalars_are_exact(gpu, port, n, work_gib):
+    """QFT-n at (20, 2) with one huge batch (2^32 scalars and more, i.e. 32 GiB
+    of dense group buffers) against 4 GiB batches: identical payload bytes,
+    peak footprint and fidelity (>= 0.99, the analytic QFT|0> ideal)."""
+    circ = gpu.generate_benchmark("qft", n)
+    big = run_fnv(gpu, port, circ, 20, 2, 1e-3, work_gib << 30)
+    small = run_fnv(gpu, port, circ, 20, 2, 1e-3, 4 << 30)
+    assert big[1].device["batches"] < small[1].device["batches"]
+    assert big[0] == small[0]
+    assert big[1].max_footprint_bytes == small[1].max_footprint_bytes
+    assert big[2] == pytest.approx(small[2], abs=1e-12) and big[2] >= 0.99
+
+
+def test_dense_b20_large_batch_matches_small(gpu, port):
+    """Dense complex state (QAOA-3reg-28 p=2 at 1e-4, every group nonzero,
+    codes ~17 bits wide): a batch of 2^31 scalars vs 1 GiB batches."""
+    circ = gpu.generate_benchmark("qaoa3reg", 28, gpu.BenchmarkParams(layers=2, seed=1))
+    a = run_fnv(gpu, port, circ, 20, 2, 1e-4, 16 << 30)
+    b = run_fnv(gpu, port, circ, 20, 2, 1e-4, 1 << 30)
+    assert a[0] == b[0] and a[1].max_footprint_bytes == b[1].max_footprint_bytes
