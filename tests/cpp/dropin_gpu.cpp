@@ -6,7 +6,7 @@
 //     1e-4) -> report fields, FNV-1a-64 of store().get(id) over all ids,
 //     store().footprint(), fidelity(dense_reference, extract_state);
 //   * parse_qasm(emit_qasm(c)) == c, and a QasmError's line / col;
-//   * assemble_group_buffer -> apply_stage -> split_buffer on a 2-block group
+//   * assemble_group_buffer -> apply_stage -> split_buffer on a 4-block group
 //     of QAOA-3reg-10 whose input and output are written to argv[1] for the
 //     test to replay through the reference kernels;
 //   * apply_unitary2 / apply_unitary4 out-of-range errors.
@@ -62,7 +62,7 @@ int main(int argc, char** argv) {
         std::printf("qasm_error %d %d %s\n", e.line(), e.col(), e.what());
     }
 
-    // kernel.hpp surface on one 2-block group of QAOA-3reg-10 at b = 4
+    // kernel.hpp surface on one group of QAOA-3reg-10 at b = 4 (inner = 1; a CX pair makes it 4 blocks)
     const cbq::Circuit small = cbq::parse_qasm(std::string(argv[3] ? argv[3] : ""));
     const cbq::Layout L = cbq::make_layout(small.num_qubits, 4);
     const cbq::PartitionPlan plan = cbq::partition_circuit(small, 4, 1);

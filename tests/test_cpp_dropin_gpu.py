@@ -75,7 +75,7 @@ def test_cpp_qasm_surface(dropin, ref):
 
 def test_cpp_apply_stage_matches_reference(dropin, gpu, ref):
     lines, blob = dropin
-    assert "apply_stage_written 2" in lines
+    assert "apply_stage_written 4" in lines  # a CX-RZ-CX stage needs both outer qubits inner: 4 blocks
     raw = open(blob, "rb").read()
     s, n_in, n_blocks, per = np.frombuffer(raw[:32], dtype=np.uint64)
     amps = np.frombuffer(raw[32: 32 + 16 * int(n_in)], dtype=np.complex128).copy()
