@@ -556,6 +556,10 @@ def main():
                     help="N>1: N independent full simulations instead of one sharded simulation")
     ap.add_argument("--sharded", action="store_true", help="use the sharded driver even at N=1")
     ap.add_argument("--no-link", action="store_true", help="skip the pinned host-link bandwidth measurement")
+    ap.add_argument("--device-pool-gib", type=float, default=0.0,
+                    help="fixed device payload arena (GiB); 0 = automatic, growing")
+    ap.add_argument("--host-pool-gib", type=float, default=0.0,
+                    help="pinned host level of the store (GiB); 0 = none")
     ap.add_argument("--e2e-once", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     env_world = os.environ.get("WORLD_SIZE")
@@ -588,7 +592,8 @@ def main():
     w = WORKLOAD
     circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
     cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
-                     identity_skip=not args.no_identity_skip)
+                     identity_skip=not args.no_identity_skip, device_pool_bytes=int(args.device_pool_gib * 2**30),
+                     host_pool_bytes=int(args.host_pool_gib * 2**30))
     sim = cbq.Simulator(circ, cfg)
     stages = len(sim.plan().stages)
     amp_stages = (1 << w["n"]) * stages
@@ -629,6 +634,8 @@ def main():
         "config": {"workload": workload_tag(w), "stages": stages,
                    "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
+                   "device_pool": f"{args.device_pool_gib:g} GiB fixed" if args.device_pool_gib else "automatic",
+                   "host_pool_gib": args.host_pool_gib,
                    "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},
         "sim_time_s": t_dev / 1e3, "wall_ms_median": statistics.median(wall_ms),
         "compression_ratio": rep.compression_ratio, "max_footprint_bytes": rep.max_footprint_bytes,
@@ -636,6 +643,9 @@ def main():
         "gpu_launches": int(rep.device["kernel_launches"]),
         "groups_processed": rep.device["groups_processed"], "groups_skipped": rep.device["groups_skipped"],
         "device_peak_bytes": int(rep.device["device_peak_bytes"]),
+        "store": {k: rep.device[k] for k in ("arena_bytes", "compactions", "compact_bytes", "pool_growths",
+                                             "host_spill_bytes", "host_peak_bytes", "link_h2d_bytes",
+                                             "link_d2h_bytes", "link_ms")},
         "roofline": roof, "clocks": clocks.summary(), "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -81,7 +81,7 @@ typedef struct bmq_config {
     uint32_t compress;           /* 1 = compressed payloads, 0 = raw little-endian doubles */
     uint32_t verify_cap_qubits;  /* default 24 */
     int32_t device;              /* CUDA ordinal, default 0 */
-    uint64_t device_pool_bytes;  /* per payload pool (x2); 0 = automatic */
+    uint64_t device_pool_bytes;  /* device payload arena capacity; 0 = automatic (grows) */
     uint64_t work_bytes;         /* dense group working set; 0 = automatic */
     uint32_t flags;              /* BMQ_FLAG_* */
     uint32_t reserved;
@@ -152,7 +152,7 @@ typedef struct bmq_report {
     uint64_t host_spill_bytes;      /* payload bytes placed in the pinned host arena */
     uint64_t host_spill_batches;    /* batches whose payloads went to the host arena */
     uint64_t code_domain_batches;   /* batches run on quantiser codes (BMQ_FLAG_CODE_DOMAIN) */
-    uint64_t pool_growths;          /* automatic payload arenas doubled after a compaction */
+    uint64_t pool_growths;          /* device arena growths (more HBM mapped in place) */
     uint64_t lazy_cx;               /* CX gates folded into a pass's index map (per batch) */
     uint64_t perm_materialisations; /* index maps materialised before a phase chain (per batch) */
     /* SURVEY 8(d) roofline numerator: for every group with at least one
@@ -164,6 +164,9 @@ typedef struct bmq_report {
     uint64_t link_h2d_bytes;        /* host-tier payload bytes moved host -> device */
     uint64_t link_d2h_bytes;        /* host-tier payload bytes moved device -> host */
     double link_ms;                 /* CUDA-event time of the host-tier copies (copy streams) */
+    uint64_t compact_bytes;         /* payload bytes moved by in-place arena compactions */
+    uint64_t host_peak_bytes;       /* high-water of live payload bytes in the pinned host level */
+    uint64_t arena_bytes;           /* device arena capacity at the end of the run */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

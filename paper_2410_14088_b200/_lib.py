@@ -67,7 +67,8 @@ class bmq_report(C.Structure):
                 ("code_domain_batches", C.c_uint64), ("pool_growths", C.c_uint64),
                 ("lazy_cx", C.c_uint64), ("perm_materialisations", C.c_uint64),
                 ("model_bytes", C.c_uint64), ("model_groups", C.c_uint64), ("link_h2d_bytes", C.c_uint64),
-                ("link_d2h_bytes", C.c_uint64), ("link_ms", C.c_double)]
+                ("link_d2h_bytes", C.c_uint64), ("link_ms", C.c_double),
+                ("compact_bytes", C.c_uint64), ("host_peak_bytes", C.c_uint64), ("arena_bytes", C.c_uint64)]
 
 
 _P = C.c_void_p
@@ -111,6 +112,8 @@ SIGNATURES = {
     "bmq_simulator_get_payloads": (C.c_int, [_P, _P, _U64, _P, C.POINTER(_U64)]),
     "bmq_simulator_put_payload": (C.c_int, [_P, _U64, _P, _U64]),
     "bmq_simulator_fidelity_dense": (C.c_int, [_P, _P, _U64, C.POINTER(_D)]),
+    "bmq_fidelity": (C.c_int, [_P, _P, _U64, C.POINTER(_D)]),
+    "bmq_simulator_footprint": (C.c_int, [_P, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),
     "bmq_simulator_fidelity": (C.c_int, [_P, _P, C.POINTER(_D)]),
     "bmq_simulator_fidelity_analytic": (C.c_int, [_P, C.c_int, C.POINTER(_D)]),
     "bmq_shard_plan": (C.c_int, [C.c_uint32, C.c_uint32, C.POINTER(bmq_stage), _U64, C.c_uint32, C.POINTER(C.c_uint32)]),

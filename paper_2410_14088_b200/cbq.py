@@ -616,7 +616,8 @@ DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks
                       "decompress_bytes", "gate_bytes", "compress_bytes", "fused_batches", "compactions",
                       "host_spill_bytes", "host_spill_batches", "code_domain_batches", "pool_growths",
                       "lazy_cx", "perm_materialisations",
-                      "model_bytes", "model_groups", "link_h2d_bytes", "link_d2h_bytes", "link_ms")
+                      "model_bytes", "model_groups", "link_h2d_bytes", "link_d2h_bytes", "link_ms",
+                      "compact_bytes", "host_peak_bytes", "arena_bytes")
 
 
 def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:

@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_cmp_plan(const CmpBlock* __res
 }
 
 // ---------------------------------------------------------------- alloc
-// Single CTA: exclusive scan of payload sizes into [cursor, cursor + total).
+// Single CTA: exclusive scan of payload sizes into [cursor[0], cursor[0] + total);
+// cursor[1] receives total, whether or not it fits.
 // virtual_zero: ALL_ZERO payloads take no space (engine pools); they are
 // materialised as the canonical 26-byte header on read.
 constexpr int kAllocThreads = 1024;
@@ -297,6 +298,7 @@ __global__ void __launch_bounds__(kAllocThreads) k_cmp_alloc(const CmpBlock* __r
     for (uint64_t i = threadIdx.x; i < nblk; i += kAllocThreads) part += placed(i);
     const unsigned long long total = Reduce(rs).Sum(part);
     if (threadIdx.x == 0) {
+        cursor[1] = total;  // bytes the batch needs (read back after DE_POOL_FULL)
         s_fits = start + total <= cap;
         if (!s_fits) {
             dev_fail(err, DE_POOL_FULL, 0);

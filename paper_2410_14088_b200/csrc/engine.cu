@@ -124,18 +124,24 @@ __global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t 
     }
 }
 
+// pf_off (optional): per batch slot, offset of the payload's prefetched copy
+// in pf_base (~0 = not prefetched: device payloads, or host payloads read in
+// place through the mapped address)
 __global__ void k_build_desc(const uint64_t* __restrict__ ids, uint64_t nblk, const uint64_t* __restrict__ off,
                              const uint64_t* __restrict__ size, const uint8_t* pool, const uint8_t* host_pool,
                              const uint8_t* zero_hdr, double* work, uint32_t* pk, uint32_t b, DecBlock* dec,
-                             CmpBlock* cmp, int codes) {
+                             CmpBlock* cmp, int codes, const uint64_t* __restrict__ pf_off = nullptr,
+                             const uint8_t* pf_base = nullptr) {
     const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (i >= nblk) return;
     const uint64_t id = ids[i];
     const uint64_t count = 2ull << b;
     double* slot = work + i * count;
     const uint64_t o = off[id];
+    const uint64_t pf = pf_off ? pf_off[i] : ~0ull;
     DecBlock d;
-    d.in = o == ~0ull ? zero_hdr : ((o & kHostTag) ? host_pool + (o & ~kHostTag) : pool + o);
+    d.in = o == ~0ull ? zero_hdr
+                      : (pf != ~0ull ? pf_base + pf : ((o & kHostTag) ? host_pool + (o & ~kHostTag) : pool + o));
     d.size = o == ~0ull ? kHeaderBytes : size[id];
     d.out = codes ? reinterpret_cast<double*>(pk + i * count) : slot;  // codes: decode to packed words
     d.expect_count = count;
@@ -153,38 +159,27 @@ __global__ void k_store_dec_sums(const DecInfo* __restrict__ di, const uint64_t*
     sums[3 * id + 2] = di[i].sum_im;
 }
 
-// Compaction: new aligned offsets for the live ids (single CTA scan).
-__global__ void __launch_bounds__(1024) k_compact_plan(const uint64_t* __restrict__ ids, uint64_t n,
-                                                       const uint64_t* __restrict__ size, uint64_t* new_off,
-                                                       uint64_t* total) {
-    using Scan = cub::BlockScan<unsigned long long, 1024>;
-    __shared__ typename Scan::TempStorage ss;
-    unsigned long long carry = 0;
-    for (uint64_t base = 0; base < n; base += 1024) {
-        const uint64_t i = base + threadIdx.x;
-        const unsigned long long sz = i < n ? (size[ids[i]] + kArenaAlign - 1) / kArenaAlign * kArenaAlign : 0;
-        unsigned long long pre, tot;
-        Scan(ss).ExclusiveSum(sz, pre, tot);
-        __syncthreads();
-        if (i < n) new_off[i] = carry + pre;
-        carry += tot;
+// In-place compaction moves (store.hpp): one CTA per payload, 16-byte words
+// (arena payloads are 16-byte aligned, sizes rounded up to whole words).
+struct Move {
+    uint64_t src, dst, words;
+};
+
+__global__ void k_move_payloads(const Move* __restrict__ mv, uint64_t n, const uint8_t* src_base, uint8_t* dst_base) {
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const Move m = mv[i];
+        const uint4* s = reinterpret_cast<const uint4*>(src_base + m.src);
+        uint4* d = reinterpret_cast<uint4*>(dst_base + m.dst);
+        for (uint64_t w = threadIdx.x; w < m.words; w += blockDim.x) d[w] = s[w];
     }
-    if (threadIdx.x == 0) *total = carry;
 }
 
-// Move live payloads (16-byte aligned at both ends) and repoint the metadata.
-__global__ void k_compact_copy(const uint64_t* __restrict__ ids, uint64_t n, uint64_t* off,
-                               const uint64_t* __restrict__ size, const uint8_t* __restrict__ from,
-                               const uint64_t* __restrict__ new_off, uint8_t* __restrict__ to) {
-    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const uint64_t id = ids[i];
-        const uint4* s = reinterpret_cast<const uint4*>(from + off[id]);
-        uint4* d = reinterpret_cast<uint4*>(to + new_off[i]);
-        const uint64_t words = (size[id] + 15) / 16;
-        for (uint64_t w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
-        __syncthreads();
-        if (threadIdx.x == 0) off[id] = new_off[i];
-    }
+// (id, off, size) triples -> per-id metadata (host-level batches)
+__global__ void k_set_meta(const uint64_t* __restrict__ t, uint64_t n, uint64_t* off, uint64_t* size) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    off[t[3 * i]] = t[3 * i + 1];
+    size[t[3 * i]] = t[3 * i + 2];
 }
 
 // Shard transfers: one CTA per payload, 16-byte words (arena payloads and
@@ -499,24 +494,45 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     hdr[25] = 1;
     zero_hdr_.alloc(sizeof hdr);
     BMQ_CUDA(cudaMemcpy(zero_hdr_.p, hdr, sizeof hdr, cudaMemcpyHostToDevice));
-    uint64_t pool = cfg.device_pool_bytes;
-    if (!pool) {  // every block at its worst-case payload size, capped
-        const uint64_t worst = nid * (compress_bound(blk_scalars) + kArenaAlign);
-        pool = std::min<uint64_t>({24ull << 30, total_b / 8, worst});
+    // Device level: one VA range for the whole device, mapped on demand.
+    // device_pool_bytes fixes the arena's capacity (unless BMQ_FLAG_POOL_GROW
+    // makes it the initial size); automatic arenas start at min(24 GiB,
+    // HBM / 8) and grow up to what the device has left.
+    const uint64_t worst = nid * (compress_bound(blk_scalars) + kArenaAlign) + 64;
+    const uint64_t others = work_.bytes() + pk_.bytes() + cplan_.bytes() + dchunk_.bytes() + zflag_.bytes() +
+                            wflag_.bytes() + 8 * (ids_.n + vtab_.n + new_off_.n + live_ids_.n + off_.n + size_.n) +
+                            sums_.bytes();
+    const uint64_t headroom = total_b > others + (6ull << 30) ? total_b - others - (6ull << 30) : (1ull << 30);
+    arena_grow_ = cfg.device_pool_bytes == 0 || (cfg.flags & BMQ_FLAG_POOL_GROW);
+    arena_max_ = arena_grow_ ? std::max<uint64_t>(std::min(worst, headroom), cfg.device_pool_bytes) : cfg.device_pool_bytes;
+    arena_.init(dev_, std::min<uint64_t>(total_b, std::max<uint64_t>(arena_max_, 1ull << 30)) + (1ull << 30));
+    const uint64_t initial = cfg.device_pool_bytes ? cfg.device_pool_bytes
+                                                   : std::min<uint64_t>({24ull << 30, total_b / 8, arena_max_});
+    if (!arena_.grow_to(initial + 64)) raise(BMQ_ERR_OUT_OF_MEMORY, "device payload arena: out of memory");
+    arena_limit_ = initial;
+    BMQ_CUDA(cudaStreamCreateWithFlags(&cp_in_, cudaStreamNonBlocking));
+    BMQ_CUDA(cudaStreamCreateWithFlags(&cp_out_, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        BMQ_CUDA(cudaEventCreateWithFlags(&ev_pf_[k], cudaEventDisableTiming));
+        BMQ_CUDA(cudaEventCreateWithFlags(&ev_dec_[k], cudaEventDisableTiming));
     }
-    pool_cap_ = pool;
-    pool_auto_ = cfg.device_pool_bytes == 0 || (cfg.flags & BMQ_FLAG_POOL_GROW);
-    pool_worst_ = nid * (compress_bound(blk_scalars) + kArenaAlign);
-    pool_[0].alloc(pool + 64);
-    pool_[1].alloc(pool + 64);
-    device_peak_ = 2 * (pool + 64) + work_.bytes() + pk_.bytes() + cplan_.bytes() + dchunk_.bytes();
+    BMQ_CUDA(cudaEventCreateWithFlags(&ev_emit_, cudaEventDisableTiming));
+    BMQ_CUDA(cudaEventCreateWithFlags(&ev_wb_, cudaEventDisableTiming));
+    device_peak_ = arena_.mapped() + others;
 }
 
 Engine::~Engine() {
-    if (st_) {
-        cudaSetDevice(dev_);
-        cudaStreamSynchronize(st_);
-        cudaStreamDestroy(st_);
+    cudaSetDevice(dev_);
+    for (cudaStream_t* q : {&st_, &cp_in_, &cp_out_})
+        if (*q) {
+            cudaStreamSynchronize(*q);
+            cudaStreamDestroy(*q);
+        }
+    for (cudaEvent_t e : {ev_pf_[0], ev_pf_[1], ev_dec_[0], ev_dec_[1], ev_emit_, ev_wb_})
+        if (e) cudaEventDestroy(e);
+    for (auto& [a, b] : link_ev_) {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
     }
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
@@ -546,75 +562,143 @@ void Engine::sync_meta_to_host() {
     BMQ_CUDA(cudaStreamSynchronize(st_));
 }
 
-// Move every stored payload into the other arena, back to back.
-void Engine::compact() {
-    sync_meta_to_host();
-    std::vector<uint64_t> live;
-    for (uint64_t id = 0; id < h_off_.size(); ++id)
-        if (h_off_[id] != ~0ull && !(h_off_[id] & kHostTag)) live.push_back(id);  // device payloads only
-    const int nxt = 1 - cur_;
-    if (live.empty()) {
-        BMQ_CUDA(cudaMemsetAsync(cursor_.p + nxt, 0, 8, st_));
-    } else {
-        BMQ_CUDA(cudaMemcpyAsync(live_ids_.p, live.data(), live.size() * 8, cudaMemcpyHostToDevice, st_));
-        k_compact_plan<<<1, 1024, 0, st_>>>(live_ids_.p, live.size(), size_.p, new_off_.p, cursor_.p + nxt);
-        k_compact_copy<<<grid_for(live.size() * 256), 256, 0, st_>>>(live_ids_.p, live.size(), off_.p, size_.p,
-                                                                     pool_[cur_].p, new_off_.p, pool_[nxt].p);
-        BMQ_CUDA(cudaGetLastError());
-        counters_.kernel_launches += 2;
-    }
-    cur_ = nxt;
-    sync_meta_to_host();
-    ++counters_.compactions;
-    maybe_grow_pools();
+uint64_t Engine::arena_used() {
+    uint64_t used = 0;
+    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p, 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    return used;
 }
 
-// Automatic arenas grow when the live state fills more than half of one
-// after compaction (dense states at b_r = 1e-3 are ~1/4 of 2^(n+4) bytes:
-// compacting every batch would copy the whole state each time). The live
-// payloads move into a new, doubled arena; on allocation failure the
-// arenas stay as they are.
-void Engine::maybe_grow_pools() {
-    if (!pool_auto_ || growing_) return;
-    struct Guard {
-        bool& f;
-        explicit Guard(bool& g) : f(g) { f = true; }
-        ~Guard() { f = false; }
-    } guard(growing_);
-    uint64_t used = 0;
-    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
-    BMQ_CUDA(cudaStreamSynchronize(st_));
-    if (2 * used <= pool_cap_ || pool_cap_ >= pool_worst_) return;
-    size_t free_b = 0, total_b = 0;
-    BMQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t new_cap = std::min<uint64_t>(2 * pool_cap_, pool_worst_);
-    // the dead arena is released first; keep a margin of HBM for others
-    if (free_b + pool_cap_ < new_cap + (8ull << 30)) return;
-    const int dead = 1 - cur_;
-    pool_[dead].release();
-    try {
-        pool_[dead].alloc(new_cap + 64);
-    } catch (const Error&) {
-        cudaGetLastError();
-        pool_[dead].alloc(pool_cap_ + 64);
-        return;
-    }
-    const uint64_t old_cap = pool_cap_;
-    pool_cap_ = new_cap;
-    compact();  // live payloads -> the new arena (cur_ flips to it)
-    const int old = 1 - cur_;
-    pool_[old].release();
-    try {
-        pool_[old].alloc(new_cap + 64);
-    } catch (const Error&) {  // keep running on one large + one old-size arena
-        cudaGetLastError();
-        pool_[old].alloc(old_cap + 64);
-        pool_cap_ = old_cap;
-        compact();
-        return;
-    }
-    device_peak_ += 2 * (new_cap - old_cap);
+bool Engine::grow_arena(uint64_t limit) {
+    if (limit <= arena_limit_) return true;
+    if (!arena_grow_ || limit > arena_max_) return false;
+    // grow by at least a quarter, so a run grows O(log) times
+    const uint64_t want = std::min(arena_max_, std::max(limit, arena_limit_ + arena_limit_ / 4));
+    if (!arena_.grow_to(want + 64) && !arena_.grow_to(limit + 64)) return false;
+    const uint64_t before = arena_.mapped();
+    arena_limit_ = std::min<uint64_t>(arena_.mapped() - 64, std::max(limit, want));
+    device_peak_ += arena_.mapped() > before ? arena_.mapped() - before : 0;
     ++counters_.pool_growths;
+    return true;
+}
+
+// Compaction in place: the device payloads of every id except `excl` (whose
+// payloads the batch in flight has already decoded) slide down to the front
+// of the arena in offset order. A window of payloads moves directly when all
+// its destinations end before its first source; otherwise (little dead space
+// in front of it) the window goes through the dead dense work buffer, packed
+// then unpacked. Destinations never pass the sources of later windows, so the
+// windows run back to back on st_.
+void Engine::compact(const uint64_t* excl, uint64_t nexcl) {
+    sync_meta_to_host();
+    const uint64_t nid = L_.num_blocks();
+    std::vector<uint8_t> dead(nid, 0);
+    for (uint64_t i = 0; i < nexcl; ++i) dead[excl[i]] = 1;
+    std::vector<uint64_t> live;
+    for (uint64_t id = 0; id < nid; ++id)
+        if (!dead[id] && h_off_[id] != ~0ull && !(h_off_[id] & kHostTag)) live.push_back(id);
+    std::sort(live.begin(), live.end(), [&](uint64_t x, uint64_t y) { return h_off_[x] < h_off_[y]; });
+    const auto bytes_of = [&](uint64_t id) { return (h_size_[id] + kArenaAlign - 1) / kArenaAlign * kArenaAlign; };
+    struct Seg {
+        size_t first, count;
+        int mode;  // 0 arena -> arena, 1 arena -> staging, 2 staging -> arena
+    };
+    std::vector<Move> mv;
+    std::vector<Seg> segs;
+    const uint64_t scap = work_.bytes() / kArenaAlign * kArenaAlign;
+    uint64_t dst = 0, moved = 0;
+    size_t i = 0;
+    while (i < live.size()) {
+        const uint64_t src0 = h_off_[live[i]];
+        if (src0 == dst) {  // already in place
+            dst += bytes_of(live[i++]);
+            continue;
+        }
+        size_t j = i;
+        for (uint64_t end = dst; j < live.size() && end + bytes_of(live[j]) <= src0; ++j) end += bytes_of(live[j]);
+        if (j > i && (j - i >= 32 || j == live.size())) {
+            segs.push_back(Seg{mv.size(), j - i, 0});
+            for (size_t k = i; k < j; ++k) {
+                const uint64_t id = live[k];
+                mv.push_back(Move{h_off_[id], dst, bytes_of(id) / kArenaAlign});
+                h_off_[id] = dst;
+                dst += bytes_of(id);
+                moved += bytes_of(id);
+            }
+        } else {
+            j = i;
+            uint64_t sp = 0;
+            while (j < live.size() && (j == i || sp + bytes_of(live[j]) <= scap)) sp += bytes_of(live[j++]);
+            if (sp > scap) raise(BMQ_ERR_STORE, "payload larger than the compaction staging buffer");
+            segs.push_back(Seg{mv.size(), j - i, 1});
+            sp = 0;
+            for (size_t k = i; k < j; ++k) {
+                mv.push_back(Move{h_off_[live[k]], sp, bytes_of(live[k]) / kArenaAlign});
+                sp += bytes_of(live[k]);
+            }
+            segs.push_back(Seg{mv.size(), j - i, 2});
+            sp = 0;
+            for (size_t k = i; k < j; ++k) {
+                const uint64_t id = live[k];
+                mv.push_back(Move{sp, dst, bytes_of(id) / kArenaAlign});
+                sp += bytes_of(id);
+                h_off_[id] = dst;
+                dst += bytes_of(id);
+                moved += 2 * bytes_of(id);
+            }
+        }
+        i = j;
+    }
+    if (!mv.empty()) {
+        DevArray<Move> dm;
+        dm.alloc(mv.size());
+        BMQ_CUDA(cudaMemcpyAsync(dm.p, mv.data(), mv.size() * sizeof(Move), cudaMemcpyHostToDevice, st_));
+        uint8_t* arena = arena_.base();
+        uint8_t* staging = reinterpret_cast<uint8_t*>(work_.p);
+        for (const Seg& g : segs) {
+            const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.count, 148 * 16));
+            k_move_payloads<<<grid, 256, 0, st_>>>(dm.p + g.first, g.count, g.mode == 2 ? staging : arena,
+                                                   g.mode == 1 ? staging : arena);
+            ++counters_.kernel_launches;
+        }
+        BMQ_CUDA(cudaGetLastError());
+        BMQ_CUDA(cudaMemcpyAsync(off_.p, h_off_.data(), off_.bytes(), cudaMemcpyHostToDevice, st_));
+    }
+    BMQ_CUDA(cudaMemcpyAsync(cursor_.p, &dst, 8, cudaMemcpyHostToDevice, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    ++counters_.compactions;
+    counters_.compact_bytes += moved;
+}
+
+// Room for `need` more bytes at the cursor. Compaction moves the live
+// payloads once, so it runs when the garbage is at least the live state
+// (amortised: one byte moved per byte written); otherwise the arena grows
+// while the device has HBM for it, and compacts as the last resort.
+bool Engine::make_room(uint64_t need, const uint64_t* excl, uint64_t nexcl) {
+    sync_meta_to_host();
+    const uint64_t used = arena_used();
+    if (used + need <= arena_limit_) return true;
+    std::vector<uint8_t> dead(L_.num_blocks(), 0);
+    for (uint64_t i = 0; i < nexcl; ++i) dead[excl[i]] = 1;
+    uint64_t live = 0;
+    for (uint64_t id = 0; id < L_.num_blocks(); ++id)
+        if (!dead[id] && h_off_[id] != ~0ull && !(h_off_[id] & kHostTag))
+            live += (h_size_[id] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+    const uint64_t garbage = used > live ? used - live : 0;
+    if (garbage >= live && live + need <= arena_limit_) {
+        compact(excl, nexcl);
+        return true;
+    }
+    if (grow_arena(used + need)) return true;
+    if (live + need <= arena_limit_) {
+        compact(excl, nexcl);
+        return true;
+    }
+    if (grow_arena(live + need)) {
+        compact(excl, nexcl);
+        return true;
+    }
+    return false;
 }
 
 void Engine::init_state() {
@@ -623,7 +707,10 @@ void Engine::init_state() {
     const uint64_t nid = L_.num_blocks();
     const double one = 1.0;
     store_.reset(nid, cfg_.memory_budget);
-    host_cursor_ = 0;
+    if (host_pool_) {
+        sync_copies();
+        host_heap_.reset(host_cap_, kArenaAlign);
+    }
     BMQ_CUDA(cudaMemsetAsync(sums_.p, 0, sums_.bytes(), st_));
     if (!cfg_.compress) {
         const uint64_t raw = 16ull << L_.b;
@@ -637,7 +724,6 @@ void Engine::init_state() {
         next_stage_ = 0;
         return;
     }
-    cur_ = 0;
     k_fill_meta<<<grid_for(nid), 256, 0, st_>>>(off_.p, size_.p, nid, kHeaderBytes);
     BMQ_CUDA(cudaMemsetAsync(cursor_.p, 0, 2 * sizeof(uint64_t), st_));
     const uint64_t cnt = 2ull << L_.b;
@@ -645,7 +731,7 @@ void Engine::init_state() {
     BMQ_CUDA(cudaMemcpyAsync(work_.p, &one, 8, cudaMemcpyHostToDevice, st_));
     const CmpBlock blk{work_.p, pk_.p, cnt, 0};
     BMQ_CUDA(cudaMemcpyAsync(cmp_.p, &blk, sizeof blk, cudaMemcpyHostToDevice, st_));
-    launch_compress(st_, cmp_.p, 1, nch_, *tabs_, pool_[0].p, pool_cap_, cursor_.p, cursor_.p + 2, bplan_.p, cplan_.p,
+    launch_compress(st_, cmp_.p, 1, nch_, *tabs_, arena_.base(), arena_limit_, cursor_.p, cursor_.p + 2, bplan_.p, cplan_.p,
                     off_.p, size_.p, true, false, err_.p, &counters_.kernel_launches);
     check_device_error("init_state: ");
     sums_ok_.assign(nid, 1);
@@ -719,42 +805,98 @@ void Engine::raw_run_stage(uint64_t s) {
     stage_decompress_calls_ += L_.num_blocks();
 }
 
-// alloc + zero + emit for the batch in flight; on a full arena, compact and
-// allocate again (the plan and the packed codes are still in place).
-void Engine::emit_batch(uint64_t nblk) {
-    bool placed = false;
-    for (int attempt = 0; attempt < 2 && !placed; ++attempt) {
-        launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, pool_[cur_].p, pool_cap_, cursor_.p + cur_,
-                             cursor_.p + 2, bplan_.p, cplan_.p, off_.p, size_.p, true, kArenaAlign, err_.p,
+// alloc + zero + emit for the batch in flight into the device arena; when it
+// does not fit, make room (compaction / growth, the batch's old payloads are
+// dead) and try again; a batch that still does not fit goes to the host level.
+void Engine::emit_batch(uint64_t nblk, const uint64_t* h_ids) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, arena_.base(), arena_limit_, cursor_.p, cursor_.p + 2,
+                             bplan_.p, cplan_.p, off_.p, size_.p, true, kArenaAlign, err_.p,
                              &counters_.kernel_launches);
-        const uint32_t code = peek_error();
-        placed = code != DE_POOL_FULL;
-        if (placed) break;
-        BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
-        if (attempt == 0) compact();
-    }
-    if (!placed) {
-        // Second level: emit into the (now dead) dense work buffer, then move
-        // the batch's payloads to the pinned host arena in one copy.
-        if (!cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
-        ensure_host_pool();
-        BMQ_CUDA(cudaMemsetAsync(cursor_.p + 4, 0, 8, st_));
-        uint8_t* staging = reinterpret_cast<uint8_t*>(work_.p);
-        launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, staging, work_.bytes() - 64, cursor_.p + 4,
-                             cursor_.p + 2, bplan_.p, cplan_.p, off_.p, size_.p, true, kArenaAlign, err_.p,
-                             &counters_.kernel_launches, host_cursor_, kHostTag);
-        if (peek_error() == DE_POOL_FULL) {
-            BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
-            raise(BMQ_ERR_STORE, "payload batch exceeds the staging buffer");
+        if (peek_error() != DE_POOL_FULL) {
+            free_host_extents(h_ids, nblk);
+            return;
         }
-        uint64_t total = 0;
-        BMQ_CUDA(cudaMemcpyAsync(&total, cursor_.p + 4, 8, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
+        uint64_t need = 0;
+        BMQ_CUDA(cudaMemcpyAsync(&need, cursor_.p + 1, 8, cudaMemcpyDeviceToHost, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
-        if (host_cursor_ + total > host_cap_) raise(BMQ_ERR_STORE, "host payload pool exhausted");
-        BMQ_CUDA(cudaMemcpyAsync(host_pool_ + host_cursor_, staging, total, cudaMemcpyDeviceToHost, st_));
-        host_cursor_ += total;
-        counters_.host_spill_bytes += total;
-        ++counters_.host_spill_batches;
+        if (!make_room(need, h_ids, nblk)) break;
+    }
+    if (!cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+    emit_to_host(nblk, h_ids);
+}
+
+// Host level: emit into the write-back staging buffer (the dead work buffer
+// when the batch outgrows it), give every payload its own host extent and
+// copy the payloads there on cp_out_ while the next batch computes.
+void Engine::emit_to_host(uint64_t nblk, const uint64_t* h_ids) {
+    ensure_host_pool();
+    BMQ_CUDA(cudaStreamWaitEvent(st_, ev_wb_, 0));  // the previous write-back has left wb_
+    uint8_t* staging = wb_.p;
+    bool in_work = false;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        BMQ_CUDA(cudaMemsetAsync(cursor_.p + 4, 0, 8, st_));
+        launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, staging, (in_work ? work_.bytes() : wb_.bytes()) - 64,
+                             cursor_.p + 4, cursor_.p + 2, bplan_.p, cplan_.p, nullptr, nullptr, true, kArenaAlign,
+                             err_.p, &counters_.kernel_launches);
+        if (peek_error() != DE_POOL_FULL) break;
+        BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
+        if (in_work) raise(BMQ_ERR_STORE, "payload batch exceeds the staging buffer");
+        staging = reinterpret_cast<uint8_t*>(work_.p);  // dead until the next batch decodes
+        in_work = true;
+    }
+    std::vector<BlockPlan> bp(nblk);
+    BMQ_CUDA(cudaMemcpyAsync(bp.data(), bplan_.p, nblk * sizeof(BlockPlan), cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaEventRecord(ev_emit_, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    free_host_extents(h_ids, nblk);  // the batch's old payloads were decoded
+    h_meta_.assign(3 * nblk, 0);
+    std::vector<void*> dst, src;
+    std::vector<size_t> len;
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < nblk; ++i) {
+        const uint64_t id = h_ids[i];
+        uint64_t off = ~0ull, size = kHeaderBytes;
+        if (!(bp[i].flags & 1)) {
+            size = bp[i].size;
+            const uint64_t ext = host_heap_.alloc(size);
+            if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
+            off = ext | kHostTag;
+            dst.push_back(host_pool_ + ext);
+            src.push_back(staging + bp[i].out_off);
+            len.push_back(size);
+            total += size;
+        }
+        h_meta_[3 * i] = id;
+        h_meta_[3 * i + 1] = off;
+        h_meta_[3 * i + 2] = size;
+        h_off_[id] = off;
+        h_size_[id] = size;
+    }
+    BMQ_CUDA(cudaStreamWaitEvent(cp_out_, ev_emit_, 0));
+    link_event_pair(cp_out_, true);
+    copy_batch(dst.data(), src.data(), len.data(), dst.size(), cp_out_);
+    link_event_pair(cp_out_, false);
+    BMQ_CUDA(cudaEventRecord(ev_wb_, cp_out_));
+    if (in_work) BMQ_CUDA(cudaStreamWaitEvent(st_, ev_wb_, 0));  // the next decode overwrites work_
+    BMQ_CUDA(cudaMemcpyAsync(d_meta_.p, h_meta_.data(), 3 * nblk * 8, cudaMemcpyHostToDevice, st_));
+    k_set_meta<<<grid_for(nblk), 256, 0, st_>>>(d_meta_.p, nblk, off_.p, size_.p);
+    ++counters_.kernel_launches;
+    BMQ_CUDA(cudaGetLastError());
+    counters_.host_spill_bytes += total;
+    counters_.link_d2h_bytes += total;
+    ++counters_.host_spill_batches;
+}
+
+void Engine::free_host_extents(const uint64_t* ids, uint64_t n) {
+    if (!host_pool_) return;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t o = h_off_[ids[i]];
+        if (o != ~0ull && (o & kHostTag)) {
+            host_heap_.free(o & ~kHostTag, h_size_[ids[i]]);
+            h_off_[ids[i]] = ~0ull;  // until the next metadata sync
+        }
     }
 }
 
@@ -763,17 +905,107 @@ void Engine::ensure_host_pool() {
     host_cap_ = cfg_.host_pool_bytes;
     BMQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool_), host_cap_ + 64,
                            cudaHostAllocMapped | cudaHostAllocPortable));
-    host_cursor_ = 0;
+    host_heap_.reset(host_cap_, kArenaAlign);
+    // staging: write-back buffer and two prefetch slots of a quarter of the
+    // dense working set each (at most 4 GiB); batches are cut so their
+    // host-level payloads fit one slot
+    const uint64_t slot = std::max<uint64_t>(std::min<uint64_t>(work_.bytes() / 4, 4ull << 30), 1ull << 20);
+    wb_.alloc(slot + 64);
+    for (int k = 0; k < 2; ++k) {
+        pf_[k].alloc(slot);
+        pf_off_[k].alloc(max_blocks_);
+        h_pf_off_[k].assign(max_blocks_, ~0ull);
+    }
+    d_meta_.alloc(3 * max_blocks_);
+    device_peak_ += wb_.bytes() + 2 * slot + 2 * 8 * max_blocks_ + 24 * max_blocks_;
 }
 
-void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk,
-                           size_t bidx) {
+void Engine::copy_batch(void** dst, void** src, size_t* sizes, size_t n, cudaStream_t s) {
+    if (!n) return;
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t idx = 0, fail = 0;
+    if (cudaMemcpyBatchAsync(dst, src, sizes, n, &attr, &idx, 1, &fail, s) == cudaSuccess) return;
+    cudaGetLastError();  // driver without batched copies: one call per payload
+    for (size_t i = 0; i < n; ++i) BMQ_CUDA(cudaMemcpyAsync(dst[i], src[i], sizes[i], cudaMemcpyDefault, s));
+}
+
+void Engine::link_event_pair(cudaStream_t s, bool start) {
+    if (start) {
+        if (link_ev_used_ == link_ev_.size()) {
+            cudaEvent_t a, b;
+            BMQ_CUDA(cudaEventCreate(&a));
+            BMQ_CUDA(cudaEventCreate(&b));
+            link_ev_.emplace_back(a, b);
+        }
+        BMQ_CUDA(cudaEventRecord(link_ev_[link_ev_used_].first, s));
+    } else {
+        BMQ_CUDA(cudaEventRecord(link_ev_[link_ev_used_++].second, s));
+    }
+}
+
+void Engine::collect_link_times() {
+    for (size_t k = 0; k < link_ev_used_; ++k) {
+        float ms = 0.f;
+        BMQ_CUDA(cudaEventElapsedTime(&ms, link_ev_[k].first, link_ev_[k].second));
+        counters_.link_ms += ms;
+    }
+    link_ev_used_ = 0;
+}
+
+// The stage barrier for the copy streams: host-level bytes are final and the
+// prefetch slots are free.
+void Engine::sync_copies() {
+    if (cp_in_) BMQ_CUDA(cudaStreamSynchronize(cp_in_));
+    if (cp_out_) BMQ_CUDA(cudaStreamSynchronize(cp_out_));
+    collect_link_times();
+    pf_live_[0] = pf_live_[1] = false;
+}
+
+bool Engine::prefetch(const uint64_t* h_ids, uint64_t nblk, int slot) {
+    if (!host_pool_ || !host_heap_.used()) return false;
+    BMQ_CUDA(cudaStreamWaitEvent(cp_in_, ev_dec_[slot], 0));  // batch k-2 has decoded out of this slot
+    uint64_t* tab = h_pf_off_[slot].data();
+    std::vector<void*> dst, src;
+    std::vector<size_t> len;
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < nblk; ++i) {
+        const uint64_t o = h_off_[h_ids[i]];
+        tab[i] = ~0ull;
+        if (o == ~0ull || !(o & kHostTag)) continue;
+        const uint64_t size = h_size_[h_ids[i]];
+        if (pos + size > pf_[slot].bytes()) continue;  // read in place through the mapped address
+        tab[i] = pos;
+        dst.push_back(pf_[slot].p + pos);
+        src.push_back(host_pool_ + (o & ~kHostTag));
+        len.push_back(size);
+        pos += (size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+    }
+    if (dst.empty()) return false;
+    BMQ_CUDA(cudaMemcpyAsync(pf_off_[slot].p, tab, nblk * 8, cudaMemcpyHostToDevice, cp_in_));
+    link_event_pair(cp_in_, true);
+    copy_batch(dst.data(), src.data(), len.data(), dst.size(), cp_in_);
+    link_event_pair(cp_in_, false);
+    BMQ_CUDA(cudaEventRecord(ev_pf_[slot], cp_in_));
+    uint64_t bytes = 0;
+    for (size_t l : len) bytes += l;
+    counters_.link_h2d_bytes += bytes;
+    return true;
+}
+
+void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t* d_ids, const uint32_t* d_vtab,
+                           uint64_t nblk, size_t bidx) {
     phase_event(4 * bidx);
     // Code-domain stages (unit-entry monomial gates only) never leave the
     // quantiser codes: decode to packed words, permute them, emit.
     const bool codes = !d_vtab && sp.prog.mono && identity_ok_ && (cfg_.flags & BMQ_FLAG_CODE_DOMAIN);
-    k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_.p, size_.p, pool_[cur_].p, host_pool_,
-                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, codes ? 1 : 0);
+    const int slot = static_cast<int>(bidx & 1);
+    const bool pf = pf_live_[slot];
+    if (pf) BMQ_CUDA(cudaStreamWaitEvent(st_, ev_pf_[slot], 0));  // host-level payloads prefetched
+    k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(d_ids, nblk, off_.p, size_.p, arena_.base(), host_pool_,
+                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, codes ? 1 : 0,
+                                                  pf ? pf_off_[slot].p : nullptr, pf_[slot].p);
     ++counters_.kernel_launches;
     // code-domain stages: all-zero chunks stay unwritten; the first
     // permutation pass reads them as zero words
@@ -785,6 +1017,8 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     if (zf) BMQ_CUDA(cudaMemsetAsync(imnz_.p, 0, sizeof(uint32_t), st_));
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
                       &counters_.kernel_launches, codes ? 1 : 0, zf, zf ? imnz_.p : nullptr);
+    if (host_pool_) BMQ_CUDA(cudaEventRecord(ev_dec_[slot], st_));  // the prefetch slot is free again
+    pf_live_[slot] = false;
     phase_event(4 * bidx + 1);
     // the stage's last gate pass quantises straight into pk_ / cplan_
     BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
@@ -802,7 +1036,7 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t*
     phase_event(4 * bidx + 2);
     launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,
                          &counters_.kernel_launches);
-    emit_batch(nblk);
+    emit_batch(nblk, h_ids);
     phase_event(4 * bidx + 3);
     if (fused) ++counters_.fused_batches;
     if (!codes) {
@@ -871,13 +1105,39 @@ void Engine::run_stage(uint64_t s) {
         BMQ_CUDA(cudaMemcpyAsync(ids_.p, work_ids.data(), nwork * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
         if (blockwise)
             BMQ_CUDA(cudaMemcpyAsync(vtab_.p, work_v.data(), nwork * sizeof(uint32_t), cudaMemcpyHostToDevice, st_));
+        // batches of whole groups, cut so that their host-level payloads fit
+        // one prefetch slot
+        const uint64_t unit = blockwise ? 1 : per;
         const uint64_t batch_blocks = blockwise ? max_blocks_ : std::max<uint64_t>(1, max_blocks_ / per) * per;
-        for (uint64_t first = 0; first < nwork; first += batch_blocks, ++nbatches) {
-            const uint64_t nblk = std::min(batch_blocks, nwork - first);
-            process_batch(sp, ids_.p + first, blockwise ? vtab_.p + first : nullptr, nblk, nbatches);
+        const uint64_t pf_cap = host_pool_ && host_heap_.used() ? pf_[0].bytes() : ~0ull;
+        std::vector<std::pair<uint64_t, uint64_t>> batches;
+        uint64_t first = 0, hb = 0;
+        for (uint64_t u = 0; u < nwork; u += unit) {
+            uint64_t ub = 0;
+            if (pf_cap != ~0ull)
+                for (uint64_t v = u; v < u + unit; ++v) {
+                    const uint64_t o = h_off_[work_ids[v]];
+                    if (o != ~0ull && (o & kHostTag)) ub += (h_size_[work_ids[v]] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+                }
+            if (u > first && (u - first + unit > batch_blocks || hb + ub > pf_cap)) {
+                batches.emplace_back(first, u - first);
+                first = u;
+                hb = 0;
+            }
+            hb += ub;
+        }
+        batches.emplace_back(first, nwork - first);
+        pf_live_[0] = prefetch(work_ids.data() + batches[0].first, batches[0].second, 0);
+        for (size_t k = 0; k < batches.size(); ++k, ++nbatches) {
+            if (k + 1 < batches.size())  // overlaps batch k on the copy engine
+                pf_live_[(k + 1) & 1] = prefetch(work_ids.data() + batches[k + 1].first, batches[k + 1].second,
+                                                 static_cast<int>((k + 1) & 1));
+            const auto [b0, nblk] = batches[k];
+            process_batch(sp, work_ids.data() + b0, ids_.p + b0, blockwise ? vtab_.p + b0 : nullptr, nblk, k);
         }
     }
     check_device_error(("stage " + std::to_string(s) + ": ").c_str());
+    sync_copies();
     sync_meta_to_host();
     collect_phase_times(nbatches);
     // accounting replay in the reference put order (groups ascending); a
@@ -987,6 +1247,9 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.link_h2d_bytes = counters_.link_h2d_bytes;
     r.link_d2h_bytes = counters_.link_d2h_bytes;
     r.link_ms = counters_.link_ms;
+    r.compact_bytes = counters_.compact_bytes;
+    r.host_peak_bytes = host_heap_.high_water();
+    r.arena_bytes = arena_limit_;
     *rep = r;
 }
 
@@ -1012,7 +1275,7 @@ void Engine::host_ids_to_device(const std::vector<uint64_t>& ids) {
 }
 
 void Engine::decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums) {
-    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_.p, size_.p, pool_[cur_].p, host_pool_,
+    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_.p, size_.p, arena_.base(), host_pool_,
                                                   zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0);
     launch_decompress(st_, dec_.p, nids, nch_, *tabs_, dinfo_.p, dchunk_.p, true, want_sums, err_.p,
                       &counters_.kernel_launches);
@@ -1035,7 +1298,7 @@ void Engine::ensure_sums(const uint64_t* ids, uint64_t n) {
     for (uint64_t first = 0; first < stale.size(); first += max_blocks_) {
         const uint64_t nb = std::min<uint64_t>(max_blocks_, stale.size() - first);
         BMQ_CUDA(cudaMemcpyAsync(ids_.p, stale.data() + first, nb * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
-        k_build_desc<<<grid_for(nb), 256, 0, st_>>>(ids_.p, nb, off_.p, size_.p, pool_[cur_].p, host_pool_,
+        k_build_desc<<<grid_for(nb), 256, 0, st_>>>(ids_.p, nb, off_.p, size_.p, arena_.base(), host_pool_,
                                                     zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0);
         launch_decompress(st_, dec_.p, nb, nch_, *tabs_, dinfo_.p, dchunk_.p, true, true, err_.p,
                           &counters_.kernel_launches, 2);
@@ -1132,7 +1395,7 @@ uint64_t Engine::get_payload(uint64_t id, uint8_t* out, uint64_t cap) {
             BMQ_CUDA(cudaStreamSynchronize(st_));
             std::memcpy(out, host_pool_ + (h_off_[id] & ~kHostTag), size);
         } else {
-            BMQ_CUDA(cudaMemcpyAsync(out, pool_[cur_].p + h_off_[id], size, cudaMemcpyDeviceToHost, st_));
+            BMQ_CUDA(cudaMemcpyAsync(out, arena_.base() + h_off_[id], size, cudaMemcpyDeviceToHost, st_));
             BMQ_CUDA(cudaStreamSynchronize(st_));
         }
     }
@@ -1171,7 +1434,7 @@ void Engine::get_payloads(uint8_t* out, uint64_t cap, uint64_t* sizes, uint64_t*
         dx.alloc(xs.size());
         BMQ_CUDA(cudaMemcpyAsync(dx.p, xs.data(), xs.size() * sizeof(Xfer), cudaMemcpyHostToDevice, st_));
         k_gather_payloads<<<static_cast<uint32_t>(std::min<uint64_t>(xs.size(), 148 * 16)), 256, 0, st_>>>(
-            dx.p, xs.size(), off_.p, pool_[cur_].p, host_pool_, zero_hdr_.p, staging);
+            dx.p, xs.size(), off_.p, arena_.base(), host_pool_, zero_hdr_.p, staging);
         ++counters_.kernel_launches;
         BMQ_CUDA(cudaGetLastError());
         BMQ_CUDA(cudaMemcpyAsync(out + base, staging, len, cudaMemcpyDeviceToHost, st_));
@@ -1199,20 +1462,27 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
         store_.put(id, raw);
         return;
     }
-    uint64_t used = 0;
-    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
-    BMQ_CUDA(cudaStreamSynchronize(st_));
-    if (used + size + kArenaAlign > pool_cap_) {
-        compact();
-        BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
-        BMQ_CUDA(cudaStreamSynchronize(st_));
-        if (used + size + kArenaAlign > pool_cap_) raise(BMQ_ERR_STORE, "device payload pool exhausted");
-    }
+    // device arena first (its previous payload stays live until the new one
+    // decodes), else a host-level extent
     const uint64_t prev_off = h_off_[id], prev_size = h_size_[id];
-    BMQ_CUDA(cudaMemcpyAsync(pool_[cur_].p + used, data, size, cudaMemcpyHostToDevice, st_));
-    const uint64_t end = (used + size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
-    BMQ_CUDA(cudaMemcpyAsync(cursor_.p + cur_, &end, 8, cudaMemcpyHostToDevice, st_));
-    BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &used, 8, cudaMemcpyHostToDevice, st_));
+    uint64_t off = ~0ull;
+    if (make_room(size + kArenaAlign, nullptr, 0)) {
+        const uint64_t used = arena_used();
+        off = used;
+        BMQ_CUDA(cudaMemcpyAsync(arena_.base() + used, data, size, cudaMemcpyHostToDevice, st_));
+        const uint64_t end = (used + size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+        BMQ_CUDA(cudaMemcpyAsync(cursor_.p, &end, 8, cudaMemcpyHostToDevice, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));  // `end` and `off` live on this frame
+    } else {
+        if (!cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+        ensure_host_pool();
+        sync_copies();
+        const uint64_t ext = host_heap_.alloc(size);
+        if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
+        std::memcpy(host_pool_ + ext, data, size);
+        off = ext | kHostTag;
+    }
+    BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &off, 8, cudaMemcpyHostToDevice, st_));
     BMQ_CUDA(cudaMemcpyAsync(size_.p + id, &size, 8, cudaMemcpyHostToDevice, st_));
     host_ids_to_device({id});
     decompress_ids(ids_.p, 1, true);
@@ -1223,9 +1493,11 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
         BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &prev_off, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaMemcpyAsync(size_.p + id, &prev_size, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
+        if (off & kHostTag) host_heap_.free(off & ~kHostTag, size);
         throw;
     }
-    h_off_[id] = used;
+    free_host_extents(&id, 1);  // the replaced payload, if it was on the host
+    h_off_[id] = off;
     h_size_[id] = size;
     sums_ok_[id] = 1;
     store_.put(id, size);
@@ -1376,7 +1648,7 @@ void Engine::export_payloads(const uint64_t* ids, uint64_t n, uint64_t* meta, vo
     dx.alloc(n);
     BMQ_CUDA(cudaMemcpyAsync(dx.p, xs.data(), n * sizeof(Xfer), cudaMemcpyHostToDevice, st_));
     k_pack_payloads<<<static_cast<uint32_t>(std::min<uint64_t>(n, 148 * 16)), 256, 0, st_>>>(
-        dx.p, n, off_.p, pool_[cur_].p, host_pool_, static_cast<uint8_t*>(dst));
+        dx.p, n, off_.p, arena_.base(), host_pool_, static_cast<uint8_t*>(dst));
     ++counters_.kernel_launches;
     BMQ_CUDA(cudaGetLastError());
     BMQ_CUDA(cudaStreamSynchronize(st_));
@@ -1400,33 +1672,35 @@ void Engine::import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* me
         xs[i] = x;
         pos += (x.size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
     }
-    // place the batch back to back: device arena (after compaction if
-    // needed), else the pinned host arena
-    uint64_t used = 0;
-    BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
-    BMQ_CUDA(cudaStreamSynchronize(st_));
-    if (used + pos > pool_cap_) {
-        compact();
-        BMQ_CUDA(cudaMemcpyAsync(&used, cursor_.p + cur_, 8, cudaMemcpyDeviceToHost, st_));
+    // the ids' previous payloads are replaced: host extents go back first
+    sync_meta_to_host();
+    sync_copies();
+    free_host_extents(ids, n);
+    // the batch back to back in the device arena (after compaction or growth
+    // if needed), else one host-level extent per payload
+    uint8_t* to = arena_.base();
+    uint64_t tag = 0, base = 0;
+    if (make_room(pos, ids, n)) {
+        base = arena_used();
+        const uint64_t end = base + pos;
+        BMQ_CUDA(cudaMemcpyAsync(cursor_.p, &end, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
-    }
-    uint8_t* to = pool_[cur_].p;
-    uint64_t tag = 0, base = used;
-    if (used + pos > pool_cap_) {
+    } else {
         if (!cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
         ensure_host_pool();
-        if (host_cursor_ + pos > host_cap_) raise(BMQ_ERR_STORE, "host payload pool exhausted");
         to = host_pool_;
         tag = kHostTag;
-        base = host_cursor_;
-        host_cursor_ += pos;
+        for (Xfer& x : xs) {
+            if (!x.size) continue;
+            const uint64_t ext = host_heap_.alloc(x.size);
+            if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
+            x.dst = ext;
+        }
         counters_.host_spill_bytes += pos;
         ++counters_.host_spill_batches;
-    } else {
-        const uint64_t end = used + pos;
-        BMQ_CUDA(cudaMemcpyAsync(cursor_.p + cur_, &end, 8, cudaMemcpyHostToDevice, st_));
     }
-    for (Xfer& x : xs) x.dst = base + x.dst;
+    if (!tag)
+        for (Xfer& x : xs) x.dst = base + x.dst;
     DevArray<Xfer> dx;
     dx.alloc(n);
     BMQ_CUDA(cudaMemcpyAsync(dx.p, xs.data(), n * sizeof(Xfer), cudaMemcpyHostToDevice, st_));
@@ -1449,6 +1723,8 @@ void Engine::drop_payloads(const uint64_t* ids, uint64_t n) {
     const uint64_t nid = L_.num_blocks();
     for (uint64_t i = 0; i < n; ++i)
         if (ids[i] >= nid) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(ids[i]));
+    sync_copies();
+    free_host_extents(ids, n);
     DevArray<uint64_t> d;
     d.alloc(n);
     BMQ_CUDA(cudaMemcpyAsync(d.p, ids, n * 8, cudaMemcpyHostToDevice, st_));

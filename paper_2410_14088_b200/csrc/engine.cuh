@@ -6,6 +6,7 @@
 
 #include "codec.cuh"
 #include "gates.cuh"
+#include "store.hpp"
 
 namespace bmq {
 
@@ -167,12 +168,22 @@ private:
     void ensure_init();
     void run_stage(uint64_t s);
     void raw_run_stage(uint64_t s);
-    void process_batch(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk, size_t bidx);
-    void emit_batch(uint64_t nblk);
-    void compact();
-    void maybe_grow_pools();
-    bool pool_auto_ = false, growing_ = false;
-    uint64_t pool_worst_ = 0;
+    void process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t* d_ids, const uint32_t* d_vtab,
+                       uint64_t nblk, size_t bidx);
+    void emit_batch(uint64_t nblk, const uint64_t* h_ids);
+    void emit_to_host(uint64_t nblk, const uint64_t* h_ids);
+
+    // ---- device level (store.hpp DeviceArena): bump cursor cursor_[0],
+    // logical capacity arena_limit_ (mapped >= limit), in-place compaction
+    uint64_t arena_used();
+    // make `need` more bytes available at the cursor: compaction (payloads
+    // of the `excl` ids are dead) and / or growth; false = the device is full
+    bool make_room(uint64_t need, const uint64_t* excl, uint64_t nexcl);
+    void compact(const uint64_t* excl, uint64_t nexcl);
+    bool grow_arena(uint64_t limit);
+    DeviceArena arena_;
+    uint64_t arena_limit_ = 0, arena_max_ = 0;
+    bool arena_grow_ = false;
     void sync_meta_to_host();
     void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
     void host_ids_to_device(const std::vector<uint64_t>& ids);
@@ -201,17 +212,38 @@ private:
     bool identity_ok_ = false;  // codec idempotent on every representable amplitude
     uint64_t next_stage_ = 0;
 
-    // compressed state: an append-only payload arena (compacted into the
-    // other one when full) + per-id metadata (off ~0 = canonical ALL_ZERO)
-    DevArray<uint8_t> pool_[2];
-    uint64_t pool_cap_ = 0;
-    int cur_ = 0;
-    DevArray<uint64_t> cursor_;  // [0..1] arena cursors, [2..3] range scratch, [4] staging cursor
-    // second level: pinned, mapped host arena (payload offsets tagged with
-    // kHostTag), allocated on the first spill; append-only this round
+    // compressed state: payloads in the device arena (16-byte aligned) or in
+    // the pinned host level, per-id metadata (off ~0 = canonical ALL_ZERO,
+    // bit 62 = host-level extent)
+    DevArray<uint64_t> cursor_;  // [0] arena cursor, [1] batch total, [2..3] range, [4] staging cursor, [5] total
+    // ---- host level (store.hpp ExtentHeap): pinned, mapped host arena with
+    // one extent per payload, freed when the block is rewritten
     uint8_t* host_pool_ = nullptr;
-    uint64_t host_cap_ = 0, host_cursor_ = 0;
+    uint64_t host_cap_ = 0;
+    ExtentHeap host_heap_;
     void ensure_host_pool();
+    void free_host_extents(const uint64_t* ids, uint64_t n);
+    // ---- copy streams ("2 streams"): host-level payloads of
+    // batch k+1 are prefetched H2D on cp_in_ while batch k computes on st_,
+    // and payloads of batch k-1 bound for the host are written back D2H from
+    // wb_ on cp_out_
+    cudaStream_t cp_in_ = nullptr, cp_out_ = nullptr;
+    cudaEvent_t ev_pf_[2] = {}, ev_dec_[2] = {}, ev_emit_ = nullptr, ev_wb_ = nullptr;
+    DevArray<uint8_t> pf_[2], wb_;
+    DevArray<uint64_t> pf_off_[2];
+    PinnedVec<uint64_t> h_pf_off_[2];
+    PinnedVec<uint64_t> h_meta_;  // (id, off, size) triples of a host-bound batch
+    DevArray<uint64_t> d_meta_;
+    bool pf_live_[2] = {false, false};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> link_ev_;
+    size_t link_ev_used_ = 0;
+    void link_event_pair(cudaStream_t s, bool start);
+    void collect_link_times();
+    // queue the H2D copies of the host-level payloads of one batch into
+    // prefetch slot `slot`; false = nothing to prefetch
+    bool prefetch(const uint64_t* h_ids, uint64_t nblk, int slot);
+    void copy_batch(void** dst, void** src, size_t* sizes, size_t n, cudaStream_t s);
+    void sync_copies();
     DevArray<uint64_t> off_, size_, new_off_, live_ids_;
     DevArray<double> sums_;       // per id: sumsq, sum_re, sum_im (3 doubles)
     DevArray<uint8_t> zero_hdr_;  // canonical ALL_ZERO payload (+ slack)

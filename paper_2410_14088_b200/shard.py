@@ -254,7 +254,7 @@ _SUMMED = ("groups_processed", "groups_skipped", "blocks_processed", "payload_by
            "dense_bytes", "kernel_launches", "gate_passes", "batches", "decompress_bytes", "gate_bytes",
            "compress_bytes", "fused_batches", "compactions", "host_spill_bytes", "host_spill_batches",
            "code_domain_batches", "pool_growths", "lazy_cx", "perm_materialisations", "model_bytes", "model_groups",
-           "link_h2d_bytes", "link_d2h_bytes", "link_ms")
+           "link_h2d_bytes", "link_d2h_bytes", "link_ms", "compact_bytes", "host_peak_bytes", "arena_bytes")
 
 
 class ShardedSimulator:

@@ -169,6 +169,46 @@ def test_host_spill_is_exact(gpu, port):
             sim.run()
 
 
+def test_host_level_reclaims_rewritten_payloads(gpu, port):
+    """The host level reuses the extents of rewritten payloads: over the run
+    far more payload bytes go to the host than the host arena holds, every
+    stage's host-level payloads are prefetched on the copy stream (H2D) and
+    written back on the other (D2H), and the result is byte-identical."""
+    c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=2))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    biggest = max(len(p) for p in want.payloads)
+    state = sum(len(p) for p in want.payloads)
+    host = 2 * state + 16 * (biggest + 16)
+    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=6 * (biggest + 16), work_bytes=4 * (16 << 12),
+                     host_pool_bytes=host)
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run()
+        d = rep.device
+        assert d["host_spill_bytes"] > host  # more than the arena holds: rewritten payloads were reclaimed
+        assert d["link_h2d_bytes"] > 0 and d["link_d2h_bytes"] > 0
+        assert d["host_peak_bytes"] <= host
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=NORM_RTOL)
+
+
+def test_in_place_compaction_keeps_live_payloads(gpu, port):
+    """A fixed device arena a little larger than the live state: compactions
+    slide the live payloads down in place (directly or through the staging
+    buffer) many times; every payload stays byte-identical."""
+    c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=3))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    state = sum((len(p) + 15) // 16 * 16 for p in want.payloads)
+    biggest = max(len(p) for p in want.payloads)
+    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=state + 5 * (biggest + 16),
+                     work_bytes=4 * (16 << 12))
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run()
+        assert rep.device["compactions"] >= rep.stage_count
+        assert rep.device["compact_bytes"] > 0
+        assert sim.payloads() == want.payloads
+
+
 def test_small_batches_are_exact(gpu, port):
     c = gpu.generate_benchmark("qaoa", 14, gpu.BenchmarkParams(layers=2))
     want = port.simulate(14, [g.as_tuple() for g in c.gates], 9, 2, 1e-3)

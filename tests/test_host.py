@@ -158,3 +158,18 @@ def test_no_cpu_fallback_without_device(cbq):
         cbq.compress_block(np.ones(8), 1e-3)
     with pytest.raises(cbq.NoDeviceError):
         cbq.Simulator(cbq.generate_benchmark("ghz", 4), cbq.Config(block_bits=2))
+
+
+def test_host_level_extent_heap(tmp_path):
+    """ExtentHeap (csrc/store.hpp), the pinned host level's allocator: random
+    alloc / free sequences against a brute-force model (no overlap, best fit,
+    coalesced free list, double frees rejected without damage, full
+    coalescing at the end). Built with g++ from the product source."""
+    exe = tmp_path / "eht"
+    csrc = os.path.join(ROOT, "paper_2410_14088_b200", "csrc")
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT}/include", f"-I{csrc}",
+                    os.path.join(ROOT, "tests", "cpp", "extent_heap_test.cpp"), os.path.join(csrc, "store_host.cpp"),
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "extent_heap ok" in out.stdout
