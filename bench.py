@@ -367,7 +367,9 @@ def roofline(d, t_dev, link):
     b_link = d["link_h2d_bytes"] + d["link_d2h_bytes"]
     bw_link = min(link["h2d_gbs"], link["d2h_gbs"]) if link else None
     t_hbm = b_hbm / (peak * 1e9)
-    t_link = b_link / (bw_link * 1e9) if (bw_link and b_link) else 0.0
+    # the link is full duplex: prefetches (H2D) and write-backs (D2H) overlap
+    t_link = max(d["link_h2d_bytes"] / (link["h2d_gbs"] * 1e9), d["link_d2h_bytes"] / (link["d2h_gbs"] * 1e9)) \
+        if (link and b_link) else 0.0
     bound = "hbm" if t_hbm >= t_link else "link"
     phases = {"decompress": (d["decompress_ms"], d["decompress_bytes"]),
               "gate": (d["gate_ms"], d["gate_bytes"]),
@@ -378,11 +380,11 @@ def roofline(d, t_dev, link):
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(dom)
+                traffic = json.load(f).get(workload_tag(WORKLOAD), {}).get(dom)
         except Exception:
             traffic = None
     achieved = (b_hbm if bound == "hbm" else b_link) / t / 1e9
-    ref_bw = peak if bound == "hbm" else bw_link
+    ref_bw = peak if bound == "hbm" else (b_link / t_link / 1e9 if t_link else bw_link)  # duplex link rate
     return {"bound": bound, "kernel": "stage loop (SURVEY 8(d) model bytes / device-timed simulation)",
             "achieved": achieved, "peak": ref_bw, "unit": "GB/s", "frac": max(t_hbm, t_link) / t,
             "peak_source": peak_kind if bound == "hbm" else "measured pinned copy (bench.py measure_link)",
@@ -558,6 +560,8 @@ def main():
     ap.add_argument("--no-link", action="store_true", help="skip the pinned host-link bandwidth measurement")
     ap.add_argument("--device-pool-gib", type=float, default=0.0,
                     help="fixed device payload arena (GiB); 0 = automatic, growing")
+    ap.add_argument("--arena", default="auto", choices=["auto", "heap", "bump"],
+                    help="device arena placement policy (payload bytes are identical)")
     ap.add_argument("--host-pool-gib", type=float, default=0.0,
                     help="pinned host level of the store (GiB); 0 = none")
     ap.add_argument("--e2e-once", action="store_true", help=argparse.SUPPRESS)
@@ -593,7 +597,7 @@ def main():
     circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
     cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
                      identity_skip=not args.no_identity_skip, device_pool_bytes=int(args.device_pool_gib * 2**30),
-                     host_pool_bytes=int(args.host_pool_gib * 2**30))
+                     host_pool_bytes=int(args.host_pool_gib * 2**30), arena=args.arena)
     sim = cbq.Simulator(circ, cfg)
     stages = len(sim.plan().stages)
     amp_stages = (1 << w["n"]) * stages
@@ -635,7 +639,7 @@ def main():
                    "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
                    "device_pool": f"{args.device_pool_gib:g} GiB fixed" if args.device_pool_gib else "automatic",
-                   "host_pool_gib": args.host_pool_gib,
+                   "host_pool_gib": args.host_pool_gib, "arena": args.arena,
                    "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},
         "sim_time_s": t_dev / 1e3, "wall_ms_median": statistics.median(wall_ms),
         "compression_ratio": rep.compression_ratio, "max_footprint_bytes": rep.max_footprint_bytes,

@@ -110,6 +110,13 @@ typedef struct bmq_config {
  * live state fills more than half of one after a compaction (always the case
  * for automatic sizing, device_pool_bytes == 0). */
 #define BMQ_FLAG_POOL_GROW 0x8u
+/* Device arena placement. Default: one extent per payload from a host-side
+ * best-fit heap when the layout has at most 2^17 blocks (freed when the block
+ * is rewritten: dense stages reuse the space they decode, no compaction), a
+ * bump cursor with in-place compaction for more, smaller blocks. These flags
+ * force either policy (payload bytes are identical). */
+#define BMQ_FLAG_HEAP_ARENA 0x10u
+#define BMQ_FLAG_BUMP_ARENA 0x20u
 
 /* cbq::SimulationReport (engine.hpp:39-53) plus device-side counters. */
 typedef struct bmq_report {

@@ -29,6 +29,8 @@ BMQ_FLAG_ZERO_GROUP_SKIP = 0x1
 BMQ_FLAG_IDENTITY_SKIP = 0x2
 BMQ_FLAG_CODE_DOMAIN = 0x4
 BMQ_FLAG_POOL_GROW = 0x8
+BMQ_FLAG_HEAP_ARENA = 0x10
+BMQ_FLAG_BUMP_ARENA = 0x20
 
 
 class bmq_gate(C.Structure):

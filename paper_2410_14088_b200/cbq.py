@@ -574,6 +574,7 @@ class Config:
     identity_skip: bool = False
     code_domain: bool = True
     pool_grow: bool = False
+    arena: str = "auto"  # device arena placement: "auto", "heap" (extent per payload) or "bump" (cursor + compaction)
     host_pool_bytes: int = 0
 
     def to_c(self) -> bmq_config:
@@ -587,7 +588,8 @@ class Config:
         c.flags = (_lib.BMQ_FLAG_ZERO_GROUP_SKIP if self.zero_group_skip else 0) | \
                   (_lib.BMQ_FLAG_IDENTITY_SKIP if self.identity_skip else 0) | \
                   (_lib.BMQ_FLAG_CODE_DOMAIN if self.code_domain else 0) | \
-                  (_lib.BMQ_FLAG_POOL_GROW if self.pool_grow else 0)
+                  (_lib.BMQ_FLAG_POOL_GROW if self.pool_grow else 0) | \
+                  {"auto": 0, "heap": _lib.BMQ_FLAG_HEAP_ARENA, "bump": _lib.BMQ_FLAG_BUMP_ARENA}[self.arena]
         return c
 
 

@@ -21,6 +21,11 @@ void launch_compress(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uin
 void launch_compress_plan(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
                           const DevTables& t, BlockPlan* d_bp, ChunkPlan* d_cp, bool have_pk, DevError* d_err,
                           uint64_t* launches);
+// edge zeroing + emit: every BlockPlan::out_off already holds its payload's
+// device address (~0 = virtual ALL_ZERO)
+void launch_compress_emit_placed(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
+                                 const DevTables& t, BlockPlan* d_bp, ChunkPlan* d_cp, DevError* d_err,
+                                 uint64_t* launches);
 void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
                           const DevTables& t, uint8_t* out, uint64_t out_cap, uint64_t* d_cursor, uint64_t* d_range,
                           BlockPlan* d_bp, ChunkPlan* d_cp, uint64_t* meta_off, uint64_t* meta_size,

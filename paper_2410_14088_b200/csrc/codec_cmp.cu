@@ -332,24 +332,40 @@ __global__ void __launch_bounds__(kAllocThreads) k_cmp_alloc(const CmpBlock* __r
     }
 }
 
-__global__ void k_zero_range(uint8_t* base, const uint64_t* range) {
-    const uint64_t a = range[0], b = range[1];
-    if (b <= a) return;
-    const uint64_t wa = (a + 3) / 4, wb = b / 4;  // whole words [wa, wb)
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    uint32_t* w = reinterpret_cast<uint32_t*>(base);
-    if (wa < wb) {
-        for (uint64_t i = wa + tid; i < wb; i += stride) w[i] = 0;
-        if (tid < 4) {
-            const uint64_t x = a + tid;
-            if (x < wa * 4) base[x] = 0;
-            const uint64_t y = wb * 4 + tid;
-            if (y < b) base[y] = 0;
-        }
-    } else if (tid < b - a) {
-        base[a + tid] = 0;
-    }
+// ----------------------------------------------------------- edge zeroing
+// The emit stores every payload byte outright except the first and last
+// 32-bit word of each bit segment it writes (sign / zero raw bitmaps, a
+// chunk's code stream): neighbouring segments share those and OR into them
+// (write_bits_block). Zeroing just those words before the emit replaces a
+// zeroing pass over the whole output. out == nullptr: out_off are addresses.
+__device__ __forceinline__ void zero_seg_edges(uint8_t* dst, uint32_t bit0, uint64_t nbits) {
+    if (nbits == 0) return;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+    uint32_t* w = reinterpret_cast<uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t s = static_cast<uint32_t>(a & 3) * 8 + bit0;
+    const uint64_t nout = (s + nbits + 31) / 32;
+    w[0] = 0;
+    w[nout - 1] = 0;
+}
+
+__global__ void k_zero_edges(const CmpBlock* __restrict__ blks, uint32_t nch_max, const ChunkPlan* __restrict__ cps,
+                             const BlockPlan* __restrict__ bps, uint8_t* out, uint64_t nblk, const DevError* err) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (t >= nblk * nch_max || err->code) return;
+    const uint64_t bi = t / nch_max;
+    const uint32_t c = static_cast<uint32_t>(t % nch_max);
+    const BlockPlan bp = bps[bi];
+    if (bp.out_off == ~0ull || (bp.flags & 1) || c >= bp.nch) return;
+    const ChunkPlan p = cps[t];
+    const uint32_t len = chunk_len(blks[bi].count, c);
+    if (p.nnz == 0 && len == kChunk) return;  // tags only
+    uint8_t* pay = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(out) + bp.out_off);
+    const uint32_t raw_bits = ((len + 7) / 8) * 8;
+    if (p.stag == 2) zero_seg_edges(pay + p.sign_off, 0, raw_bits);
+    if (p.ztag == 2) zero_seg_edges(pay + p.zero_off, 0, raw_bits);
+    const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix) * bp.width;
+    zero_seg_edges(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7),
+                   static_cast<uint64_t>(p.nnz) * bp.width);
 }
 
 // ----------------------------------------------------------------- emit
@@ -496,7 +512,8 @@ __global__ void __launch_bounds__(kChunkThreads, 9) k_cmp_emit(const CmpBlock* _
     if (failed) return;
     if (c > 0 && c >= bp.nch) return;  // (an empty block still gets its header from chunk 0)
     if (bp.out_off == ~0ull) return;   // virtual ALL_ZERO
-    uint8_t* pay = out + bp.out_off;
+    // (out == nullptr: out_off is the payload's device address, placed by the caller)
+    uint8_t* pay = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(out) + bp.out_off);
     const int tid = threadIdx.x;
     if (c == 0 && tid == 0) {  // header (codec.hpp:282-286)
         uint64_t v[3];
@@ -567,11 +584,26 @@ void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk
     if (nblk == 0) return;
     k_cmp_alloc<<<1, kAllocThreads, 0, st>>>(d_blks, nblk, d_bp, d_cursor, out_cap, d_range, virtual_zero ? 1 : 0,
                                              align, meta_off, meta_size, meta_base, meta_tag, d_err);
-    k_zero_range<<<296, 256, 0, st>>>(out, d_range);
+    const uint64_t nthr = nblk * nch_max;
+    k_zero_edges<<<static_cast<uint32_t>((nthr + 255) / 256), 256, 0, st>>>(d_blks, nch_max, d_cp, d_bp, out, nblk,
+                                                                          d_err);
     k_cmp_emit<<<static_cast<uint32_t>(nblk * nch_max), kChunkThreads, 0, st>>>(d_blks, nch_max, d_cp, d_bp, out, t,
                                                                                  d_err);
     BMQ_CUDA(cudaGetLastError());
     if (launches) *launches += 3;
+}
+
+void launch_compress_emit_placed(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max,
+                                 const DevTables& t, BlockPlan* d_bp, ChunkPlan* d_cp, DevError* d_err,
+                                 uint64_t* launches) {
+    if (nblk == 0) return;
+    const uint64_t nthr = nblk * nch_max;
+    k_zero_edges<<<static_cast<uint32_t>((nthr + 255) / 256), 256, 0, st>>>(d_blks, nch_max, d_cp, d_bp, nullptr, nblk,
+                                                                          d_err);
+    k_cmp_emit<<<static_cast<uint32_t>(nblk * nch_max), kChunkThreads, 0, st>>>(d_blks, nch_max, d_cp, d_bp, nullptr,
+                                                                                 t, d_err);
+    BMQ_CUDA(cudaGetLastError());
+    if (launches) *launches += 2;
 }
 
 void launch_compress(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,

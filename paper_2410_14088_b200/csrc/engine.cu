@@ -174,6 +174,27 @@ __global__ void k_move_payloads(const Move* __restrict__ mv, uint64_t n, const u
     }
 }
 
+// Heap-mode placement: per block the payload size (~0: virtual ALL_ZERO) for
+// the host allocator, then the chosen places back into the plans and metadata
+__global__ void k_plan_sizes(const BlockPlan* __restrict__ bps, uint64_t n, uint64_t* out) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = (bps[i].flags & 1) ? ~0ull : bps[i].size;
+}
+
+// place[2i]: the payload's device address (arena or write-back staging),
+// place[2i + 1]: its metadata offset (arena offset, or host extent | tag)
+__global__ void k_place(BlockPlan* __restrict__ bps, const CmpBlock* __restrict__ blks, uint64_t n,
+                        const uint64_t* __restrict__ place, uint64_t* off, uint64_t* size) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    BlockPlan& p = bps[i];
+    const uint64_t id = blks[i].id;
+    const bool virt = (p.flags & 1) != 0;
+    p.out_off = virt ? ~0ull : place[2 * i];
+    off[id] = virt ? ~0ull : place[2 * i + 1];
+    size[id] = p.size;
+}
+
 // (id, off, size) triples -> per-id metadata (host-level batches)
 __global__ void k_set_meta(const uint64_t* __restrict__ t, uint64_t n, uint64_t* off, uint64_t* size) {
     const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -510,6 +531,10 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
                                                    : std::min<uint64_t>({24ull << 30, total_b / 8, arena_max_});
     if (!arena_.grow_to(initial + 64)) raise(BMQ_ERR_OUT_OF_MEMORY, "device payload arena: out of memory");
     arena_limit_ = initial;
+    heap_mode_ = (cfg.flags & BMQ_FLAG_HEAP_ARENA) != 0;
+    arena_auto_ = !(cfg.flags & (BMQ_FLAG_HEAP_ARENA | BMQ_FLAG_BUMP_ARENA)) && nid <= (1ull << 17);
+    h_place_.assign(2 * max_blocks_, 0);
+    d_place_.alloc(2 * max_blocks_);
     BMQ_CUDA(cudaStreamCreateWithFlags(&cp_in_, cudaStreamNonBlocking));
     BMQ_CUDA(cudaStreamCreateWithFlags(&cp_out_, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
@@ -574,8 +599,8 @@ bool Engine::grow_arena(uint64_t limit) {
     if (!arena_grow_ || limit > arena_max_) return false;
     // grow by at least a quarter, so a run grows O(log) times
     const uint64_t want = std::min(arena_max_, std::max(limit, arena_limit_ + arena_limit_ / 4));
-    if (!arena_.grow_to(want + 64) && !arena_.grow_to(limit + 64)) return false;
     const uint64_t before = arena_.mapped();
+    if (!arena_.grow_to(want + 64) && !arena_.grow_to(limit + 64)) return false;
     arena_limit_ = std::min<uint64_t>(arena_.mapped() - 64, std::max(limit, want));
     device_peak_ += arena_.mapped() > before ? arena_.mapped() - before : 0;
     ++counters_.pool_growths;
@@ -595,8 +620,11 @@ void Engine::compact(const uint64_t* excl, uint64_t nexcl) {
     std::vector<uint8_t> dead(nid, 0);
     for (uint64_t i = 0; i < nexcl; ++i) dead[excl[i]] = 1;
     std::vector<uint64_t> live;
-    for (uint64_t id = 0; id < nid; ++id)
-        if (!dead[id] && h_off_[id] != ~0ull && !(h_off_[id] & kHostTag)) live.push_back(id);
+    for (uint64_t id = 0; id < nid; ++id) {
+        const bool dev = h_off_[id] != ~0ull && !(h_off_[id] & kHostTag);
+        if (dev && dead[id]) h_off_[id] = ~0ull;  // the batch in flight decoded it: gone (its emit rewrites it)
+        if (dev && !dead[id]) live.push_back(id);
+    }
     std::sort(live.begin(), live.end(), [&](uint64_t x, uint64_t y) { return h_off_[x] < h_off_[y]; });
     const auto bytes_of = [&](uint64_t id) { return (h_size_[id] + kArenaAlign - 1) / kArenaAlign * kArenaAlign; };
     struct Seg {
@@ -666,6 +694,14 @@ void Engine::compact(const uint64_t* excl, uint64_t nexcl) {
     }
     BMQ_CUDA(cudaMemcpyAsync(cursor_.p, &dst, 8, cudaMemcpyHostToDevice, st_));
     BMQ_CUDA(cudaStreamSynchronize(st_));
+    // automatic policy: a live state that fills a quarter of the arena is
+    // rewritten at a cost this compaction just paid; from here on every
+    // payload gets its own extent instead (no further compactions)
+    if (arena_auto_ && !heap_mode_ && 4 * dst >= arena_limit_) heap_mode_ = true;
+    if (heap_mode_) {  // the live payloads now fill [0, dst)
+        dev_heap_.reset(arena_limit_, kArenaAlign);
+        if (dst) dev_heap_.alloc(dst);
+    }
     ++counters_.compactions;
     counters_.compact_bytes += moved;
 }
@@ -737,6 +773,11 @@ void Engine::init_state() {
     sums_ok_.assign(nid, 1);
     sums_ok_[0] = 0;
     sync_meta_to_host();
+    heap_mode_ = (cfg_.flags & BMQ_FLAG_HEAP_ARENA) != 0;  // each run starts on the configured policy
+    if (heap_mode_) {  // block 0's payload sits at offset 0
+        dev_heap_.reset(arena_limit_, kArenaAlign);
+        if (h_off_[0] != ~0ull) dev_heap_.alloc(h_size_[0]);
+    }
     store_.put(0, h_size_[0]);
     if (nid > 1) store_.put_shared(1, nid, kHeaderBytes);  // one zero payload, counted once
     initialized_ = true;
@@ -809,12 +850,13 @@ void Engine::raw_run_stage(uint64_t s) {
 // does not fit, make room (compaction / growth, the batch's old payloads are
 // dead) and try again; a batch that still does not fit goes to the host level.
 void Engine::emit_batch(uint64_t nblk, const uint64_t* h_ids) {
+    if (heap_mode_) return emit_placed(nblk, h_ids);
     for (int attempt = 0; attempt < 3; ++attempt) {
         launch_compress_emit(st_, cmp_.p, nblk, nch_, *tabs_, arena_.base(), arena_limit_, cursor_.p, cursor_.p + 2,
                              bplan_.p, cplan_.p, off_.p, size_.p, true, kArenaAlign, err_.p,
                              &counters_.kernel_launches);
         if (peek_error() != DE_POOL_FULL) {
-            free_host_extents(h_ids, nblk);
+            free_extents(h_ids, nblk);
             return;
         }
         BMQ_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(DevError), st_));
@@ -822,6 +864,7 @@ void Engine::emit_batch(uint64_t nblk, const uint64_t* h_ids) {
         BMQ_CUDA(cudaMemcpyAsync(&need, cursor_.p + 1, 8, cudaMemcpyDeviceToHost, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
         if (!make_room(need, h_ids, nblk)) break;
+        if (heap_mode_) return emit_placed(nblk, h_ids);  // the compaction switched the arena policy
     }
     if (!cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
     emit_to_host(nblk, h_ids);
@@ -850,7 +893,7 @@ void Engine::emit_to_host(uint64_t nblk, const uint64_t* h_ids) {
     BMQ_CUDA(cudaMemcpyAsync(bp.data(), bplan_.p, nblk * sizeof(BlockPlan), cudaMemcpyDeviceToHost, st_));
     BMQ_CUDA(cudaEventRecord(ev_emit_, st_));
     BMQ_CUDA(cudaStreamSynchronize(st_));
-    free_host_extents(h_ids, nblk);  // the batch's old payloads were decoded
+    free_extents(h_ids, nblk);  // the batch's old payloads were decoded
     h_meta_.assign(3 * nblk, 0);
     std::vector<void*> dst, src;
     std::vector<size_t> len;
@@ -889,15 +932,111 @@ void Engine::emit_to_host(uint64_t nblk, const uint64_t* h_ids) {
     ++counters_.host_spill_batches;
 }
 
-void Engine::free_host_extents(const uint64_t* ids, uint64_t n) {
-    if (!host_pool_) return;
+void Engine::free_extents(const uint64_t* ids, uint64_t n) {
+    if (!host_pool_ && !heap_mode_) return;
     for (uint64_t i = 0; i < n; ++i) {
         const uint64_t o = h_off_[ids[i]];
-        if (o != ~0ull && (o & kHostTag)) {
+        if (o == ~0ull) continue;
+        if (o & kHostTag)
             host_heap_.free(o & ~kHostTag, h_size_[ids[i]]);
-            h_off_[ids[i]] = ~0ull;  // until the next metadata sync
-        }
+        else if (heap_mode_)
+            dev_heap_.free(o, h_size_[ids[i]]);
+        else
+            continue;  // bump mode: garbage until the next compaction
+        h_off_[ids[i]] = ~0ull;  // until the next metadata sync
     }
+}
+
+uint64_t Engine::dev_alloc(uint64_t size) {
+    uint64_t off = dev_heap_.alloc(size);
+    if (off != ExtentHeap::kNone) return off;
+    if (!grow_arena(arena_limit_ + size + kArenaAlign)) return ExtentHeap::kNone;
+    dev_heap_.extend(arena_limit_);
+    return dev_heap_.alloc(size);
+}
+
+// Heap mode: the batch's payload sizes come back to the host (the batch's old
+// payloads, already decoded, are freed first), every payload gets an arena
+// extent, or a host extent through the write-back staging buffer when the
+// device is full, and the emit writes each payload in place.
+void Engine::emit_placed(uint64_t nblk, const uint64_t* h_ids) {
+    k_plan_sizes<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, nblk, d_place_.p);
+    ++counters_.kernel_launches;
+    BMQ_CUDA(cudaMemcpyAsync(h_place_.data(), d_place_.p, nblk * 8, cudaMemcpyDeviceToHost, st_));
+    BMQ_CUDA(cudaStreamSynchronize(st_));
+    std::vector<uint64_t> sz(h_place_.data(), h_place_.data() + nblk);
+    free_extents(h_ids, nblk);
+    std::vector<uint64_t> dev(nblk, ExtentHeap::kNone);
+    std::vector<uint64_t> to_host;
+    for (int attempt = 0;; ++attempt) {
+        to_host.clear();
+        for (uint64_t i = 0; i < nblk; ++i)
+            if (sz[i] != ~0ull && (dev[i] = dev_alloc(sz[i])) == ExtentHeap::kNone) to_host.push_back(i);
+        if (to_host.empty() || cfg_.host_pool_bytes || attempt > 0) break;
+        // no host level: defragment once (the batch's ids hold nothing yet)
+        for (uint64_t i = 0; i < nblk; ++i)
+            if (dev[i] != ExtentHeap::kNone) dev_heap_.free(dev[i], sz[i]);
+        compact(h_ids, nblk);
+    }
+    if (!to_host.empty() && !cfg_.host_pool_bytes) raise(BMQ_ERR_STORE, "device payload pool exhausted");
+    uint8_t* staging = nullptr;
+    std::vector<void*> dst, src;
+    std::vector<size_t> len;
+    uint64_t total = 0;
+    if (!to_host.empty()) {
+        ensure_host_pool();
+        uint64_t need = 0;
+        for (uint64_t i : to_host) need += (sz[i] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+        staging = need <= wb_.bytes() ? wb_.p : reinterpret_cast<uint8_t*>(work_.p);  // work_ is dead until the next decode
+        if (need > work_.bytes()) raise(BMQ_ERR_STORE, "payload batch exceeds the staging buffer");
+        BMQ_CUDA(cudaStreamWaitEvent(st_, ev_wb_, 0));  // the previous write-back has left the staging buffer
+    }
+    uint64_t pos = 0;
+    size_t th = 0;
+    for (uint64_t i = 0; i < nblk; ++i) {
+        const uint64_t id = h_ids[i];
+        uint64_t addr = 0, meta = ~0ull;
+        if (sz[i] == ~0ull) {
+            h_size_[id] = kHeaderBytes;
+        } else if (dev[i] != ExtentHeap::kNone) {
+            addr = reinterpret_cast<uint64_t>(arena_.base()) + dev[i];
+            meta = dev[i];
+            h_size_[id] = sz[i];
+        } else {
+            const uint64_t ext = host_heap_.alloc(sz[i]);
+            if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
+            addr = reinterpret_cast<uint64_t>(staging) + pos;
+            meta = ext | kHostTag;
+            dst.push_back(host_pool_ + ext);
+            src.push_back(staging + pos);
+            len.push_back(sz[i]);
+            total += sz[i];
+            pos += (sz[i] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+            ++th;
+        }
+        h_place_[2 * i] = addr;
+        h_place_[2 * i + 1] = meta;
+        h_off_[id] = meta;
+    }
+    BMQ_CUDA(cudaMemcpyAsync(d_place_.p, h_place_.data(), 2 * nblk * 8, cudaMemcpyHostToDevice, st_));
+    k_place<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, cmp_.p, nblk, d_place_.p, off_.p, size_.p);
+    launch_compress_emit_placed(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, err_.p,
+                                &counters_.kernel_launches);
+    ++counters_.kernel_launches;
+    if (th) {
+        BMQ_CUDA(cudaEventRecord(ev_emit_, st_));
+        BMQ_CUDA(cudaStreamWaitEvent(cp_out_, ev_emit_, 0));
+        link_event_pair(cp_out_, true);
+        copy_batch(dst.data(), src.data(), len.data(), dst.size(), cp_out_);
+        link_event_pair(cp_out_, false);
+        BMQ_CUDA(cudaEventRecord(ev_wb_, cp_out_));
+        if (staging != wb_.p) BMQ_CUDA(cudaStreamWaitEvent(st_, ev_wb_, 0));  // the next decode overwrites work_
+        counters_.host_spill_bytes += total;
+        counters_.link_d2h_bytes += total;
+        ++counters_.host_spill_batches;
+    }
+    // (h_place_ is read by the H2D copy above; the next batch's emit only
+    // rewrites it after a D2H copy into it on st_ has completed)
 }
 
 void Engine::ensure_host_pool() {
@@ -1466,7 +1605,15 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
     // decodes), else a host-level extent
     const uint64_t prev_off = h_off_[id], prev_size = h_size_[id];
     uint64_t off = ~0ull;
-    if (make_room(size + kArenaAlign, nullptr, 0)) {
+    if (heap_mode_) {
+        sync_copies();
+        off = dev_alloc(size);
+        if (off != ExtentHeap::kNone)
+            BMQ_CUDA(cudaMemcpyAsync(arena_.base() + off, data, size, cudaMemcpyHostToDevice, st_));
+    }
+    if (heap_mode_ && off != ExtentHeap::kNone) {
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+    } else if (!heap_mode_ && make_room(size + kArenaAlign, nullptr, 0)) {
         const uint64_t used = arena_used();
         off = used;
         BMQ_CUDA(cudaMemcpyAsync(arena_.base() + used, data, size, cudaMemcpyHostToDevice, st_));
@@ -1493,10 +1640,13 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
         BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &prev_off, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaMemcpyAsync(size_.p + id, &prev_size, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
-        if (off & kHostTag) host_heap_.free(off & ~kHostTag, size);
+        if (off & kHostTag)
+            host_heap_.free(off & ~kHostTag, size);
+        else if (heap_mode_)
+            dev_heap_.free(off, size);
         throw;
     }
-    free_host_extents(&id, 1);  // the replaced payload, if it was on the host
+    free_extents(&id, 1);  // the replaced payload, if it was on the host
     h_off_[id] = off;
     h_size_[id] = size;
     sums_ok_[id] = 1;
@@ -1675,12 +1825,15 @@ void Engine::import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* me
     // the ids' previous payloads are replaced: host extents go back first
     sync_meta_to_host();
     sync_copies();
-    free_host_extents(ids, n);
+    free_extents(ids, n);
     // the batch back to back in the device arena (after compaction or growth
     // if needed), else one host-level extent per payload
     uint8_t* to = arena_.base();
     uint64_t tag = 0, base = 0;
-    if (make_room(pos, ids, n)) {
+    const uint64_t ext = heap_mode_ && pos ? dev_alloc(pos) : ExtentHeap::kNone;
+    if (heap_mode_ && (ext != ExtentHeap::kNone || !pos)) {
+        base = pos ? ext : 0;
+    } else if (!heap_mode_ && make_room(pos, ids, n)) {
         base = arena_used();
         const uint64_t end = base + pos;
         BMQ_CUDA(cudaMemcpyAsync(cursor_.p, &end, 8, cudaMemcpyHostToDevice, st_));
@@ -1724,7 +1877,7 @@ void Engine::drop_payloads(const uint64_t* ids, uint64_t n) {
     for (uint64_t i = 0; i < n; ++i)
         if (ids[i] >= nid) raise(BMQ_ERR_STORE, "unknown block id " + std::to_string(ids[i]));
     sync_copies();
-    free_host_extents(ids, n);
+    free_extents(ids, n);
     DevArray<uint64_t> d;
     d.alloc(n);
     BMQ_CUDA(cudaMemcpyAsync(d.p, ids, n * 8, cudaMemcpyHostToDevice, st_));

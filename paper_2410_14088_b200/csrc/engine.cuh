@@ -184,6 +184,17 @@ private:
     DeviceArena arena_;
     uint64_t arena_limit_ = 0, arena_max_ = 0;
     bool arena_grow_ = false;
+    // Heap mode (large blocks, few ids): every payload gets its own arena
+    // extent from dev_heap_, freed when the block is rewritten, so dense
+    // stages reuse the space of the payloads they decoded (no compaction);
+    // a batch whose payloads do not all fit sends the rest to the host level.
+    // Bump mode (many small payloads): cursor_[0] + in-place compaction.
+    bool heap_mode_ = false, arena_auto_ = false;  // auto: bump until a compaction finds a dense state
+    ExtentHeap dev_heap_;
+    uint64_t dev_alloc(uint64_t size);  // heap mode; ExtentHeap::kNone when the device is full
+    void emit_placed(uint64_t nblk, const uint64_t* h_ids);
+    PinnedVec<uint64_t> h_place_;
+    DevArray<uint64_t> d_place_;
     void sync_meta_to_host();
     void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
     void host_ids_to_device(const std::vector<uint64_t>& ids);
@@ -222,7 +233,9 @@ private:
     uint64_t host_cap_ = 0;
     ExtentHeap host_heap_;
     void ensure_host_pool();
-    void free_host_extents(const uint64_t* ids, uint64_t n);
+    // the payload extents of rewritten / dropped ids: host level, and the
+    // device arena in heap mode
+    void free_extents(const uint64_t* ids, uint64_t n);
     // ---- copy streams ("2 streams"): host-level payloads of
     // batch k+1 are prefetched H2D on cp_in_ while batch k computes on st_,
     // and payloads of batch k-1 bound for the host are written back D2H from

@@ -660,6 +660,11 @@ __device__ __forceinline__ uint64_t planar_addr(uint64_t p, uint32_t lb, uint64_
 constexpr int kFastThreads = 256;
 constexpr int kPer = 16;  // tile positions per thread: k = tid + 256 j
 
+// kParMask[m] bit j = parity(m & j), j < 16: the parity of a tile row's bits
+// 8..11 (m) over the row index j of k = tid + 256 j
+__constant__ uint32_t kParMask[16] = {0x0000, 0xaaaa, 0xcccc, 0x6666, 0xf0f0, 0x5a5a, 0x3c3c, 0x9696,
+                                      0xff00, 0x55aa, 0x33cc, 0x9966, 0x0ff0, 0xa55a, 0xc33c, 0x6996};
+
 // Diagonal ops [q0, q1) on one amplitude with full buffer index x; chain
 // phase tables live in shared memory (stab).
 // Walk the set bits of s in the chain's program order, multiplying by the
@@ -989,7 +994,10 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             }
             continue;
         }
-        bool owners_only = true;
+        // barrier scope owed by the ops since the last barrier: 0 = every
+        // thread touched only its own positions (tid + 256 j), 1 = positions
+        // of its warp, 2 = any position of the tile
+        uint32_t scope = 0;
         uint32_t cvec = 0;  // lazy CX: affine part of the tile's index map
         for (uint32_t i = 0; i < pass.nops;) {
             const FastOp& g = sops[i];
@@ -1016,7 +1024,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                 for (int j = 0; j < kPer; ++j) tile_s[tid + 256u * j] = v[j];
                 cvec = 0;
                 if (S) S = 0x80000fffu;  // (conservative: the map moved the support)
-                owners_only = true;
+                scope = 0;
                 ++i;
                 continue;
             }
@@ -1068,8 +1076,9 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                         continue;
                     }
                 }
-                if (!owners_only) __syncthreads();
-                owners_only = true;
+                if (scope == 2) __syncthreads();
+                else if (scope == 1) __syncwarp();
+                scope = 0;
                 if (S == 0) {  // an all-zero tile: nothing to do
                     i = i2;
                     continue;
@@ -1086,7 +1095,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                         const C2 o = apply_diag_run(sops, stab, i, i2, xb, C2{v.x, v.y}, cvec_in, k);
                         tile_s[k] = make_double2(o.re, o.im);
                     }
-                    owners_only = false;
+                    scope = 2;
                     i = i2;
                     continue;
                 }
@@ -1114,7 +1123,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                             const C2 o = chain_walk(x & R, desc, tab, C2{v.x, v.y});
                             tile_s[k] = make_double2(o.re, o.im);
                         }
-                        owners_only = false;
+                        scope = 2;
                     } else if (active) {
                         __syncthreads();  // positions cross thread ownership
                         const uint32_t rounds = (pc >= 0 ? 2048u : 4096u) / (256u * kLanesPerStep);
@@ -1124,7 +1133,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                             else
                                 chain_walk8<false>(tile_s, tab, tid, xlo, lut_lo, lut_hi, pc, R, plan, rd);
                         }
-                        owners_only = false;
+                        scope = 2;
                     }
                 } else if (!run_chain) {
                     // plain diagonal gates: op by op, each a branch-free
@@ -1154,11 +1163,17 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                             const uint32_t cl = !cd ? 1u
                                                     : (o.in_lo ? (cv >> o.tp_lo) & 1u
                                                                : static_cast<uint32_t>((xbase >> o.lo) & 1));
+                            // bit j of `on`: amplitude k = tid + 256 j takes entry u1. A
+                            // row's parity over k splits into the thread's bits (tid)
+                            // and the row index j (kParMask), so the per-amplitude
+                            // test is one bit of a per-op mask
+                            const uint32_t ph = (__popc(rh & tid) ^ ch) & 1u, pl = (__popc(rl & tid) ^ cl) & 1u;
+                            const uint32_t on = ((kParMask[(rh >> 8) & 15u] ^ (0u - ph)) &
+                                                 (kParMask[(rl >> 8) & 15u] ^ (0u - pl))) >> h;
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const uint32_t k = tid + 256u * (h + j);
-                                const bool on = ((__popc(rh & k) ^ ch) & (__popc(rl & k) ^ cl) & 1u) != 0;
-                                a[j] = cmul(on ? r1 : r0, on ? i1 : i0, a[j]);
+                                const bool b = (on >> j) & 1u;
+                                a[j] = cmul(b ? r1 : r0, b ? i1 : i0, a[j]);
                             }
                         }
 #pragma unroll
@@ -1177,57 +1192,80 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
             }
             ++i;
             if (S == 0) continue;  // zeros map to zeros (tile-uniform)
-            __syncthreads();
-            owners_only = false;
             // U2 on logical tile bit t: physical pairs (x, x ^ dvec); x is
             // the |0> side when parity(mrow & x) ^ c_t is 0
             const uint32_t dv = g.dvec, piv = __ffs(dv) - 1, ct = (cvec >> g.tp_hi) & 1u;
-            if (S == 0) continue;  // zeros map to zeros
             const uint32_t S2 = (S | dv) & 0xfffu;
             const bool dense = __popc(S2) == 12;  // (11 support bits: 1024 pairs, none all-zero by construction)
             const uint32_t npairs = dense ? 2048u : (1u << (__popc(S2) - 1)), pm = S2 & ~(1u << piv);
             S = S2 | 0x80000000u;
+            // Dense sweeps pair positions inside the smallest owner set that
+            // holds both partners: a thread's own 16 positions (dvec in tile
+            // bits 8..11), its warp's 512 (bits 0..4 and 8..11), else the
+            // tile; the barrier before the sweep only spans that set and what
+            // earlier ops touched since the last one.
+            const uint32_t lvl = !dense ? 2u : (!(dv & 0xffu) ? 0u : (!(dv & 0xe0u) ? 1u : 2u));
+            const uint32_t need = scope > lvl ? scope : lvl;
+            if (need == 2) __syncthreads();
+            else if (need == 1) __syncwarp();
+            scope = lvl;
+            const uint32_t lane = tid & 31u, wbase = tid & ~31u;
             // (op fields are read into registers once: tile_s stores could alias sops)
             const uint32_t mrow = g.mrow;
+            // visit every pair of this thread: sparse, tile-, warp- or thread-local enumeration
+            const auto sweep = [&](auto&& body) {
+                if (!dense) {
+                    for (uint32_t r = tid; r < npairs; r += kFastThreads) body(deposit12(r, pm));
+                } else if (lvl == 2) {
+#pragma unroll 2
+                    for (uint32_t m = 0; m < 8; ++m) body(insert0(tid + kFastThreads * m, piv));
+                } else if (lvl == 1) {  // warp-local index: bits 0..4 lanes, 5..8 rows (tile bits 8..11)
+#pragma unroll 2
+                    for (uint32_t m = 0; m < 8; ++m) {
+                        const uint32_t u = insert0(lane + 32u * m, piv);
+                        body((u & 31u) | wbase | ((u >> 5) << 8));
+                    }
+                } else {
+#pragma unroll 2
+                    for (uint32_t m = 0; m < 8; ++m) body(tid + 256u * insert0(m, piv - 8));
+                }
+            };
             if (g.pad) {  // all entries real: u*a = (u*ar, u*ai) exactly
                 const double u00 = g.m[0], u01 = g.m[2], u10 = g.m[4], u11 = g.m[6];
-                const auto pair = [&](uint32_t x0, bool skip_zero) {
+                sweep([&](uint32_t x0) {
                     const uint32_t x1 = x0 ^ dv;
                     const bool sw = (__popc(mrow & x0) ^ ct) & 1u;
                     const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
                     const double2 v0 = tile_s[i0], v1 = tile_s[i1];
                     // a pair of exact zeros maps to zeros (+-0 for the codec); only
                     // worth testing in full sweeps, where S may be a loose superset
-                    if (skip_zero && v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) return;
+                    if (dense && v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) return;
                     tile_s[i0] = make_double2(__dadd_rn(__dmul_rn(u00, v0.x), __dmul_rn(u01, v1.x)),
                                               __dadd_rn(__dmul_rn(u00, v0.y), __dmul_rn(u01, v1.y)));
                     tile_s[i1] = make_double2(__dadd_rn(__dmul_rn(u10, v0.x), __dmul_rn(u11, v1.x)),
                                               __dadd_rn(__dmul_rn(u10, v0.y), __dmul_rn(u11, v1.y)));
-                };
-                if (dense)
-                    for (uint32_t r = tid; r < npairs; r += kFastThreads) pair(insert0(r, piv), true);
-                else
-                    for (uint32_t r = tid; r < npairs; r += kFastThreads) pair(deposit12(r, pm), false);
+                });
             } else {
                 uint8_t et[4];
                 double m[8];
                 memcpy(et, g.et, sizeof et);
                 memcpy(m, g.m, sizeof m);
-                for (uint32_t r = tid; r < npairs; r += kFastThreads) {
-                    const uint32_t x0 = dense ? insert0(r, piv) : deposit12(r, pm), x1 = x0 ^ dv;
+                sweep([&](uint32_t x0) {
+                    const uint32_t x1 = x0 ^ dv;
                     const bool sw = (__popc(mrow & x0) ^ ct) & 1u;
                     const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
                     const double2 v0 = tile_s[i0], v1 = tile_s[i1];
-                    if (v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) continue;
+                    if (v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) return;
                     const C2 a0{v0.x, v0.y}, a1{v1.x, v1.y};
                     const C2 o0 = row2(et, m, 0, a0, a1), o1 = row2(et, m, 1, a0, a1);
                     tile_s[i0] = make_double2(o0.re, o0.im);
                     tile_s[i1] = make_double2(o1.re, o1.im);
-                }
+                });
             }
         }
         const bool gather = pass.final_perm || cvec;  // logical y lives at M^-1 (y ^ c)
-        if (!owners_only || gather) __syncthreads();
+        if (scope == 2 || gather) __syncthreads();
+        else if (scope == 1) __syncwarp();
         if (quant.pk) {
             quant_epilogue(quant, tile_s, tid, pbt, pjoff, jnew, lb, gather, cvec, gat_lo, gat_hi);
             continue;

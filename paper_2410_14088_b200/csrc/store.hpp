@@ -30,6 +30,8 @@ public:
     // equals); kNone when no extent is large enough
     uint64_t alloc(uint64_t size);
     void free(uint64_t off, uint64_t size);
+    // grow the capacity to `capacity` (the new tail is free)
+    void extend(uint64_t capacity);
     uint64_t capacity() const { return cap_; }
     uint64_t used() const { return used_; }
     uint64_t high_water() const { return high_; }

@@ -66,6 +66,15 @@ void ExtentHeap::free(uint64_t off, uint64_t size) {
     insert(off, len);
 }
 
+void ExtentHeap::extend(uint64_t capacity) {
+    const uint64_t cap = capacity / align_ * align_;
+    if (cap <= cap_) return;
+    const uint64_t old = cap_;
+    cap_ = cap;
+    used_ += cap - old;  // the new tail enters as one allocated extent and is freed (coalescing)
+    free(old, cap - old);
+}
+
 bool ExtentHeap::check() const {
     uint64_t end = 0, free_total = 0;
     bool first = true;

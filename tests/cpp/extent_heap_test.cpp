@@ -3,7 +3,8 @@
 // Checks that live extents never overlap and stay inside the capacity, that
 // the free list stays coalesced and sums to capacity - used, that alloc fails
 // only when no free extent is large enough (best fit), that a double free is
-// rejected, and that freeing everything coalesces back to one extent.
+// rejected, that growth adds a free tail, and that freeing everything
+// coalesces back to one extent.
 #include <cstdio>
 #include <map>
 #include <random>
@@ -67,6 +68,9 @@ int main() {
             CHECK(threw);
             live.erase(live.begin());
         }
+        const uint64_t before = h.capacity(), grown = before + 16 * (1 + rng() % 4096);  // the new tail is free
+        h.extend(grown);
+        CHECK(h.capacity() == grown && h.check() && h.largest_free() >= grown - before);
         for (auto& [o, s] : live) h.free(o, s);
         CHECK(h.used() == 0 && h.extents() == 1 && h.largest_free() == h.capacity() && h.check());
     }

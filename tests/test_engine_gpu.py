@@ -138,14 +138,15 @@ def test_arena_compaction_is_exact(gpu, port):
     want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
     biggest = max(len(p) for p in want.payloads)
     pool = 24 * (biggest + 16)  # the live state plus about two batches
-    with gpu.Simulator(c, gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool,
+    with gpu.Simulator(c, gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, arena="bump",
                                      work_bytes=4 * (16 << 12))) as sim:
         rep = sim.run()
         assert rep.device["compactions"] > 0
         assert sim.payloads() == want.payloads
 
 
-def test_host_spill_is_exact(gpu, port):
+@pytest.mark.parametrize("arena", ["heap", "bump"])
+def test_host_spill_is_exact(gpu, port, arena):
     """Two-level store (store.hpp:47-300): with a device arena far smaller than
     the live state, payloads land in the pinned host arena and are read back
     from there by the next stage; the result is unchanged byte for byte."""
@@ -154,7 +155,7 @@ def test_host_spill_is_exact(gpu, port):
     biggest = max(len(p) for p in want.payloads)
     pool = 6 * (biggest + 16)  # about one batch: most payloads must go to the host
     cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, work_bytes=4 * (16 << 12),
-                     host_pool_bytes=64 << 20)
+                     host_pool_bytes=64 << 20, arena=arena)
     with gpu.Simulator(c, cfg) as sim:
         rep = sim.run()
         assert rep.device["host_spill_batches"] > 0
@@ -163,13 +164,14 @@ def test_host_spill_is_exact(gpu, port):
         for i in (0, 3, 15):
             assert sim.get_payload(i) == want.payloads[i]
         assert abs(sim.state_norm() - want.report["final_norm"]) <= NORM_RTOL * want.report["final_norm"]
-    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, work_bytes=4 * (16 << 12))
+    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, work_bytes=4 * (16 << 12), arena=arena)
     with gpu.Simulator(c, cfg) as sim:
         with pytest.raises(gpu.StoreError):
             sim.run()
 
 
-def test_host_level_reclaims_rewritten_payloads(gpu, port):
+@pytest.mark.parametrize("arena", ["heap", "bump"])
+def test_host_level_reclaims_rewritten_payloads(gpu, port, arena):
     """The host level reuses the extents of rewritten payloads: over the run
     far more payload bytes go to the host than the host arena holds, every
     stage's host-level payloads are prefetched on the copy stream (H2D) and
@@ -180,7 +182,7 @@ def test_host_level_reclaims_rewritten_payloads(gpu, port):
     state = sum(len(p) for p in want.payloads)
     host = 2 * state + 16 * (biggest + 16)
     cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=6 * (biggest + 16), work_bytes=4 * (16 << 12),
-                     host_pool_bytes=host)
+                     host_pool_bytes=host, arena=arena)
     with gpu.Simulator(c, cfg) as sim:
         rep = sim.run()
         d = rep.device
@@ -201,12 +203,42 @@ def test_in_place_compaction_keeps_live_payloads(gpu, port):
     state = sum((len(p) + 15) // 16 * 16 for p in want.payloads)
     biggest = max(len(p) for p in want.payloads)
     cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=state + 5 * (biggest + 16),
-                     work_bytes=4 * (16 << 12))
+                     work_bytes=4 * (16 << 12), arena="bump")
     with gpu.Simulator(c, cfg) as sim:
         rep = sim.run()
         assert rep.device["compactions"] >= rep.stage_count
         assert rep.device["compact_bytes"] > 0
         assert sim.payloads() == want.payloads
+
+
+def test_heap_arena_reuses_decoded_extents(gpu, port):
+    """Heap-mode arena (one extent per payload, freed when its block is
+    rewritten): a fixed arena only a few payloads larger than the live state
+    runs every dense stage without compaction or host spill, byte-exact."""
+    c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=3))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    state = sum((len(p) + 15) // 16 * 16 for p in want.payloads)
+    biggest = max(len(p) for p in want.payloads)
+    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=state + 8 * (biggest + 16),
+                     work_bytes=4 * (16 << 12), arena="heap")
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run()
+        assert rep.device["host_spill_bytes"] == 0
+        assert rep.device["compactions"] <= 1
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+
+
+@pytest.mark.parametrize("arena", ["heap", "bump"])
+@pytest.mark.parametrize("name,layers", [("qft", 1), ("qaoa3reg", 2), ("random", 12)])
+def test_arena_policies_are_exact(gpu, port, arena, name, layers):
+    """Both device-arena policies on automatic sizing give the oracle's bytes."""
+    c = gpu.generate_benchmark(name, 16, gpu.BenchmarkParams(layers=layers, seed=3))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 10, 2, 1e-3)
+    with gpu.Simulator(c, gpu.Config(block_bits=10, inner_size=2, arena=arena, work_bytes=8 * (16 << 10))) as sim:
+        rep = sim.run()
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
 
 
 def test_small_batches_are_exact(gpu, port):
@@ -375,7 +407,8 @@ def test_code_domain_qft_swaps(gpu, port):
         assert sim.fidelity_analytic("uniform") == pytest.approx(abs(amps.sum()) / np.sqrt(len(amps)), rel=1e-9)
 
 
-def test_pool_growth_is_exact(gpu, port):
+@pytest.mark.parametrize("arena", ["heap", "bump"])
+def test_pool_growth_is_exact(gpu, port, arena):
     """Arenas that start small double after compactions (BMQ_FLAG_POOL_GROW);
     payloads stay byte-identical to the oracle."""
     c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=2))
@@ -383,7 +416,7 @@ def test_pool_growth_is_exact(gpu, port):
     biggest = max(len(p) for p in want.payloads)
     pool = 8 * (biggest + 16)
     with gpu.Simulator(c, gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, pool_grow=True,
-                                     work_bytes=4 * (16 << 12))) as sim:
+                                     work_bytes=4 * (16 << 12), arena=arena)) as sim:
         rep = sim.run()
         assert rep.device["pool_growths"] > 0
         assert sim.payloads() == want.payloads
