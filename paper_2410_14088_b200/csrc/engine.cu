@@ -1060,14 +1060,17 @@ void Engine::ensure_host_pool() {
 }
 
 void Engine::copy_batch(void** dst, void** src, size_t* sizes, size_t n, cudaStream_t s) {
-    if (!n) return;
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t idx = 0, fail = 0;
-    if (cudaMemcpyBatchAsync(dst, src, sizes, n, &attr, &idx, 1, &fail, s) == cudaSuccess) return;
-    cudaGetLastError();  // driver without batched copies: one call per payload
-    for (size_t i = 0; i < n; ++i) BMQ_CUDA(cudaMemcpyAsync(dst[i], src[i], sizes[i], cudaMemcpyDefault, s));
+    // one cudaMemcpyAsync per run of payloads that are contiguous on both
+    // sides (extents are placed in id order, so most batches collapse to a
+    // few large copies)
+    size_t i = 0;
+    while (i < n) {
+        char* d = static_cast<char*>(dst[i]);
+        char* a = static_cast<char*>(src[i]);
+        size_t len = sizes[i++];
+        while (i < n && static_cast<char*>(dst[i]) == d + len && static_cast<char*>(src[i]) == a + len) len += sizes[i++];
+        if (len) BMQ_CUDA(cudaMemcpyAsync(d, a, len, cudaMemcpyDefault, s));
+    }
 }
 
 void Engine::link_event_pair(cudaStream_t s, bool start) {

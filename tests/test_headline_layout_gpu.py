@@ -61,7 +61,11 @@ def test_b20_matches_reference(gpu, port, case, identity_skip):
         assert rep.spilled_blocks == want["spilled_blocks"]
         assert rep.stage_compress_calls == want["stage_compress_calls"]
         assert rep.stage_decompress_calls == want["stage_decompress_calls"]
-        assert rep.final_norm == pytest.approx(want["final_norm"], rel=NORM_RTOL)
+        # payloads are byte-identical (above), so the states are equal; the
+        # norms differ only by summation order: the reference adds std::norm
+        # serially over 2^n amplitudes (engine.hpp:150-158), whose rounding
+        # error is bounded by 2^n * 2^-53 relative (1.9e-9 at n = 24)
+        assert rep.final_norm == pytest.approx(want["final_norm"], rel=max(NORM_RTOL, 2.0 ** (case["n"] - 53)))
         if want.get("has_fidelity"):
             f = sim.fidelity_dense(gpu.dense_reference(c))
             assert abs(f - want["fidelity"]) <= FIDELITY_ATOL
