@@ -117,6 +117,9 @@ typedef struct bmq_config {
  * force either policy (payload bytes are identical). */
 #define BMQ_FLAG_HEAP_ARENA 0x10u
 #define BMQ_FLAG_BUMP_ARENA 0x20u
+/* Plan with bmq_plan_device_aware (this device's work buffer and HBM, world
+ * 1, inner_size as the cap) instead of partition_circuit(inner_size). */
+#define BMQ_FLAG_DEVICE_PLAN 0x40u
 
 /* cbq::SimulationReport (engine.hpp:39-53) plus device-side counters. */
 typedef struct bmq_report {
@@ -204,6 +207,39 @@ int bmq_generate_benchmark(const char* name, uint32_t num_qubits, uint32_t layer
 /* partition_circuit (partition.hpp:59-101). */
 int bmq_partition(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, uint32_t block_bits,
                   uint32_t inner_size, bmq_stage* out, uint64_t cap, uint64_t* num_stages);
+
+/* Device-aware planning (optional). partition_circuit's
+ * inner_size is a fixed user knob; this picks it for the device: it builds
+ * partition_circuit(circuit, block_bits, k) for every feasible k (group
+ * buffer 2^(b+k) complex doubles <= work_bytes, k <= c - log2(world),
+ * k <= max_inner when nonzero) and keeps the plan whose modelled time is
+ * least: per stage, the HBM bytes of this engine's decode -> tile passes ->
+ * quantise -> emit trip (passes counted as gates.cu splits them) at hbm_gbs,
+ * plus stage_overhead_s, plus (world > 1) the payload remaps of the shard
+ * plan at link_gbs. The result is always a partition_circuit plan, so the
+ * reference replays it with inner_size = choice->inner_size. */
+typedef struct bmq_plan_model {
+    uint64_t work_bytes;      /* group buffer budget (bytes) */
+    double hbm_gbs;           /* per-GPU HBM bandwidth */
+    double link_gbs;          /* per-GPU peer bandwidth for remaps (world > 1) */
+    double ratio;             /* expected compression ratio (payload bytes = 16 / ratio per amplitude) */
+    double stage_overhead_s;  /* fixed cost per stage (launches, syncs) */
+    uint32_t world;           /* GPUs (power of two) */
+    uint32_t max_inner;       /* 0 = no cap */
+} bmq_plan_model;
+typedef struct bmq_plan_choice {
+    uint32_t inner_size;      /* chosen k */
+    uint32_t candidates;      /* entries of inner / model_s */
+    uint64_t stages, passes;  /* of the chosen plan */
+    uint32_t remaps, reserved;
+    double model_s_best;
+    uint32_t inner[16];
+    double model_s[16];
+} bmq_plan_choice;
+void bmq_plan_model_default(bmq_plan_model* model);
+int bmq_plan_device_aware(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, uint32_t block_bits,
+                          const bmq_plan_model* model, bmq_stage* out, uint64_t cap, uint64_t* num_stages,
+                          bmq_plan_choice* choice);
 
 /* enumerate_groups (partition.hpp:120-153): block ids row-major
  * (group o, inner value v) -> ids[o * 2^|inner| + v]. */

@@ -31,6 +31,7 @@ BMQ_FLAG_CODE_DOMAIN = 0x4
 BMQ_FLAG_POOL_GROW = 0x8
 BMQ_FLAG_HEAP_ARENA = 0x10
 BMQ_FLAG_BUMP_ARENA = 0x20
+BMQ_FLAG_DEVICE_PLAN = 0x40
 
 
 class bmq_gate(C.Structure):
@@ -49,6 +50,18 @@ class bmq_config(C.Structure):
                 ("verify_cap_qubits", C.c_uint32), ("device", C.c_int32), ("device_pool_bytes", C.c_uint64),
                 ("work_bytes", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32),
                 ("host_pool_bytes", C.c_uint64)]
+
+
+class bmq_plan_model(C.Structure):
+    _fields_ = [("work_bytes", C.c_uint64), ("hbm_gbs", C.c_double), ("link_gbs", C.c_double),
+                ("ratio", C.c_double), ("stage_overhead_s", C.c_double), ("world", C.c_uint32),
+                ("max_inner", C.c_uint32)]
+
+
+class bmq_plan_choice(C.Structure):
+    _fields_ = [("inner_size", C.c_uint32), ("candidates", C.c_uint32), ("stages", C.c_uint64),
+                ("passes", C.c_uint64), ("remaps", C.c_uint32), ("reserved", C.c_uint32),
+                ("model_s_best", C.c_double), ("inner", C.c_uint32 * 16), ("model_s", C.c_double * 16)]
 
 
 class bmq_report(C.Structure):
@@ -87,6 +100,9 @@ SIGNATURES = {
     "bmq_gate_unitary": (C.c_int, [C.POINTER(bmq_gate), _P]),
     "bmq_circuit_validate": (C.c_int, [_U32, _P, _U64]),
     "bmq_generate_benchmark": (C.c_int, [C.c_char_p, _U32, _U32, _U64, C.c_char_p, _P, _U64, C.POINTER(_U64)]),
+    "bmq_plan_model_default": (None, [C.POINTER(bmq_plan_model)]),
+    "bmq_plan_device_aware": (C.c_int, [_U32, _P, _U64, _U32, C.POINTER(bmq_plan_model), _P, _U64, C.POINTER(_U64),
+                                        C.POINTER(bmq_plan_choice)]),
     "bmq_partition": (C.c_int, [_U32, _P, _U64, _U32, _U32, _P, _U64, C.POINTER(_U64)]),
     "bmq_enumerate_groups": (C.c_int, [_U32, _U32, C.POINTER(bmq_stage), _P, _U64, C.POINTER(_U64)]),
     "bmq_buffer_bit_of_qubit": (C.c_int, [_U32, _U32, C.POINTER(bmq_stage), _U32, C.POINTER(_U32)]),

@@ -373,6 +373,41 @@ def partition_circuit(circuit: Circuit, block_bits: int, inner_size: int) -> Par
 
 
 @dataclass
+class PlanChoice:
+    """What plan_device_aware chose and the modelled time of every candidate."""
+    inner_size: int
+    stages: int
+    passes: int
+    remaps: int
+    model_s: float
+    candidates: dict  # inner size -> modelled seconds
+
+
+def plan_device_aware(circuit: Circuit, block_bits: int, *, work_bytes: int = 16 << 30, hbm_gbs: float = 6500.0,
+                      link_gbs: float = 700.0, ratio: float = 4.0, stage_overhead_s: float = 100e-6,
+                      world: int = 1, max_inner: int = 0):
+    """Device-aware staging (bmq_plan_device_aware): the
+    partition_circuit plan (partition.hpp:59-101) at the inner size this
+    engine's cost model prefers for the device; returns (PartitionPlan,
+    PlanChoice). Replaying it in the reference needs inner_size =
+    choice.inner_size."""
+    layout = make_layout(circuit.num_qubits, block_bits)
+    m = _lib.bmq_plan_model()
+    lib.bmq_plan_model_default(C.byref(m))
+    m.work_bytes, m.hbm_gbs, m.link_gbs, m.ratio = work_bytes, hbm_gbs, link_gbs, ratio
+    m.stage_overhead_s, m.world, m.max_inner = stage_overhead_s, world, max_inner
+    cap = max(1, len(circuit.gates))
+    out = (bmq_stage * cap)()
+    ns = C.c_uint64()
+    ch = _lib.bmq_plan_choice()
+    _check(lib.bmq_plan_device_aware(circuit.num_qubits, circuit.c_array(), len(circuit.gates), block_bits,
+                                     C.byref(m), out, cap, C.byref(ns), C.byref(ch)))
+    choice = PlanChoice(ch.inner_size, ch.stages, ch.passes, ch.remaps, ch.model_s_best,
+                        {ch.inner[i]: ch.model_s[i] for i in range(ch.candidates)})
+    return PartitionPlan(layout, ch.inner_size, [Stage.from_c(out[i]) for i in range(ns.value)]), choice
+
+
+@dataclass
 class SVGroup:
     outer_value: int = 0
     block_ids: list = field(default_factory=list)
@@ -576,6 +611,7 @@ class Config:
     pool_grow: bool = False
     arena: str = "auto"  # device arena placement: "auto", "heap" (extent per payload) or "bump" (cursor + compaction)
     host_pool_bytes: int = 0
+    device_plan: bool = False  # plan with plan_device_aware (inner_size = cap) instead of partition_circuit
 
     def to_c(self) -> bmq_config:
         c = bmq_config()
@@ -589,6 +625,7 @@ class Config:
                   (_lib.BMQ_FLAG_IDENTITY_SKIP if self.identity_skip else 0) | \
                   (_lib.BMQ_FLAG_CODE_DOMAIN if self.code_domain else 0) | \
                   (_lib.BMQ_FLAG_POOL_GROW if self.pool_grow else 0) | \
+                  (_lib.BMQ_FLAG_DEVICE_PLAN if self.device_plan else 0) | \
                   {"auto": 0, "heap": _lib.BMQ_FLAG_HEAP_ARENA, "bump": _lib.BMQ_FLAG_BUMP_ARENA}[self.arena]
         return c
 

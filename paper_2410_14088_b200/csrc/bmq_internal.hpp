@@ -42,6 +42,11 @@ Layout make_layout(uint32_t n, uint32_t b);
 std::vector<bmq_stage> partition_plan(uint32_t n, const bmq_gate* gates, uint64_t count,
                                       uint32_t block_bits, uint32_t inner_size);
 
+// Device-aware plan: partition_plan at the inner size the
+// engine's cost model prefers for this device (bmq_plan_device_aware).
+std::vector<bmq_stage> plan_device_aware(uint32_t n, const bmq_gate* gates, uint64_t count, uint32_t block_bits,
+                                         const bmq_plan_model& model, bmq_plan_choice* choice);
+
 // Group geometry of one stage: block id of (outer value o, inner value v) is
 // pdep(o, outer_mask) | pdep(v, inner_mask) over the c global-index bits.
 struct GroupGeometry {

@@ -108,6 +108,29 @@ int bmq_partition(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, ui
     });
 }
 
+void bmq_plan_model_default(bmq_plan_model* model) {
+    if (!model) return;
+    *model = bmq_plan_model{};
+    model->work_bytes = 16ull << 30;  // the engine's automatic work buffer on a B200
+    model->hbm_gbs = 6500.0;          // measured copy bandwidth (MEASURED_PEAKS.json)
+    model->link_gbs = 700.0;          // NVLink 5 per GPU and direction, after protocol
+    model->ratio = 4.0;
+    model->stage_overhead_s = 100e-6;
+    model->world = 1;
+}
+
+int bmq_plan_device_aware(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, uint32_t block_bits,
+                          const bmq_plan_model* model, bmq_stage* out, uint64_t cap, uint64_t* num_stages,
+                          bmq_plan_choice* choice) {
+    return guarded([&] {
+        null_check(model, "model");
+        const auto plan = bmq::plan_device_aware(num_qubits, gates, count, block_bits, *model, choice);
+        *num_stages = plan.size();
+        if (plan.size() > cap) bmq::raise(BMQ_ERR_BUFFER_TOO_SMALL, "stage buffer too small");
+        std::memcpy(out, plan.data(), plan.size() * sizeof(bmq_stage));
+    });
+}
+
 int bmq_enumerate_groups(uint32_t num_qubits, uint32_t block_bits, const bmq_stage* stage, uint64_t* ids,
                          uint64_t cap, uint64_t* count) {
     return guarded([&] {

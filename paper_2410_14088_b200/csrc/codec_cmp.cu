@@ -20,6 +20,7 @@
 
 #include <cfloat>
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -118,6 +119,29 @@ const DevTables& device_tables(double b_r) {
     t.b_r = h.b_r;
     t.inv_ba = 1.0 / h.b_a;
     t.est_eps = 1e-6 * t.inv_ba + 1e-6;
+    {
+        // quantize_pack_f32: x = e * inv_ba + lg * inv_ba with e * fH exact,
+        // u = e * fL + frac(e * fH), s = lg * finv + u, q = floor(e * fH) + rint(s).
+        // Error of s against log2|v| / b_a - floor(e * fH): the double estimate's
+        // bound (lg2 approximation, mantissa truncation, reference rounding),
+        // finv's rounding (lg < 1), fL's rounding times |e| <= 1074, and one
+        // ulp for each of the two float FMAs.
+        int ex = 0;
+        const double f = std::frexp(t.inv_ba, &ex);
+        const double H = std::ldexp(std::nearbyint(std::ldexp(f, 13)), ex - 13);
+        const double L = t.inv_ba - H;
+        const auto ulp32 = [](double z) { return std::ldexp(1.0, std::ilogb(std::max(z, 1e-30)) - 23); };
+        const double umax = 1.0 + 1074.0 * std::fabs(L), smax = umax + t.inv_ba + 1.0;
+        const double eps = t.est_eps + t.inv_ba * 0x1p-24 + 1074.0 * std::fabs(L) * 0x1p-24 + ulp32(umax) + ulp32(smax);
+        t.fH = static_cast<float>(H);
+        t.fL = static_cast<float>(L);
+        t.finv = static_cast<float>(t.inv_ba);
+        float tie = static_cast<float>(0.5 - eps);
+        if (static_cast<double>(tie) > 0.5 - eps) tie = std::nextafter(tie, 0.0f);
+        t.ftie = tie;
+        t.qlo32 = static_cast<int32_t>(std::max<int64_t>(h.qlo, INT32_MIN));
+        t.f32 = (eps < 0.05 && static_cast<double>(t.fH) == H && h.qlo >= -(1ll << 30) && h.qhi <= (1ll << 30)) ? 1u : 0u;
+    }
     return cache.emplace(std::make_pair(dev, key), t).first->second;
 }
 
@@ -136,22 +160,36 @@ __global__ void __launch_bounds__(kChunkThreads) k_cmp_stats(const CmpBlock* __r
     const double* src = blk.in + static_cast<uint64_t>(c) * kChunk;
     uint32_t* dst = blk.pk + static_cast<uint64_t>(c) * kChunk;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    ChunkAcc acc;
+    RowAcc acc;
     bool bad = false, oow = false;
     const double qlo_d = static_cast<double>(t.qlo);
     const int span = static_cast<int>(t.qhi - t.qlo);
+    if (len == kChunk) {  // full chunk: every lane holds a word in every row
 #pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t s = 128 * j + 32 * w + lane;
-        if (s < len) {
-            const uint32_t pk = quantize_pack_fast(__ldg(src + s), t, qlo_d, span, bad, oow);
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t s = 128 * j + 32 * w + lane;
+            const double v = __ldg(src + s);
+            const uint32_t pk = t.f32 ? quantize_pack_f32(v, t, span, bad, oow)
+                                      : quantize_pack_fast(v, t, qlo_d, span, bad, oow);
             dst[s] = pk;
             acc.add(pk);
+        }
+    } else {
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t s = 128 * j + 32 * w + lane;
+            if (s < len) {
+                const uint32_t pk = quantize_pack_fast(__ldg(src + s), t, qlo_d, span, bad, oow);
+                dst[s] = pk;
+                acc.add(pk);
+            }
         }
     }
     if (bad) dev_fail(err, DE_NONFINITE, bi);
     if (oow) dev_fail(err, DE_WINDOW, bi);
-    flush_chunk(cps + static_cast<uint64_t>(bi) * nch_max + c, acc);
+    // words this warp quantised (a lane past len adds none: RowAcc's identity)
+    uint32_t mine = 0;
+    for (int j = 0; j < 32; ++j) mine += (128u * j + 32u * w) < len ? min(32u, len - (128u * j + 32u * w)) : 0u;
+    flush_rows(cps + static_cast<uint64_t>(bi) * nch_max + c, acc, mine);
 }
 
 // ----------------------------------------------------------------- plan

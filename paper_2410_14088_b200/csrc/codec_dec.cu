@@ -455,6 +455,42 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
                 __stcs(reinterpret_cast<double2*>(dst + s0 + 2), make_double2(v[2], v[3]));
             }
         }
+    } else if (kMode == kDoubles && len == kChunk && !check && width <= 30 && nnz_chunk == kChunk) {
+        // No zero in the chunk, wider codes: scalar s has rank s, its code at
+        // bit cb0 + s w. Eight words per round: all code fetches, then all
+        // dequantisation gathers (the latency-bound part) in flight together.
+        const uintptr_t cs = reinterpret_cast<uintptr_t>(codes);
+        const uint64_t cb = static_cast<uint64_t>(cs & 3) * 8 + static_cast<uint64_t>(d.nz_prefix) * width;
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3)) + (cb >> 5);
+        const uint32_t cb0 = static_cast<uint32_t>(cb & 31), cmask = (1u << width) - 1;
+        const uint32_t qb = static_cast<uint32_t>(qbase);
+        const int lane = tid & 31, w = tid >> 5;
+        if (gflag && tid < 128) gflag[tid] = 1;  // zero-free chunk
+#pragma unroll 1
+        for (int h = 0; h < 32; h += 8) {
+            uint32_t code[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t a = cb0 + (32u * (4u * (h + e) + w) + lane) * width;
+                code[e] = __funnelshift_r(__ldg(cw + (a >> 5)), __ldg(cw + (a >> 5) + 1), a & 31) & cmask;
+            }
+            double m[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) m[e] = __ldg(t.dequant + (qb + code[e]));
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t k = 4u * (h + e) + w, sidx = 32u * k + lane;
+                const double v = ((s_sign[k] >> lane) & 1u) ? -m[e] : m[e];
+                if (sums) {
+                    sq += m[e] * m[e];
+                    if (g0 + sidx < half)
+                        sre += v;
+                    else
+                        sim += v;
+                }
+                __stcs(dst + sidx, v);
+            }
+        }
     } else if (len == kChunk && !check)
         dec_scalars<kMode, true, false>(s_sign, s_nz, s_pre, codes, width, d.nz_prefix, len, qbase, lo, hi, t, dst,
                                         cdst, half, g0, sums, sq, sre, sim, bad, gflag);

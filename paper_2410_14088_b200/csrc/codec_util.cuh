@@ -111,4 +111,81 @@ __device__ __forceinline__ uint32_t quantize_pack_fast(double v, const DevTables
     return pack_code(qoff, v < 0.0, false);
 }
 
+// The exact settling of quantize_pack_fast for a scalar whose estimate is
+// near a half-integer or outside the window (about 2 est_eps of them):
+// probe the two neighbouring thresholds, else search.
+__device__ __forceinline__ uint32_t quantize_settle(double v, uint64_t bits, int qoff, int span, const DevTables& t,
+                                                 bool& oow) {
+    uint32_t qo = static_cast<uint32_t>(min(max(qoff, 0), span));
+    const uint64_t lo = __ldg(t.thresh + qo), hi = __ldg(t.thresh + qo + 1);
+    if (!(bits >= lo && bits < hi)) qo = static_cast<uint32_t>(quantize(v, t, oow) - t.qlo);
+    return qo;
+}
+
+// quantize_pack_fast with a single-precision estimate (t.f32): with
+// v = m 2^e (m in [1, 2)), log2|v| / b_a = e fH + e fL + log2(m) / b_a where
+// e fH is exact in float, so q = floor(e fH) + rint(s) for
+// s = log2(m) finv + (e fL + frac(e fH)) whenever s lies more than
+// 0.5 - ftie from a half-integer (DevTables::ftie, codec_cmp.cu). Zeros,
+// subnormals, infinities and NaNs leave through one unsigned range test.
+__device__ __forceinline__ float lg2_approx(float m) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(m));
+    return r;
+}
+__device__ __forceinline__ uint32_t quantize_pack_f32(double v, const DevTables& t, int span, bool& bad, bool& oow) {
+    const uint32_t hi = static_cast<uint32_t>(__double2hiint(v)), lo = static_cast<uint32_t>(__double2loint(v));
+    const uint32_t ahi = hi & 0x7fffffffu;
+    if (ahi - 0x00100000u >= 0x7fe00000u) [[unlikely]] {  // not a normal number
+        if (ahi >= 0x7ff00000u) {
+            bad = true;
+            return 1u;
+        }
+        if ((ahi | lo) == 0u) return 1u;
+        return pack_code(static_cast<uint32_t>(quantize(v, t, oow) - t.qlo), (hi >> 31) != 0u, false);
+    }
+    const float ef = static_cast<float>(static_cast<int>(ahi >> 20) - 1023);
+    const float m = __int_as_float(0x3f800000 | (__funnelshift_l(lo, ahi, 3) & 0x7fffffu));
+    const float P = __fmul_rn(ef, t.fH);  // exact
+    const float Pi = floorf(P);
+    const float u = __fmaf_rn(ef, t.fL, __fsub_rn(P, Pi));
+    const float s = __fmaf_rn(lg2_approx(m), t.finv, u);
+    const float r = rintf(s);
+    const int qoff = __float2int_rz(Pi) + __float2int_rz(r) - t.qlo32;
+    uint32_t qo = static_cast<uint32_t>(qoff);
+    if (!(fabsf(__fsub_rn(s, r)) < t.ftie && qo <= static_cast<uint32_t>(span))) [[unlikely]]
+        qo = quantize_settle(v, (static_cast<uint64_t>(ahi) << 32) | lo, qoff, span, t, oow);
+    return (qo << 2) | ((hi >> 30) & 2u);
+}
+
+// Per-thread counters of one chunk over packed words, reduced per warp with
+// REDUX at the flush (ChunkAcc's fields, cheaper per scalar):
+//   mn = min over words of (pk ^ 1) - 1  (a zero word 1 -> 0xffffffff, else pk)
+//   mx = max over words of pk            (a zero word 1 never exceeds a code)
+//   zn = zero words + (negative words << 16)
+struct RowAcc {
+    uint32_t mn = ~0u, mx = 0, zn = 0;
+    __device__ __forceinline__ void add(uint32_t pk) {
+        mn = min(mn, (pk ^ 1u) - 1u);
+        mx = max(mx, pk);
+        zn += (pk & 1u) | ((pk & 2u) << 15);
+    }
+};
+
+// Warp flush of RowAcc over `scalars` words (all 32 lanes call, same cp).
+__device__ __forceinline__ void flush_rows(ChunkPlan* cp, const RowAcc& a, uint32_t scalars) {
+    const uint32_t mn = __reduce_min_sync(0xffffffffu, a.mn), mx = __reduce_max_sync(0xffffffffu, a.mx);
+    const uint32_t zn = __reduce_add_sync(0xffffffffu, a.zn);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nnz = scalars - (zn & 0xffffu), nneg = zn >> 16;
+    if (lane < 4u && nnz) {
+        if (lane == 0) atomicMax(&cp->qmin_inv, kQOffMax - (mn >> 2));
+        else if (lane == 1) atomicMax(&cp->qmax_off, mx >> 2);
+        else if (lane == 2) atomicAdd(&cp->nnz, nnz);
+        else if (nneg) atomicAdd(&cp->nneg, nneg);
+    } else if (lane == 3u && nneg) {
+        atomicAdd(&cp->nneg, nneg);
+    }
+}
+
 }  // namespace bmq

@@ -61,6 +61,12 @@ struct DevTables {
     double b_r;               // relative bound written into headers
     double inv_ba;            // 1 / b_a, estimate only
     double est_eps;           // bound on |estimate - log2(v)/b_a| (see quantize_estimate_x)
+    // Single-precision estimate (quantize_pack_f32): 1 / b_a = fH + fL with
+    // fH carrying 13 significant bits, so e * fH is exact in float for every
+    // binary exponent e (|e| < 2^11); ftie = 0.5 - (its error bound).
+    float fH, fL, finv, ftie;
+    int32_t qlo32;            // qlo (fits: |q| < 2^31 whenever f32 is set)
+    uint32_t f32;             // the float estimate is usable for this bound
 };
 
 // Device copy of host_tables(b_r) on the current device (cached).

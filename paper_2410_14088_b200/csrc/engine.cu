@@ -403,7 +403,15 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     check_circuit(n, gates, ngates);
     gates_.assign(gates, gates + ngates);
     L_ = make_layout(n, cfg.block_bits);
-    plan_ = partition_plan(n, gates, ngates, cfg.block_bits, cfg.inner_size);
+    if (cfg.flags & BMQ_FLAG_DEVICE_PLAN) {
+        bmq_plan_model pm;
+        bmq_plan_model_default(&pm);
+        if (cfg.work_bytes) pm.work_bytes = cfg.work_bytes;
+        pm.max_inner = cfg.inner_size;
+        plan_ = plan_device_aware(n, gates, ngates, cfg.block_bits, pm, &plan_choice_);
+    } else {
+        plan_ = partition_plan(n, gates, ngates, cfg.block_bits, cfg.inner_size);
+    }
     if (!(cfg.error_bound > 0.0) || std::isinf(cfg.error_bound))
         raise(BMQ_ERR_INVALID_ARGUMENT, "relative error bound must be positive and finite");
     if (cfg.workers < 1) raise(BMQ_ERR_INVALID_ARGUMENT, "worker count must be at least 1");
@@ -1176,6 +1184,14 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t*
                             &qo, d_vtab, nblk, zf, nch_, zf ? imnz_.p : nullptr);
     }
     phase_event(4 * bidx + 2);
+    if (getenv("BMQ_DBG_CPLAN")) {  // development aid: the quantiser's chunk counters
+        std::vector<ChunkPlan> h(nblk * nch_);
+        BMQ_CUDA(cudaMemcpyAsync(h.data(), cplan_.p, h.size() * sizeof(ChunkPlan), cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        for (size_t i = 0; i < h.size() && i < 64; ++i)
+            fprintf(stderr, "chunk %zu: qmin_inv %u qmax %u nnz %u nneg %u\n", i, h[i].qmin_inv, h[i].qmax_off, h[i].nnz,
+                    h[i].nneg);
+    }
     launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,
                          &counters_.kernel_launches);
     emit_batch(nblk, h_ids);

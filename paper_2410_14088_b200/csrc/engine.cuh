@@ -213,6 +213,7 @@ private:
     bmq_config cfg_;
     std::vector<bmq_gate> gates_;
     std::vector<bmq_stage> plan_;
+    bmq_plan_choice plan_choice_{};  // BMQ_FLAG_DEVICE_PLAN: the planner's choice
     std::vector<std::unique_ptr<StagePlan>> stage_plans_;
     const DevTables* tabs_ = nullptr;
     int dev_ = 0;

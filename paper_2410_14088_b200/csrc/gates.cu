@@ -468,6 +468,66 @@ void lazify(std::vector<FastOp>& fops, FastPass& fp, uint32_t& ncx, uint32_t& np
 
 }  // namespace
 
+// Register-streaming form of a pass (see StreamPass), or null when the pass
+// needs the tiled kernel: other op types (U4; phase chains are formed from
+// CDIAG runs, which stream op by op), more than two mixing bits above bit 4,
+// or too many ops for per-amplitude application to beat the tile's chains.
+static std::shared_ptr<StreamPass> make_stream(const std::vector<GateOp>& ops, uint32_t begin, uint32_t end,
+                                        uint32_t total_bits) {
+    if (total_bits < 12 || end - begin > static_cast<uint32_t>(kMaxStreamOps)) return nullptr;
+    uint64_t R = 0;
+    for (uint32_t i = begin; i < end; ++i) {
+        const uint8_t t = ops[i].type;
+        if (t != OP_U2 && t != OP_DIAG && t != OP_CDIAG && t != OP_CX) return nullptr;
+        R |= mixing_bits(ops[i]) & ~31ull;
+    }
+    if (__builtin_popcountll(R) > kStreamNQ) return nullptr;
+    uint64_t Q = R;
+    for (uint32_t b = 5; __builtin_popcountll(Q) < kStreamNQ; ++b) Q |= 1ull << b;
+    auto sp = std::make_shared<StreamPass>();
+    std::memset(sp.get(), 0, sizeof(StreamPass));
+    uint32_t qi = 0;
+    for (uint32_t b = 0; b < 64; ++b)
+        if (Q >> b & 1) sp->qbit[qi++] = static_cast<uint8_t>(b);
+    const uint64_t all = total_bits >= 64 ? ~0ull : (1ull << total_bits) - 1;
+    sp->base = make_runs(~(Q | 31ull) & all, total_bits, static_cast<int>(total_bits));
+    const auto where = [&](uint32_t b, uint8_t& src, uint8_t& idx) {
+        if (b < 5) {
+            src = 0;
+            idx = static_cast<uint8_t>(b);
+        } else if (Q >> b & 1) {
+            src = 1;
+            idx = rank_in(Q, b);
+        } else {
+            src = 2;
+            idx = static_cast<uint8_t>(b);
+        }
+    };
+    for (uint32_t i = begin; i < end; ++i) {
+        const GateOp& g = ops[i];
+        StreamOp& o = sp->ops[sp->nops++];
+        o.type = g.type;
+        o.hi = g.hi;
+        o.lo = g.lo;
+        where(g.hi, o.src_hi, o.idx_hi);
+        where(g.lo, o.src_lo, o.idx_lo);
+        const auto take = [&](int slot, int e) {
+            o.et[slot] = g.et[e];
+            o.m[2 * slot] = g.m[2 * e];
+            o.m[2 * slot + 1] = g.m[2 * e + 1];
+        };
+        if (g.type == OP_U2) {
+            for (int e = 0; e < 4; ++e) take(e, e);
+        } else if (g.type == OP_DIAG) {
+            take(0, 0);
+            take(1, 3);
+        } else if (g.type == OP_CDIAG) {
+            take(0, 15);
+        }
+    }
+    return sp;
+}
+
 void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bits) {
     prog.total_bits = total_bits;
     prog.passes.clear();
@@ -532,6 +592,7 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
                 }
                 p.fast = true;
                 p.fp = fp;
+                p.sp = make_stream(ops, begin, end, total_bits);
             }
         }
         prog.passes.push_back(p);
@@ -826,46 +887,67 @@ __device__ __forceinline__ bool has_chain(const FastOp* ops, uint32_t q0, uint32
 // Quantisation epilogue: amplitudes j of this thread -> packed words and
 // per-chunk counters. Lanes of a warp hold 32 consecutive locals (tile
 // positions 0..4 are buffer bits 0..4), so (block slot, chunk) is
-// warp-uniform and counters are reduced per warp before one set of atomics.
-__device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t pbt,
-                                               const uint64_t* pjoff, uint32_t jnew, uint32_t lb, bool gather,
-                                               uint32_t cvec, const uint16_t* gat_lo, const uint16_t* gat_hi) {
+// warp-uniform: each thread keeps RowAcc counters for the current chunk and
+// the warp reduces them with REDUX when the chunk changes (rows in jnew).
+template <bool kF32>
+__device__ __forceinline__ void quant_rows(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t pbt,
+                                           const uint64_t* pjoff, uint32_t jnew, uint32_t lb, bool gather,
+                                           uint32_t cvec, const uint16_t* gat_lo, const uint16_t* gat_hi) {
     // pbt: planar index of (tile base | thread offset); pjoff[j]: of row j
     const uint64_t im_off = 1ull << lb;
     const double qlo_d = static_cast<double>(q.t.qlo);
     const int span = static_cast<int>(q.t.qhi - q.t.qlo);
-    ChunkAcc acc_re, acc_im;
+    uint32_t* const pk = q.pk + pbt;
+    RowAcc acc_re, acc_im;
     // chunks are 4096 scalars and 2^(lb+1) / 4096 = nch per block (lb >= 12),
     // so the chunk of a scalar is its planar index >> 12; the bits of pbt and
     // pjoff[j] are disjoint, so row j's chunk is (pbt >> 12) | (pjoff[j] >> 12)
     // and it changes only at the rows set in jnew (the same for every tile)
     const uint64_t kb = pbt >> 12, kim = im_off >> 12;
     uint64_t key = kb | (pjoff[0] >> 12);
+    uint32_t rows = 0;
     bool bad = false, oow = false;
 #pragma unroll 1
     for (int j = 0; j < kPer; ++j) {
         uint32_t y = tid + 256 * j;
         if (gather) y = gat_lo[(y ^ cvec) & 63] ^ gat_hi[(y ^ cvec) >> 6];
         const double2 a = tile_s[y];
-        const uint32_t pr = quantize_pack_fast(a.x, q.t, qlo_d, span, bad, oow);
-        const uint32_t pi = quantize_pack_fast(a.y, q.t, qlo_d, span, bad, oow);
-        const uint64_t a_re = pbt + pjoff[j];
-        if ((jnew >> j) & 1u) {  // warp-uniform
-            flush_chunk(q.cps + key, acc_re);
-            flush_chunk(q.cps + key + kim, acc_im);
-            acc_re = ChunkAcc{};
-            acc_im = ChunkAcc{};
-            key = kb | (pjoff[j] >> 12);
+        uint32_t pr, pi;
+        if constexpr (kF32) {
+            pr = quantize_pack_f32(a.x, q.t, span, bad, oow);
+            pi = quantize_pack_f32(a.y, q.t, span, bad, oow);
+        } else {
+            pr = quantize_pack_fast(a.x, q.t, qlo_d, span, bad, oow);
+            pi = quantize_pack_fast(a.y, q.t, qlo_d, span, bad, oow);
         }
-        q.pk[a_re] = pr;
-        q.pk[a_re + im_off] = pi;
+        const uint64_t o = pjoff[j];
+        if ((jnew >> j) & 1u) {  // warp-uniform
+            flush_rows(q.cps + key, acc_re, 32u * rows);
+            flush_rows(q.cps + key + kim, acc_im, 32u * rows);
+            acc_re = RowAcc{};
+            acc_im = RowAcc{};
+            rows = 0;
+            key = kb | (o >> 12);
+        }
+        pk[o] = pr;
+        pk[o + im_off] = pi;
         acc_re.add(pr);
         acc_im.add(pi);
+        ++rows;
     }
-    flush_chunk(q.cps + key, acc_re);
-    flush_chunk(q.cps + key + kim, acc_im);
+    flush_rows(q.cps + key, acc_re, 32u * rows);
+    flush_rows(q.cps + key + kim, acc_im, 32u * rows);
     if (bad) dev_fail(q.err, DE_NONFINITE, 0);
     if (oow) dev_fail(q.err, DE_WINDOW, 0);
+}
+
+__device__ __forceinline__ void quant_epilogue(const QuantOut& q, const double2* tile_s, uint32_t tid, uint64_t pbt,
+                                               const uint64_t* pjoff, uint32_t jnew, uint32_t lb, bool gather,
+                                               uint32_t cvec, const uint16_t* gat_lo, const uint16_t* gat_hi) {
+    if (q.t.f32)
+        quant_rows<true>(q, tile_s, tid, pbt, pjoff, jnew, lb, gather, cvec, gat_lo, gat_hi);
+    else
+        quant_rows<false>(q, tile_s, tid, pbt, pjoff, jnew, lb, gather, cvec, gat_lo, gat_hi);
 }
 
 __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __restrict__ buf, uint32_t lb,
@@ -1300,6 +1382,199 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
         }
     }
     if (wf && __syncthreads_or(set_wz) && tid == 0) *wz = 1;
+}
+
+// ------------------------------------------------ register-streaming pass
+// See StreamPass (gates.cuh). Lane l, value r of unit u holds buffer index
+// base(u) | l | dep(r); ops run in program order on registers with the
+// tiled kernel's arithmetic (cmul / row2: the reference's products, exact
+// up to the sign of an exact zero, which the codec never stores).
+constexpr int kStreamThreads = 256;
+constexpr int kNV = 1 << kStreamNQ;
+
+__device__ __forceinline__ uint32_t stream_bit(uint8_t src, uint8_t idx, uint32_t lane, uint32_t r, uint64_t xb) {
+    return src == 0 ? (lane >> idx) & 1u : (src == 1 ? (r >> idx) & 1u : static_cast<uint32_t>((xb >> idx) & 1));
+}
+
+__device__ __forceinline__ C2 shfl_c2(C2 a, uint32_t m) {
+    return C2{__shfl_xor_sync(0xffffffffu, a.re, m), __shfl_xor_sync(0xffffffffu, a.im, m)};
+}
+
+// pairs (r, r | 1 << kB) of the register values
+template <int kB, typename F>
+__device__ __forceinline__ void reg_pairs(F&& f) {
+#pragma unroll
+    for (int r = 0; r < kNV; ++r)
+        if (!((r >> kB) & 1)) f(r, r | (1 << kB));
+}
+
+template <bool kQuant>
+__global__ void __launch_bounds__(kStreamThreads) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
+                                                                const __grid_constant__ StreamPass pass,
+                                                                const __grid_constant__ QuantOut q,
+                                                                const uint32_t* __restrict__ vtab,
+                                                                uint8_t* __restrict__ wf, uint32_t* wz) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kStreamThreads + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kStreamThreads) >> 5;
+    // a contiguous range of units per warp: consecutive units mostly share
+    // their chunks, so the epilogue's counters flush once per run
+    const uint64_t per = (nunits + nwarps - 1) / nwarps;
+    const uint64_t u0 = warp * per, u1 = min(nunits, u0 + per);
+    if (u0 >= u1) return;
+    const uint64_t lmask = (1ull << lb) - 1, im_off = 1ull << lb;
+    uint64_t pdep[kNV];  // planar offsets of the register rows (planar_addr is OR-linear)
+#pragma unroll
+    for (int r = 0; r < kNV; ++r) {
+        uint64_t d = 0;
+#pragma unroll
+        for (int i = 0; i < kStreamNQ; ++i) d |= static_cast<uint64_t>((r >> i) & 1) << pass.qbit[i];
+        pdep[r] = planar_addr(d, lb, lmask, 0);
+    }
+    // *wz == 0: every 32-scalar group of the input is stored (flags all 1)
+    const bool wf_read = wf && *reinterpret_cast<volatile uint32_t*>(wz) != 0;
+    bool set_wz = false;
+    bool bad = false, oow = false;
+    const int span = static_cast<int>(q.t.qhi - q.t.qlo);
+    const double qlo_d = static_cast<double>(q.t.qlo);
+    RowAcc acc[kNV][2];
+#pragma unroll
+    for (int r = 0; r < kNV; ++r) acc[r][0] = acc[r][1] = RowAcc{};
+    uint64_t run_pb = 0;  // planar base of the current counter run
+    uint32_t run_len = 0;
+    const auto flush = [&]() {
+#pragma unroll
+        for (int r = 0; r < kNV; ++r) {
+            const uint64_t key = (run_pb | pdep[r]) >> 12;
+            flush_rows(q.cps + key, acc[r][0], 32u * run_len);
+            flush_rows(q.cps + key + (im_off >> 12), acc[r][1], 32u * run_len);
+            acc[r][0] = RowAcc{};
+            acc[r][1] = RowAcc{};
+        }
+        run_len = 0;
+    };
+    for (uint64_t u = u0; u < u1; ++u) {
+        const uint64_t base = runs_deposit(u, pass.base);
+        const uint64_t pb = planar_addr(base, lb, lmask, 0);
+        const uint64_t xb = vtab ? ((static_cast<uint64_t>(vtab[base >> lb]) << lb) | (base & lmask)) : base;
+        C2 a[kNV];
+#pragma unroll
+        for (int r = 0; r < kNV; ++r) {
+            const uint64_t p = pb + pdep[r];
+            if (wf_read) {  // rows flagged zero were not stored (warp-uniform tests)
+                a[r].re = wf[p >> 5] ? buf[p + lane] : 0.0;
+                a[r].im = wf[(p + im_off) >> 5] ? buf[p + im_off + lane] : 0.0;
+            } else {
+                a[r].re = buf[p + lane];
+                a[r].im = buf[p + im_off + lane];
+            }
+        }
+        for (uint32_t i = 0; i < pass.nops; ++i) {
+            const StreamOp& o = pass.ops[i];
+            if (o.type == OP_DIAG) {
+#pragma unroll
+                for (int r = 0; r < kNV; ++r) {
+                    const uint32_t e = stream_bit(o.src_hi, o.idx_hi, lane, r, xb);
+                    a[r] = cmul(e ? o.m[2] : o.m[0], e ? o.m[3] : o.m[1], a[r]);
+                }
+            } else if (o.type == OP_CDIAG) {
+#pragma unroll
+                for (int r = 0; r < kNV; ++r)
+                    if (stream_bit(o.src_hi, o.idx_hi, lane, r, xb) & stream_bit(o.src_lo, o.idx_lo, lane, r, xb))
+                        a[r] = cmul(o.m[0], o.m[1], a[r]);
+            } else if (o.type == OP_CX) {  // control hi, target lo: an exact permutation
+                if (o.src_lo == 1) {
+                    const auto sw = [&](int r0, int r1) {
+                        if (stream_bit(o.src_hi, o.idx_hi, lane, r0, xb)) {
+                            const C2 t = a[r0];
+                            a[r0] = a[r1];
+                            a[r1] = t;
+                        }
+                    };
+                    if (o.idx_lo == 0)
+                        reg_pairs<0>(sw);
+                    else
+                        reg_pairs<1>(sw);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) {
+                        const C2 pv = shfl_c2(a[r], 1u << o.idx_lo);
+                        if (stream_bit(o.src_hi, o.idx_hi, lane, r, xb)) a[r] = pv;
+                    }
+                }
+            } else {  // OP_U2 on hi
+                if (o.src_hi == 1) {
+                    const auto mix = [&](int r0, int r1) {
+                        const C2 a0 = a[r0], a1 = a[r1];
+                        a[r0] = row2(o.et, o.m, 0, a0, a1);
+                        a[r1] = row2(o.et, o.m, 1, a0, a1);
+                    };
+                    if (o.idx_hi == 0)
+                        reg_pairs<0>(mix);
+                    else
+                        reg_pairs<1>(mix);
+                } else {
+                    // partner across lanes; each lane forms its own row with
+                    // the generic product (exact for every entry class)
+                    const uint32_t me = (lane >> o.idx_hi) & 1u;
+                    const double w0r = me ? o.m[4] : o.m[0], w0i = me ? o.m[5] : o.m[1];
+                    const double w1r = me ? o.m[6] : o.m[2], w1i = me ? o.m[7] : o.m[3];
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) {
+                        const C2 pv = shfl_c2(a[r], 1u << o.idx_hi);
+                        const C2 a0 = me ? pv : a[r], a1 = me ? a[r] : pv;
+                        a[r] = cadd(cmul(w0r, w0i, a0), cmul(w1r, w1i, a1));
+                    }
+                }
+            }
+        }
+        if constexpr (kQuant) {
+            if (run_len && ((pb ^ run_pb) >> 12)) flush();
+            if (!run_len) run_pb = pb;
+#pragma unroll
+            for (int r = 0; r < kNV; ++r) {
+                uint32_t pr, pi;
+                if (q.t.f32) {
+                    pr = quantize_pack_f32(a[r].re, q.t, span, bad, oow);
+                    pi = quantize_pack_f32(a[r].im, q.t, span, bad, oow);
+                } else {
+                    pr = quantize_pack_fast(a[r].re, q.t, qlo_d, span, bad, oow);
+                    pi = quantize_pack_fast(a[r].im, q.t, qlo_d, span, bad, oow);
+                }
+                const uint64_t p = pb + pdep[r] + lane;
+                q.pk[p] = pr;
+                q.pk[p + im_off] = pi;
+                acc[r][0].add(pr);
+                acc[r][1].add(pi);
+            }
+            ++run_len;
+        } else {
+#pragma unroll
+            for (int r = 0; r < kNV; ++r) {
+                const uint64_t p = pb + pdep[r];
+                if (wf) {  // an all-zero 32-scalar group is flagged instead of stored
+                    const bool nr = __any_sync(0xffffffffu, a[r].re != 0.0), ni = __any_sync(0xffffffffu, a[r].im != 0.0);
+                    if (lane == 0) {
+                        wf[p >> 5] = nr;
+                        wf[(p + im_off) >> 5] = ni;
+                    }
+                    set_wz = set_wz || !(nr && ni);
+                    if (nr) buf[p + lane] = a[r].re;
+                    if (ni) buf[p + im_off + lane] = a[r].im;
+                } else {
+                    buf[p + lane] = a[r].re;
+                    buf[p + im_off + lane] = a[r].im;
+                }
+            }
+        }
+    }
+    if constexpr (kQuant) {
+        if (run_len) flush();
+        if (bad) dev_fail(q.err, DE_NONFINITE, 0);
+        if (oow) dev_fail(q.err, DE_WINDOW, 0);
+    } else {
+        if (set_wz && lane == 0) *wz = 1;
+    }
 }
 
 // ------------------------------------------------------ general pass (SMEM)
@@ -1806,6 +2081,13 @@ bool full_support_debug() {
     return on;
 }
 
+// BMQ_DBG_NO_STREAM=1 keeps every pass on the tiled kernel (A/B and
+// bisecting); read once.
+bool stream_off() {
+    static const bool on = getenv("BMQ_DBG_NO_STREAM") != nullptr;
+    return on;
+}
+
 bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved) {
     if (interleaved || lb < 12 || prog.passes.empty()) return false;
     for (const GatePass& p : prog.passes)
@@ -1838,11 +2120,22 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
     for (size_t pi = 0; pi < prog.passes.size(); ++pi) {
         const GatePass& p = prog.passes[pi];
         const uint64_t tiles = vtab ? nblocks << (lb - p.tb) : nreps << (prog.total_bits - p.tb);
-        if (p.fast) {
+        const bool last = pi + 1 == prog.passes.size();
+        if (p.sp && !interleaved && lb >= 12 && !stream_off() &&
+            (!vtab || !((1ull << p.sp->qbit[kStreamNQ - 1]) >> lb))) {
+            const uint64_t units = (vtab ? nblocks << lb : nreps << prog.total_bits) >> (5 + kStreamNQ);
+            const uint64_t warps_per_cta = kStreamThreads / 32;
+            const uint64_t grid = std::min<uint64_t>((units + warps_per_cta - 1) / warps_per_cta, 148ull * 8);
+            if (fuse && last)
+                k_stream_pass<true><<<static_cast<uint32_t>(grid), kStreamThreads, 0, st>>>(
+                    buf, lb, units, *p.sp, *quant, vtab, const_cast<uint8_t*>(zflag), wz);
+            else
+                k_stream_pass<false><<<static_cast<uint32_t>(grid), kStreamThreads, 0, st>>>(
+                    buf, lb, units, *p.sp, none, vtab, const_cast<uint8_t*>(zflag), wz);
+        } else if (p.fast) {
             const size_t smem = tile_bytes + p.fp->tab_entries * sizeof(double2) + p.fp->nops * sizeof(FastOp);
             const uint64_t per_sm = std::max<uint64_t>(1, (227ull * 1024) / (smem + 2048));
             const uint64_t grid = std::min<uint64_t>(tiles, 148ull * per_sm * 8);
-            const bool last = pi + 1 == prog.passes.size();
             k_gate_pass_fast<<<static_cast<uint32_t>(grid), kFastThreads, smem, st>>>(
                 buf, lb, interleaved ? 1 : 0, tiles, *p.fp, (fuse && last) ? *quant : none, vtab,
                 full_support_debug() ? 1 : 0, const_cast<uint8_t*>(zflag), wz);

@@ -118,6 +118,35 @@ struct PermPass {
     const uint16_t* table;          // [1 << npat_bits][4096] (device)
 };
 
+// Register-streaming pass (k_stream_pass): for passes whose gates are
+// U2 / DIAG / CDIAG / CX only and mix at most two buffer bits above bit 4.
+// A warp owns "units" of 128 amplitudes: buffer bits 0..4 are its lanes and
+// two more bits Q (the mixing bits, filled up with the lowest free bits) are
+// the index of four values each lane holds in registers. Gates run in
+// program order on registers (a lane-bit partner through shuffles), with the
+// reference's rounding sequence (cmul / row2, as the tiled kernel); no
+// shared memory and no barriers. Units are dealt to warps in contiguous
+// ranges so the quantising epilogue's per-chunk counters reduce per run.
+constexpr int kStreamNQ = 2;  // register bits per lane (4 values)
+constexpr int kMaxStreamOps = 48;
+struct StreamOp {
+    uint8_t type, hi, lo;
+    uint8_t src_hi, src_lo;   // where the bit lives: 0 lane bit, 1 register bit, 2 base bit
+    uint8_t idx_hi, idx_lo;   // lane bit number / register bit number (base bits: the buffer bit)
+    uint8_t pad;
+    double m[8];              // U2: u00 u01 u10 u11; DIAG: u00 u11; CDIAG: u33 (interleaved re/im)
+    uint8_t et[4];            // entry classes (U2: row-major; DIAG: u00 u11; CDIAG: u33)
+    uint32_t pad2;
+};
+struct StreamPass {
+    BitRuns base;             // unit index -> buffer bits outside {0..4} and Q
+    uint8_t qbit[kStreamNQ];  // register bit i -> buffer bit
+    uint8_t pad[6];
+    uint32_t nops;
+    uint32_t pad2;
+    StreamOp ops[kMaxStreamOps];
+};
+
 struct GatePass {
     uint64_t tile_mask;   // buffer bits spanned by one CTA tile
     uint32_t tb;          // popcount(tile_mask)
@@ -126,6 +155,7 @@ struct GatePass {
     std::shared_ptr<FastPass> fp;
     std::shared_ptr<MonoPass> mp;  // set on every pass when GateProgram::mono
     std::shared_ptr<PermPass> pp;  // table form of mp (when the pattern bits fit)
+    std::shared_ptr<StreamPass> sp;  // register-streaming form (set when the pass qualifies)
 };
 
 struct GateProgram {

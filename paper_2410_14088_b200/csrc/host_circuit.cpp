@@ -299,6 +299,119 @@ std::vector<bmq_stage> partition_plan(uint32_t n, const bmq_gate* gates, uint64_
     return stages;
 }
 
+// ------------------------------------------------ device-aware planning
+// An optional alternative to the fixed inner_size of
+// partition_circuit: every greedy plan partition_plan(n, b, k) is a legal
+// staging, and on this engine a stage costs about one trip of the state
+// through HBM per tile pass (decode -> passes -> quantise -> emit), so fewer
+// stages (larger k) win until the extra tile passes of wider stages, the
+// group buffer (2^(b+k) complex doubles must fit the work budget) or, for
+// world > 1, the device bits (k <= c - log2 world) and the payload remaps
+// between stages take over. The chosen plan is partition_plan at the best k,
+// so it can be replayed by the reference (partition.hpp:59-101) with
+// inner_size = k.
+
+namespace {
+
+bool gate_mixes(uint32_t kind) {
+    switch (kind) {
+    case BMQ_GATE_H: case BMQ_GATE_X: case BMQ_GATE_Y: case BMQ_GATE_RX: case BMQ_GATE_RY: case BMQ_GATE_CX:
+        return true;
+    default:
+        return false;
+    }
+}
+
+// Tile passes of one stage (gates.cu build_program): a pass holds buffer
+// bits 0..4 plus the mixing bits of its gates, at most 12.
+uint32_t stage_passes(const Layout& L, const bmq_stage& st, const bmq_gate* gates) {
+    const uint32_t total = L.b + st.inner_count;
+    const uint32_t tb = std::min<uint32_t>(total, 12);
+    const uint64_t coalesce = (1ull << std::min<uint32_t>(5, total)) - 1;
+    uint32_t passes = 1;
+    uint64_t mix = 0;
+    for (uint64_t i = st.gate_begin; i < st.gate_end; ++i) {
+        const bmq_gate& g = gates[i];
+        if (!gate_mixes(g.kind)) continue;
+        const uint32_t q = g.kind == BMQ_GATE_CX ? g.q1 : g.q0;
+        const uint64_t m = 1ull << buffer_bit(L, st, q);
+        if (static_cast<uint32_t>(__builtin_popcountll(mix | m | coalesce)) > tb && mix) {
+            ++passes;
+            mix = 0;
+        }
+        mix |= m;
+    }
+    return passes;
+}
+
+}  // namespace
+
+std::vector<bmq_stage> plan_device_aware(uint32_t n, const bmq_gate* gates, uint64_t count, uint32_t block_bits,
+                                         const bmq_plan_model& model, bmq_plan_choice* choice) {
+    check_circuit(n, gates, count);
+    const Layout L = make_layout(n, block_bits);
+    if (model.world == 0 || (model.world & (model.world - 1)))
+        raise(BMQ_ERR_INVALID_ARGUMENT, "shard count must be a power of two");
+    if (!(model.hbm_gbs > 0.0) || (model.world > 1 && !(model.link_gbs > 0.0)) || !(model.ratio > 0.0))
+        raise(BMQ_ERR_INVALID_ARGUMENT, "plan model needs positive bandwidths and compression ratio");
+    uint32_t m = 0;
+    while ((1u << m) < model.world) ++m;
+    if (m > L.c) raise(BMQ_ERR_INVALID_ARGUMENT, "more shards than blocks");
+    // largest inner size: outer bits left for the device bits, group buffer within the work budget
+    uint32_t kmax = std::min<uint32_t>(L.c - m, model.max_inner ? model.max_inner : 64);
+    while (kmax > 2 && (16ull << (L.b + kmax)) > model.work_bytes) --kmax;
+    kmax = std::max<uint32_t>(kmax, std::min<uint32_t>(2, L.c - m));
+    const double amps = std::ldexp(1.0, static_cast<int>(n)) / model.world;  // per GPU
+    const double cbytes = 16.0 / model.ratio;                               // payload bytes per amplitude
+    std::vector<bmq_stage> best;
+    double best_s = 0.0;
+    bmq_plan_choice ch{};
+    ch.candidates = 0;
+    for (uint32_t k = 2; k <= std::max<uint32_t>(kmax, 2); ++k) {
+        std::vector<bmq_stage> plan = partition_plan(n, gates, count, block_bits, k);
+        double bytes = 0.0;
+        uint64_t passes = 0;
+        for (const bmq_stage& st : plan) {
+            const uint32_t p = stage_passes(L, st, gates);
+            passes += p;
+            // decode writes 16 B, the first pass reads 16, each further pass
+            // moves 32, the last pass writes 8 B of codes that emit reads back
+            bytes += amps * (2.0 * cbytes + 48.0 + 32.0 * (p - 1));
+        }
+        double secs = bytes / (model.hbm_gbs * 1e9) + plan.size() * model.stage_overhead_s;
+        uint32_t remaps = 0;
+        if (m && !plan.empty()) {
+            // a remap moves the payloads whose owner changes: 1 - 2^-s of this
+            // GPU's share for s re-chosen device bits, over the peer link
+            const std::vector<uint32_t> dev = shard_plan(L, plan, model.world);
+            for (size_t s = 1; s < plan.size(); ++s) {
+                uint32_t moved = 0;
+                for (uint32_t j = 0; j < m; ++j) moved += dev[s * m + j] != dev[(s - 1) * m + j];
+                if (moved) {
+                    ++remaps;
+                    secs += amps * cbytes * (1.0 - std::ldexp(1.0, -static_cast<int>(moved))) / (model.link_gbs * 1e9);
+                }
+            }
+        }
+        if (ch.candidates < 16) {
+            ch.inner[ch.candidates] = k;
+            ch.model_s[ch.candidates] = secs;
+            ++ch.candidates;
+        }
+        if (best.empty() || secs < best_s) {
+            best = std::move(plan);
+            best_s = secs;
+            ch.inner_size = k;
+            ch.stages = best.size();
+            ch.passes = passes;
+            ch.remaps = remaps;
+            ch.model_s_best = secs;
+        }
+    }
+    if (choice) *choice = ch;
+    return best;
+}
+
 uint64_t GroupGeometry::block_id(uint64_t outer, uint64_t v) const {
     return deposit_bits(outer, outer_mask) | deposit_bits(v, inner_mask);
 }

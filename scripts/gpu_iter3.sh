@@ -1,0 +1,11 @@
+#!/bin/bash
+# iteration check: codec + engine parity, then dense bench lines and the headline
+timeout 900 python -m pytest tests/test_codec_gpu.py tests/test_engine_gpu.py tests/test_headline_layout_gpu.py -q -x 2>&1 | tail -4
+for wl in "--workload qaoa3reg --qubits 30 --error-bound 1e-4" "--workload qaoa3reg --qubits 30 --error-bound 1e-3" "--workload random --qubits 30 --layers 20"; do
+  timeout 600 python bench.py $wl --steps 3 --warmup 3 --no-e2e --no-link --no-cpu-baseline 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; ph=r['phases']
+print(d['config']['workload'], 'ms %.1f'%d['ms_per_step'], 'frac %.3f'%r['frac'], ' '.join('%s %.0fms %.2f'%(k,v['ms'],v['frac']) for k,v in ph.items()), 'fid', d['fidelity'])"
+done
+timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-link --no-cpu-baseline 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; ph=r['phases']
+print(d['config']['workload'], 'ms %.1f'%d['ms_per_step'], 'frac %.3f'%r['frac'], ' '.join('%s %.0fms'%(k,v['ms']) for k,v in ph.items()))"

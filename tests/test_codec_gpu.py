@@ -136,3 +136,20 @@ def test_quantiser_near_rounding_ties(gpu, port, br):
     x *= np.where(rng.random(q.size) < 0.5, -1.0, 1.0)
     x = np.concatenate([x, np.exp2(q * ba), rng.standard_normal(2192) * 1e-3])
     assert gpu.compress_block(x, br) == port.compress_block(x, br)
+
+
+@pytest.mark.parametrize("br", [1e-2, 1e-3, 1e-4, 2e-5])
+def test_quantiser_float_estimate_log_uniform(gpu, port, br):
+    """4 M scalars log-uniform over 600 decades (every binary exponent of
+    the normal range the amplitudes can take, both signs, some subnormals
+    and zeros): the single-precision estimate (quantize_pack_f32, full
+    chunks) and its tie margin must reproduce the reference's codes."""
+    rng = np.random.default_rng(int(1 / br) % 997)
+    n = 1 << 22
+    # (below ~1e-4 the device table is a window: codec_tables.cpp kMaxEntries)
+    lo = -300 if br >= 1e-4 else -9
+    x = np.sign(rng.standard_normal(n)) * 10.0 ** rng.uniform(lo, 2, n)
+    x[rng.random(n) < 0.01] = 0.0
+    if br >= 1e-4:
+        x[rng.random(n) < 0.001] *= 1e-20  # some subnormals
+    assert gpu.compress_block(x, br) == port.compress_block(x, br)

@@ -525,3 +525,19 @@ def test_checkpoint_resume_is_exact(gpu, tmp_path, name, n, b, cut):
     with gpu.Simulator(c, cfg) as other:
         with pytest.raises(Exception, match="checkpoint"):
             other.load(bad)
+
+
+@pytest.mark.parametrize("name,n,layers,b,br", [("qft", 18, 1, 12, 1e-3), ("qaoa3reg", 18, 2, 12, 1e-4),
+                                                ("random", 17, 8, 12, 1e-3)])
+def test_device_plan_matches_reference_at_chosen_inner(gpu, port, name, n, layers, b, br):
+    """Config.device_plan (BMQ_FLAG_DEVICE_PLAN): the engine
+    plans with plan_device_aware (cap inner_size) and the result is the
+    reference's run at the inner size it chose, byte for byte."""
+    c = gpu.generate_benchmark(name, n, gpu.BenchmarkParams(layers=layers, seed=1))
+    plan, ch = gpu.plan_device_aware(c, b, max_inner=n - b)
+    want = port.simulate(n, [g.as_tuple() for g in c.gates], b, ch.inner_size, br)
+    with gpu.Simulator(c, gpu.Config(block_bits=b, inner_size=n - b, error_bound=br, device_plan=True)) as sim:
+        rep = sim.run()
+        assert rep.stage_count == len(plan.stages) == want.report["stage_count"]
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]

@@ -173,3 +173,35 @@ def test_host_level_extent_heap(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "extent_heap ok" in out.stdout
+
+
+@pytest.mark.parametrize("name,n,layers,b", [("qft", 34, 1, 20), ("qaoa3reg", 34, 4, 20), ("random", 30, 20, 14),
+                                             ("ghz", 30, 1, 20)])
+def test_device_aware_plan(cbq, name, n, layers, b):
+    """plan_device_aware returns partition_circuit's plan at
+    the inner size whose modelled time is least, never beyond the work
+    budget (2^(b+k) complex doubles) or the outer bits the shards need."""
+    c = cbq.generate_benchmark(name, n, cbq.BenchmarkParams(layers=layers, seed=1))
+    for world, work in ((1, 16 << 30), (8, 16 << 30), (1, 16 << (b + 3))):
+        plan, ch = cbq.plan_device_aware(c, b, world=world, work_bytes=work)
+        k = ch.inner_size
+        assert plan.stages == cbq.partition_circuit(c, b, k).stages
+        assert ch.stages == len(plan.stages) and ch.model_s == min(ch.candidates.values())
+        assert ch.model_s == ch.candidates[k]
+        assert (16 << (b + k)) <= work or k == 2
+        assert k <= (n - b) - (world.bit_length() - 1)
+        assert all(len(s.inner) <= k for s in plan.stages)
+        assert world > 1 or ch.remaps == 0
+    default = cbq.partition_circuit(c, b, 2)
+    plan, ch = cbq.plan_device_aware(c, b)
+    assert len(plan.stages) <= len(default.stages)
+
+
+def test_device_aware_plan_errors(cbq):
+    c = cbq.generate_benchmark("qft", 12)
+    with pytest.raises(cbq.InvalidArgument, match="power of two"):
+        cbq.plan_device_aware(c, 6, world=3)
+    with pytest.raises(cbq.InvalidArgument, match="positive"):
+        cbq.plan_device_aware(c, 6, hbm_gbs=0.0)
+    plan, ch = cbq.plan_device_aware(c, 6, max_inner=3)
+    assert ch.inner_size <= 3
