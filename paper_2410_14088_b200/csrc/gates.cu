@@ -469,48 +469,64 @@ void lazify(std::vector<FastOp>& fops, FastPass& fp, uint32_t& ncx, uint32_t& np
 }  // namespace
 
 // Register-streaming form of a pass (see StreamPass), or null when the pass
-// needs the tiled kernel: other op types (U4; phase chains are formed from
-// CDIAG runs, which stream op by op), more than two mixing bits above bit 4,
-// or too many ops for per-amplitude application to beat the tile's chains.
+// needs the tiled kernel: other op types (U4), partners outside the lane
+// bits and two more bits, a CX map that is not the identity at the end, or
+// too many ops for per-amplitude application to beat the tile's phase chains.
 static std::shared_ptr<StreamPass> make_stream(const std::vector<GateOp>& ops, uint32_t begin, uint32_t end,
-                                        uint32_t total_bits) {
-    if (total_bits < 12 || end - begin > static_cast<uint32_t>(kMaxStreamOps)) return nullptr;
+                                               uint32_t total_bits) {
+    if (total_bits < 12 || total_bits > 63) return nullptr;
+    // lazy CX: rows of M (logical bit t = parity(row[t] & x)) and columns of M^-1
+    uint64_t row[64], col[64];
+    for (uint32_t t = 0; t < total_bits; ++t) row[t] = col[t] = 1ull << t;
     uint64_t R = 0;
+    uint32_t nops = 0;
     for (uint32_t i = begin; i < end; ++i) {
-        const uint8_t t = ops[i].type;
-        if (t != OP_U2 && t != OP_DIAG && t != OP_CDIAG && t != OP_CX) return nullptr;
-        R |= mixing_bits(ops[i]) & ~31ull;
+        const GateOp& g = ops[i];
+        if (g.type == OP_CX) {
+            row[g.lo] ^= row[g.hi];
+            col[g.hi] ^= col[g.lo];
+        } else if (g.type == OP_U2) {
+            R |= col[g.hi] & ~31ull;
+            ++nops;
+        } else if (g.type == OP_DIAG || g.type == OP_CDIAG) {
+            ++nops;
+        } else {
+            return nullptr;
+        }
     }
-    if (__builtin_popcountll(R) > kStreamNQ) return nullptr;
+    for (uint32_t t = 0; t < total_bits; ++t)
+        if (row[t] != 1ull << t) return nullptr;  // the pass would end permuted
+    if (__builtin_popcountll(R) > kStreamNQ || nops > static_cast<uint32_t>(kMaxStreamOps)) return nullptr;
     uint64_t Q = R;
     for (uint32_t b = 5; __builtin_popcountll(Q) < kStreamNQ; ++b) Q |= 1ull << b;
     auto sp = std::make_shared<StreamPass>();
     std::memset(sp.get(), 0, sizeof(StreamPass));
     uint32_t qi = 0;
+    uint64_t dep[1 << kStreamNQ] = {};
     for (uint32_t b = 0; b < 64; ++b)
         if (Q >> b & 1) sp->qbit[qi++] = static_cast<uint8_t>(b);
-    const uint64_t all = total_bits >= 64 ? ~0ull : (1ull << total_bits) - 1;
+    for (uint32_t r = 0; r < (1u << kStreamNQ); ++r)
+        for (uint32_t k = 0; k < kStreamNQ; ++k)
+            if (r >> k & 1) dep[r] |= 1ull << sp->qbit[k];
+    const uint64_t all = (1ull << total_bits) - 1;
     sp->base = make_runs(~(Q | 31ull) & all, total_bits, static_cast<int>(total_bits));
-    const auto where = [&](uint32_t b, uint8_t& src, uint8_t& idx) {
-        if (b < 5) {
-            src = 0;
-            idx = static_cast<uint8_t>(b);
-        } else if (Q >> b & 1) {
-            src = 1;
-            idx = rank_in(Q, b);
-        } else {
-            src = 2;
-            idx = static_cast<uint8_t>(b);
-        }
+    const auto pat = [&](uint64_t rw) {
+        uint8_t p = 0;
+        for (uint32_t r = 0; r < (1u << kStreamNQ); ++r) p |= static_cast<uint8_t>((__builtin_popcountll(rw & dep[r]) & 1) << r);
+        return p;
     };
+    for (uint32_t t = 0; t < total_bits; ++t) row[t] = col[t] = 1ull << t;
     for (uint32_t i = begin; i < end; ++i) {
         const GateOp& g = ops[i];
+        if (g.type == OP_CX) {
+            row[g.lo] ^= row[g.hi];
+            col[g.hi] ^= col[g.lo];
+            continue;
+        }
         StreamOp& o = sp->ops[sp->nops++];
         o.type = g.type;
-        o.hi = g.hi;
-        o.lo = g.lo;
-        where(g.hi, o.src_hi, o.idx_hi);
-        where(g.lo, o.src_lo, o.idx_lo);
+        o.row = row[g.hi] & ~Q;
+        o.rpat = pat(row[g.hi]);
         const auto take = [&](int slot, int e) {
             o.et[slot] = g.et[e];
             o.m[2 * slot] = g.m[2 * e];
@@ -518,11 +534,24 @@ static std::shared_ptr<StreamPass> make_stream(const std::vector<GateOp>& ops, u
         };
         if (g.type == OP_U2) {
             for (int e = 0; e < 4; ++e) take(e, e);
+            // specialised forms (k_stream_pass): real diagonal entries with real
+            // or imaginary off-diagonal ones, no zero among them (row2 skips
+            // zero products, the specialised form adds +-0: equal up to the
+            // sign of a zero)
+            const auto cls = [&](int e) { return g.et[e] == ET_ONE || g.et[e] == ET_NEG ? ET_REAL : g.et[e]; };
+            if (cls(0) == ET_REAL && cls(3) == ET_REAL && cls(1) == ET_REAL && cls(2) == ET_REAL) o.pad = 1;
+            if (cls(0) == ET_REAL && cls(3) == ET_REAL && cls(1) == ET_IMAG && cls(2) == ET_IMAG) o.pad = 2;
+            const uint64_t d = col[g.hi];
+            o.dl = static_cast<uint32_t>(d & 31);
+            for (uint32_t k = 0; k < kStreamNQ; ++k)
+                if (d >> sp->qbit[k] & 1) o.dq |= static_cast<uint8_t>(1u << k);
         } else if (g.type == OP_DIAG) {
             take(0, 0);
             take(1, 3);
-        } else if (g.type == OP_CDIAG) {
+        } else {
             take(0, 15);
+            o.row2 = row[g.lo] & ~Q;
+            o.rpat2 = pat(row[g.lo]);
         }
     }
     return sp;
@@ -592,7 +621,11 @@ void build_program(GateProgram& prog, std::vector<GateOp> ops, uint32_t total_bi
                 }
                 p.fast = true;
                 p.fp = fp;
-                p.sp = make_stream(ops, begin, end, total_bits);
+                // phase chains (QFT) walk only the set bits of each amplitude and the
+                // tiled kernel tracks sparse tile support: those passes stay tiled
+                bool chains = false;
+                for (const FastOp& o : fops) chains = chains || o.type == OP_CHAIN;
+                if (!chains) p.sp = make_stream(ops, begin, end, total_bits);
             }
         }
         prog.passes.push_back(p);
@@ -1392,24 +1425,12 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
 constexpr int kStreamThreads = 256;
 constexpr int kNV = 1 << kStreamNQ;
 
-__device__ __forceinline__ uint32_t stream_bit(uint8_t src, uint8_t idx, uint32_t lane, uint32_t r, uint64_t xb) {
-    return src == 0 ? (lane >> idx) & 1u : (src == 1 ? (r >> idx) & 1u : static_cast<uint32_t>((xb >> idx) & 1));
-}
-
 __device__ __forceinline__ C2 shfl_c2(C2 a, uint32_t m) {
     return C2{__shfl_xor_sync(0xffffffffu, a.re, m), __shfl_xor_sync(0xffffffffu, a.im, m)};
 }
 
-// pairs (r, r | 1 << kB) of the register values
-template <int kB, typename F>
-__device__ __forceinline__ void reg_pairs(F&& f) {
-#pragma unroll
-    for (int r = 0; r < kNV; ++r)
-        if (!((r >> kB) & 1)) f(r, r | (1 << kB));
-}
-
 template <bool kQuant>
-__global__ void __launch_bounds__(kStreamThreads) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
+__global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
                                                                 const __grid_constant__ StreamPass pass,
                                                                 const __grid_constant__ QuantOut q,
                                                                 const uint32_t* __restrict__ vtab,
@@ -1453,78 +1474,114 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream_pass(double* __restri
         }
         run_len = 0;
     };
+    // one unit's values in flight ahead of the one being processed
+    const auto load_unit = [&](uint64_t pbu, C2* v) {
+#pragma unroll
+        for (int r = 0; r < kNV; ++r) {
+            const uint64_t p = pbu + pdep[r];
+            if (wf_read) {  // rows flagged zero were not stored (warp-uniform tests)
+                v[r].re = wf[p >> 5] ? __ldcs(buf + p + lane) : 0.0;
+                v[r].im = wf[(p + im_off) >> 5] ? __ldcs(buf + p + im_off + lane) : 0.0;
+            } else {
+                v[r].re = __ldcs(buf + p + lane);
+                v[r].im = __ldcs(buf + p + im_off + lane);
+            }
+        }
+    };
+    C2 nxt[kNV];
+    uint64_t nbase = runs_deposit(u0, pass.base);
+    load_unit(planar_addr(nbase, lb, lmask, 0), nxt);
     for (uint64_t u = u0; u < u1; ++u) {
-        const uint64_t base = runs_deposit(u, pass.base);
+        const uint64_t base = nbase;
         const uint64_t pb = planar_addr(base, lb, lmask, 0);
         const uint64_t xb = vtab ? ((static_cast<uint64_t>(vtab[base >> lb]) << lb) | (base & lmask)) : base;
         C2 a[kNV];
 #pragma unroll
-        for (int r = 0; r < kNV; ++r) {
-            const uint64_t p = pb + pdep[r];
-            if (wf_read) {  // rows flagged zero were not stored (warp-uniform tests)
-                a[r].re = wf[p >> 5] ? buf[p + lane] : 0.0;
-                a[r].im = wf[(p + im_off) >> 5] ? buf[p + im_off + lane] : 0.0;
-            } else {
-                a[r].re = buf[p + lane];
-                a[r].im = buf[p + im_off + lane];
-            }
+        for (int r = 0; r < kNV; ++r) a[r] = nxt[r];
+        if (u + 1 < u1) {
+            nbase = runs_deposit(u + 1, pass.base);
+            load_unit(planar_addr(nbase, lb, lmask, 0), nxt);
         }
+        const uint64_t xl = xb | lane;  // condition index without the register bits
         for (uint32_t i = 0; i < pass.nops; ++i) {
             const StreamOp& o = pass.ops[i];
+            const uint32_t lp = __popcll(o.row & xl) & 1u;
             if (o.type == OP_DIAG) {
+                // entries of logical bit 0 / 1 for this lane; register r takes B where rpat says so
+                const double Ar = lp ? o.m[2] : o.m[0], Ai = lp ? o.m[3] : o.m[1];
+                const double Br = lp ? o.m[0] : o.m[2], Bi = lp ? o.m[1] : o.m[3];
 #pragma unroll
                 for (int r = 0; r < kNV; ++r) {
-                    const uint32_t e = stream_bit(o.src_hi, o.idx_hi, lane, r, xb);
-                    a[r] = cmul(e ? o.m[2] : o.m[0], e ? o.m[3] : o.m[1], a[r]);
+                    if ((o.rpat >> r) & 1u)  // uniform
+                        a[r] = cmul(Br, Bi, a[r]);
+                    else
+                        a[r] = cmul(Ar, Ai, a[r]);
                 }
             } else if (o.type == OP_CDIAG) {
+                const uint32_t lp2 = __popcll(o.row2 & xl) & 1u;
+                const uint32_t on = (o.rpat ^ (0u - lp)) & (o.rpat2 ^ (0u - lp2));
 #pragma unroll
                 for (int r = 0; r < kNV; ++r)
-                    if (stream_bit(o.src_hi, o.idx_hi, lane, r, xb) & stream_bit(o.src_lo, o.idx_lo, lane, r, xb))
-                        a[r] = cmul(o.m[0], o.m[1], a[r]);
-            } else if (o.type == OP_CX) {  // control hi, target lo: an exact permutation
-                if (o.src_lo == 1) {
-                    const auto sw = [&](int r0, int r1) {
-                        if (stream_bit(o.src_hi, o.idx_hi, lane, r0, xb)) {
-                            const C2 t = a[r0];
-                            a[r0] = a[r1];
-                            a[r1] = t;
-                        }
-                    };
-                    if (o.idx_lo == 0)
-                        reg_pairs<0>(sw);
-                    else
-                        reg_pairs<1>(sw);
-                } else {
+                    if ((on >> r) & 1u) a[r] = cmul(o.m[0], o.m[1], a[r]);
+            } else {  // OP_U2: partner x ^ d; this value is the |1> side where its logical bit is 1
+                // partner register r ^ dq (dq uniform: one branch, constant indices,
+                // so the values stay in registers)
+                C2 pv[kNV];
+                switch (o.dq & (kNV - 1)) {
+                case 0:
 #pragma unroll
-                    for (int r = 0; r < kNV; ++r) {
-                        const C2 pv = shfl_c2(a[r], 1u << o.idx_lo);
-                        if (stream_bit(o.src_hi, o.idx_hi, lane, r, xb)) a[r] = pv;
-                    }
+                    for (int r = 0; r < kNV; ++r) pv[r] = a[r];
+                    break;
+                case 1:
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) pv[r] = a[r ^ 1];
+                    break;
+                case 2:
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) pv[r] = a[r ^ 2];
+                    break;
+                default:
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) pv[r] = a[r ^ 3];
+                    break;
                 }
-            } else {  // OP_U2 on hi
-                if (o.src_hi == 1) {
-                    const auto mix = [&](int r0, int r1) {
-                        const C2 a0 = a[r0], a1 = a[r1];
-                        a[r0] = row2(o.et, o.m, 0, a0, a1);
-                        a[r1] = row2(o.et, o.m, 1, a0, a1);
-                    };
-                    if (o.idx_hi == 0)
-                        reg_pairs<0>(mix);
-                    else
-                        reg_pairs<1>(mix);
-                } else {
-                    // partner across lanes; each lane forms its own row with
-                    // the generic product (exact for every entry class)
-                    const uint32_t me = (lane >> o.idx_hi) & 1u;
-                    const double w0r = me ? o.m[4] : o.m[0], w0i = me ? o.m[5] : o.m[1];
-                    const double w1r = me ? o.m[6] : o.m[2], w1i = me ? o.m[7] : o.m[3];
+                if (o.dl) {
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) pv[r] = shfl_c2(pv[r], o.dl);
+                }
+                const uint32_t side = o.rpat ^ (0u - lp);
+                // out = u[b][b] mine + u[b][!b] partner for logical bit b of this
+                // value: row 0 = u00 a0 + u01 a1, row 1 = u10 a0 + u11 a1 (the sum
+                // commutes exactly). When u00, u11 and u01, u10 share their entry
+                // classes (H, X, Y, RX, RY, ...) one specialised product serves
+                // both rows (o.pad: 1 real / imaginary pair, see make_stream).
+                if (o.pad == 1) {  // cm real, cp real
 #pragma unroll
                     for (int r = 0; r < kNV; ++r) {
-                        const C2 pv = shfl_c2(a[r], 1u << o.idx_hi);
-                        const C2 a0 = me ? pv : a[r], a1 = me ? a[r] : pv;
-                        a[r] = cadd(cmul(w0r, w0i, a0), cmul(w1r, w1i, a1));
+                        const uint32_t me = (side >> r) & 1u;
+                        const double cm = me ? o.m[6] : o.m[0], cp = me ? o.m[4] : o.m[2];
+                        a[r] = C2{__dadd_rn(__dmul_rn(cm, a[r].re), __dmul_rn(cp, pv[r].re)),
+                                  __dadd_rn(__dmul_rn(cm, a[r].im), __dmul_rn(cp, pv[r].im))};
                     }
+                } else if (o.pad == 2) {  // cm real, cp imaginary: cp * z = (-ci zi, ci zr)
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) {
+                        const uint32_t me = (side >> r) & 1u;
+                        const double cm = me ? o.m[6] : o.m[0], ci = me ? o.m[5] : o.m[3];
+                        a[r] = C2{__dadd_rn(__dmul_rn(cm, a[r].re), -__dmul_rn(ci, pv[r].im)),
+                                  __dadd_rn(__dmul_rn(cm, a[r].im), __dmul_rn(ci, pv[r].re))};
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) {
+                        const uint32_t me = (side >> r) & 1u;
+                        const C2 a0 = me ? pv[r] : a[r], a1 = me ? a[r] : pv[r];
+                        const double w0r = me ? o.m[4] : o.m[0], w0i = me ? o.m[5] : o.m[1];
+                        const double w1r = me ? o.m[6] : o.m[2], w1i = me ? o.m[7] : o.m[3];
+                        pv[r] = cadd(cmul(w0r, w0i, a0), cmul(w1r, w1i, a1));
+                    }
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) a[r] = pv[r];
                 }
             }
         }

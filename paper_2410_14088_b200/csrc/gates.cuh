@@ -118,25 +118,32 @@ struct PermPass {
     const uint16_t* table;          // [1 << npat_bits][4096] (device)
 };
 
-// Register-streaming pass (k_stream_pass): for passes whose gates are
-// U2 / DIAG / CDIAG / CX only and mix at most two buffer bits above bit 4.
-// A warp owns "units" of 128 amplitudes: buffer bits 0..4 are its lanes and
-// two more bits Q (the mixing bits, filled up with the lowest free bits) are
-// the index of four values each lane holds in registers. Gates run in
-// program order on registers (a lane-bit partner through shuffles), with the
-// reference's rounding sequence (cmul / row2, as the tiled kernel); no
-// shared memory and no barriers. Units are dealt to warps in contiguous
-// ranges so the quantising epilogue's per-chunk counters reduce per run.
+// Register-streaming pass (k_stream_pass): for passes of U2 / DIAG / CDIAG /
+// CX gates whose partners stay within the lane bits 0..4 and two more bits Q.
+// A warp owns "units" of 128 amplitudes: lane l, register value r of unit u
+// holds buffer index x = base(u) | l | dep(r), dep(r) spreading r over Q.
+// CX moves no data (as the tiled kernel's lazy CX): the host folds every CX
+// into a GF(2) map y = M x from physical to logical index, so a diagonal gate
+// on logical bit t multiplies by the entry of parity(row_t & x), and a U2 on
+// logical bit t pairs x with x ^ d, d = column t of M^-1 (lane bits through a
+// shuffle, Q bits as another register). A pass qualifies only if M is the
+// identity again at its end (QAOA's CX-RZ-CX is). The parity over the
+// register bits is a host-made 4-bit pattern per op (rpat), the rest one
+// popcount per lane. Arithmetic is the tiled kernel's (cmul / row2: the
+// reference's products, exact up to the sign of an exact zero). No shared
+// memory, no barriers; units are dealt to warps in contiguous ranges so the
+// quantising epilogue's per-chunk counters reduce once per run.
 constexpr int kStreamNQ = 2;  // register bits per lane (4 values)
 constexpr int kMaxStreamOps = 48;
 struct StreamOp {
-    uint8_t type, hi, lo;
-    uint8_t src_hi, src_lo;   // where the bit lives: 0 lane bit, 1 register bit, 2 base bit
-    uint8_t idx_hi, idx_lo;   // lane bit number / register bit number (base bits: the buffer bit)
-    uint8_t pad;
+    uint8_t type;             // OP_DIAG, OP_CDIAG or OP_U2 (CX folded into the rows)
+    uint8_t rpat, rpat2;      // bit r: parity(row & dep(r)) (row2: CDIAG's second bit)
+    uint8_t dq;               // U2: partner register = r ^ dq
+    uint32_t dl;              // U2: partner lane = lane ^ dl
+    uint64_t row, row2;       // logical bit(s) = parity(row & x) over the non-register bits of x
     double m[8];              // U2: u00 u01 u10 u11; DIAG: u00 u11; CDIAG: u33 (interleaved re/im)
     uint8_t et[4];            // entry classes (U2: row-major; DIAG: u00 u11; CDIAG: u33)
-    uint32_t pad2;
+    uint32_t pad;             // U2: 1 = real 2x2, 2 = real diagonal + imaginary off-diagonal, 0 = general
 };
 struct StreamPass {
     BitRuns base;             // unit index -> buffer bits outside {0..4} and Q
