@@ -158,6 +158,29 @@ __device__ __forceinline__ uint32_t quantize_pack_f32(double v, const DevTables&
     return (qo << 2) | ((hi >> 30) & 2u);
 }
 
+// The branch-free part of quantize_pack_f32: the packed word when the
+// estimate decides it (a normal number away from a rounding tie, inside the
+// window) or when v is +-0; otherwise `need` is set and the caller settles
+// the scalar with quantize_pack_fast (zeros, subnormals, infinities, NaNs,
+// ties: the exact reference decision). Callers batch several scalars and
+// take the (rare) settling path once per batch.
+__device__ __forceinline__ uint32_t quant_est_f32(double v, const DevTables& t, int span, bool& need) {
+    const uint32_t hi = static_cast<uint32_t>(__double2hiint(v)), lo = static_cast<uint32_t>(__double2loint(v));
+    const uint32_t ahi = hi & 0x7fffffffu;
+    const bool normal = ahi - 0x00100000u < 0x7fe00000u;
+    const float ef = static_cast<float>(static_cast<int>(ahi >> 20) - 1023);
+    const float m = __int_as_float(0x3f800000 | (__funnelshift_l(lo, ahi, 3) & 0x7fffffu));
+    const float P = __fmul_rn(ef, t.fH);  // exact
+    const float Pi = floorf(P);
+    const float u = __fmaf_rn(ef, t.fL, __fsub_rn(P, Pi));
+    const float s = __fmaf_rn(lg2_approx(m), t.finv, u);
+    const float r = rintf(s);
+    const uint32_t qo = static_cast<uint32_t>(__float2int_rz(Pi) + __float2int_rz(r) - t.qlo32);
+    const bool zero = (ahi | lo) == 0u;
+    need = !zero && !(normal && fabsf(__fsub_rn(s, r)) < t.ftie && qo <= static_cast<uint32_t>(span));
+    return zero ? 1u : ((qo << 2) | ((hi >> 30) & 2u));
+}
+
 // Per-thread counters of one chunk over packed words, reduced per warp with
 // REDUX at the flush (ChunkAcc's fields, cheaper per scalar):
 //   mn = min over words of (pk ^ 1) - 1  (a zero word 1 -> 0xffffffff, else pk)

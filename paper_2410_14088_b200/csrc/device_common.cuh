@@ -80,7 +80,15 @@ constexpr int kHeaderBytes = 26;
 // Exact reference quantiser q = llround(log2|v| / b_a) for finite v != 0.
 // A float log2 estimate lands within +-1 of the true code; the table
 // thresholds then settle it bit-exactly (see codec_tables.cpp).
-__device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& out_of_window) {
+struct QuantSearch {
+    int64_t q;
+    bool out_of_window;
+};
+// Out of line: the settling path of every quantiser variant is rare, and
+// inlining its search loops into each call site bloats the hot kernels'
+// instruction footprint.
+static __device__ __noinline__ QuantSearch quantize_search(double v, const uint64_t* __restrict__ T, int64_t qlo,
+                                                    int64_t qhi, double inv_ba) {
     const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v)) & 0x7fffffffffffffffull;
     const uint32_t ex = static_cast<uint32_t>(bits >> 52);
     uint64_t man = bits & 0xfffffffffffffull;
@@ -93,27 +101,29 @@ __device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& 
         e2 = static_cast<int>(ex) - 1023;
     }
     const float m = __int_as_float(0x3f800000 | static_cast<int>(man >> 29));  // mantissa truncated to float
-    const double x = (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * t.inv_ba;
+    const double x = (static_cast<double>(e2) + static_cast<double>(__log2f(m))) * inv_ba;
     int64_t q = __double2ll_rn(x);
-    q = q < t.qlo ? t.qlo : (q > t.qhi ? t.qhi : q);
-    const uint64_t* T = t.thresh;
-    int64_t i = q - t.qlo;
+    q = q < qlo ? qlo : (q > qhi ? qhi : q);
+    int64_t i = q - qlo;
     while (bits < __ldg(T + i)) {
-        if (i == 0) {
-            out_of_window = true;
-            return t.qlo;
-        }
+        if (i == 0) return QuantSearch{qlo, true};
         --i;
     }
-    const int64_t last = t.qhi - t.qlo;  // T[last + 1] bounds the window from above
+    const int64_t last = qhi - qlo;  // T[last + 1] bounds the window from above
     while (bits >= __ldg(T + i + 1)) {
-        if (i == last) {
-            out_of_window = true;
-            return t.qhi;
-        }
+        if (i == last) return QuantSearch{qhi, true};
         ++i;
     }
-    return t.qlo + i;
+    return QuantSearch{qlo + i, false};
+}
+
+// Exact reference quantiser q = llround(log2|v| / b_a) for finite v != 0.
+// A float log2 estimate lands within +-1 of the true code; the table
+// thresholds then settle it bit-exactly (see codec_tables.cpp).
+__device__ __forceinline__ int64_t quantize(double v, const DevTables& t, bool& out_of_window) {
+    const QuantSearch r = quantize_search(v, t.thresh, t.qlo, t.qhi, t.inv_ba);
+    if (r.out_of_window) out_of_window = true;
+    return r.q;
 }
 
 // x ~ log2|v| / b_a for finite v != 0 from a float log2 of the mantissa.

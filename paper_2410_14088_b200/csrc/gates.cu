@@ -1474,36 +1474,43 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
         }
         run_len = 0;
     };
-    // one unit's values in flight ahead of the one being processed
+    // one unit's values in flight ahead of the one being processed; returns
+    // true when every row of the unit is flagged zero (nothing was loaded)
     const auto load_unit = [&](uint64_t pbu, C2* v) {
+        bool any = !wf_read;
 #pragma unroll
         for (int r = 0; r < kNV; ++r) {
             const uint64_t p = pbu + pdep[r];
             if (wf_read) {  // rows flagged zero were not stored (warp-uniform tests)
-                v[r].re = wf[p >> 5] ? __ldcs(buf + p + lane) : 0.0;
-                v[r].im = wf[(p + im_off) >> 5] ? __ldcs(buf + p + im_off + lane) : 0.0;
+                const bool fr = wf[p >> 5] != 0, fi = wf[(p + im_off) >> 5] != 0;
+                v[r].re = fr ? __ldcs(buf + p + lane) : 0.0;
+                v[r].im = fi ? __ldcs(buf + p + im_off + lane) : 0.0;
+                any = any || fr || fi;
             } else {
                 v[r].re = __ldcs(buf + p + lane);
                 v[r].im = __ldcs(buf + p + im_off + lane);
             }
         }
+        return !any;
     };
     C2 nxt[kNV];
     uint64_t nbase = runs_deposit(u0, pass.base);
-    load_unit(planar_addr(nbase, lb, lmask, 0), nxt);
+    bool nzero = load_unit(planar_addr(nbase, lb, lmask, 0), nxt);
     for (uint64_t u = u0; u < u1; ++u) {
         const uint64_t base = nbase;
         const uint64_t pb = planar_addr(base, lb, lmask, 0);
         const uint64_t xb = vtab ? ((static_cast<uint64_t>(vtab[base >> lb]) << lb) | (base & lmask)) : base;
+        const bool zunit = nzero;  // all zero: gates keep it zero (partners lie inside the unit)
         C2 a[kNV];
 #pragma unroll
         for (int r = 0; r < kNV; ++r) a[r] = nxt[r];
         if (u + 1 < u1) {
             nbase = runs_deposit(u + 1, pass.base);
-            load_unit(planar_addr(nbase, lb, lmask, 0), nxt);
+            nzero = load_unit(planar_addr(nbase, lb, lmask, 0), nxt);
         }
+        if (zunit && !kQuant) continue;  // flags stay 0, nothing stored
         const uint64_t xl = xb | lane;  // condition index without the register bits
-        for (uint32_t i = 0; i < pass.nops; ++i) {
+        for (uint32_t i = 0; i < (zunit ? 0u : pass.nops); ++i) {
             const StreamOp& o = pass.ops[i];
             const uint32_t lp = __popcll(o.row & xl) & 1u;
             if (o.type == OP_DIAG) {
@@ -1588,21 +1595,42 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
         if constexpr (kQuant) {
             if (run_len && ((pb ^ run_pb) >> 12)) flush();
             if (!run_len) run_pb = pb;
+            uint32_t pk[2 * kNV];
+            if (zunit) {
+#pragma unroll
+                for (int k = 0; k < 2 * kNV; ++k) pk[k] = 1u;
+            } else if (q.t.f32) {
+                uint32_t need = 0;
+#pragma unroll
+                for (int r = 0; r < kNV; ++r) {
+                    bool n0, n1;
+                    pk[2 * r] = quant_est_f32(a[r].re, q.t, span, n0);
+                    pk[2 * r + 1] = quant_est_f32(a[r].im, q.t, span, n1);
+                    need |= (n0 ? 1u : 0u) << (2 * r);
+                    need |= (n1 ? 1u : 0u) << (2 * r + 1);
+                }
+                if (need) [[unlikely]] {  // ties, subnormals, non-finite: the exact decision
+#pragma unroll
+                    for (int r = 0; r < kNV; ++r) {
+                        if (need >> (2 * r) & 1u) pk[2 * r] = quantize_pack_fast(a[r].re, q.t, qlo_d, span, bad, oow);
+                        if (need >> (2 * r + 1) & 1u)
+                            pk[2 * r + 1] = quantize_pack_fast(a[r].im, q.t, qlo_d, span, bad, oow);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < kNV; ++r) {
+                    pk[2 * r] = quantize_pack_fast(a[r].re, q.t, qlo_d, span, bad, oow);
+                    pk[2 * r + 1] = quantize_pack_fast(a[r].im, q.t, qlo_d, span, bad, oow);
+                }
+            }
 #pragma unroll
             for (int r = 0; r < kNV; ++r) {
-                uint32_t pr, pi;
-                if (q.t.f32) {
-                    pr = quantize_pack_f32(a[r].re, q.t, span, bad, oow);
-                    pi = quantize_pack_f32(a[r].im, q.t, span, bad, oow);
-                } else {
-                    pr = quantize_pack_fast(a[r].re, q.t, qlo_d, span, bad, oow);
-                    pi = quantize_pack_fast(a[r].im, q.t, qlo_d, span, bad, oow);
-                }
                 const uint64_t p = pb + pdep[r] + lane;
-                q.pk[p] = pr;
-                q.pk[p + im_off] = pi;
-                acc[r][0].add(pr);
-                acc[r][1].add(pi);
+                __stcs(q.pk + p, pk[2 * r]);
+                __stcs(q.pk + p + im_off, pk[2 * r + 1]);
+                acc[r][0].add(pk[2 * r]);
+                acc[r][1].add(pk[2 * r + 1]);
             }
             ++run_len;
         } else {
