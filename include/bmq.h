@@ -177,6 +177,8 @@ typedef struct bmq_report {
     uint64_t compact_bytes;         /* payload bytes moved by in-place arena compactions */
     uint64_t host_peak_bytes;       /* high-water of live payload bytes in the pinned host level */
     uint64_t arena_bytes;           /* device arena capacity at the end of the run */
+    uint64_t fused_decode_batches;  /* batches whose first gate pass decoded the payload rows itself */
+    uint64_t stream_passes;         /* gate passes with a register-streaming form (k_stream_pass; blocks of >= 2^12) */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

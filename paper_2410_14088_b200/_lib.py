@@ -83,7 +83,8 @@ class bmq_report(C.Structure):
                 ("lazy_cx", C.c_uint64), ("perm_materialisations", C.c_uint64),
                 ("model_bytes", C.c_uint64), ("model_groups", C.c_uint64), ("link_h2d_bytes", C.c_uint64),
                 ("link_d2h_bytes", C.c_uint64), ("link_ms", C.c_double),
-                ("compact_bytes", C.c_uint64), ("host_peak_bytes", C.c_uint64), ("arena_bytes", C.c_uint64)]
+                ("compact_bytes", C.c_uint64), ("host_peak_bytes", C.c_uint64), ("arena_bytes", C.c_uint64),
+                ("fused_decode_batches", C.c_uint64), ("stream_passes", C.c_uint64)]
 
 
 _P = C.c_void_p

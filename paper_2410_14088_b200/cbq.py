@@ -656,7 +656,7 @@ DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks
                       "host_spill_bytes", "host_spill_batches", "code_domain_batches", "pool_growths",
                       "lazy_cx", "perm_materialisations",
                       "model_bytes", "model_groups", "link_h2d_bytes", "link_d2h_bytes", "link_ms",
-                      "compact_bytes", "host_peak_bytes", "arena_bytes")
+                      "compact_bytes", "host_peak_bytes", "arena_bytes", "fused_decode_batches", "stream_passes")
 
 
 def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:

@@ -501,11 +501,45 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
     if (kMode == kSumsOnly || (kMode == kDoubles && want_sums)) block_sums3(sq, sre, sim, s_red, &infos[bi].sumsq);
 }
 
+// Mode 3: per-word row records instead of scalars (DecRow): a gate pass
+// then decodes each 32-scalar row itself (k_stream_pass, FusedDecode). A
+// failed or ALL_ZERO block gets all-zero rows (a failure is reported by the
+// index kernel and raised after the stage).
+__global__ void __launch_bounds__(kChunkThreads) k_dec_rows(const DecBlock* __restrict__ blks, uint32_t nch_max,
+                                                            const DecInfo* __restrict__ infos,
+                                                            const DecChunk* __restrict__ dcs,
+                                                            DecRow* __restrict__ rows) {
+    const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
+    const DecInfo info = infos[bi];
+    const DecBlock blk = blks[bi];
+    const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
+    const uint32_t tid = threadIdx.x;
+    DecRow* out = rows + (static_cast<uint64_t>(bi) * nch_max + c) * kWordsPerChunk;
+    const uint64_t nch = (info.count + kChunk - 1) / kChunk;
+    if ((info.flags & 3) || c >= nch) {
+        out[tid] = DecRow{0u, 0u, 0u, 0u};
+        return;
+    }
+    const uint32_t len = chunk_len(info.count, c);
+    const uint32_t vm = word_mask(len, tid);
+    uint32_t sw = 0, zw = 0;
+    if (vm) {
+        sw = d.stag == 1 ? vm : (d.stag == 2 ? load_u32_unaligned(blk.in + d.sign_off + 4 * tid) & vm : 0);
+        zw = d.ztag == 1 ? vm : (d.ztag == 2 ? load_u32_unaligned(blk.in + d.zero_off + 4 * tid) & vm : 0);
+    }
+    const uint32_t nz = ~zw & vm;
+    using Scan = cub::BlockScan<uint32_t, kChunkThreads>;
+    __shared__ typename Scan::TempStorage ss;
+    uint32_t pre;
+    Scan(ss).ExclusiveSum(static_cast<uint32_t>(__popc(nz)), pre);
+    out[tid] = DecRow{nz, sw & nz, d.nz_prefix + pre, 0u};
+}
+
 }  // namespace
 
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
-                       uint64_t* launches, int mode, uint8_t* zflag, uint32_t* imnz) {
+                       uint64_t* launches, int mode, uint8_t* zflag, uint32_t* imnz, DecRow* rows) {
     if (nblk == 0) return;
     BMQ_CUDA(cudaMemsetAsync(d_info, 0, nblk * sizeof(DecInfo), st));
     // mode 1: zflag = per-chunk zero flags (index kernel); mode 0: zflag =
@@ -516,7 +550,9 @@ void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, u
                                                                         mode == 1 && zflag ? imnz : nullptr,
                                                                         mode == 0 && zflag ? imnz : nullptr);
     const uint32_t grid = static_cast<uint32_t>(nblk * nch_max);
-    if (mode == 1)
+    if (mode == 3)
+        k_dec_rows<<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, rows);
+    else if (mode == 1)
         k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err,
                                                              zflag ? 1 : 0, nullptr);
     else if (mode == 2)

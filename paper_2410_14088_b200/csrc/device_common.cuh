@@ -284,6 +284,16 @@ struct DecChunk {
     uint8_t stag, ztag, pad0, pad1;
 };
 
+// Row index of a batch for decoding straight into a gate pass (mode 3 of
+// launch_decompress): one record per 32-scalar bitmap word in the planar
+// layout of the work buffer (word w covers planar scalars 32 w .. 32 w + 31).
+struct DecRow {
+    uint32_t nz;    // bit i: scalar i nonzero
+    uint32_t sign;  // bit i: scalar i negative
+    uint32_t rank;  // codes before this word in its block (the first nonzero's rank)
+    uint32_t pad;
+};
+
 struct DecInfo {
     uint64_t count;
     int64_t code_min;

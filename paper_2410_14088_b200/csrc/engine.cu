@@ -511,6 +511,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     zflag_.alloc(max_blocks_ * nch_);
     imnz_.alloc(1);
     wflag_.alloc(work_scalars_ / 32);
+    if (L_.b >= 12 && getenv("BMQ_FUSED_DECODE")) rows_.alloc(work_scalars_ / 32);
     ids_.alloc(std::max<uint64_t>(nid, max_blocks_));
     vtab_.alloc(std::max<uint64_t>(nid, max_blocks_));
     new_off_.alloc(nid);
@@ -529,7 +530,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     // HBM / 8) and grow up to what the device has left.
     const uint64_t worst = nid * (compress_bound(blk_scalars) + kArenaAlign) + 64;
     const uint64_t others = work_.bytes() + pk_.bytes() + cplan_.bytes() + dchunk_.bytes() + zflag_.bytes() +
-                            wflag_.bytes() + 8 * (ids_.n + vtab_.n + new_off_.n + live_ids_.n + off_.n + size_.n) +
+                            wflag_.bytes() + rows_.bytes() + 8 * (ids_.n + vtab_.n + new_off_.n + live_ids_.n + off_.n + size_.n) +
                             sums_.bytes();
     const uint64_t headroom = total_b > others + (6ull << 30) ? total_b - others - (6ull << 30) : (1ull << 30);
     arena_grow_ = cfg.device_pool_bytes == 0 || (cfg.flags & BMQ_FLAG_POOL_GROW);
@@ -1165,8 +1166,17 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t*
                         : (program_zero_skip(sp.prog, L_.b, false) ? wflag_.p : nullptr);
     // imnz_: code domain, some imaginary-half chunk nonzero; FP: some group flag 0
     if (zf) BMQ_CUDA(cudaMemsetAsync(imnz_.p, 0, sizeof(uint32_t), st_));
+    // Opt-in (BMQ_FUSED_DECODE=1): FP stages whose first pass streams decode
+    // the payload rows inside it and the decoder only writes per-word row
+    // records (no 16 B per amplitude round trip through HBM). Measured slower
+    // on B200 (QAOA-3reg-30 @1e-4: 2.44 s against 1.80 s): the pass's
+    // dependent record -> code -> dequantisation loads are latency-bound at
+    // its occupancy, where the separate decoder hides them.
+    static const bool fused_on = getenv("BMQ_FUSED_DECODE") != nullptr;
+    const bool fdec = !codes && rows_.p && fused_on && stream_first_pass(sp.prog, L_.b, false, d_vtab != nullptr);
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
-                      &counters_.kernel_launches, codes ? 1 : 0, zf, zf ? imnz_.p : nullptr);
+                      &counters_.kernel_launches, fdec ? 3 : (codes ? 1 : 0), fdec ? nullptr : zf,
+                      (zf && !fdec) ? imnz_.p : nullptr, rows_.p);
     if (host_pool_) BMQ_CUDA(cudaEventRecord(ev_dec_[slot], st_));  // the prefetch slot is free again
     pf_live_[slot] = false;
     phase_event(4 * bidx + 1);
@@ -1180,8 +1190,19 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t*
                          zf ? imnz_.p : nullptr);
         ++counters_.code_domain_batches;
     } else {
+        FusedDecode fd{};
+        if (fdec) {
+            fd.blks = dec_.p;
+            fd.infos = dinfo_.p;
+            fd.rows = rows_.p;
+            fd.dequant = tabs_->dequant;
+            fd.qlo = tabs_->qlo;
+            fd.qhi = tabs_->qhi;
+            fd.err = err_.p;
+            ++counters_.fused_decode_batches;
+        }
         fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per, &counters_.kernel_launches,
-                            &qo, d_vtab, nblk, zf, nch_, zf ? imnz_.p : nullptr);
+                            &qo, d_vtab, nblk, zf, nch_, zf ? imnz_.p : nullptr, fdec ? &fd : nullptr);
     }
     phase_event(4 * bidx + 2);
     if (getenv("BMQ_DBG_CPLAN")) {  // development aid: the quantiser's chunk counters
@@ -1202,6 +1223,8 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t*
         counters_.perm_materialisations += sp.prog.perms;
     }
     counters_.gate_passes += sp.prog.passes.size();
+    if (!codes)
+        for (const GatePass& gp : sp.prog.passes) counters_.stream_passes += gp.sp && !stream_off() ? 1 : 0;
 }
 
 void Engine::run_stage(uint64_t s) {
@@ -1408,6 +1431,8 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.compact_bytes = counters_.compact_bytes;
     r.host_peak_bytes = host_heap_.high_water();
     r.arena_bytes = arena_limit_;
+    r.fused_decode_batches = counters_.fused_decode_batches;
+    r.stream_passes = counters_.stream_passes;
     *rep = r;
 }
 

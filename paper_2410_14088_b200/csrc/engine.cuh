@@ -277,6 +277,7 @@ private:
     DevArray<DecChunk> dchunk_;
     DevArray<uint8_t> zflag_;  // per (batch slot, chunk): all-zero input chunk (code-domain stages)
     DevArray<uint32_t> imnz_;  // 1 word: code domain, some imaginary-half input chunk is nonzero; FP, some group flag is 0
+    DevArray<DecRow> rows_;    // per 32 scalars of work_: decode rows of a streaming first pass (fused decode)
     DevArray<uint8_t> wflag_;  // per 32 scalars of work_: group stored (1) or all zero (0), FP stages
     DevArray<uint64_t> ids_;
     DevArray<uint32_t> vtab_;

@@ -1429,12 +1429,13 @@ __device__ __forceinline__ C2 shfl_c2(C2 a, uint32_t m) {
     return C2{__shfl_xor_sync(0xffffffffu, a.re, m), __shfl_xor_sync(0xffffffffu, a.im, m)};
 }
 
-template <bool kQuant>
+template <bool kQuant, bool kDecode>
 __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
                                                                 const __grid_constant__ StreamPass pass,
                                                                 const __grid_constant__ QuantOut q,
                                                                 const uint32_t* __restrict__ vtab,
-                                                                uint8_t* __restrict__ wf, uint32_t* wz) {
+                                                                uint8_t* __restrict__ wf, uint32_t* wz,
+                                                                const __grid_constant__ FusedDecode dec) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kStreamThreads + threadIdx.x) >> 5;
     const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kStreamThreads) >> 5;
@@ -1458,30 +1459,74 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
     bool bad = false, oow = false;
     const int span = static_cast<int>(q.t.qhi - q.t.qlo);
     const double qlo_d = static_cast<double>(q.t.qlo);
-    RowAcc acc[kNV][2];
+    // Per-chunk counters of the current run, reduced per row with REDUX as it
+    // is quantised: warp-uniform values (uniform registers, not 24 per-lane
+    // ones), fields as RowAcc's.
+    uint32_t amn[kNV][2], amx[kNV][2], azn[kNV][2];
 #pragma unroll
-    for (int r = 0; r < kNV; ++r) acc[r][0] = acc[r][1] = RowAcc{};
+    for (int r = 0; r < kNV; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) amn[r][h] = ~0u, amx[r][h] = 0u, azn[r][h] = 0u;
     uint64_t run_pb = 0;  // planar base of the current counter run
     uint32_t run_len = 0;
     const auto flush = [&]() {
 #pragma unroll
         for (int r = 0; r < kNV; ++r) {
-            const uint64_t key = (run_pb | pdep[r]) >> 12;
-            flush_rows(q.cps + key, acc[r][0], 32u * run_len);
-            flush_rows(q.cps + key + (im_off >> 12), acc[r][1], 32u * run_len);
-            acc[r][0] = RowAcc{};
-            acc[r][1] = RowAcc{};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                ChunkPlan* cp = q.cps + (((run_pb | pdep[r]) >> 12) + (h ? (im_off >> 12) : 0));
+                const uint32_t nnz = 32u * run_len - (azn[r][h] & 0xffffu), nneg = azn[r][h] >> 16;
+                if (lane == 0 && nnz) atomicMax(&cp->qmin_inv, kQOffMax - (amn[r][h] >> 2));
+                if (lane == 1 && nnz) atomicMax(&cp->qmax_off, amx[r][h] >> 2);
+                if (lane == 2 && nnz) atomicAdd(&cp->nnz, nnz);
+                if (lane == 3 && nneg) atomicAdd(&cp->nneg, nneg);
+                amn[r][h] = ~0u;
+                amx[r][h] = 0u;
+                azn[r][h] = 0u;
+            }
         }
         run_len = 0;
     };
     // one unit's values in flight ahead of the one being processed; returns
-    // true when every row of the unit is flagged zero (nothing was loaded)
+    // true when every row of the unit is zero (nothing was loaded)
+    constexpr bool decode = kDecode;
+    const int dspan = static_cast<int>(dec.qhi - dec.qlo);
+    bool dbad = false;
+    const uint32_t lt = (1u << lane) - 1;
+    // one 32-scalar row straight from its payload (decompress_block,
+    // codec.hpp:333-342): rank of this lane's code from the row record
+    const auto decode_row = [&](uint64_t p, bool& any) -> double {
+        const DecRow rec = dec.rows[p >> 5];
+        if (!rec.nz) return 0.0;  // warp-uniform
+        any = true;
+        const uint64_t slot = p >> (lb + 1);
+        const uint8_t* codes = dec.blks[slot].in;
+        const DecInfo& di = dec.infos[slot];
+        const uint32_t width = di.width;
+        const uintptr_t cs = reinterpret_cast<uintptr_t>(codes + di.code_seg);
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(cs & ~uintptr_t(3));
+        const uint64_t bit = static_cast<uint64_t>(cs & 3) * 8 +
+                             static_cast<uint64_t>(rec.rank + __popc(rec.nz & lt)) * width;
+        if (!((rec.nz >> lane) & 1u)) return 0.0;
+        const uint32_t code = __funnelshift_r(__ldg(cw + (bit >> 5)), __ldg(cw + (bit >> 5) + 1), bit & 31) &
+                              (width >= 32 ? ~0u : (1u << width) - 1);
+        const int qi = static_cast<int>(di.code_min - dec.qlo) + static_cast<int>(code);
+        if (static_cast<unsigned>(qi) > static_cast<unsigned>(dspan)) {
+            dbad = true;
+            return 0.0;
+        }
+        const double m = __ldg(dec.dequant + qi);
+        return ((rec.sign >> lane) & 1u) ? -m : m;
+    };
     const auto load_unit = [&](uint64_t pbu, C2* v) {
-        bool any = !wf_read;
+        bool any = !wf_read && !decode;
 #pragma unroll
         for (int r = 0; r < kNV; ++r) {
             const uint64_t p = pbu + pdep[r];
-            if (wf_read) {  // rows flagged zero were not stored (warp-uniform tests)
+            if (decode) {
+                v[r].re = decode_row(p, any);
+                v[r].im = decode_row(p + im_off, any);
+            } else if (wf_read) {  // rows flagged zero were not stored (warp-uniform tests)
                 const bool fr = wf[p >> 5] != 0, fi = wf[(p + im_off) >> 5] != 0;
                 v[r].re = fr ? __ldcs(buf + p + lane) : 0.0;
                 v[r].im = fi ? __ldcs(buf + p + im_off + lane) : 0.0;
@@ -1508,7 +1553,17 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
             nbase = runs_deposit(u + 1, pass.base);
             nzero = load_unit(planar_addr(nbase, lb, lmask, 0), nxt);
         }
-        if (zunit && !kQuant) continue;  // flags stay 0, nothing stored
+        if (zunit && !kQuant) {  // nothing stored: the flags say so (already, unless decoding)
+            if (decode && wf && lane == 0) {
+#pragma unroll
+                for (int r = 0; r < kNV; ++r) {
+                    wf[(pb + pdep[r]) >> 5] = 0;
+                    wf[(pb + pdep[r] + im_off) >> 5] = 0;
+                }
+                set_wz = true;
+            }
+            continue;
+        }
         const uint64_t xl = xb | lane;  // condition index without the register bits
         for (uint32_t i = 0; i < (zunit ? 0u : pass.nops); ++i) {
             const StreamOp& o = pass.ops[i];
@@ -1629,8 +1684,13 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
                 const uint64_t p = pb + pdep[r] + lane;
                 __stcs(q.pk + p, pk[2 * r]);
                 __stcs(q.pk + p + im_off, pk[2 * r + 1]);
-                acc[r][0].add(pk[2 * r]);
-                acc[r][1].add(pk[2 * r + 1]);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t w = pk[2 * r + h];
+                    amn[r][h] = min(amn[r][h], __reduce_min_sync(0xffffffffu, (w ^ 1u) - 1u));
+                    amx[r][h] = max(amx[r][h], __reduce_max_sync(0xffffffffu, w));
+                    azn[r][h] += __reduce_add_sync(0xffffffffu, (w & 1u) | ((w & 2u) << 15));
+                }
             }
             ++run_len;
         } else {
@@ -1653,6 +1713,7 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
             }
         }
     }
+    if (dbad) dev_fail(dec.err, DE_CODE_WINDOW, 0);
     if constexpr (kQuant) {
         if (run_len) flush();
         if (bad) dev_fail(q.err, DE_NONFINITE, 0);
@@ -2173,6 +2234,12 @@ bool stream_off() {
     return on;
 }
 
+bool stream_first_pass(const GateProgram& prog, uint32_t lb, bool interleaved, bool blockwise) {
+    if (prog.passes.empty() || interleaved || lb < 12 || stream_off()) return false;
+    const GatePass& p = prog.passes[0];
+    return p.sp && (!blockwise || !((1ull << p.sp->qbit[kStreamNQ - 1]) >> lb));
+}
+
 bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved) {
     if (interleaved || lb < 12 || prog.passes.empty()) return false;
     for (const GatePass& p : prog.passes)
@@ -2182,7 +2249,7 @@ bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved) {
 
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant, const uint32_t* vtab,
-                 uint64_t nblocks, const uint8_t* zflag, uint32_t nch, uint32_t* wz) {
+                 uint64_t nblocks, const uint8_t* zflag, uint32_t nch, uint32_t* wz, const FusedDecode* dec) {
     if (zflag && !wz) raise(BMQ_ERR_LOGIC, "zero-group flags need their summary word");
     if (zflag && !program_zero_skip(prog, lb, interleaved))
         raise(BMQ_ERR_LOGIC, "zero-group skipping needs fast passes only");
@@ -2206,17 +2273,27 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
         const GatePass& p = prog.passes[pi];
         const uint64_t tiles = vtab ? nblocks << (lb - p.tb) : nreps << (prog.total_bits - p.tb);
         const bool last = pi + 1 == prog.passes.size();
+        const FusedDecode fd = (pi == 0 && dec) ? *dec : FusedDecode{};
+        if (pi == 0 && dec && !stream_first_pass(prog, lb, interleaved, vtab != nullptr))
+            raise(BMQ_ERR_LOGIC, "fused decoding needs a streaming first pass");
         if (p.sp && !interleaved && lb >= 12 && !stream_off() &&
             (!vtab || !((1ull << p.sp->qbit[kStreamNQ - 1]) >> lb))) {
             const uint64_t units = (vtab ? nblocks << lb : nreps << prog.total_bits) >> (5 + kStreamNQ);
             const uint64_t warps_per_cta = kStreamThreads / 32;
             const uint64_t grid = std::min<uint64_t>((units + warps_per_cta - 1) / warps_per_cta, 148ull * 8);
-            if (fuse && last)
-                k_stream_pass<true><<<static_cast<uint32_t>(grid), kStreamThreads, 0, st>>>(
-                    buf, lb, units, *p.sp, *quant, vtab, const_cast<uint8_t*>(zflag), wz);
-            else
-                k_stream_pass<false><<<static_cast<uint32_t>(grid), kStreamThreads, 0, st>>>(
-                    buf, lb, units, *p.sp, none, vtab, const_cast<uint8_t*>(zflag), wz);
+            uint8_t* zf = const_cast<uint8_t*>(zflag);
+            const dim3 g(static_cast<uint32_t>(grid)), b(kStreamThreads);
+            if (fuse && last) {
+                if (fd.rows)
+                    k_stream_pass<true, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
+                else
+                    k_stream_pass<true, false><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
+            } else {
+                if (fd.rows)
+                    k_stream_pass<false, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, none, vtab, zf, wz, fd);
+                else
+                    k_stream_pass<false, false><<<g, b, 0, st>>>(buf, lb, units, *p.sp, none, vtab, zf, wz, fd);
+            }
         } else if (p.fast) {
             const size_t smem = tile_bytes + p.fp->tab_entries * sizeof(double2) + p.fp->nops * sizeof(FastOp);
             const uint64_t per_sm = std::max<uint64_t>(1, (227ull * 1024) / (smem + 2048));

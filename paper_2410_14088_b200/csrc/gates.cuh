@@ -204,6 +204,20 @@ struct QuantOut {
     DevError* err;
 };
 
+// First pass decodes its input rows itself (mode 3 of launch_decompress):
+// the payload of block slot s is blks[s].in, its code segment, width and
+// code_min in infos[s]; rows[w] describes planar word w of the batch.
+struct FusedDecode {
+    const DecBlock* blks = nullptr;
+    const DecInfo* infos = nullptr;
+    const DecRow* rows = nullptr;
+    const double* dequant = nullptr;
+    int64_t qlo = 0, qhi = 0;
+    DevError* err = nullptr;
+};
+bool stream_first_pass(const GateProgram& prog, uint32_t lb, bool interleaved, bool blockwise);
+bool stream_off();  // BMQ_DBG_NO_STREAM
+
 // Apply every pass in place to nreps consecutive buffers of
 // 2^total_bits amplitudes (e.g. the groups of a batch). Layout: interleaved
 // complex (lb ignored) or planar per block of 2^lb amplitudes. With quant
@@ -222,7 +236,7 @@ bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved);
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant = nullptr,
                  const uint32_t* vtab = nullptr, uint64_t nblocks = 0, const uint8_t* zflag = nullptr,
-                 uint32_t nch = 0, uint32_t* wz = nullptr);
+                 uint32_t nch = 0, uint32_t* wz = nullptr, const FusedDecode* dec = nullptr);
 
 // Code-domain program (prog.mono): the passes permute packed code words in
 // place (planar per block of 2^lb amplitudes, CmpBlock::pk layout); the last

@@ -7,6 +7,7 @@ import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; ph=r['phases']
 print('$2', d['config']['workload'], 'ms %.1f'%d['ms_per_step'], 'frac %.3f'%r['frac'], ' '.join('%s %.0fms %.2f'%(k,v['ms'],v['frac']) for k,v in ph.items()), 'fid', d['fidelity'])"
 }
 for wl in "--workload qaoa3reg --qubits 30 --error-bound 1e-4" "--workload random --qubits 30 --layers 20" ""; do
+  BMQ_FUSED_DECODE=1 line "$wl" fused
   line "$wl" stream
   BMQ_DBG_NO_STREAM=1 line "$wl" tiled
 done
