@@ -325,6 +325,14 @@ int bmq_simulator_state_norm(bmq_simulator* sim, double* norm);
 int bmq_simulator_extract_state(bmq_simulator* sim, double* amps, uint64_t namps);
 /* single amplitude query (new: the reference only has the dense extract). */
 int bmq_simulator_amplitude(bmq_simulator* sim, uint64_t index, double* re, double* im);
+/* Sampling (the reference has only the dense extract_state,
+ * engine.hpp:138-147): nshots basis-state indices drawn from |a_i|^2 / norm^2
+ * of the stored (decompressed) state, deterministic for a seed (mt19937_64).
+ * Only blocks that receive shots are decoded. */
+int bmq_simulator_sample(bmq_simulator* sim, uint64_t nshots, uint64_t seed, uint64_t* out);
+/* The k amplitudes of largest |a|^2 (ties to the lower index), largest
+ * first; *count = min(k, number of nonzero amplitudes). */
+int bmq_simulator_top_k(bmq_simulator* sim, uint64_t k, uint64_t* idx, double* re, double* im, uint64_t* count);
 /* store().get(id) (store.hpp:120-136): exact payload bytes of block id. */
 int bmq_simulator_get_payload(bmq_simulator* sim, uint64_t id, uint8_t* out, uint64_t cap,
                               uint64_t* size);

@@ -502,6 +502,22 @@ public:
         detail::check(bmq_simulator_amplitude(sim_, index, &re, &im));
         return {re, im};
     }
+    // Sampling / top-k queries (bmq_simulator_sample / _top_k; beyond the
+    // reference, whose only state query is the dense extract_state).
+    std::vector<std::uint64_t> sample(std::uint64_t shots, std::uint64_t seed = 1) {
+        std::vector<std::uint64_t> out(shots);
+        detail::check(bmq_simulator_sample(sim_, shots, seed, out.data()));
+        return out;
+    }
+    std::vector<std::pair<std::uint64_t, Complex>> top_k(std::uint64_t k) {
+        std::vector<std::uint64_t> idx(k);
+        std::vector<double> re(k), im(k);
+        std::uint64_t n = 0;
+        detail::check(bmq_simulator_top_k(sim_, k, idx.data(), re.data(), im.data(), &n));
+        std::vector<std::pair<std::uint64_t, Complex>> out;
+        for (std::uint64_t i = 0; i < n; ++i) out.emplace_back(idx[i], Complex(re[i], im[i]));
+        return out;
+    }
 
     std::vector<std::uint8_t> get_payload(std::uint64_t id) const {  // store().get(id)
         std::uint64_t size = 0;

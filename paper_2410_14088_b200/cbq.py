@@ -759,6 +759,24 @@ class Simulator:
         _check(lib.bmq_simulator_amplitude(self._h, index, C.byref(re), C.byref(im)))
         return complex(re.value, im.value)
 
+    def sample(self, shots: int, seed: int = 1) -> np.ndarray:
+        """Basis-state indices drawn from |a_i|^2 of the stored state
+        (bmq_simulator_sample), deterministic for a seed."""
+        out = np.empty(max(1, shots), dtype=np.uint64)
+        _check(lib.bmq_simulator_sample(self._h, shots, seed, _ptr(out)))
+        return out[:shots]
+
+    def top_k(self, k: int):
+        """(indices, amplitudes) of the k largest |a|^2, largest first, ties to
+        the lower index (bmq_simulator_top_k)."""
+        idx = np.empty(max(1, k), dtype=np.uint64)
+        re = np.empty(max(1, k))
+        im = np.empty(max(1, k))
+        n = C.c_uint64()
+        _check(lib.bmq_simulator_top_k(self._h, k, _ptr(idx), _ptr(re), _ptr(im), C.byref(n)))
+        m = n.value
+        return idx[:m], re[:m] + 1j * im[:m]
+
     def get_payload(self, block_id: int) -> bytes:
         size = C.c_uint64()
         _check(lib.bmq_simulator_get_payload(self._h, block_id, None, 0, C.byref(size)))

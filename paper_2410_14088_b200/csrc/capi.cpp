@@ -323,6 +323,27 @@ int bmq_simulator_amplitude(bmq_simulator* sim, uint64_t index, double* re, doub
     });
 }
 
+int bmq_simulator_sample(bmq_simulator* sim, uint64_t nshots, uint64_t seed, uint64_t* out) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        if (nshots) null_check(out, "out");
+        sim->engine->sample(nshots, seed, out);
+    });
+}
+
+int bmq_simulator_top_k(bmq_simulator* sim, uint64_t k, uint64_t* idx, double* re, double* im, uint64_t* count) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        null_check(count, "count");
+        if (k) {
+            null_check(idx, "idx");
+            null_check(re, "re");
+            null_check(im, "im");
+        }
+        *count = sim->engine->top_k(k, idx, re, im);
+    });
+}
+
 int bmq_simulator_get_payload(bmq_simulator* sim, uint64_t id, uint8_t* out, uint64_t cap, uint64_t* size) {
     return guarded([&] {
         null_check(sim, "simulator");

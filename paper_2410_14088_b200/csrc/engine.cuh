@@ -119,6 +119,9 @@ public:
     double state_norm();
     void extract_state(double* amps, uint64_t namps);
     void amplitude(uint64_t index, double* re, double* im);
+    // queries.cu: shots in basis-index form; top-k by |a|^2
+    void sample(uint64_t nshots, uint64_t seed, uint64_t* out);
+    uint64_t top_k(uint64_t k, uint64_t* idx, double* re, double* im);
     uint64_t get_payload(uint64_t id, uint8_t* out, uint64_t cap);
     void get_payloads(uint8_t* out, uint64_t cap, uint64_t* sizes, uint64_t* total);
     void put_payload(uint64_t id, const uint8_t* data, uint64_t size);
@@ -197,6 +200,7 @@ private:
     DevArray<uint64_t> d_place_;
     void sync_meta_to_host();
     void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
+    const double* decoded_batch(const uint64_t* h_ids, uint64_t n);
     void host_ids_to_device(const std::vector<uint64_t>& ids);
     // Per-id dequantised sums are computed lazily (the emit kernel does not
     // produce them): ensure_sums decodes the payloads of stale ids, all ids
