@@ -390,6 +390,29 @@ int bmq_simulator_footprint(bmq_simulator* sim, uint64_t* resident_bytes, uint64
 /* Report of the stages run so far (final_norm, wall_ms, device_ms = 0). */
 int bmq_simulator_report(bmq_simulator* sim, bmq_report* report);
 
+/* ---- multi-GPU stage loop behind the C ABI ----
+ * A collective names this rank of a sharded run. NCCL: one process per GPU;
+ * rank 0 gets a 128-byte id from bmq_nccl_unique_id and hands it to every
+ * rank by the caller's own means (libnccl.so.2 is loaded at run time).
+ * Local: `world` collectives for `world` simulators driven by `world`
+ * threads of one process (any devices, e.g. several ranks on one GPU).
+ * bmq_simulator_run_sharded is Simulator::run (engine.hpp:97-134) for one
+ * rank: every rank calls it (SPMD) with its own simulator of the same
+ * circuit and config; device qubits (bmq_shard_plan) keep every stage's
+ * groups on one rank, payloads whose owner changes between stages move over
+ * the collective, the BlockStore accounting is replayed from all-reduced
+ * sizes, and the report's norm and counters are global. Final payloads equal
+ * the single-GPU run's; each rank holds the blocks it owns under the last
+ * stage (the others read ALL_ZERO). */
+typedef struct bmq_collective bmq_collective;
+int bmq_nccl_unique_id(uint8_t id[128]);
+int bmq_collective_nccl_create(const uint8_t id[128], uint32_t rank, uint32_t world, int32_t device,
+                               bmq_collective** out);
+int bmq_collective_local_create(uint32_t world, bmq_collective** ranks);
+int bmq_collective_destroy(bmq_collective* col);
+int bmq_simulator_run_sharded(bmq_simulator* sim, bmq_collective* col, bmq_report* report, double* stage_ms,
+                              uint64_t stage_cap);
+
 /* ---- checkpoint / resume (the reference keeps no persisted
  * index, store.hpp:36-46) ----
  * save: every payload (exact bytes, codec.hpp:33-54) with its block sums,

@@ -101,6 +101,11 @@ SIGNATURES = {
     "bmq_gate_unitary": (C.c_int, [C.POINTER(bmq_gate), _P]),
     "bmq_circuit_validate": (C.c_int, [_U32, _P, _U64]),
     "bmq_generate_benchmark": (C.c_int, [C.c_char_p, _U32, _U32, _U64, C.c_char_p, _P, _U64, C.POINTER(_U64)]),
+    "bmq_nccl_unique_id": (C.c_int, [_P]),
+    "bmq_collective_nccl_create": (C.c_int, [_P, _U32, _U32, C.c_int32, _P]),
+    "bmq_collective_local_create": (C.c_int, [_U32, _P]),
+    "bmq_collective_destroy": (C.c_int, [_P]),
+    "bmq_simulator_run_sharded": (C.c_int, [_P, _P, C.POINTER(bmq_report), _P, _U64]),
     "bmq_simulator_sample": (C.c_int, [_P, _U64, _U64, _P]),
     "bmq_simulator_top_k": (C.c_int, [_P, _U64, _P, _P, _P, C.POINTER(_U64)]),
     "bmq_plan_model_default": (None, [C.POINTER(bmq_plan_model)]),

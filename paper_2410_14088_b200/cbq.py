@@ -630,6 +630,44 @@ class Config:
         return c
 
 
+class Collective:
+    """One rank's collective of a sharded run (bmq_collective): NCCL (one
+    process per GPU) or in-process (one thread per rank, any devices)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @staticmethod
+    def local(world: int) -> list:
+        hs = (C.c_void_p * world)()
+        _check(lib.bmq_collective_local_create(world, hs))
+        return [Collective(C.c_void_p(h)) for h in hs]
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib.bmq_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl(uid: bytes, rank: int, world: int, device: int = 0) -> "Collective":
+        h = C.c_void_p()
+        _check(lib.bmq_collective_nccl_create((C.c_uint8 * 128).from_buffer_copy(uid), rank, world, device,
+                                              C.byref(h)))
+        return Collective(h)
+
+    def close(self):
+        if self._h:
+            lib.bmq_collective_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class SimulationReport:
     """cbq::SimulationReport (engine.hpp:39-53) plus device counters."""
@@ -714,6 +752,16 @@ class Simulator:
         nst = max(1, len(self.circuit.gates))
         stage_ms = np.zeros(nst)
         _check(lib.bmq_simulator_run(self._h, C.byref(r), _ptr(stage_ms), nst))
+        return report_from_c(r, stage_ms[: r.stage_count].tolist())
+
+    def run_sharded(self, col: "Collective") -> SimulationReport:
+        """Simulator::run as one rank of a sharded run (bmq_simulator_run_sharded,
+        SURVEY §8e): every rank calls it with its own simulator of the same
+        circuit and config; the report's norm and counters are global."""
+        r = bmq_report()
+        nst = max(1, len(self.circuit.gates))
+        stage_ms = np.zeros(nst)
+        _check(lib.bmq_simulator_run_sharded(self._h, col._h, C.byref(r), _ptr(stage_ms), nst))
         return report_from_c(r, stage_ms[: r.stage_count].tolist())
 
     def reset(self) -> None:

@@ -12,9 +12,14 @@
 #include "bmq.h"
 #include "bmq_internal.hpp"
 #include "engine.cuh"
+#include "shard_run.hpp"
 
 struct bmq_simulator {
     std::unique_ptr<bmq::Engine> engine;
+};
+
+struct bmq_collective {
+    std::unique_ptr<bmq::Collective> col;
 };
 
 namespace {
@@ -402,6 +407,49 @@ int bmq_shard_plan(uint32_t num_qubits, uint32_t block_bits, const bmq_stage* st
         }
         const auto bits = bmq::shard_plan(L, plan, world);
         for (size_t i = 0; i < bits.size(); ++i) device_qubits[i] = bits[i] + L.b;
+    });
+}
+
+int bmq_nccl_unique_id(uint8_t id[128]) {
+    return guarded([&] {
+        null_check(id, "id");
+        bmq::nccl_unique_id(id);
+    });
+}
+
+int bmq_collective_nccl_create(const uint8_t id[128], uint32_t rank, uint32_t world, int32_t device,
+                               bmq_collective** out) {
+    return guarded([&] {
+        null_check(id, "id");
+        null_check(out, "out");
+        auto c = std::make_unique<bmq_collective>();
+        c->col = bmq::make_nccl_collective(id, rank, world, device);
+        *out = c.release();
+    });
+}
+
+int bmq_collective_local_create(uint32_t world, bmq_collective** ranks) {
+    return guarded([&] {
+        null_check(ranks, "ranks");
+        auto cols = bmq::make_local_collectives(world);
+        for (uint32_t r = 0; r < world; ++r) {
+            ranks[r] = new bmq_collective;
+            ranks[r]->col = std::move(cols[r]);
+        }
+    });
+}
+
+int bmq_collective_destroy(bmq_collective* col) {
+    delete col;
+    return BMQ_OK;
+}
+
+int bmq_simulator_run_sharded(bmq_simulator* sim, bmq_collective* col, bmq_report* report, double* stage_ms,
+                              uint64_t stage_cap) {
+    return guarded([&] {
+        null_check(sim, "simulator");
+        null_check(col, "collective");
+        bmq::run_sharded(*sim->engine, *col->col, report, stage_ms, stage_cap);
     });
 }
 

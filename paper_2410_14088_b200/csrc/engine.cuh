@@ -135,6 +135,15 @@ public:
     // partial sums. The host driver moves payloads between stages.
     void shard(uint32_t rank, uint32_t world);
     const std::vector<uint32_t>& device_bits() const { return dev_bits_; }
+    uint32_t shard_world() const { return shard_world_; }
+    bool initialized() const { return initialized_; }
+    uint32_t owner_of(uint64_t id, uint64_t s) const { return owner(id, s); }
+    // the device bits of stage s differ from those of stage s - 1
+    bool owners_changed(uint64_t s) const {
+        for (uint32_t j = 0; j < shard_m_; ++j)
+            if (dev_bits_[s * shard_m_ + j] != dev_bits_[(s - 1) * shard_m_ + j]) return true;
+        return false;
+    }
     // meta per id: {size (0 = ALL_ZERO), sumsq, sum_re, sum_im (f64 bits)}
     void export_payloads(const uint64_t* ids, uint64_t n, uint64_t* meta, void* dst, uint64_t cap);
     void import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* meta, const void* src);

@@ -232,3 +232,64 @@ def test_nccl_world1_path(gpu, port):
             be.close()
     finally:
         dist.destroy_process_group()
+
+
+def _merged(per_rank):
+    """Each id's payload from the rank that holds it (the others read ALL_ZERO)."""
+    out = []
+    for ps in zip(*per_rank):
+        held = [p for p in ps if len(p) > 26 or (len(p) == 26 and p[25] != 1)]
+        out.append(held[0] if held else ps[0])
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name,n,layers,b,br", [("qft", 18, 1, 12, 1e-3), ("qaoa3reg", 18, 2, 12, 1e-4)])
+def test_c_abi_sharded_run_matches_single(gpu, port, world, name, n, layers, b, br):
+    """bmq_simulator_run_sharded (host C++ driver) with the
+    in-process collective: `world` engines on one GPU driven by threads;
+    payloads (each from its owner), peak footprint and norm equal the
+    single-GPU run's, which equals the oracle's."""
+    import threading
+    c = gpu.generate_benchmark(name, n, gpu.BenchmarkParams(layers=layers, seed=1))
+    cfg = gpu.Config(block_bits=b, inner_size=2, error_bound=br)
+    want = port.simulate(n, [g.as_tuple() for g in c.gates], b, 2, br)
+    cols = gpu.Collective.local(world)
+    sims = [gpu.Simulator(c, cfg) for _ in range(world)]
+    reps, errs = [None] * world, []
+
+    def go(r):
+        try:
+            reps[r] = sims[r].run_sharded(cols[r])
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=go, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert _merged([s.payloads() for s in sims]) == want.payloads
+    for rep in reps:
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=1e-10)
+    for s in sims:
+        s.close()
+    for col in cols:
+        col.close()
+
+
+@pytest.mark.gpu
+def test_c_abi_sharded_run_nccl_world1(gpu, port):
+    """The NCCL collective (libnccl.so.2 at run time) for one rank."""
+    c = gpu.generate_benchmark("qft", 16)
+    cfg = gpu.Config(block_bits=12, inner_size=2, error_bound=1e-3)
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    col = gpu.Collective.nccl(gpu.Collective.nccl_unique_id(), 0, 1, 0)
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run_sharded(col)
+        assert sim.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+    col.close()
