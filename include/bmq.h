@@ -90,6 +90,14 @@ typedef struct bmq_config {
      * host level: a full device arena is a StoreError). Device kernels read
      * and write it directly through the mapped address. */
     uint64_t host_pool_bytes;
+    /* Third level (the reference's spill file, store.hpp:234-283):
+     * payloads that fit neither the device arena nor the host level go to an
+     * anonymous spill file in disk_dir (NULL: /tmp) of disk_pool_bytes,
+     * moved device <-> file through a pinned bounce buffer (pread/pwrite),
+     * or by GPUDirect Storage (cuFile) with BMQ_GDS=1 in the environment.
+     * Needs host_pool_bytes > 0. */
+    uint64_t disk_pool_bytes;
+    const char* disk_dir;
 } bmq_config;
 
 /* Skip groups whose blocks are all ALL_ZERO (bit-exact: linear gates map
@@ -179,6 +187,10 @@ typedef struct bmq_report {
     uint64_t arena_bytes;           /* device arena capacity at the end of the run */
     uint64_t fused_decode_batches;  /* batches whose first gate pass decoded the payload rows itself */
     uint64_t stream_passes;         /* gate passes with a register-streaming form (k_stream_pass; blocks of >= 2^12) */
+    uint64_t disk_spill_bytes;      /* payload bytes written to the disk level */
+    uint64_t disk_read_bytes;       /* payload bytes read back from the disk level */
+    uint64_t disk_peak_bytes;       /* high-water of live payload bytes on the disk level */
+    uint64_t disk_gds;              /* 1 when the disk level moves data with GPUDirect Storage (cuFile) */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

@@ -390,6 +390,8 @@ struct Config {  // engine.hpp:23-37 (+ device knobs)
     std::uint64_t device_pool_bytes = 0;  // 0 = automatic
     std::uint64_t work_bytes = 0;         // 0 = automatic
     std::uint64_t host_pool_bytes = 0;    // pinned host level of the store; 0 = none
+    std::uint64_t disk_pool_bytes = 0;    // disk level beneath it (spill file); 0 = none
+    std::string disk_dir;                 // spill file directory ("" = /tmp)
     bmq_config c() const {
         bmq_config k;
         bmq_config_default(&k);
@@ -404,6 +406,8 @@ struct Config {  // engine.hpp:23-37 (+ device knobs)
         k.device_pool_bytes = device_pool_bytes;
         k.work_bytes = work_bytes;
         k.host_pool_bytes = host_pool_bytes;
+        k.disk_pool_bytes = disk_pool_bytes;
+        k.disk_dir = disk_dir.empty() ? nullptr : disk_dir.c_str();
         k.flags = (zero_group_skip ? BMQ_FLAG_ZERO_GROUP_SKIP : 0u) | (identity_skip ? BMQ_FLAG_IDENTITY_SKIP : 0u) |
                   (code_domain ? BMQ_FLAG_CODE_DOMAIN : 0u) | (pool_grow ? BMQ_FLAG_POOL_GROW : 0u) |
                   (arena == Arena::Heap ? BMQ_FLAG_HEAP_ARENA : 0u) | (arena == Arena::Bump ? BMQ_FLAG_BUMP_ARENA : 0u);

@@ -49,7 +49,7 @@ class bmq_config(C.Structure):
                 ("memory_budget", C.c_uint64), ("workers", C.c_uint32), ("compress", C.c_uint32),
                 ("verify_cap_qubits", C.c_uint32), ("device", C.c_int32), ("device_pool_bytes", C.c_uint64),
                 ("work_bytes", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32),
-                ("host_pool_bytes", C.c_uint64)]
+                ("host_pool_bytes", C.c_uint64), ("disk_pool_bytes", C.c_uint64), ("disk_dir", C.c_char_p)]
 
 
 class bmq_plan_model(C.Structure):
@@ -84,7 +84,9 @@ class bmq_report(C.Structure):
                 ("model_bytes", C.c_uint64), ("model_groups", C.c_uint64), ("link_h2d_bytes", C.c_uint64),
                 ("link_d2h_bytes", C.c_uint64), ("link_ms", C.c_double),
                 ("compact_bytes", C.c_uint64), ("host_peak_bytes", C.c_uint64), ("arena_bytes", C.c_uint64),
-                ("fused_decode_batches", C.c_uint64), ("stream_passes", C.c_uint64)]
+                ("fused_decode_batches", C.c_uint64), ("stream_passes", C.c_uint64),
+                ("disk_spill_bytes", C.c_uint64), ("disk_read_bytes", C.c_uint64), ("disk_peak_bytes", C.c_uint64),
+                ("disk_gds", C.c_uint64)]
 
 
 _P = C.c_void_p

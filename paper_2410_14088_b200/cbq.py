@@ -612,6 +612,8 @@ class Config:
     arena: str = "auto"  # device arena placement: "auto", "heap" (extent per payload) or "bump" (cursor + compaction)
     host_pool_bytes: int = 0
     device_plan: bool = False  # plan with plan_device_aware (inner_size = cap) instead of partition_circuit
+    disk_pool_bytes: int = 0   # third level: spill file beneath the host level (needs host_pool_bytes)
+    disk_dir: str = ""         # directory of the spill file ("" = /tmp)
 
     def to_c(self) -> bmq_config:
         c = bmq_config()
@@ -621,6 +623,9 @@ class Config:
         c.verify_cap_qubits, c.device = self.verify_cap_qubits, self.device
         c.device_pool_bytes, c.work_bytes = self.device_pool_bytes, self.work_bytes
         c.host_pool_bytes = self.host_pool_bytes
+        c.disk_pool_bytes = self.disk_pool_bytes
+        self._disk_dir_c = self.disk_dir.encode() if self.disk_dir else None  # kept alive with the config
+        c.disk_dir = self._disk_dir_c
         c.flags = (_lib.BMQ_FLAG_ZERO_GROUP_SKIP if self.zero_group_skip else 0) | \
                   (_lib.BMQ_FLAG_IDENTITY_SKIP if self.identity_skip else 0) | \
                   (_lib.BMQ_FLAG_CODE_DOMAIN if self.code_domain else 0) | \
@@ -694,7 +699,8 @@ DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks
                       "host_spill_bytes", "host_spill_batches", "code_domain_batches", "pool_growths",
                       "lazy_cx", "perm_materialisations",
                       "model_bytes", "model_groups", "link_h2d_bytes", "link_d2h_bytes", "link_ms",
-                      "compact_bytes", "host_peak_bytes", "arena_bytes", "fused_decode_batches", "stream_passes")
+                      "compact_bytes", "host_peak_bytes", "arena_bytes", "fused_decode_batches", "stream_passes",
+                      "disk_spill_bytes", "disk_read_bytes", "disk_peak_bytes", "disk_gds")
 
 
 def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:

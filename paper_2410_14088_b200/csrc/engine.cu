@@ -116,6 +116,8 @@ namespace {
 
 constexpr uint32_t kArenaAlign = 16;
 constexpr uint64_t kHostTag = 1ull << 62;  // payload offset refers to the pinned host arena
+constexpr uint64_t kDiskTag = 1ull << 61;  // payload offset refers to the disk level (store_disk.cpp)
+constexpr uint64_t kLevelTags = kHostTag | kDiskTag;
 
 __global__ void k_fill_meta(uint64_t* off, uint64_t* size, uint64_t n, uint64_t zero_size) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -217,6 +219,7 @@ __global__ void k_pack_payloads(const Xfer* __restrict__ xs, uint64_t n, const u
         const Xfer x = xs[i];
         if (!x.size) continue;
         const uint64_t o = off[x.id];
+        if (o & kDiskTag) continue;  // read from the disk level by the host
         const uint4* s = reinterpret_cast<const uint4*>((o & kHostTag) ? host_pool + (o & ~kHostTag) : pool + o);
         uint4* d = reinterpret_cast<uint4*>(out + x.xoff);
         const uint64_t words = (x.size + 15) / 16;
@@ -232,6 +235,7 @@ __global__ void k_gather_payloads(const Xfer* __restrict__ xs, uint64_t n, const
     for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
         const Xfer x = xs[i];
         const uint64_t o = off[x.id];
+        if (o != ~0ull && (o & kDiskTag)) continue;  // read from the disk level by the host
         const uint8_t* s = o == ~0ull ? zero_hdr : ((o & kHostTag) ? host_pool + (o & ~kHostTag) : pool + o);
         uint8_t* d = out + x.xoff;
         const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;  // bytes until d is 16-aligned
@@ -401,6 +405,10 @@ std::vector<uint8_t> touched_table(const GateProgram& prog, uint32_t b, uint32_t
 
 Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_config& cfg) : cfg_(cfg) {
     check_circuit(n, gates, ngates);
+    if (cfg.disk_dir) disk_dir_ = cfg.disk_dir;  // (the caller's string need not outlive the call)
+    cfg_.disk_dir = nullptr;
+    if (cfg.disk_pool_bytes && !cfg.host_pool_bytes)
+        raise(BMQ_ERR_INVALID_ARGUMENT, "the disk level needs a host level (host_pool_bytes > 0)");
     gates_.assign(gates, gates + ngates);
     L_ = make_layout(n, cfg.block_bits);
     if (cfg.flags & BMQ_FLAG_DEVICE_PLAN) {
@@ -630,7 +638,7 @@ void Engine::compact(const uint64_t* excl, uint64_t nexcl) {
     for (uint64_t i = 0; i < nexcl; ++i) dead[excl[i]] = 1;
     std::vector<uint64_t> live;
     for (uint64_t id = 0; id < nid; ++id) {
-        const bool dev = h_off_[id] != ~0ull && !(h_off_[id] & kHostTag);
+        const bool dev = h_off_[id] != ~0ull && !(h_off_[id] & kLevelTags);
         if (dev && dead[id]) h_off_[id] = ~0ull;  // the batch in flight decoded it: gone (its emit rewrites it)
         if (dev && !dead[id]) live.push_back(id);
     }
@@ -727,7 +735,7 @@ bool Engine::make_room(uint64_t need, const uint64_t* excl, uint64_t nexcl) {
     for (uint64_t i = 0; i < nexcl; ++i) dead[excl[i]] = 1;
     uint64_t live = 0;
     for (uint64_t id = 0; id < L_.num_blocks(); ++id)
-        if (!dead[id] && h_off_[id] != ~0ull && !(h_off_[id] & kHostTag))
+        if (!dead[id] && h_off_[id] != ~0ull && !(h_off_[id] & kLevelTags))
             live += (h_size_[id] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
     const uint64_t garbage = used > live ? used - live : 0;
     if (garbage >= live && live + need <= arena_limit_) {
@@ -756,6 +764,7 @@ void Engine::init_state() {
         sync_copies();
         host_heap_.reset(host_cap_, kArenaAlign);
     }
+    if (disk_.is_open()) disk_.heap().reset(cfg_.disk_pool_bytes, kArenaAlign);
     BMQ_CUDA(cudaMemsetAsync(sums_.p, 0, sums_.bytes(), st_));
     if (!cfg_.compress) {
         const uint64_t raw = 16ull << L_.b;
@@ -913,12 +922,18 @@ void Engine::emit_to_host(uint64_t nblk, const uint64_t* h_ids) {
         if (!(bp[i].flags & 1)) {
             size = bp[i].size;
             const uint64_t ext = host_heap_.alloc(size);
-            if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
-            off = ext | kHostTag;
-            dst.push_back(host_pool_ + ext);
-            src.push_back(staging + bp[i].out_off);
-            len.push_back(size);
-            total += size;
+            if (ext == ExtentHeap::kNone) {  // host level full: the disk level
+                const uint64_t d = disk_alloc(size);
+                disk_.write_from_device(staging + bp[i].out_off, size, d);
+                off = d | kDiskTag;
+                counters_.disk_spill_bytes += size;
+            } else {
+                off = ext | kHostTag;
+                dst.push_back(host_pool_ + ext);
+                src.push_back(staging + bp[i].out_off);
+                len.push_back(size);
+                total += size;
+            }
         }
         h_meta_[3 * i] = id;
         h_meta_[3 * i + 1] = off;
@@ -941,12 +956,21 @@ void Engine::emit_to_host(uint64_t nblk, const uint64_t* h_ids) {
     ++counters_.host_spill_batches;
 }
 
+uint64_t Engine::disk_alloc(uint64_t size) {
+    if (!disk_.is_open()) raise(BMQ_ERR_STORE, "host payload pool exhausted");
+    const uint64_t d = disk_.heap().alloc(size);
+    if (d == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "disk payload level exhausted");
+    return d;
+}
+
 void Engine::free_extents(const uint64_t* ids, uint64_t n) {
     if (!host_pool_ && !heap_mode_) return;
     for (uint64_t i = 0; i < n; ++i) {
         const uint64_t o = h_off_[ids[i]];
         if (o == ~0ull) continue;
-        if (o & kHostTag)
+        if (o & kDiskTag)
+            disk_.heap().free(o & ~kDiskTag, h_size_[ids[i]]);
+        else if (o & kHostTag)
             host_heap_.free(o & ~kHostTag, h_size_[ids[i]]);
         else if (heap_mode_)
             dev_heap_.free(o, h_size_[ids[i]]);
@@ -1002,6 +1026,11 @@ void Engine::emit_placed(uint64_t nblk, const uint64_t* h_ids) {
     }
     uint64_t pos = 0;
     size_t th = 0;
+    struct DiskWrite {
+        const uint8_t* src;
+        uint64_t size, off;
+    };
+    std::vector<DiskWrite> disk_w;
     for (uint64_t i = 0; i < nblk; ++i) {
         const uint64_t id = h_ids[i];
         uint64_t addr = 0, meta = ~0ull;
@@ -1013,15 +1042,20 @@ void Engine::emit_placed(uint64_t nblk, const uint64_t* h_ids) {
             h_size_[id] = sz[i];
         } else {
             const uint64_t ext = host_heap_.alloc(sz[i]);
-            if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
             addr = reinterpret_cast<uint64_t>(staging) + pos;
-            meta = ext | kHostTag;
-            dst.push_back(host_pool_ + ext);
-            src.push_back(staging + pos);
-            len.push_back(sz[i]);
-            total += sz[i];
+            if (ext == ExtentHeap::kNone) {  // host level full: the disk level, written after the emit
+                const uint64_t d = disk_alloc(sz[i]);
+                meta = d | kDiskTag;
+                disk_w.push_back({staging + pos, sz[i], d});
+            } else {
+                meta = ext | kHostTag;
+                dst.push_back(host_pool_ + ext);
+                src.push_back(staging + pos);
+                len.push_back(sz[i]);
+                total += sz[i];
+                ++th;
+            }
             pos += (sz[i] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
-            ++th;
         }
         h_place_[2 * i] = addr;
         h_place_[2 * i + 1] = meta;
@@ -1032,6 +1066,13 @@ void Engine::emit_placed(uint64_t nblk, const uint64_t* h_ids) {
     launch_compress_emit_placed(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, err_.p,
                                 &counters_.kernel_launches);
     ++counters_.kernel_launches;
+    if (!disk_w.empty()) {  // the staged payloads are final once the emit has run
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        for (const DiskWrite& w : disk_w) {
+            disk_.write_from_device(w.src, w.size, w.off);
+            counters_.disk_spill_bytes += w.size;
+        }
+    }
     if (th) {
         BMQ_CUDA(cudaEventRecord(ev_emit_, st_));
         BMQ_CUDA(cudaStreamWaitEvent(cp_out_, ev_emit_, 0));
@@ -1066,6 +1107,8 @@ void Engine::ensure_host_pool() {
     }
     d_meta_.alloc(3 * max_blocks_);
     device_peak_ += wb_.bytes() + 2 * slot + 2 * 8 * max_blocks_ + 24 * max_blocks_;
+    if (cfg_.disk_pool_bytes && !disk_.is_open())
+        disk_.open(disk_dir_, cfg_.disk_pool_bytes, kArenaAlign);
 }
 
 void Engine::copy_batch(void** dst, void** src, size_t* sizes, size_t n, cudaStream_t s) {
@@ -1115,17 +1158,28 @@ void Engine::sync_copies() {
 }
 
 bool Engine::prefetch(const uint64_t* h_ids, uint64_t nblk, int slot) {
-    if (!host_pool_ || !host_heap_.used()) return false;
+    if (!host_pool_ || (!host_heap_.used() && !(disk_.is_open() && disk_.heap().used()))) return false;
     BMQ_CUDA(cudaStreamWaitEvent(cp_in_, ev_dec_[slot], 0));  // batch k-2 has decoded out of this slot
     uint64_t* tab = h_pf_off_[slot].data();
     std::vector<void*> dst, src;
     std::vector<size_t> len;
     uint64_t pos = 0;
+    bool waited = false;
     for (uint64_t i = 0; i < nblk; ++i) {
         const uint64_t o = h_off_[h_ids[i]];
         tab[i] = ~0ull;
-        if (o == ~0ull || !(o & kHostTag)) continue;
+        if (o == ~0ull || !(o & kLevelTags)) continue;
         const uint64_t size = h_size_[h_ids[i]];
+        if (o & kDiskTag) {  // no mapped address: always through the slot (batches are cut to fit)
+            if (pos + size > pf_[slot].bytes()) raise(BMQ_ERR_LOGIC, "disk-level payloads exceed the staging slot");
+            if (!waited) BMQ_CUDA(cudaEventSynchronize(ev_dec_[slot]));  // (host-side writes into the slot)
+            waited = true;
+            disk_.read_to_device(pf_[slot].p + pos, size, o & ~kDiskTag);
+            counters_.disk_read_bytes += size;
+            tab[i] = pos;
+            pos += (size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+            continue;
+        }
         if (pos + size > pf_[slot].bytes()) continue;  // read in place through the mapped address
         tab[i] = pos;
         dst.push_back(pf_[slot].p + pos);
@@ -1133,7 +1187,7 @@ bool Engine::prefetch(const uint64_t* h_ids, uint64_t nblk, int slot) {
         len.push_back(size);
         pos += (size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
     }
-    if (dst.empty()) return false;
+    if (dst.empty() && !waited) return false;
     BMQ_CUDA(cudaMemcpyAsync(pf_off_[slot].p, tab, nblk * 8, cudaMemcpyHostToDevice, cp_in_));
     link_event_pair(cp_in_, true);
     copy_batch(dst.data(), src.data(), len.data(), dst.size(), cp_in_);
@@ -1290,7 +1344,8 @@ void Engine::run_stage(uint64_t s) {
         // one prefetch slot
         const uint64_t unit = blockwise ? 1 : per;
         const uint64_t batch_blocks = blockwise ? max_blocks_ : std::max<uint64_t>(1, max_blocks_ / per) * per;
-        const uint64_t pf_cap = host_pool_ && host_heap_.used() ? pf_[0].bytes() : ~0ull;
+        const uint64_t pf_cap =
+            host_pool_ && (host_heap_.used() || (disk_.is_open() && disk_.heap().used())) ? pf_[0].bytes() : ~0ull;
         std::vector<std::pair<uint64_t, uint64_t>> batches;
         uint64_t first = 0, hb = 0;
         for (uint64_t u = 0; u < nwork; u += unit) {
@@ -1298,7 +1353,7 @@ void Engine::run_stage(uint64_t s) {
             if (pf_cap != ~0ull)
                 for (uint64_t v = u; v < u + unit; ++v) {
                     const uint64_t o = h_off_[work_ids[v]];
-                    if (o != ~0ull && (o & kHostTag)) ub += (h_size_[work_ids[v]] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+                    if (o != ~0ull && (o & kLevelTags)) ub += (h_size_[work_ids[v]] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
                 }
             if (u > first && (u - first + unit > batch_blocks || hb + ub > pf_cap)) {
                 batches.emplace_back(first, u - first);
@@ -1433,6 +1488,10 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.arena_bytes = arena_limit_;
     r.fused_decode_batches = counters_.fused_decode_batches;
     r.stream_passes = counters_.stream_passes;
+    r.disk_spill_bytes = counters_.disk_spill_bytes;
+    r.disk_read_bytes = counters_.disk_read_bytes;
+    r.disk_peak_bytes = disk_.is_open() ? disk_.heap().high_water() : 0;
+    r.disk_gds = disk_.gds() ? 1 : 0;
     *rep = r;
 }
 
@@ -1457,11 +1516,66 @@ void Engine::host_ids_to_device(const std::vector<uint64_t>& ids) {
     BMQ_CUDA(cudaMemcpyAsync(ids_.p, ids.data(), ids.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
 }
 
-void Engine::decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums) {
-    k_build_desc<<<grid_for(nids), 256, 0, st_>>>(d_ids, nids, off_.p, size_.p, arena_.base(), host_pool_,
-                                                  zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0);
-    launch_decompress(st_, dec_.p, nids, nch_, *tabs_, dinfo_.p, dchunk_.p, true, want_sums, err_.p,
-                      &counters_.kernel_launches);
+// Disk-level payloads of ids[0..n) (host ids) read into prefetch slot 0 for
+// a decode outside the stage loop; the slot table for k_build_desc, or null
+// when none of the ids is on disk. n must satisfy disk_fit.
+const uint64_t* Engine::stage_disk_reads(const uint64_t* h_ids, uint64_t n) {
+    if (!disk_.is_open() || !disk_.heap().used()) return nullptr;
+    bool any = false;
+    for (uint64_t i = 0; i < n && !any; ++i) any = h_off_[h_ids[i]] != ~0ull && (h_off_[h_ids[i]] & kDiskTag);
+    if (!any) return nullptr;
+    sync_copies();
+    BMQ_CUDA(cudaStreamSynchronize(st_));  // earlier decodes have left the slot
+    uint64_t* tab = h_pf_off_[0].data();
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t o = h_off_[h_ids[i]];
+        tab[i] = ~0ull;
+        if (o == ~0ull || !(o & kDiskTag)) continue;
+        const uint64_t size = h_size_[h_ids[i]];
+        if (pos + size > pf_[0].bytes()) raise(BMQ_ERR_LOGIC, "disk-level payloads exceed the staging slot");
+        disk_.read_to_device(pf_[0].p + pos, size, o & ~kDiskTag);
+        counters_.disk_read_bytes += size;
+        tab[i] = pos;
+        pos += (size + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+    }
+    BMQ_CUDA(cudaMemcpyAsync(pf_off_[0].p, tab, n * 8, cudaMemcpyHostToDevice, st_));
+    return pf_off_[0].p;
+}
+
+// Largest prefix of ids whose disk-level payloads fit one staging slot.
+uint64_t Engine::disk_fit(const uint64_t* h_ids, uint64_t n) {
+    if (!disk_.is_open() || !disk_.heap().used()) return n;
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t o = h_off_[h_ids[i]];
+        if (o == ~0ull || !(o & kDiskTag)) continue;
+        pos += (h_size_[h_ids[i]] + kArenaAlign - 1) / kArenaAlign * kArenaAlign;
+        if (pos > pf_[0].bytes()) return std::max<uint64_t>(i, 1);
+    }
+    return n;
+}
+
+void Engine::decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums, const uint64_t* h_ids) {
+    std::vector<uint64_t> hv;
+    if (disk_.is_open() && disk_.heap().used() && !h_ids) {
+        hv.resize(nids);
+        BMQ_CUDA(cudaMemcpyAsync(hv.data(), d_ids, nids * 8, cudaMemcpyDeviceToHost, st_));
+        BMQ_CUDA(cudaStreamSynchronize(st_));
+        h_ids = hv.data();
+    }
+    const uint64_t count = 2ull << L_.b;
+    for (uint64_t k = 0; k < nids;) {
+        const uint64_t m = h_ids ? disk_fit(h_ids + k, nids - k) : nids - k;
+        const uint64_t* tab = h_ids ? stage_disk_reads(h_ids + k, m) : nullptr;
+        k_build_desc<<<grid_for(m), 256, 0, st_>>>(d_ids + k, m, off_.p, size_.p, arena_.base(), host_pool_,
+                                                   zero_hdr_.p, work_.p + k * count, pk_.p + k * count, L_.b,
+                                                   dec_.p + k, cmp_.p + k, 0, tab, pf_[0].p);
+        launch_decompress(st_, dec_.p + k, m, nch_, *tabs_, dinfo_.p + k, dchunk_.p + k * nch_, true, want_sums,
+                          err_.p, &counters_.kernel_launches);
+        k += m;
+        if (k < nids && tab) BMQ_CUDA(cudaStreamSynchronize(st_));  // the slot is reused
+    }
 }
 
 void Engine::ensure_sums(const uint64_t* ids, uint64_t n) {
@@ -1478,16 +1592,20 @@ void Engine::ensure_sums(const uint64_t* ids, uint64_t n) {
         for (uint64_t id = 0; id < sums_ok_.size(); ++id) visit(id);
     }
     for (uint64_t id : zero) BMQ_CUDA(cudaMemsetAsync(sums_.p + 3 * id, 0, 3 * sizeof(double), st_));
-    for (uint64_t first = 0; first < stale.size(); first += max_blocks_) {
-        const uint64_t nb = std::min<uint64_t>(max_blocks_, stale.size() - first);
+    for (uint64_t first = 0; first < stale.size();) {
+        uint64_t nb = std::min<uint64_t>(max_blocks_, stale.size() - first);
+        nb = disk_fit(stale.data() + first, nb);
         BMQ_CUDA(cudaMemcpyAsync(ids_.p, stale.data() + first, nb * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
+        const uint64_t* tab = stage_disk_reads(stale.data() + first, nb);
         k_build_desc<<<grid_for(nb), 256, 0, st_>>>(ids_.p, nb, off_.p, size_.p, arena_.base(), host_pool_,
-                                                    zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0);
+                                                    zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0, tab,
+                                                    pf_[0].p);
         launch_decompress(st_, dec_.p, nb, nch_, *tabs_, dinfo_.p, dchunk_.p, true, true, err_.p,
                           &counters_.kernel_launches, 2);
         k_store_dec_sums<<<grid_for(nb), 256, 0, st_>>>(dinfo_.p, ids_.p, nb, sums_.p);
         counters_.kernel_launches += 2;
         BMQ_CUDA(cudaStreamSynchronize(st_));  // ids_ is reused by the next batch
+        first += nb;
     }
     if (!stale.empty()) check_device_error("sums: ");
 }
@@ -1574,7 +1692,9 @@ uint64_t Engine::get_payload(uint64_t id, uint8_t* out, uint64_t cap) {
     if (h_off_[id] == ~0ull) return zero_payload(out, cap);
     const uint64_t size = h_size_[id];
     if (out && cap >= size) {
-        if (h_off_[id] & kHostTag) {
+        if (h_off_[id] & kDiskTag) {
+            disk_.read_to_host(out, size, h_off_[id] & ~kDiskTag);
+        } else if (h_off_[id] & kHostTag) {
             BMQ_CUDA(cudaStreamSynchronize(st_));
             std::memcpy(out, host_pool_ + (h_off_[id] & ~kHostTag), size);
         } else {
@@ -1622,6 +1742,9 @@ void Engine::get_payloads(uint8_t* out, uint64_t cap, uint64_t* sizes, uint64_t*
         BMQ_CUDA(cudaGetLastError());
         BMQ_CUDA(cudaMemcpyAsync(out + base, staging, len, cudaMemcpyDeviceToHost, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
+        for (const Xfer& x : xs)  // disk-level payloads (skipped by the gather)
+            if (h_off_[x.id] != ~0ull && (h_off_[x.id] & kDiskTag))
+                disk_.read_to_host(out + base + x.xoff, x.size, h_off_[x.id] & ~kDiskTag);
         xs.clear();
     };
     for (uint64_t id = 0; id < nid; ++id) {
@@ -1846,6 +1969,18 @@ void Engine::export_payloads(const uint64_t* ids, uint64_t n, uint64_t* meta, vo
     ++counters_.kernel_launches;
     BMQ_CUDA(cudaGetLastError());
     BMQ_CUDA(cudaStreamSynchronize(st_));
+    cudaPointerAttributes pa{};
+    const bool dst_dev = cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    for (uint64_t i = 0; i < n; ++i) {  // disk-level payloads (skipped by the pack)
+        const uint64_t o = h_off_[ids[i]];
+        if (o == ~0ull || !(o & kDiskTag)) continue;
+        uint8_t* d = static_cast<uint8_t*>(dst) + xs[i].xoff;
+        if (dst_dev)
+            disk_.read_to_device(d, xs[i].size, o & ~kDiskTag);
+        else
+            disk_.read_to_host(d, xs[i].size, o & ~kDiskTag);
+    }
 }
 
 void Engine::import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* meta, const void* src) {

@@ -7,6 +7,7 @@
 #include "codec.cuh"
 #include "gates.cuh"
 #include "store.hpp"
+#include "store_disk.hpp"
 
 namespace bmq {
 
@@ -208,7 +209,12 @@ private:
     PinnedVec<uint64_t> h_place_;
     DevArray<uint64_t> d_place_;
     void sync_meta_to_host();
-    void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums);
+    void decompress_ids(const uint64_t* d_ids, uint64_t nids, bool want_sums, const uint64_t* h_ids = nullptr);
+    const uint64_t* stage_disk_reads(const uint64_t* h_ids, uint64_t n);
+    uint64_t disk_fit(const uint64_t* h_ids, uint64_t n);
+    uint64_t disk_alloc(uint64_t size);
+    DiskLevel disk_;
+    std::string disk_dir_;
     const double* decoded_batch(const uint64_t* h_ids, uint64_t n);
     void host_ids_to_device(const std::vector<uint64_t>& ids);
     // Per-id dequantised sums are computed lazily (the emit kernel does not

@@ -541,3 +541,59 @@ def test_device_plan_matches_reference_at_chosen_inner(gpu, port, name, n, layer
         assert rep.stage_count == len(plan.stages) == want.report["stage_count"]
         assert sim.payloads() == want.payloads
         assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+
+
+@pytest.mark.parametrize("arena", ["heap", "bump"])
+def test_disk_level_is_exact(gpu, port, arena):
+    """Third level (the reference's spill file, store.hpp:234-283):
+    device arena and host level both far smaller than the live state, so most
+    payloads go to the spill file (pread / pwrite through a pinned bounce;
+    cuFile with BMQ_GDS=1) and every stage reads them back; payloads,
+    peak footprint, norm and the per-payload reads are unchanged."""
+    c = gpu.generate_benchmark("qaoa", 16, gpu.BenchmarkParams(layers=2))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    biggest = max(len(p) for p in want.payloads)
+    pool = 6 * (biggest + 16)
+    cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, work_bytes=4 * (16 << 12),
+                     host_pool_bytes=3 * (biggest + 16), disk_pool_bytes=64 << 20, arena=arena)
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run()
+        d = rep.device
+        assert d["disk_spill_bytes"] > 0 and d["disk_read_bytes"] > 0
+        assert d["disk_peak_bytes"] <= 64 << 20
+        assert sim.payloads() == want.payloads
+        for i in (0, 3, 15):
+            assert sim.get_payload(i) == want.payloads[i]
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert abs(sim.state_norm() - want.report["final_norm"]) <= NORM_RTOL * want.report["final_norm"]
+        psi = sim.extract_state()  # decode path outside the stage loop
+        assert abs(np.linalg.norm(psi) - want.report["final_norm"]) <= 1e-9
+    with pytest.raises(gpu.InvalidArgument, match="host level"):
+        gpu.Simulator(c, gpu.Config(block_bits=12, disk_pool_bytes=1 << 20))
+
+
+def test_disk_level_posix_path(gpu, port, tmp_path):
+    """Same run with GPUDirect Storage explicitly off (BMQ_NO_GDS): pread /
+    pwrite through the pinned bounce buffer, spill file in a given directory."""
+    import subprocess
+    import sys
+    code = f"""
+import sys; sys.path.insert(0, {repr(os.path.dirname(GOLDEN) + '/../..')})
+sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(GOLDEN)))})
+from paper_2410_14088_b200 import cbq
+from oracle import oracle
+port = oracle.port()
+c = cbq.generate_benchmark("qaoa", 16, cbq.BenchmarkParams(layers=2))
+want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+big = max(len(p) for p in want.payloads)
+cfg = cbq.Config(block_bits=12, inner_size=2, device_pool_bytes=6 * (big + 16), work_bytes=4 * (16 << 12),
+                 host_pool_bytes=3 * (big + 16), disk_pool_bytes=64 << 20, disk_dir={repr(str(tmp_path))})
+with cbq.Simulator(c, cfg) as sim:
+    rep = sim.run()
+    assert rep.device["disk_gds"] == 0 and rep.device["disk_spill_bytes"] > 0
+    assert sim.payloads() == want.payloads
+print("ok")
+"""
+    env = dict(os.environ, BMQ_NO_GDS="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
