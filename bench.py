@@ -397,6 +397,89 @@ def roofline(d, t_dev, link):
             "dominant_phase": dom}
 
 
+def main_sharded_capi(args, world, rank, local, dist, circ, cfg):
+    """N GPUs, one simulation through the C ABI's sharded stage loop
+    (bmq_simulator_run_sharded: host C++ driver over an NCCL communicator that
+    libbmq creates from a unique id broadcast by rank 0)."""
+    import torch
+    from paper_2410_14088_b200 import cbq
+    w = WORKLOAD
+    uid = [cbq.Collective.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    col = cbq.Collective.nccl(uid[0], rank, world, local)
+    sim = cbq.Simulator(circ, cfg)
+    stages = len(sim.plan().stages)
+    amp_stages = (1 << w["n"]) * stages
+    for _ in range(args.warmup):
+        sim.run_sharded(col)
+    reps, dev_ms = [], []
+    barrier_sync(dist)
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            barrier_sync(dist)
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            reps.append(sim.run_sharded(col))
+            torch.cuda.synchronize()
+            ev1.record()
+            ev1.synchronize()
+            dev_ms.append(ev0.elapsed_time(ev1))
+        barrier_sync(dist)
+    t_dev = max_over_ranks(dist, statistics.median(dev_ms))
+    rep = reps[-1]
+    fidelity = None
+    if w["name"] == "qft":  # |<u|psi>| from the all-reduced block sums of every rank's share
+        import ctypes
+        import numpy as np
+        s3 = (ctypes.c_double * 3)()
+        cbq._check(cbq.lib.bmq_simulator_partial_sums(sim._h, s3))
+        sums = torch.tensor(list(s3), dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(sums)
+        fidelity = float(np.hypot(float(sums[1]), float(sums[2])) * 2.0 ** (-0.5 * w["n"]))
+    value = amp_stages / (t_dev / 1e3)
+    e2e = None
+    if not args.no_e2e:
+        times, h2d, d2h = [], 0, 0
+        gates_arr = circ.c_array()
+        for step in range(max(1, min(args.steps, 3)) + 1):
+            barrier_sync(dist)
+            t0 = time.perf_counter()
+            with cbq.Simulator(circ, cfg) as s2:
+                s2.run_sharded(col)
+                pays = s2.payloads()  # this rank's blocks (the others read as ALL_ZERO headers)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if step > 0:
+                times.append(dt)
+            h2d = len(bytes(gates_arr)) + 8
+            d2h = sum(len(p) for p in pays)
+        t_e2e = max_over_ranks(dist, statistics.median(times))
+        e2e = {"value": amp_stages / t_e2e, "unit": "amp-stages/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "seconds": t_e2e}
+    sim.close()
+    col.close()
+    line = {
+        "metric": metric_name(w), "value": value, "unit": "amp-stages/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": data_desc(w),
+        "config": {"workload": workload_tag(w), "stages": stages,
+                   "parallelism": f"shard{world} (device qubits; C ABI driver, NCCL payload remaps)",
+                   "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
+                   "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},
+        "sim_time_s": t_dev / 1e3, "compression_ratio": rep.compression_ratio,
+        "max_footprint_bytes": rep.max_footprint_bytes, "fidelity": fidelity, "final_norm": rep.final_norm,
+        "gpu_launches": int(rep.device["kernel_launches"]),
+        "clocks": clocks.summary(), "e2e": e2e,
+    }
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
 def main_sharded(args, world, rank, local, dist):
     """N GPUs, one simulation: the stage loop sharded over device qubits with
     payload remaps over NCCL (paper_2410_14088_b200/shard.py). Total work is
@@ -414,6 +497,8 @@ def main_sharded(args, world, rank, local, dist):
     circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
     cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
                      identity_skip=not args.no_identity_skip)
+    if not args.py_shard:
+        return main_sharded_capi(args, world, rank, local, dist, circ, cfg)
     col = TorchCollective(torch.device("cuda", local))
     be = EngineShard(circ, cfg, rank, world)
     ssim = ShardedSimulator(be, col)
@@ -564,6 +649,12 @@ def main():
                     help="device arena placement policy (payload bytes are identical)")
     ap.add_argument("--host-pool-gib", type=float, default=0.0,
                     help="pinned host level of the store (GiB); 0 = none")
+    ap.add_argument("--disk-pool-gib", type=float, default=0.0,
+                    help="disk level beneath the host level (spill file, GiB); 0 = none")
+    ap.add_argument("--device-plan", action="store_true",
+                    help="plan with bmq_plan_device_aware (inner size chosen for the device, --inner-size caps it)")
+    ap.add_argument("--py-shard", action="store_true",
+                    help="N>1: the Python sharded driver (shard.py over torch.distributed) instead of the C ABI one")
     ap.add_argument("--e2e-once", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     env_world = os.environ.get("WORLD_SIZE")
@@ -597,9 +688,11 @@ def main():
     circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
     cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
                      identity_skip=not args.no_identity_skip, device_pool_bytes=int(args.device_pool_gib * 2**30),
-                     host_pool_bytes=int(args.host_pool_gib * 2**30), arena=args.arena)
+                     host_pool_bytes=int(args.host_pool_gib * 2**30), arena=args.arena,
+                     disk_pool_bytes=int(args.disk_pool_gib * 2**30), device_plan=args.device_plan)
     sim = cbq.Simulator(circ, cfg)
-    stages = len(sim.plan().stages)
+    plan = sim.plan().stages
+    stages = len(plan)
     amp_stages = (1 << w["n"]) * stages
     reps = []
     for _ in range(args.warmup):
@@ -633,9 +726,12 @@ def main():
     line = {
         "metric": metric_name(w), "value": value, "unit": "amp-stages/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": data_desc(w),
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": data_desc(w),
         "config": {"workload": workload_tag(w), "stages": stages,
+                   "plan": ("device-aware (bmq_plan_device_aware): inner "
+                            f"{max((len(s.inner) for s in plan), default=0)}" if args.device_plan
+                            else f"partition_circuit inner_size={w['inner']}"),
                    "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
                    "device_pool": f"{args.device_pool_gib:g} GiB fixed" if args.device_pool_gib else "automatic",
@@ -649,7 +745,9 @@ def main():
         "device_peak_bytes": int(rep.device["device_peak_bytes"]),
         "store": {k: rep.device[k] for k in ("arena_bytes", "compactions", "compact_bytes", "pool_growths",
                                              "host_spill_bytes", "host_peak_bytes", "link_h2d_bytes",
-                                             "link_d2h_bytes", "link_ms")},
+                                             "link_d2h_bytes", "link_ms", "disk_spill_bytes", "disk_read_bytes",
+                                             "disk_peak_bytes", "disk_gds")},
+        "gate_passes": {"total": int(rep.device["gate_passes"]), "streaming": int(rep.device["stream_passes"])},
         "roofline": roof, "clocks": clocks.summary(), "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
