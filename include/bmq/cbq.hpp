@@ -468,10 +468,20 @@ public:
 
     void init_state() { detail::check(bmq_simulator_init_state(sim_)); }
 
-    SimulationReport run() {
+    SimulationReport run() { return run_on(nullptr); }
+
+    // One rank of a sharded run (bmq_simulator_run_sharded): every rank
+    // calls it with its own simulator; norm, counters and peak are global.
+    SimulationReport run_sharded(bmq_collective* col) { return run_on(col); }
+
+private:
+    SimulationReport run_on(bmq_collective* col) {
         bmq_report r{};
         std::vector<double> stage_ms(std::max<std::size_t>(1, circuit_.gates.size()));
-        detail::check(bmq_simulator_run(sim_, &r, stage_ms.data(), stage_ms.size()));
+        if (col)
+            detail::check(bmq_simulator_run_sharded(sim_, col, &r, stage_ms.data(), stage_ms.size()));
+        else
+            detail::check(bmq_simulator_run(sim_, &r, stage_ms.data(), stage_ms.size()));
         SimulationReport out;
         out.qubits = r.qubits;
         out.gate_count = r.gate_count;
@@ -489,6 +499,7 @@ public:
         return out;
     }
 
+public:
     std::vector<Complex> extract_state() const {
         std::vector<Complex> st(1ull << circuit_.num_qubits);
         detail::check(bmq_simulator_extract_state(sim_, reinterpret_cast<double*>(st.data()), st.size()));
