@@ -244,7 +244,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": metric_name(w), "value": value,
         "unit": "amp-stages/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.median(walls), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": statistics.median(walls), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (QFT|0> circuit; stratified per-stage sample)",
         "config": {"workload": workload_tag(w), "stages": len(plan), "sample_groups": len(samples)},
         "extrapolated_full_run_s": statistics.median(fulls),
