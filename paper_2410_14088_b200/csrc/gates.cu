@@ -1429,8 +1429,10 @@ __device__ __forceinline__ C2 shfl_c2(C2 a, uint32_t m) {
     return C2{__shfl_xor_sync(0xffffffffu, a.re, m), __shfl_xor_sync(0xffffffffu, a.im, m)};
 }
 
-template <bool kQuant, bool kDecode>
-__global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
+// kSame: every register row of a unit lies in the unit's 4096-scalar chunk
+// (the register bits are below bit 12), so one accumulator pair serves them.
+template <bool kQuant, bool kDecode, bool kSame = false>
+__global__ void __launch_bounds__(kStreamThreads, (kQuant && !kSame) ? 2 : 3) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
                                                                 const __grid_constant__ StreamPass pass,
                                                                 const __grid_constant__ QuantOut q,
                                                                 const uint32_t* __restrict__ vtab,
@@ -1462,20 +1464,21 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
     // Per-chunk counters of the current run, reduced per row with REDUX as it
     // is quantised: warp-uniform values (uniform registers, not 24 per-lane
     // ones), fields as RowAcc's.
-    uint32_t amn[kNV][2], amx[kNV][2], azn[kNV][2];
+    constexpr int kAcc = kSame ? 1 : kNV;
+    uint32_t amn[kAcc][2], amx[kAcc][2], azn[kAcc][2];
 #pragma unroll
-    for (int r = 0; r < kNV; ++r)
+    for (int r = 0; r < kAcc; ++r)
 #pragma unroll
         for (int h = 0; h < 2; ++h) amn[r][h] = ~0u, amx[r][h] = 0u, azn[r][h] = 0u;
     uint64_t run_pb = 0;  // planar base of the current counter run
     uint32_t run_len = 0;
     const auto flush = [&]() {
 #pragma unroll
-        for (int r = 0; r < kNV; ++r) {
+        for (int r = 0; r < kAcc; ++r) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 ChunkPlan* cp = q.cps + (((run_pb | pdep[r]) >> 12) + (h ? (im_off >> 12) : 0));
-                const uint32_t nnz = 32u * run_len - (azn[r][h] & 0xffffu), nneg = azn[r][h] >> 16;
+                const uint32_t nnz = 32u * (kNV / kAcc) * run_len - (azn[r][h] & 0xffffu), nneg = azn[r][h] >> 16;
                 if (lane == 0 && nnz) atomicMax(&cp->qmin_inv, kQOffMax - (amn[r][h] >> 2));
                 if (lane == 1 && nnz) atomicMax(&cp->qmax_off, amx[r][h] >> 2);
                 if (lane == 2 && nnz) atomicAdd(&cp->nnz, nnz);
@@ -1687,9 +1690,10 @@ __global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t w = pk[2 * r + h];
-                    amn[r][h] = min(amn[r][h], __reduce_min_sync(0xffffffffu, (w ^ 1u) - 1u));
-                    amx[r][h] = max(amx[r][h], __reduce_max_sync(0xffffffffu, w));
-                    azn[r][h] += __reduce_add_sync(0xffffffffu, (w & 1u) | ((w & 2u) << 15));
+                    const int ra = kSame ? 0 : r;
+                    amn[ra][h] = min(amn[ra][h], __reduce_min_sync(0xffffffffu, (w ^ 1u) - 1u));
+                    amx[ra][h] = max(amx[ra][h], __reduce_max_sync(0xffffffffu, w));
+                    azn[ra][h] += __reduce_add_sync(0xffffffffu, (w & 1u) | ((w & 2u) << 15));
                 }
             }
             ++run_len;
@@ -2286,6 +2290,8 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
             if (fuse && last) {
                 if (fd.rows)
                     k_stream_pass<true, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
+                else if (p.sp->qbit[kStreamNQ - 1] < 12)
+                    k_stream_pass<true, false, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
                 else
                     k_stream_pass<true, false><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
             } else {
