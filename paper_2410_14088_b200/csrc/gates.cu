@@ -144,6 +144,8 @@ FastOp to_fast(const GateOp& g) {
         bool real = true;
         for (int e = 0; e < 4; ++e) real = real && g.m[2 * e + 1] == 0.0;
         f.pad = real ? 1 : 0;
+        // real diagonal, imaginary off-diagonal (RX): one specialised form too
+        if (!real && g.m[1] == 0.0 && g.m[7] == 0.0 && g.m[2] == 0.0 && g.m[4] == 0.0) f.pad = 2;
     } else if (g.type == OP_DIAG) {
         take(0, 0);
         take(1, 3);
@@ -1345,7 +1347,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                     for (uint32_t m = 0; m < 8; ++m) body(tid + 256u * insert0(m, piv - 8));
                 }
             };
-            if (g.pad) {  // all entries real: u*a = (u*ar, u*ai) exactly
+            if (g.pad == 1) {  // all entries real: u*a = (u*ar, u*ai) exactly
                 const double u00 = g.m[0], u01 = g.m[2], u10 = g.m[4], u11 = g.m[6];
                 sweep([&](uint32_t x0) {
                     const uint32_t x1 = x0 ^ dv;
@@ -1359,6 +1361,19 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_gate_pass_fast(double* __re
                                               __dadd_rn(__dmul_rn(u00, v0.y), __dmul_rn(u01, v1.y)));
                     tile_s[i1] = make_double2(__dadd_rn(__dmul_rn(u10, v0.x), __dmul_rn(u11, v1.x)),
                                               __dadd_rn(__dmul_rn(u10, v0.y), __dmul_rn(u11, v1.y)));
+                });
+            } else if (g.pad == 2) {  // u00, u11 real, u01, u10 imaginary (RX): row2's products, fixed classes
+                const double u00 = g.m[0], u01i = g.m[3], u10i = g.m[5], u11 = g.m[6];
+                sweep([&](uint32_t x0) {
+                    const uint32_t x1 = x0 ^ dv;
+                    const bool sw = (__popc(mrow & x0) ^ ct) & 1u;
+                    const uint32_t i0 = sw ? x1 : x0, i1 = sw ? x0 : x1;
+                    const double2 v0 = tile_s[i0], v1 = tile_s[i1];
+                    if (dense && v0.x == 0.0 && v0.y == 0.0 && v1.x == 0.0 && v1.y == 0.0) return;
+                    tile_s[i0] = make_double2(__dadd_rn(__dmul_rn(u00, v0.x), -__dmul_rn(u01i, v1.y)),
+                                              __dadd_rn(__dmul_rn(u00, v0.y), __dmul_rn(u01i, v1.x)));
+                    tile_s[i1] = make_double2(__dadd_rn(-__dmul_rn(u10i, v0.y), __dmul_rn(u11, v1.x)),
+                                              __dadd_rn(__dmul_rn(u10i, v0.x), __dmul_rn(u11, v1.y)));
                 });
             } else {
                 uint8_t et[4];

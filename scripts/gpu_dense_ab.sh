@@ -8,3 +8,5 @@ print('$2', d['config']['workload'], 'ms %.1f'%d['ms_per_step'], 'frac %.3f'%r['
 for wl in "--workload qaoa3reg --qubits 30 --error-bound 1e-4" "--workload random --qubits 30 --layers 20" "--workload qaoa3reg --qubits 32 --error-bound 1e-3" ""; do
   line "$wl" new
 done
+line "--workload qaoa3reg --qubits 30 --error-bound 1e-4 --device-plan --inner-size 16" devplan
+line "--workload random --qubits 30 --layers 20 --device-plan --inner-size 16" devplan
