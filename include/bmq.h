@@ -228,9 +228,9 @@ int bmq_partition(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, ui
  * buffer 2^(b+k) complex doubles <= work_bytes, k <= c - log2(world),
  * k <= max_inner when nonzero) and keeps the plan whose modelled time is
  * least: per stage, the HBM bytes of this engine's decode -> tile passes ->
- * quantise -> emit trip (passes counted as gates.cu splits them) at hbm_gbs,
- * plus stage_overhead_s, plus (world > 1) the payload remaps of the shard
- * plan at link_gbs. The result is always a partition_circuit plan, so the
+ * quantise -> emit trip (passes counted as gates.cu splits them) at the
+ * fractions codec_eff / pass_eff of hbm_gbs, plus stage_overhead_s, plus
+ * (world > 1) the payload remaps of the shard plan at link_gbs. The result is always a partition_circuit plan, so the
  * reference replays it with inner_size = choice->inner_size. */
 typedef struct bmq_plan_model {
     uint64_t work_bytes;      /* group buffer budget (bytes) */
@@ -240,6 +240,8 @@ typedef struct bmq_plan_model {
     double stage_overhead_s;  /* fixed cost per stage (launches, syncs) */
     uint32_t world;           /* GPUs (power of two) */
     uint32_t max_inner;       /* 0 = no cap */
+    double codec_eff;         /* fraction of hbm_gbs the decode / emit kernels reach (measured ~0.4) */
+    double pass_eff;          /* fraction of hbm_gbs the gate passes reach (measured ~0.5) */
 } bmq_plan_model;
 typedef struct bmq_plan_choice {
     uint32_t inner_size;      /* chosen k */

@@ -55,7 +55,7 @@ class bmq_config(C.Structure):
 class bmq_plan_model(C.Structure):
     _fields_ = [("work_bytes", C.c_uint64), ("hbm_gbs", C.c_double), ("link_gbs", C.c_double),
                 ("ratio", C.c_double), ("stage_overhead_s", C.c_double), ("world", C.c_uint32),
-                ("max_inner", C.c_uint32)]
+                ("max_inner", C.c_uint32), ("codec_eff", C.c_double), ("pass_eff", C.c_double)]
 
 
 class bmq_plan_choice(C.Structure):

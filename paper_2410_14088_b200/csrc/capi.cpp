@@ -122,6 +122,8 @@ void bmq_plan_model_default(bmq_plan_model* model) {
     model->ratio = 4.0;
     model->stage_overhead_s = 100e-6;
     model->world = 1;
+    model->codec_eff = 0.4;  // decode / emit ~2.6 TB/s of 6.5 (profiles/r2b_ncu_qaoa28.txt)
+    model->pass_eff = 0.5;   // streaming 5.4 TB/s, tiled 1.8-2.2 TB/s
 }
 
 int bmq_plan_device_aware(uint32_t num_qubits, const bmq_gate* gates, uint64_t count, uint32_t block_bits,

@@ -352,8 +352,9 @@ std::vector<bmq_stage> plan_device_aware(uint32_t n, const bmq_gate* gates, uint
     const Layout L = make_layout(n, block_bits);
     if (model.world == 0 || (model.world & (model.world - 1)))
         raise(BMQ_ERR_INVALID_ARGUMENT, "shard count must be a power of two");
-    if (!(model.hbm_gbs > 0.0) || (model.world > 1 && !(model.link_gbs > 0.0)) || !(model.ratio > 0.0))
-        raise(BMQ_ERR_INVALID_ARGUMENT, "plan model needs positive bandwidths and compression ratio");
+    if (!(model.hbm_gbs > 0.0) || (model.world > 1 && !(model.link_gbs > 0.0)) || !(model.ratio > 0.0) ||
+        !(model.codec_eff > 0.0) || !(model.pass_eff > 0.0))
+        raise(BMQ_ERR_INVALID_ARGUMENT, "plan model needs positive bandwidths, efficiencies and compression ratio");
     uint32_t m = 0;
     while ((1u << m) < model.world) ++m;
     if (m > L.c) raise(BMQ_ERR_INVALID_ARGUMENT, "more shards than blocks");
@@ -371,14 +372,19 @@ std::vector<bmq_stage> plan_device_aware(uint32_t n, const bmq_gate* gates, uint
         std::vector<bmq_stage> plan = partition_plan(n, gates, count, block_bits, k);
         double bytes = 0.0;
         uint64_t passes = 0;
+        double secs = 0.0;
         for (const bmq_stage& st : plan) {
             const uint32_t p = stage_passes(L, st, gates);
             passes += p;
-            // decode writes 16 B, the first pass reads 16, each further pass
-            // moves 32, the last pass writes 8 B of codes that emit reads back
-            bytes += amps * (2.0 * cbytes + 48.0 + 32.0 * (p - 1));
+            // codec trip: payloads read and written, decode's 16 B write and
+            // emit's 8 B read of codes; gate passes: 16 B in + 8 B of codes out
+            // for the first / last, 32 B for each further pass. Each at the
+            // fraction of HBM its kernels reach
+            const double codec = amps * (2.0 * cbytes + 24.0), gate = amps * (24.0 + 32.0 * (p - 1));
+            bytes += codec + gate;
+            secs += codec / (model.codec_eff * model.hbm_gbs * 1e9) + gate / (model.pass_eff * model.hbm_gbs * 1e9);
         }
-        double secs = bytes / (model.hbm_gbs * 1e9) + plan.size() * model.stage_overhead_s;
+        secs += plan.size() * model.stage_overhead_s;
         uint32_t remaps = 0;
         if (m && !plan.empty()) {
             // a remap moves the payloads whose owner changes: 1 - 2^-s of this
