@@ -278,6 +278,7 @@ void Engine::sample(uint64_t nshots, uint64_t seed, uint64_t* out) {
 uint64_t Engine::top_k(uint64_t k, uint64_t* idx, double* re, double* im) {
     BMQ_CUDA(cudaSetDevice(dev_));
     ensure_init();
+    if (k == 0) return 0;
     const uint64_t nid = L_.num_blocks();
     // blocks that can hold a nonzero amplitude, ascending
     std::vector<uint64_t> ids;

@@ -242,8 +242,8 @@ void run_sharded(Engine& e, Collective& col, bmq_report* rep, double* stage_ms, 
     const uint32_t world = col.world(), rank = col.rank();
     if (world & (world - 1)) raise(BMQ_ERR_INVALID_ARGUMENT, "shard count must be a power of two");
     const auto t_start = std::chrono::steady_clock::now();
+    if (e.initialized()) e.reset();  // (shard() needs an uninitialised state)
     if (world > 1 && e.shard_world() != world) e.shard(rank, world);
-    if (e.initialized()) e.reset();
     e.init_state();
     const Layout& L = e.layout();
     const uint64_t nid = L.num_blocks(), ns = e.plan().size();

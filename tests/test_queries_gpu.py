@@ -55,6 +55,7 @@ def test_top_k_matches_dense(gpu, k):
 
 def test_top_k_sparse_and_ties(gpu):
     with run(gpu, "ghz", 20, 12) as sim:
+        assert sim.top_k(0)[0].size == 0
         idx, amp = sim.top_k(3)
         assert idx.tolist() == [0, (1 << 20) - 1]  # equal magnitudes: lower index first
         assert np.allclose(np.abs(amp), 2 ** -0.5, rtol=2e-3)
