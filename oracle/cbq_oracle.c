@@ -902,7 +902,7 @@ int cbqo_simulate(uint32_t n, const cbqo_gate* g, uint64_t ng, uint32_t b, uint3
             }
             if (!rc) comp_calls += per;
             if (rc) {
-                char msg[512];
+                char msg[640];
                 snprintf(msg, sizeof msg, "stage %llu: group with outer value %llu: %s",
                          (unsigned long long)si, (unsigned long long)gi, g_err);
                 rc = fail(CBQO_ENGINE, "%s", msg);
