@@ -254,14 +254,15 @@ __global__ void k_unpack_payloads(const Xfer* __restrict__ xs, uint64_t n, const
                                   uint8_t* to, uint64_t tag, uint64_t* off, uint64_t* size, double* sums) {
     for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
         const Xfer x = xs[i];
-        if (x.size) {
+        const bool disk = (x.dst & kDiskTag) != 0;  // written to the disk level by the host
+        if (x.size && !disk) {
             const uint4* s = reinterpret_cast<const uint4*>(in + x.xoff);
             uint4* d = reinterpret_cast<uint4*>(to + x.dst);
             const uint64_t words = (x.size + 15) / 16;
             for (uint64_t w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
         }
         if (threadIdx.x == 0) {
-            off[x.id] = x.size ? (x.dst | tag) : ~0ull;
+            off[x.id] = x.size ? (disk ? x.dst : (x.dst | tag)) : ~0ull;
             size[x.id] = x.size ? x.size : kHeaderBytes;
             for (int k = 0; k < 3; ++k) sums[3 * x.id + k] = x.sums[k];
         }
@@ -1792,9 +1793,14 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
         ensure_host_pool();
         sync_copies();
         const uint64_t ext = host_heap_.alloc(size);
-        if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
-        std::memcpy(host_pool_ + ext, data, size);
-        off = ext | kHostTag;
+        if (ext != ExtentHeap::kNone) {
+            std::memcpy(host_pool_ + ext, data, size);
+            off = ext | kHostTag;
+        } else {  // host level full: the disk level
+            const uint64_t d = disk_alloc(size);
+            disk_.write_from_host(data, size, d);
+            off = d | kDiskTag;
+        }
     }
     BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &off, 8, cudaMemcpyHostToDevice, st_));
     BMQ_CUDA(cudaMemcpyAsync(size_.p + id, &size, 8, cudaMemcpyHostToDevice, st_));
@@ -1807,7 +1813,9 @@ void Engine::put_payload(uint64_t id, const uint8_t* data, uint64_t size) {
         BMQ_CUDA(cudaMemcpyAsync(off_.p + id, &prev_off, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaMemcpyAsync(size_.p + id, &prev_size, 8, cudaMemcpyHostToDevice, st_));
         BMQ_CUDA(cudaStreamSynchronize(st_));
-        if (off & kHostTag)
+        if (off & kDiskTag)
+            disk_.heap().free(off & ~kDiskTag, size);
+        else if (off & kHostTag)
             host_heap_.free(off & ~kHostTag, size);
         else if (heap_mode_)
             dev_heap_.free(off, size);
@@ -2025,8 +2033,7 @@ void Engine::import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* me
         for (Xfer& x : xs) {
             if (!x.size) continue;
             const uint64_t ext = host_heap_.alloc(x.size);
-            if (ext == ExtentHeap::kNone) raise(BMQ_ERR_STORE, "host payload pool exhausted");
-            x.dst = ext;
+            x.dst = ext != ExtentHeap::kNone ? ext : (disk_alloc(x.size) | kDiskTag);  // host level full: disk
         }
         counters_.host_spill_bytes += pos;
         ++counters_.host_spill_batches;
@@ -2041,8 +2048,20 @@ void Engine::import_payloads(const uint64_t* ids, uint64_t n, const uint64_t* me
     ++counters_.kernel_launches;
     BMQ_CUDA(cudaGetLastError());
     BMQ_CUDA(cudaStreamSynchronize(st_));
+    cudaPointerAttributes pa{};
+    const bool src_dev = src && cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
     for (const Xfer& x : xs) {
-        h_off_[x.id] = x.size ? (x.dst | tag) : ~0ull;
+        const bool disk = x.size && (x.dst & kDiskTag);
+        if (disk) {
+            const uint8_t* from = static_cast<const uint8_t*>(src) + x.xoff;
+            if (src_dev)
+                disk_.write_from_device(from, x.size, x.dst & ~kDiskTag);
+            else
+                disk_.write_from_host(from, x.size, x.dst & ~kDiskTag);
+            counters_.disk_spill_bytes += x.size;
+        }
+        h_off_[x.id] = x.size ? (disk ? x.dst : (x.dst | tag)) : ~0ull;
         h_size_[x.id] = x.size ? x.size : kHeaderBytes;
         sums_ok_[x.id] = 1;  // the sums travelled with the payload
     }

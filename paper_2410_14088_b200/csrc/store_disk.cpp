@@ -133,6 +133,15 @@ void DiskLevel::read_to_device(void* dev, uint64_t size, uint64_t off) {
     bytes_read_ += size;
 }
 
+void DiskLevel::write_from_host(const void* host, uint64_t size, uint64_t off) {
+    for (uint64_t done = 0; done < size;) {
+        const ssize_t n = pwrite(fd_, static_cast<const uint8_t*>(host) + done, size - done, static_cast<off_t>(off + done));
+        if (n <= 0) raise(BMQ_ERR_STORE, "disk level: write failed");
+        done += static_cast<uint64_t>(n);
+    }
+    bytes_written_ += size;
+}
+
 void DiskLevel::read_to_host(void* host, uint64_t size, uint64_t off) {
     for (uint64_t done = 0; done < size;) {
         const ssize_t n = pread(fd_, static_cast<uint8_t*>(host) + done, size - done, static_cast<off_t>(off + done));

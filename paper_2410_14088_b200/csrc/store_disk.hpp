@@ -25,6 +25,7 @@ public:
     void write_from_device(const void* dev, uint64_t size, uint64_t off);
     void read_to_device(void* dev, uint64_t size, uint64_t off);
     void read_to_host(void* host, uint64_t size, uint64_t off);
+    void write_from_host(const void* host, uint64_t size, uint64_t off);
     uint64_t bytes_written() const { return bytes_written_; }
     uint64_t bytes_read() const { return bytes_read_; }
 

@@ -597,3 +597,34 @@ print("ok")
     env = dict(os.environ, BMQ_NO_GDS="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_three_levels_with_device_plan_queries_and_checkpoint(gpu, port, tmp_path):
+    """The optional pieces together: a device-aware plan (equal to the
+    reference at the chosen inner size) on a state spilled across all three
+    store levels; sampling / top-k / amplitude queries and a checkpoint read
+    the disk-resident payloads; the resumed run equals the uninterrupted one."""
+    c = gpu.generate_benchmark("qaoa3reg", 16, gpu.BenchmarkParams(layers=2, seed=1))
+    plan, ch = gpu.plan_device_aware(c, 12, max_inner=3)
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, ch.inner_size, 1e-3, want_state=True)
+    biggest = max(len(p) for p in want.payloads)
+    cfg = gpu.Config(block_bits=12, inner_size=3, error_bound=1e-3, device_plan=True, work_bytes=8 * (16 << 12),
+                     device_pool_bytes=5 * (biggest + 16), host_pool_bytes=3 * (biggest + 16),
+                     disk_pool_bytes=16 << 20, disk_dir=str(tmp_path))
+    with gpu.Simulator(c, cfg) as sim:
+        rep = sim.run()
+        assert rep.device["disk_spill_bytes"] > 0
+        assert sim.payloads() == want.payloads
+        psi = sim.extract_state()
+        idx, amp = sim.top_k(5)
+        key = psi.real * psi.real + psi.imag * psi.imag
+        nz = np.flatnonzero(key)
+        assert np.array_equal(idx.astype(np.int64), nz[np.lexsort((nz, -key[nz]))][:5])
+        assert sim.amplitude(int(idx[0])) == psi[int(idx[0])]
+        s = sim.sample(2000, seed=5)
+        assert np.all(key[s.astype(np.int64)] > 0)
+        ck = str(tmp_path / "state.bmqckpt")
+        sim.save(ck)
+    with gpu.Simulator(c, cfg) as sim2:
+        assert sim2.load(ck) == rep.stage_count
+        assert sim2.payloads() == want.payloads

@@ -293,3 +293,39 @@ def test_c_abi_sharded_run_nccl_world1(gpu, port):
         assert sim.payloads() == want.payloads
         assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
     col.close()
+
+
+@pytest.mark.gpu
+def test_c_abi_sharded_run_with_host_level(gpu, port):
+    """Sharded ranks whose device arenas overflow into their pinned host
+    levels: remaps export payloads from either level; the result is the
+    single-GPU run's."""
+    import threading
+    c = gpu.generate_benchmark("qaoa3reg", 16, gpu.BenchmarkParams(layers=2, seed=1))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-3)
+    biggest = max(len(p) for p in want.payloads)
+    cfg = gpu.Config(block_bits=12, inner_size=2, error_bound=1e-3, work_bytes=4 * (16 << 12),
+                     device_pool_bytes=3 * (biggest + 16), host_pool_bytes=32 << 20)
+    cols = gpu.Collective.local(2)
+    sims = [gpu.Simulator(c, cfg) for _ in range(2)]
+    reps, errs = [None, None], []
+
+    def go(r):
+        try:
+            reps[r] = sims[r].run_sharded(cols[r])
+        except Exception as e:
+            errs.append(e)
+
+    th = [threading.Thread(target=go, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert sum(r.device["host_spill_bytes"] for r in reps) > 0
+    assert _merged([s.payloads() for s in sims]) == want.payloads
+    assert reps[0].max_footprint_bytes == want.report["max_footprint_bytes"]
+    for s in sims:
+        s.close()
+    for col in cols:
+        col.close()
