@@ -450,6 +450,34 @@ __device__ __forceinline__ void emit_chunk(const ChunkPlan& p, uint32_t len, con
                          kChunk, tid, kChunkThreads);
         return;
     }
+    if (!kW1 && kFull && p.nnz == kChunk) {
+        // no zero in the chunk: scalar s has rank s, so word k's codes start
+        // at stage bit 32 k w (no compaction, no prefix scan, no zero bitmap)
+        uint32_t pkv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pkv[j] = __ldcs(src + 128 * j + 32 * w + lane);
+        for (uint32_t i = tid; i < nstage; i += kChunkThreads) sm.stage[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t k = 4 * j + w;
+            const uint32_t pk = pkv[j];
+            const uint32_t sw = __ballot_sync(0xffffffffu, (pk >> 1) & 1u);
+            if (lane == 0) sm.sign[k] = sw;
+            const uint32_t code = (pk >> 2) - qmin_off;
+            const uint32_t pbit = (32u * k + lane) * w_bits, wi = pbit >> 5, sh = pbit & 31;
+            if (code) {
+                atomicOr(&sm.stage[wi], code << sh);
+                if (sh + w_bits > 32) atomicOr(&sm.stage[wi + 1], code >> (32 - sh));
+            }
+        }
+        __syncthreads();
+        if (p.stag == 2) write_bits_block(pay + p.sign_off, 0, sm.sign, kChunk, tid, kChunkThreads);
+        const uint64_t start_bit = static_cast<uint64_t>(p.nz_prefix) * w_bits;
+        write_bits_block(pay + bp.code_seg + (start_bit >> 3), static_cast<uint32_t>(start_bit & 7), sm.stage,
+                         code_bits, tid, kChunkThreads);
+        return;
+    }
     // A: all loads in flight; B: ballots -> bitmap words, width-1 code words,
     // or (wider codes) the nonzero codes compacted per word into sm.cw
     {
