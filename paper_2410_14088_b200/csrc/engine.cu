@@ -521,6 +521,23 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     imnz_.alloc(1);
     wflag_.alloc(work_scalars_ / 32);
     if (L_.b >= 12 && getenv("BMQ_FUSED_DECODE")) rows_.alloc(work_scalars_ / 32);
+    // second buffer set (batch k+1's front overlaps batch k's back): when
+    // the device has room for it next to a payload arena of the same size
+    two_sets_ = cfg.compress && !getenv("BMQ_DBG_ONE_SET") &&
+                4 * (work_.bytes() + pk_.bytes() + wflag_.bytes()) < total_b;
+    if (two_sets_) {
+        work2_.alloc(work_scalars_);
+        pk2_.alloc(work_scalars_);
+        cmp2_.alloc(max_blocks_);
+        dec2_.alloc(max_blocks_);
+        cplan2_.alloc(max_blocks_ * nch_);
+        bplan2_.alloc(max_blocks_);
+        dinfo2_.alloc(max_blocks_);
+        dchunk2_.alloc(max_blocks_ * nch_);
+        zflag2_.alloc(max_blocks_ * nch_);
+        imnz2_.alloc(1);
+        wflag2_.alloc(work_scalars_ / 32);
+    }
     ids_.alloc(std::max<uint64_t>(nid, max_blocks_));
     vtab_.alloc(std::max<uint64_t>(nid, max_blocks_));
     new_off_.alloc(nid);
@@ -539,7 +556,8 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     // HBM / 8) and grow up to what the device has left.
     const uint64_t worst = nid * (compress_bound(blk_scalars) + kArenaAlign) + 64;
     const uint64_t others = work_.bytes() + pk_.bytes() + cplan_.bytes() + dchunk_.bytes() + zflag_.bytes() +
-                            wflag_.bytes() + rows_.bytes() + 8 * (ids_.n + vtab_.n + new_off_.n + live_ids_.n + off_.n + size_.n) +
+                            wflag_.bytes() + rows_.bytes() + work2_.bytes() + pk2_.bytes() + cplan2_.bytes() +
+                            dchunk2_.bytes() + zflag2_.bytes() + wflag2_.bytes() + 8 * (ids_.n + vtab_.n + new_off_.n + live_ids_.n + off_.n + size_.n) +
                             sums_.bytes();
     const uint64_t headroom = total_b > others + (6ull << 30) ? total_b - others - (6ull << 30) : (1ull << 30);
     arena_grow_ = cfg.device_pool_bytes == 0 || (cfg.flags & BMQ_FLAG_POOL_GROW);
@@ -553,6 +571,13 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     arena_auto_ = !(cfg.flags & (BMQ_FLAG_HEAP_ARENA | BMQ_FLAG_BUMP_ARENA)) && nid <= (1ull << 17);
     h_place_.assign(2 * max_blocks_, 0);
     d_place_.alloc(2 * max_blocks_);
+    if (two_sets_) {
+        h_place2_.assign(2 * max_blocks_, 0);
+        d_place2_.alloc(2 * max_blocks_);
+        BMQ_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+        BMQ_CUDA(cudaEventCreateWithFlags(&ev_emitted_, cudaEventDisableTiming));
+        BMQ_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
     BMQ_CUDA(cudaStreamCreateWithFlags(&cp_in_, cudaStreamNonBlocking));
     BMQ_CUDA(cudaStreamCreateWithFlags(&cp_out_, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
@@ -566,12 +591,13 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
 
 Engine::~Engine() {
     cudaSetDevice(dev_);
-    for (cudaStream_t* q : {&st_, &cp_in_, &cp_out_})
+    use_set(0);
+    for (cudaStream_t* q : {&st_, &st2_, &cp_in_, &cp_out_})
         if (*q) {
             cudaStreamSynchronize(*q);
             cudaStreamDestroy(*q);
         }
-    for (cudaEvent_t e : {ev_pf_[0], ev_pf_[1], ev_dec_[0], ev_dec_[1], ev_emit_, ev_wb_})
+    for (cudaEvent_t e : {ev_pf_[0], ev_pf_[1], ev_dec_[0], ev_dec_[1], ev_emit_, ev_wb_, ev_emitted_, ev_join_})
         if (e) cudaEventDestroy(e);
     for (auto& [a, b] : link_ev_) {
         cudaEventDestroy(a);
@@ -633,6 +659,8 @@ bool Engine::grow_arena(uint64_t limit) {
 // then unpacked. Destinations never pass the sources of later windows, so the
 // windows run back to back on st_.
 void Engine::compact(const uint64_t* excl, uint64_t nexcl) {
+    // the other buffer set's batch may still be decoding payloads this moves
+    if (two_sets_) BMQ_CUDA(cudaStreamSynchronize(st2_));
     sync_meta_to_host();
     const uint64_t nid = L_.num_blocks();
     std::vector<uint8_t> dead(nid, 0);
@@ -1107,6 +1135,7 @@ void Engine::ensure_host_pool() {
         h_pf_off_[k].assign(max_blocks_, ~0ull);
     }
     d_meta_.alloc(3 * max_blocks_);
+    if (two_sets_) d_meta2_.alloc(3 * max_blocks_);
     device_peak_ += wb_.bytes() + 2 * slot + 2 * 8 * max_blocks_ + 24 * max_blocks_;
     if (cfg_.disk_pool_bytes && !disk_.is_open())
         disk_.open(disk_dir_, cfg_.disk_pool_bytes, kArenaAlign);
@@ -1200,12 +1229,46 @@ bool Engine::prefetch(const uint64_t* h_ids, uint64_t nblk, int slot) {
     return true;
 }
 
-void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t* d_ids, const uint32_t* d_vtab,
-                           uint64_t nblk, size_t bidx) {
+// Swap the current buffer set / stream with the other one (see BatchFront).
+void Engine::use_set(int set) {
+    if (!two_sets_ || set == cur_set_) return;
+    std::swap(st_, st2_);
+    work_.swap_with(work2_);
+    pk_.swap_with(pk2_);
+    cmp_.swap_with(cmp2_);
+    dec_.swap_with(dec2_);
+    cplan_.swap_with(cplan2_);
+    bplan_.swap_with(bplan2_);
+    dinfo_.swap_with(dinfo2_);
+    dchunk_.swap_with(dchunk2_);
+    zflag_.swap_with(zflag2_);
+    imnz_.swap_with(imnz2_);
+    wflag_.swap_with(wflag2_);
+    d_place_.swap_with(d_place2_);
+    h_place_.swap_with(h_place2_);
+    d_meta_.swap_with(d_meta2_);
+    h_meta_.swap_with(h_meta2_);
+    cur_set_ = set;
+}
+
+// Back on set 0 with everything the other stream queued ordered before
+// what st_ runs next.
+void Engine::join_sets() {
+    use_set(0);
+    if (!two_sets_) return;
+    BMQ_CUDA(cudaEventRecord(ev_join_, st2_));
+    BMQ_CUDA(cudaStreamWaitEvent(st_, ev_join_, 0));
+    emitted_live_ = false;
+}
+
+Engine::BatchFront Engine::process_front(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab,
+                                         uint64_t nblk, size_t bidx) {
+    BatchFront f;
     phase_event(4 * bidx);
     // Code-domain stages (unit-entry monomial gates only) never leave the
     // quantiser codes: decode to packed words, permute them, emit.
     const bool codes = !d_vtab && sp.prog.mono && identity_ok_ && (cfg_.flags & BMQ_FLAG_CODE_DOMAIN);
+    f.codes = codes;
     const int slot = static_cast<int>(bidx & 1);
     const bool pf = pf_live_[slot];
     if (pf) BMQ_CUDA(cudaStreamWaitEvent(st_, ev_pf_[slot], 0));  // host-level payloads prefetched
@@ -1228,7 +1291,8 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t*
     // dependent record -> code -> dequantisation loads are latency-bound at
     // its occupancy, where the separate decoder hides them.
     static const bool fused_on = getenv("BMQ_FUSED_DECODE") != nullptr;
-    const bool fdec = !codes && rows_.p && fused_on && stream_first_pass(sp.prog, L_.b, false, d_vtab != nullptr);
+    const bool fdec = !codes && rows_.p && fused_on && !two_sets_ &&
+                      stream_first_pass(sp.prog, L_.b, false, d_vtab != nullptr);
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
                       &counters_.kernel_launches, fdec ? 3 : (codes ? 1 : 0), fdec ? nullptr : zf,
                       (zf && !fdec) ? imnz_.p : nullptr, rows_.p);
@@ -1239,7 +1303,6 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t*
     BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
     const QuantOut qo{pk_.p, cplan_.p, nch_, *tabs_, err_.p};
     const uint64_t per = sp.gg.per_group();
-    bool fused = true;
     if (codes) {
         run_mono_program(st_, sp.prog, pk_.p, L_.b, nblk / per, &counters_.kernel_launches, qo, zf,
                          zf ? imnz_.p : nullptr);
@@ -1256,29 +1319,33 @@ void Engine::process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t*
             fd.err = err_.p;
             ++counters_.fused_decode_batches;
         }
-        fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per, &counters_.kernel_launches,
-                            &qo, d_vtab, nblk, zf, nch_, zf ? imnz_.p : nullptr, fdec ? &fd : nullptr);
+        f.fused = run_program(st_, sp.prog, work_.p, L_.b, false, d_vtab ? 0 : nblk / per,
+                              &counters_.kernel_launches, &qo, d_vtab, nblk, zf, nch_, zf ? imnz_.p : nullptr,
+                              fdec ? &fd : nullptr);
     }
     phase_event(4 * bidx + 2);
-    if (getenv("BMQ_DBG_CPLAN")) {  // development aid: the quantiser's chunk counters
-        std::vector<ChunkPlan> h(nblk * nch_);
-        BMQ_CUDA(cudaMemcpyAsync(h.data(), cplan_.p, h.size() * sizeof(ChunkPlan), cudaMemcpyDeviceToHost, st_));
-        BMQ_CUDA(cudaStreamSynchronize(st_));
-        for (size_t i = 0; i < h.size() && i < 64; ++i)
-            fprintf(stderr, "chunk %zu: qmin_inv %u qmax %u nnz %u nneg %u\n", i, h[i].qmin_inv, h[i].qmax_off, h[i].nnz,
-                    h[i].nneg);
-    }
-    launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,
+    launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, f.fused, err_.p,
                          &counters_.kernel_launches);
+    return f;
+}
+
+void Engine::process_back(StagePlan& sp, const BatchFront& f, const uint64_t* h_ids, uint64_t nblk, size_t bidx) {
+    // payload placement stays in batch order (the arena cursor / heap and the
+    // reference's put order): wait for the previous batch's emit
+    if (emitted_live_) BMQ_CUDA(cudaStreamWaitEvent(st_, ev_emitted_, 0));
     emit_batch(nblk, h_ids);
+    if (two_sets_) {
+        BMQ_CUDA(cudaEventRecord(ev_emitted_, st_));
+        emitted_live_ = true;
+    }
     phase_event(4 * bidx + 3);
-    if (fused) ++counters_.fused_batches;
-    if (!codes) {
+    if (f.fused) ++counters_.fused_batches;
+    if (!f.codes) {
         counters_.lazy_cx += sp.prog.lazy_cx;
         counters_.perm_materialisations += sp.prog.perms;
     }
     counters_.gate_passes += sp.prog.passes.size();
-    if (!codes)
+    if (!f.codes)
         for (const GatePass& gp : sp.prog.passes) counters_.stream_passes += gp.sp && !stream_off() ? 1 : 0;
 }
 
@@ -1364,14 +1431,30 @@ void Engine::run_stage(uint64_t s) {
             hb += ub;
         }
         batches.emplace_back(first, nwork - first);
+        if (two_sets_) {  // the other stream reads the ids / table just uploaded on st_
+            BMQ_CUDA(cudaEventRecord(ev_join_, st_));
+            BMQ_CUDA(cudaStreamWaitEvent(st2_, ev_join_, 0));
+        }
+        const auto front = [&](size_t k) {
+            const auto [b0, nblk] = batches[k];
+            use_set(static_cast<int>(k & 1));
+            return process_front(sp, ids_.p + b0, blockwise ? vtab_.p + b0 : nullptr, nblk, k);
+        };
         pf_live_[0] = prefetch(work_ids.data() + batches[0].first, batches[0].second, 0);
+        BatchFront cur = front(0), next;
         for (size_t k = 0; k < batches.size(); ++k, ++nbatches) {
-            if (k + 1 < batches.size())  // overlaps batch k on the copy engine
+            if (k + 1 < batches.size()) {
+                // overlaps batch k on the copy engine
                 pf_live_[(k + 1) & 1] = prefetch(work_ids.data() + batches[k + 1].first, batches[k + 1].second,
                                                  static_cast<int>((k + 1) & 1));
+                if (two_sets_) next = front(k + 1);  // decode of k+1 overlaps the passes of k
+            }
             const auto [b0, nblk] = batches[k];
-            process_batch(sp, work_ids.data() + b0, ids_.p + b0, blockwise ? vtab_.p + b0 : nullptr, nblk, k);
+            use_set(static_cast<int>(k & 1));
+            process_back(sp, cur, work_ids.data() + b0, nblk, k);
+            if (k + 1 < batches.size()) cur = two_sets_ ? next : front(k + 1);
         }
+        join_sets();
     }
     check_device_error(("stage " + std::to_string(s) + ": ").c_str());
     sync_copies();

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "codec.cuh"
@@ -30,6 +31,10 @@ struct DevArray {
         n = 0;
     }
     size_t bytes() const { return n * sizeof(T); }
+    void swap_with(DevArray& o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+    }
 };
 
 // Page-locked host array (cudaMallocHost), owned RAII: the engine's host
@@ -63,6 +68,10 @@ public:
     const T& operator[](size_t i) const { return p_[i]; }
     T* begin() { return p_; }
     T* end() { return p_ + n_; }
+    void swap_with(PinnedVec& o) {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
+    }
 
 private:
     void release() {
@@ -181,8 +190,24 @@ private:
     void ensure_init();
     void run_stage(uint64_t s);
     void raw_run_stage(uint64_t s);
-    void process_batch(StagePlan& sp, const uint64_t* h_ids, const uint64_t* d_ids, const uint32_t* d_vtab,
-                       uint64_t nblk, size_t bidx);
+    // Batches alternate between two buffer sets and two streams: the front
+    // of batch k+1 (descriptors, decode, gate passes, plan) is queued before
+    // the back of batch k (allocation + emit, with its host synchronisation),
+    // so the decode of one batch overlaps the passes of the other. Emits stay
+    // in batch order (ev_emitted_), and compaction waits for the other set.
+    struct BatchFront {
+        bool codes = false, fused = true;
+    };
+    BatchFront process_front(StagePlan& sp, const uint64_t* d_ids, const uint32_t* d_vtab, uint64_t nblk,
+                             size_t bidx);
+    void process_back(StagePlan& sp, const BatchFront& f, const uint64_t* h_ids, uint64_t nblk, size_t bidx);
+    void use_set(int s);
+    void join_sets();
+    int cur_set_ = 0;
+    bool two_sets_ = false;
+    cudaStream_t st2_ = nullptr;
+    cudaEvent_t ev_emitted_ = nullptr, ev_join_ = nullptr;
+    bool emitted_live_ = false;
     void emit_batch(uint64_t nblk, const uint64_t* h_ids);
     void emit_to_host(uint64_t nblk, const uint64_t* h_ids);
 
@@ -298,6 +323,18 @@ private:
     DevArray<uint32_t> imnz_;  // 1 word: code domain, some imaginary-half input chunk is nonzero; FP, some group flag is 0
     DevArray<DecRow> rows_;    // per 32 scalars of work_: decode rows of a streaming first pass (fused decode)
     DevArray<uint8_t> wflag_;  // per 32 scalars of work_: group stored (1) or all zero (0), FP stages
+    // the second buffer set (use_set swaps it with the members above)
+    DevArray<double> work2_;
+    DevArray<uint32_t> pk2_, imnz2_;
+    DevArray<CmpBlock> cmp2_;
+    DevArray<DecBlock> dec2_;
+    DevArray<ChunkPlan> cplan2_;
+    DevArray<BlockPlan> bplan2_;
+    DevArray<DecInfo> dinfo2_;
+    DevArray<DecChunk> dchunk2_;
+    DevArray<uint8_t> zflag2_, wflag2_;
+    DevArray<uint64_t> d_place2_, d_meta2_;
+    PinnedVec<uint64_t> h_place2_, h_meta2_;
     DevArray<uint64_t> ids_;
     DevArray<uint32_t> vtab_;
     DevArray<DevError> err_;
