@@ -40,7 +40,7 @@ void launch_compress_emit(cudaStream_t st, const CmpBlock* d_blks, uint64_t nblk
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
                        uint64_t* launches, int mode = 0, uint8_t* zflag = nullptr, uint32_t* imnz = nullptr,
-                       DecRow* rows = nullptr);
+                       DecRow* rows = nullptr, PermSrc* psrc = nullptr);
 // (zflag, mode 1: one byte per (block, chunk) marking all-zero chunks, which
 // are then not written (k_dec_index); mode 0: one byte per 32-scalar group of
 // the output, 0 for an all-zero group that was not stored.)

@@ -313,14 +313,35 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_chunk(const DecBlock* __r
                                                              DecInfo* __restrict__ infos,
                                                              const DecChunk* __restrict__ dcs, DevTables t,
                                                              int want_sums, DevError* err, int skip_zero_chunks,
-                                                             uint8_t* __restrict__ wflag) {
+                                                             uint8_t* __restrict__ wflag,
+                                                             PermSrc* __restrict__ psrc = nullptr) {
     // the CTA's records, loaded together (one memory round trip)
     const uint32_t bi = blockIdx.x / nch_max, c = blockIdx.x % nch_max;
     const DecInfo info = infos[bi];
     const DecBlock blk = blks[bi];
     const DecChunk d = dcs[static_cast<uint64_t>(bi) * nch_max + c];
-    if (info.flags & 2) return;
     const uint64_t nch = (info.count + kChunk - 1) / kChunk;
+    if (kMode == kCodes && psrc) {
+        // a chunk the first permutation pass can read from the payload (see
+        // PermSrc) is not decoded here; every other chunk gets meta 0
+        PermSrc r{nullptr, 0u, 0u};
+        const bool full = c < nch && chunk_len(info.count, c) == kChunk;
+        if ((info.flags & 3) == 1 || (!(info.flags & 3) && full && d.ztag == 1)) r.meta = 1u << 13;  // all zero
+        if (!(info.flags & 3) && c < nch && chunk_len(info.count, c) == kChunk && d.ztag == 0 && d.stag != 2 && info.width >= 1 && info.width <= 16) {
+            const int64_t qbase = info.code_min - t.qlo;
+            const int64_t top = qbase + static_cast<int64_t>((1ull << info.width) - 1);
+            if (qbase >= t.idem_lo - t.qlo && top <= t.idem_hi - t.qlo) {
+                const uintptr_t cs = reinterpret_cast<uintptr_t>(blk.in + info.code_seg);
+                const uint64_t cb = static_cast<uint64_t>(cs & 7) * 8 + static_cast<uint64_t>(d.nz_prefix) * info.width;
+                r.cw = reinterpret_cast<const uint64_t*>(cs & ~uintptr_t(7)) + (cb >> 6);
+                r.qb = static_cast<uint32_t>(qbase);
+                r.meta = static_cast<uint32_t>(cb & 63) | (info.width << 6) | (d.stag == 1 ? 1u << 11 : 0u) | (1u << 12);
+            }
+        }
+        if (threadIdx.x == 0) psrc[blockIdx.x] = r;
+        if (r.meta & (1u << 12)) return;
+    }
+    if (info.flags & 2) return;
     if (c >= nch) return;
     const uint32_t len = chunk_len(info.count, c);
     double* dst = blk.out + static_cast<uint64_t>(c) * kChunk;
@@ -539,7 +560,8 @@ __global__ void __launch_bounds__(kChunkThreads) k_dec_rows(const DecBlock* __re
 
 void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, uint32_t nch_max, const DevTables& t,
                        DecInfo* d_info, DecChunk* d_dc, bool check_bound, bool want_sums, DevError* d_err,
-                       uint64_t* launches, int mode, uint8_t* zflag, uint32_t* imnz, DecRow* rows) {
+                       uint64_t* launches, int mode, uint8_t* zflag, uint32_t* imnz, DecRow* rows,
+                       PermSrc* psrc) {
     if (nblk == 0) return;
     BMQ_CUDA(cudaMemsetAsync(d_info, 0, nblk * sizeof(DecInfo), st));
     // mode 1: zflag = per-chunk zero flags (index kernel); mode 0: zflag =
@@ -554,7 +576,7 @@ void launch_decompress(cudaStream_t st, const DecBlock* d_blks, uint64_t nblk, u
         k_dec_rows<<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, rows);
     else if (mode == 1)
         k_dec_chunk<kCodes><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 0, d_err,
-                                                             zflag ? 1 : 0, nullptr);
+                                                             zflag ? 1 : 0, nullptr, psrc);
     else if (mode == 2)
         k_dec_chunk<kSumsOnly><<<grid, kChunkThreads, 0, st>>>(d_blks, nch_max, d_info, d_dc, t, 1, d_err, 0,
                                                                nullptr);

@@ -294,6 +294,20 @@ struct DecRow {
     uint32_t pad;
 };
 
+// Code-domain stages (mode 1 of launch_decompress with a PermSrc array): one
+// record per (block slot, chunk). A zero-free full chunk of all-positive or
+// all-negative scalars whose codes are at most 16 bits wide and inside the
+// idempotent window is not decoded to packed words; the first permutation
+// pass reads its codes from the payload through this record instead (meta
+// bit 12 set): scalar s of the chunk has rank s, so its code sits at bit
+// (meta & 63) + s * width of cw.
+struct __align__(16) PermSrc {
+    const uint64_t* cw;  // 8-byte aligned base of the chunk's codes
+    uint32_t qb;         // packed offset of code 0 (code_min - qlo)
+    uint32_t meta;       // bits 0-5: bit offset, 6-10: width, 11: negative, 12: read from the payload,
+                         // 13: all-zero chunk (not written; read as zero words)
+};
+
 struct DecInfo {
     uint64_t count;
     int64_t code_min;

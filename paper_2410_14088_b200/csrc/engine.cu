@@ -518,6 +518,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     dinfo_.alloc(max_blocks_);
     dchunk_.alloc(max_blocks_ * nch_);
     zflag_.alloc(max_blocks_ * nch_);
+    psrc_.alloc(max_blocks_ * nch_);
     imnz_.alloc(1);
     wflag_.alloc(work_scalars_ / 32);
     if (L_.b >= 12 && getenv("BMQ_FUSED_DECODE")) rows_.alloc(work_scalars_ / 32);
@@ -535,6 +536,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
         dinfo2_.alloc(max_blocks_);
         dchunk2_.alloc(max_blocks_ * nch_);
         zflag2_.alloc(max_blocks_ * nch_);
+        psrc2_.alloc(max_blocks_ * nch_);
         imnz2_.alloc(1);
         wflag2_.alloc(work_scalars_ / 32);
     }
@@ -557,7 +559,7 @@ Engine::Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_con
     const uint64_t worst = nid * (compress_bound(blk_scalars) + kArenaAlign) + 64;
     const uint64_t others = work_.bytes() + pk_.bytes() + cplan_.bytes() + dchunk_.bytes() + zflag_.bytes() +
                             wflag_.bytes() + rows_.bytes() + work2_.bytes() + pk2_.bytes() + cplan2_.bytes() +
-                            dchunk2_.bytes() + zflag2_.bytes() + wflag2_.bytes() + 8 * (ids_.n + vtab_.n + new_off_.n + live_ids_.n + off_.n + size_.n) +
+                            dchunk2_.bytes() + zflag2_.bytes() + wflag2_.bytes() + psrc_.bytes() + psrc2_.bytes() + 8 * (ids_.n + vtab_.n + new_off_.n + live_ids_.n + off_.n + size_.n) +
                             sums_.bytes();
     const uint64_t headroom = total_b > others + (6ull << 30) ? total_b - others - (6ull << 30) : (1ull << 30);
     arena_grow_ = cfg.device_pool_bytes == 0 || (cfg.flags & BMQ_FLAG_POOL_GROW);
@@ -1130,7 +1132,7 @@ void Engine::ensure_host_pool() {
     const uint64_t slot = std::max<uint64_t>(std::min<uint64_t>(work_.bytes() / 4, 4ull << 30), 1ull << 20);
     wb_.alloc(slot + 64);
     for (int k = 0; k < 2; ++k) {
-        pf_[k].alloc(slot);
+        pf_[k].alloc(slot + 64);  // (+64: decoders read whole words past a payload's last code)
         pf_off_[k].alloc(max_blocks_);
         h_pf_off_[k].assign(max_blocks_, ~0ull);
     }
@@ -1242,6 +1244,7 @@ void Engine::use_set(int set) {
     dinfo_.swap_with(dinfo2_);
     dchunk_.swap_with(dchunk2_);
     zflag_.swap_with(zflag2_);
+    psrc_.swap_with(psrc2_);
     imnz_.swap_with(imnz2_);
     wflag_.swap_with(wflag2_);
     d_place_.swap_with(d_place2_);
@@ -1293,10 +1296,15 @@ Engine::BatchFront Engine::process_front(StagePlan& sp, const uint64_t* d_ids, c
     static const bool fused_on = getenv("BMQ_FUSED_DECODE") != nullptr;
     const bool fdec = !codes && rows_.p && fused_on && !two_sets_ &&
                       stream_first_pass(sp.prog, L_.b, false, d_vtab != nullptr);
+    // code-domain stages: zero-free narrow chunks stay in the payload and the
+    // first permutation pass reads their codes there (PermSrc; BMQ_DBG_NO_PERMSRC=1 decodes every chunk)
+    static const bool permsrc_off = getenv("BMQ_DBG_NO_PERMSRC") != nullptr;
+    PermSrc* ps = (codes && zf && !permsrc_off) ? psrc_.p : nullptr;
     launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
                       &counters_.kernel_launches, fdec ? 3 : (codes ? 1 : 0), fdec ? nullptr : zf,
-                      (zf && !fdec) ? imnz_.p : nullptr, rows_.p);
-    if (host_pool_) BMQ_CUDA(cudaEventRecord(ev_dec_[slot], st_));  // the prefetch slot is free again
+                      (zf && !fdec) ? imnz_.p : nullptr, rows_.p, ps);
+    // the prefetch slot is free again (after the permutation passes when they read payloads)
+    if (host_pool_ && !ps) BMQ_CUDA(cudaEventRecord(ev_dec_[slot], st_));
     pf_live_[slot] = false;
     phase_event(4 * bidx + 1);
     // the stage's last gate pass quantises straight into pk_ / cplan_
@@ -1305,7 +1313,8 @@ Engine::BatchFront Engine::process_front(StagePlan& sp, const uint64_t* d_ids, c
     const uint64_t per = sp.gg.per_group();
     if (codes) {
         run_mono_program(st_, sp.prog, pk_.p, L_.b, nblk / per, &counters_.kernel_launches, qo, zf,
-                         zf ? imnz_.p : nullptr);
+                         zf ? imnz_.p : nullptr, ps);
+        if (host_pool_ && ps) BMQ_CUDA(cudaEventRecord(ev_dec_[slot], st_));
         ++counters_.code_domain_batches;
     } else {
         FusedDecode fd{};

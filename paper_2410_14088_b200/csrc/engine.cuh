@@ -320,6 +320,7 @@ private:
     DevArray<DecInfo> dinfo_;
     DevArray<DecChunk> dchunk_;
     DevArray<uint8_t> zflag_;  // per (batch slot, chunk): all-zero input chunk (code-domain stages)
+    DevArray<PermSrc> psrc_;   // per (batch slot, chunk): chunk read from the payload by the first permutation pass
     DevArray<uint32_t> imnz_;  // 1 word: code domain, some imaginary-half input chunk is nonzero; FP, some group flag is 0
     DevArray<DecRow> rows_;    // per 32 scalars of work_: decode rows of a streaming first pass (fused decode)
     DevArray<uint8_t> wflag_;  // per 32 scalars of work_: group stored (1) or all zero (0), FP stages
@@ -333,6 +334,7 @@ private:
     DevArray<DecInfo> dinfo2_;
     DevArray<DecChunk> dchunk2_;
     DevArray<uint8_t> zflag2_, wflag2_;
+    DevArray<PermSrc> psrc2_;
     DevArray<uint64_t> d_place2_, d_meta2_;
     PinnedVec<uint64_t> h_place2_, h_meta2_;
     DevArray<uint64_t> ids_;

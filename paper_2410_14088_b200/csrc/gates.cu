@@ -2040,11 +2040,38 @@ __device__ __forceinline__ void apply_ent(uint32_t e, const uint2* tile_s, uint3
 
 constexpr int kPermGroups = 4;  // 4 x 4 positions per thread
 
-template <bool kLast>
+// Four consecutive code words (chunk positions s .. s + 3, s a multiple of
+// 4) of a chunk read from its payload through a PermSrc record (meta bit 12):
+// fetch the two aligned 64-bit words holding their 4 w <= 64 bits, then unpack.
+struct PayloadWords {
+    uint64_t lo, hi;
+    uint32_t sh;
+};
+__device__ __forceinline__ PayloadWords psrc_fetch(const PermSrc& r, uint32_t s) {
+    const uint32_t a = (r.meta & 63u) + s * ((r.meta >> 6) & 31u);
+    const uint64_t* p = r.cw + (a >> 6);
+    return PayloadWords{__ldg(p), __ldg(p + 1), a & 63u};
+}
+__device__ __forceinline__ uint4 psrc_unpack(const PayloadWords& f, uint32_t qb, uint32_t meta) {
+    const uint32_t w = (meta >> 6) & 31u, mask = (1u << w) - 1, ng = ((meta >> 11) & 1u) << 1;
+    const uint64_t win = (f.lo >> f.sh) | ((f.hi << 1) << (63u - f.sh));
+    uint4 o;
+    o.x = ((qb + (static_cast<uint32_t>(win) & mask)) << 2) | ng;
+    o.y = ((qb + (static_cast<uint32_t>(win >> w) & mask)) << 2) | ng;
+    o.z = ((qb + (static_cast<uint32_t>(win >> (2 * w)) & mask)) << 2) | ng;
+    o.w = ((qb + (static_cast<uint32_t>(win >> (3 * w)) & mask)) << 2) | ng;
+    return o;
+}
+
+template <bool kLast, bool kPsrc>
 __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict__ pk, uint32_t lb, uint64_t ntiles,
                                                             const __grid_constant__ PermPass pass,
                                                             ChunkPlan* __restrict__ cps, const uint8_t* __restrict__ zf,
-                                                            uint32_t nch, const uint32_t* __restrict__ imnz) {
+                                                            uint32_t nch, const uint32_t* __restrict__ imnz,
+                                                            const PermSrc* __restrict__ psrc) {
+    // kPsrc: the input chunks are described by PermSrc records (psrc; first
+    // pass of a code-domain stage): zero chunks and chunks left in the
+    // payload were not decoded to pk, the latter are read from the payload
     __shared__ __align__(16) uint2 tile_s[1 << kMaxTileBits];
     const uint32_t tid = threadIdx.x;
     const uint64_t lmask = (1ull << lb) - 1;
@@ -2057,6 +2084,11 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
     }
     const uint32_t kshift = lb >= 12 ? 12 : lb + 1;
     const uint64_t kim = lb >= 12 ? (1ull << (lb - 12)) : 0;
+    // (slot, chunk) index of a planar address: slots are 2^(lb+1) scalars and
+    // chunks 4096 (kPsrc needs lb >= 12), so it is the address >> 12
+    const auto chunk_of = [&](uint64_t addr) -> uint64_t {
+        return kPsrc ? addr >> 12 : (addr >> (lb + 1)) * nch + ((addr & ((2ull << lb) - 1)) >> 12);
+    };
     // imaginary halves all zero (and no pass swaps re / im): they stay zero,
     // and the real halves permute alone (no entry has the swap bit)
     const bool im_zero = imnz && *imnz == 0;
@@ -2067,15 +2099,40 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
         // The copies are issued unconditionally (an all-zero chunk the decoder
         // left unwritten is read stale); its flag, loaded with the copies and
         // used one tile later, has the thread overwrite its own slots with
-        // zero words once they have landed.
+        // zero words once they have landed. kPsrc: groups of chunks left in
+        // the payload fetch their payload words instead, unpacked into the
+        // buffer at the start of the tile's iteration.
+        PayloadWords pw[kPermGroups];
+        uint32_t pqb[kPermGroups], pmeta[kPermGroups];
+        uint32_t pend = 0;  // groups of the next tile held in pw
         const auto issue = [&](uint64_t base, uint32_t* dst) -> uint32_t {
             const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
             uint32_t zm = 0;
+            if constexpr (kPsrc) {
+                PermSrc r[kPermGroups];
 #pragma unroll
-            for (int g = 0; g < kPermGroups; ++g) {
-                const uint64_t addr = pb + toffp[g];
-                cp_async16(dst + 4u * tid + 1024u * g, pk + addr);
-                if (zf && zf[(addr >> (lb + 1)) * nch + ((addr & ((2ull << lb) - 1)) >> 12)]) zm |= 1u << g;
+                for (int g = 0; g < kPermGroups; ++g) r[g] = psrc[chunk_of(pb + toffp[g])];
+#pragma unroll
+                for (int g = 0; g < kPermGroups; ++g) {
+                    const uint64_t addr = pb + toffp[g];
+                    if (r[g].meta & (1u << 12)) {
+                        pw[g] = psrc_fetch(r[g], static_cast<uint32_t>(addr & 4095u));
+                        pqb[g] = r[g].qb;
+                        pmeta[g] = r[g].meta;
+                        pend |= 1u << g;
+                    } else if (r[g].meta & (1u << 13)) {
+                        zm |= 1u << g;
+                    } else {
+                        cp_async16(dst + 4u * tid + 1024u * g, pk + addr);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int g = 0; g < kPermGroups; ++g) {
+                    const uint64_t addr = pb + toffp[g];
+                    cp_async16(dst + 4u * tid + 1024u * g, pk + addr);
+                    if (zf && zf[chunk_of(addr)]) zm |= 1u << g;
+                }
             }
             cp_async_commit();
             return zm;
@@ -2083,9 +2140,24 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
         uint64_t tile = blockIdx.x;
         uint64_t base_next = tile < ntiles ? runs_deposit(tile, pass.base) : 0;
         uint32_t zcur = tile < ntiles ? issue(base_next, tile_w) : 0u;
+        // one table (no pattern bits): its entries stay in registers
+        const bool one_tab = pass.npat_bits == 0;
+        uint2 ent[kPermGroups];
+        if (one_tab) {
+#pragma unroll
+            for (int g = 0; g < kPermGroups; ++g)
+                ent[g] = __ldg(reinterpret_cast<const uint2*>(pass.table + 4u * tid + 1024u * g));
+        }
         CodeAcc4 acc;  // last pass: counters of the real halves (see PermPass::chunk_mode)
         for (uint32_t k = 0; tile < ntiles; tile += gridDim.x, ++k) {
             uint32_t* cur = tile_w + ((k & 1u) << kMaxTileBits);
+            if (kPsrc && pend) {  // this tile's payload-read groups
+#pragma unroll
+                for (int g = 0; g < kPermGroups; ++g)
+                    if ((pend >> g) & 1u)
+                        *reinterpret_cast<uint4*>(cur + 4u * tid + 1024u * g) = psrc_unpack(pw[g], pqb[g], pmeta[g]);
+                pend = 0;
+            }
             const uint64_t base = base_next;
             uint32_t znext = 0;
             if (tile + gridDim.x < ntiles) {
@@ -2095,14 +2167,15 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
                 cp_async_commit();  // (an empty group keeps the wait count uniform)
             }
             const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
-            uint32_t pat = 0;
-            for (uint32_t i = 0; i < pass.npat_bits; ++i)
-                pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
-            const uint16_t* tab = pass.table + (static_cast<uint64_t>(pat) << kMaxTileBits);
-            uint2 ent[kPermGroups];
+            if (!one_tab) {
+                uint32_t pat = 0;
+                for (uint32_t i = 0; i < pass.npat_bits; ++i)
+                    pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
+                const uint16_t* tab = pass.table + (static_cast<uint64_t>(pat) << kMaxTileBits);
 #pragma unroll
-            for (int g = 0; g < kPermGroups; ++g)
-                ent[g] = __ldg(reinterpret_cast<const uint2*>(tab + 4u * tid + 1024u * g));
+                for (int g = 0; g < kPermGroups; ++g)
+                    ent[g] = __ldg(reinterpret_cast<const uint2*>(tab + 4u * tid + 1024u * g));
+            }
             cp_async_wait<1>();  // this tile's group has landed
             if (zcur) {
 #pragma unroll
@@ -2140,19 +2213,39 @@ __global__ void __launch_bounds__(kFastThreads) k_perm_pass(uint32_t* __restrict
         const uint64_t base = runs_deposit(tile, pass.base);
         const uint64_t pb = ((base >> lb) << (lb + 1)) | (base & lmask);
         uint4 re[kPermGroups], im[kPermGroups];
+        if constexpr (kPsrc) {
+            PermSrc rr[kPermGroups], ri[kPermGroups];
 #pragma unroll
-        for (int g = 0; g < kPermGroups; ++g) {
-            const uint64_t addr = pb + toffp[g];
-            if (zf) {  // all-zero input chunks were not written: read them as zero words
-                const uint64_t slot = addr >> (lb + 1), off = addr & ((2ull << lb) - 1);
-                const uint8_t* zs = zf + slot * nch;
-                re[g] = zs[off >> 12] ? make_uint4(1u, 1u, 1u, 1u) : __ldcs(reinterpret_cast<const uint4*>(pk + addr));
-                im[g] = im_zero || zs[(off + im_off) >> 12] ? make_uint4(1u, 1u, 1u, 1u)
-                                                             : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
-                continue;
+            for (int g = 0; g < kPermGroups; ++g) {
+                rr[g] = psrc[chunk_of(pb + toffp[g])];
+                ri[g] = psrc[chunk_of(pb + toffp[g] + im_off)];
             }
-            re[g] = __ldcs(reinterpret_cast<const uint4*>(pk + addr));
-            im[g] = im_zero ? make_uint4(1u, 1u, 1u, 1u) : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
+            const auto load = [&](const PermSrc& r, uint64_t addr) -> uint4 {
+                if (r.meta & (1u << 12)) return psrc_unpack(psrc_fetch(r, static_cast<uint32_t>(addr & 4095u)), r.qb, r.meta);
+                if (r.meta & (1u << 13)) return make_uint4(1u, 1u, 1u, 1u);
+                return __ldcs(reinterpret_cast<const uint4*>(pk + addr));
+            };
+#pragma unroll
+            for (int g = 0; g < kPermGroups; ++g) {
+                const uint64_t addr = pb + toffp[g];
+                re[g] = load(rr[g], addr);
+                im[g] = im_zero ? make_uint4(1u, 1u, 1u, 1u) : load(ri[g], addr + im_off);
+            }
+        } else {
+#pragma unroll
+            for (int g = 0; g < kPermGroups; ++g) {
+                const uint64_t addr = pb + toffp[g];
+                if (zf) {  // all-zero input chunks were not written: read them as zero words
+                    const uint64_t slot = addr >> (lb + 1), off = addr & ((2ull << lb) - 1);
+                    const uint8_t* zs = zf + slot * nch;
+                    re[g] = zs[off >> 12] ? make_uint4(1u, 1u, 1u, 1u) : __ldcs(reinterpret_cast<const uint4*>(pk + addr));
+                    im[g] = im_zero || zs[(off + im_off) >> 12] ? make_uint4(1u, 1u, 1u, 1u)
+                                                                 : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
+                    continue;
+                }
+                re[g] = __ldcs(reinterpret_cast<const uint4*>(pk + addr));
+                im[g] = im_zero ? make_uint4(1u, 1u, 1u, 1u) : __ldcs(reinterpret_cast<const uint4*>(pk + addr + im_off));
+            }
         }
         uint32_t pat = 0;
         for (uint32_t i = 0; i < pass.npat_bits; ++i) pat |= static_cast<uint32_t>((base >> pass.pat_bits[i]) & 1) << i;
@@ -2206,8 +2299,10 @@ bool mono_zero_skip(const GateProgram& prog, uint32_t lb) {
 }
 
 void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
-                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag, const uint32_t* imnz) {
-    if (zflag && !mono_zero_skip(prog, lb)) raise(BMQ_ERR_LOGIC, "zero-chunk skipping needs a table first pass");
+                      uint64_t* launches, const QuantOut& quant, const uint8_t* zflag, const uint32_t* imnz,
+                      const PermSrc* psrc) {
+    if ((zflag || psrc) && !mono_zero_skip(prog, lb))
+        raise(BMQ_ERR_LOGIC, "zero-chunk skipping needs a table first pass");
     if (!prog.mono) raise(BMQ_ERR_LOGIC, "stage is not a code-domain program");
     // imaginary halves can stay untouched only if every pass is a table pass that never swaps re / im
     if (!zflag) imnz = nullptr;
@@ -2221,15 +2316,17 @@ void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, ui
         if (p.pp && lb >= 4) {  // 16-byte groups of four code words stay inside a block half
             const uint64_t g2 = std::min<uint64_t>(tiles, 148ull * 4 * 16);
             const uint8_t* zf = pi == 0 ? zflag : nullptr;
+            const PermSrc* ps = pi == 0 ? psrc : nullptr;
             PermPass pp = *p.pp;
             pp.chunk_mode = 0;
             if (lb >= 12 && !(pp.lane_bits >> 12)) pp.chunk_mode = (pp.group_bits >> 12) ? 1u : 2u;
+            const auto launch = [&](auto kern, ChunkPlan* cps) {
+                kern<<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, pp, cps, zf, quant.nch, imnz, ps);
+            };
             if (last)
-                k_perm_pass<true><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, pp, quant.cps,
-                                                                                     zf, quant.nch, imnz);
+                ps ? launch(k_perm_pass<true, true>, quant.cps) : launch(k_perm_pass<true, false>, quant.cps);
             else
-                k_perm_pass<false><<<static_cast<uint32_t>(g2), kFastThreads, 0, st>>>(pk, lb, tiles, pp, nullptr,
-                                                                                      zf, quant.nch, imnz);
+                ps ? launch(k_perm_pass<false, true>, nullptr) : launch(k_perm_pass<false, false>, nullptr);
         } else {
             k_code_pass<<<static_cast<uint32_t>(grid), kFastThreads, 0, st>>>(pk, lb, tiles, *p.mp,
                                                                               last ? quant.cps : nullptr, quant.nch);

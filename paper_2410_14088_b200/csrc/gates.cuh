@@ -246,9 +246,12 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
 // imnz (optional, with zflag): device word, 0 when every imaginary-half chunk
 // of the input is all zero (launch_decompress); if no pass swaps re / im the
 // imaginary halves then stay zero and are neither read nor written.
+// psrc (optional, with zflag): per (slot, chunk) PermSrc records (mode 1 of
+// launch_decompress); chunks with meta != 0 were not decoded and the first
+// pass reads their codes from the payload.
 bool mono_zero_skip(const GateProgram& prog, uint32_t lb);
 void run_mono_program(cudaStream_t st, const GateProgram& prog, uint32_t* pk, uint32_t lb, uint64_t nreps,
                       uint64_t* launches, const QuantOut& quant, const uint8_t* zflag = nullptr,
-                      const uint32_t* imnz = nullptr);
+                      const uint32_t* imnz = nullptr, const PermSrc* psrc = nullptr);
 
 }  // namespace bmq
