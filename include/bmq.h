@@ -128,6 +128,17 @@ typedef struct bmq_config {
 /* Plan with bmq_plan_device_aware (this device's work buffer and HBM, world
  * 1, inner_size as the cap) instead of partition_circuit(inner_size). */
 #define BMQ_FLAG_DEVICE_PLAN 0x40u
+/* Stage fusion: runs of consecutive FP stages of the plan run over the groups
+ * of the union of their inner qubits, decoded once and emitted once. Between
+ * two fused stages every amplitude is quantised and dequantised in place
+ * (v -> +-E[q(v)], zero -> 0: exactly decompress_block(compress_block(.)),
+ * whose result depends on each scalar's code only, not on the block's
+ * code_min / width), and the intermediate stage's payload sizes come from the
+ * same per-chunk counters the emit would use, so the payloads, the peak and
+ * every reported size equal the unfused run's (codec.hpp:227-344). Not used
+ * with a host level, code-domain or identity-skipped (diagonal block-wise)
+ * stages, or sharded runs. */
+#define BMQ_FLAG_STAGE_FUSION 0x80u
 
 /* cbq::SimulationReport (engine.hpp:39-53) plus device-side counters. */
 typedef struct bmq_report {
@@ -191,6 +202,8 @@ typedef struct bmq_report {
     uint64_t disk_read_bytes;       /* payload bytes read back from the disk level */
     uint64_t disk_peak_bytes;       /* high-water of live payload bytes on the disk level */
     uint64_t disk_gds;              /* 1 when the disk level moves data with GPUDirect Storage (cuFile) */
+    uint64_t fused_stages;          /* stages run inside a fused run (BMQ_FLAG_STAGE_FUSION) */
+    uint64_t fused_sets;            /* fused runs of consecutive stages */
 } bmq_report;
 
 /* ------------------------------------------------------------ host-only

@@ -32,6 +32,7 @@ BMQ_FLAG_POOL_GROW = 0x8
 BMQ_FLAG_HEAP_ARENA = 0x10
 BMQ_FLAG_BUMP_ARENA = 0x20
 BMQ_FLAG_DEVICE_PLAN = 0x40
+BMQ_FLAG_STAGE_FUSION = 0x80
 
 
 class bmq_gate(C.Structure):
@@ -86,7 +87,7 @@ class bmq_report(C.Structure):
                 ("compact_bytes", C.c_uint64), ("host_peak_bytes", C.c_uint64), ("arena_bytes", C.c_uint64),
                 ("fused_decode_batches", C.c_uint64), ("stream_passes", C.c_uint64),
                 ("disk_spill_bytes", C.c_uint64), ("disk_read_bytes", C.c_uint64), ("disk_peak_bytes", C.c_uint64),
-                ("disk_gds", C.c_uint64)]
+                ("disk_gds", C.c_uint64), ("fused_stages", C.c_uint64), ("fused_sets", C.c_uint64)]
 
 
 _P = C.c_void_p

@@ -612,6 +612,7 @@ class Config:
     arena: str = "auto"  # device arena placement: "auto", "heap" (extent per payload) or "bump" (cursor + compaction)
     host_pool_bytes: int = 0
     device_plan: bool = False  # plan with plan_device_aware (inner_size = cap) instead of partition_circuit
+    fuse_stages: bool = False  # BMQ_FLAG_STAGE_FUSION: consecutive FP stages decoded / emitted once
     disk_pool_bytes: int = 0   # third level: spill file beneath the host level (needs host_pool_bytes)
     disk_dir: str = ""         # directory of the spill file ("" = /tmp)
 
@@ -631,6 +632,7 @@ class Config:
                   (_lib.BMQ_FLAG_CODE_DOMAIN if self.code_domain else 0) | \
                   (_lib.BMQ_FLAG_POOL_GROW if self.pool_grow else 0) | \
                   (_lib.BMQ_FLAG_DEVICE_PLAN if self.device_plan else 0) | \
+                  (_lib.BMQ_FLAG_STAGE_FUSION if self.fuse_stages else 0) | \
                   {"auto": 0, "heap": _lib.BMQ_FLAG_HEAP_ARENA, "bump": _lib.BMQ_FLAG_BUMP_ARENA}[self.arena]
         return c
 
@@ -700,7 +702,8 @@ DEVICE_REPORT_KEYS = ("device_ms", "groups_processed", "groups_skipped", "blocks
                       "lazy_cx", "perm_materialisations",
                       "model_bytes", "model_groups", "link_h2d_bytes", "link_d2h_bytes", "link_ms",
                       "compact_bytes", "host_peak_bytes", "arena_bytes", "fused_decode_batches", "stream_passes",
-                      "disk_spill_bytes", "disk_read_bytes", "disk_peak_bytes", "disk_gds")
+                      "disk_spill_bytes", "disk_read_bytes", "disk_peak_bytes", "disk_gds",
+                      "fused_stages", "fused_sets")
 
 
 def report_from_c(r: bmq_report, stage_ms: list) -> SimulationReport:

@@ -183,6 +183,26 @@ __global__ void k_plan_sizes(const BlockPlan* __restrict__ bps, uint64_t n, uint
     if (i < n) out[i] = (bps[i].flags & 1) ? ~0ull : bps[i].size;
 }
 
+// Stage fusion: the intermediate stage's packed code words back to doubles,
+// +-E[q] or +0 — decompress_block(compress_block(.)) scalar by scalar
+// (codec.hpp:333-342), which depends on each scalar's code only.
+__global__ void k_round(const uint4* __restrict__ pk, double2* __restrict__ out, uint64_t nquads,
+                        const double* __restrict__ dequant) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nquads;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint4 w = __ldcs(pk + i);
+        const uint32_t c[4] = {w.x, w.y, w.z, w.w};
+        double v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const double m = (c[e] & 1u) ? 0.0 : __ldg(dequant + (c[e] >> 2));
+            v[e] = (c[e] & 3u) == 2u ? -m : m;
+        }
+        __stcs(out + 2 * i, make_double2(v[0], v[1]));
+        __stcs(out + 2 * i + 1, make_double2(v[2], v[3]));
+    }
+}
+
 // place[2i]: the payload's device address (arena or write-back staging),
 // place[2i + 1]: its metadata offset (arena offset, or host extent | tag)
 __global__ void k_place(BlockPlan* __restrict__ bps, const CmpBlock* __restrict__ blks, uint64_t n,
@@ -1498,6 +1518,204 @@ void Engine::run_stage(uint64_t s) {
     stage_decompress_calls_ += nid;
 }
 
+// ------------------------------------------------------------ stage fusion
+// A stage joins a fused run when it is an FP stage the engine would run on
+// the whole working set (not on codes, not block-wise): its programs are
+// rebuilt over the union layout, where the same gates act on the same
+// amplitudes in the same order (buffer bits are a relabelling).
+bool Engine::fusable(uint64_t s) const {
+    const StagePlan& sp = *stage_plans_[s];
+    const bool skip_zero = cfg_.flags & BMQ_FLAG_ZERO_GROUP_SKIP;
+    const bool codes = sp.prog.mono && identity_ok_ && (cfg_.flags & BMQ_FLAG_CODE_DOMAIN);
+    const bool blockwise = sp.diag_only && identity_ok_ && skip_zero && (cfg_.flags & BMQ_FLAG_IDENTITY_SKIP);
+    return !codes && !blockwise && !sp.prog.passes.empty();
+}
+
+void Engine::plan_fusion() {
+    fusion_planned_ = true;
+    fused_at_.assign(plan_.size(), -1);
+    if (!(cfg_.flags & BMQ_FLAG_STAGE_FUSION) || !cfg_.compress || sharded() || cfg_.host_pool_bytes || L_.b < 12)
+        return;
+    // union inner sets up to 2^10 blocks per group and within one batch
+    uint32_t kcap = 10;
+    while (kcap > 0 && (1ull << kcap) > max_blocks_) --kcap;
+    for (uint64_t s = 0; s < plan_.size();) {
+        if (!fusable(s)) {
+            ++s;
+            continue;
+        }
+        uint64_t mask = 0, e = s;
+        for (; e < plan_.size() && fusable(e); ++e) {
+            uint64_t m = mask;
+            for (uint32_t i = 0; i < plan_[e].inner_count; ++i) m |= 1ull << plan_[e].inner[i];
+            if (static_cast<uint32_t>(__builtin_popcountll(m)) > kcap) break;
+            mask = m;
+        }
+        if (e - s < 2) {
+            s = std::max(e, s + 1);
+            continue;
+        }
+        auto fs = std::make_unique<FusedSet>();
+        fs->s0 = s;
+        fs->s1 = e;
+        bmq_stage U{};
+        U.gate_begin = plan_[s].gate_begin;
+        U.gate_end = plan_[e - 1].gate_end;
+        for (uint32_t q = 0; q < 64; ++q)
+            if (mask >> q & 1) U.inner[U.inner_count++] = q;
+        fs->gg = group_geometry(L_, U);
+        for (uint64_t j = s; j < e; ++j) {
+            std::vector<GateOp> ops;
+            for (uint64_t i = plan_[j].gate_begin; i < plan_[j].gate_end; ++i) {
+                const bmq_gate& g = gates_[i];
+                const bool two = gate_is_two_qubit(g.kind);
+                ops.push_back(make_op(g, buffer_bit(L_, U, g.q0), two ? buffer_bit(L_, U, g.q1) : 0));
+            }
+            auto prog = std::make_unique<GateProgram>();
+            build_program(*prog, std::move(ops), L_.b + U.inner_count);
+            fs->progs.push_back(std::move(prog));
+        }
+        fused_at_[s] = static_cast<int64_t>(fused_sets_.size());
+        fused_sets_.push_back(std::move(fs));
+        s = e;
+    }
+    uint64_t nfs = 0;
+    for (const auto& fs : fused_sets_) nfs = std::max<uint64_t>(nfs, fs->s1 - fs->s0 - 1);
+    if (nfs) fsz_.alloc(nfs * max_blocks_);
+}
+
+// Stages [fs.s0, fs.s1) over the union groups: one decode, the stages'
+// programs in order with the quantiser round trip between them (the last
+// pass's codes -> k_round), one emit; the intermediate stages' payload sizes
+// (k_cmp_plan on the same counters the emit would use) are replayed into the
+// store model in the reference's put order of each stage.
+void Engine::run_fused(const FusedSet& fs) {
+    use_set(0);
+    const GroupGeometry& gg = fs.gg;
+    const uint64_t per = gg.per_group(), ngroups = gg.groups(), nid = L_.num_blocks();
+    const uint64_t m = fs.s1 - fs.s0;
+    const bool skip_zero = cfg_.flags & BMQ_FLAG_ZERO_GROUP_SKIP;
+    std::vector<uint64_t> inner(per);
+    for (uint64_t v = 0; v < per; ++v) inner[v] = deposit_bits(v, gg.inner_mask);
+    std::vector<uint64_t> work_ids;
+    work_ids.reserve(nid);
+    uint64_t o = 0;
+    for (uint64_t g = 0; g < ngroups; ++g) {
+        bool nonzero = !skip_zero;
+        for (uint64_t v = 0; v < per && !nonzero; ++v) nonzero = h_off_[o | inner[v]] != ~0ull;
+        if (nonzero)
+            for (uint64_t v = 0; v < per; ++v) work_ids.push_back(o | inner[v]);
+        o = ((o | ~gg.outer_mask) + 1) & gg.outer_mask;
+    }
+    const uint64_t nwork = work_ids.size();
+    // sizes after each stage of the run (the last one is h_size_ after the emit)
+    std::vector<std::vector<uint64_t>> sizes(m);
+    sizes[0].assign(h_size_.data(), h_size_.data() + nid);  // before the run
+    uint64_t rd = 0;
+    for (uint64_t id : work_ids) rd += h_off_[id] == ~0ull ? 0 : h_size_[id];
+    std::vector<std::vector<uint64_t>> after(m - 1, sizes[0]);
+    size_t nbatches = 0;
+    if (nwork) {
+        BMQ_CUDA(cudaMemcpyAsync(ids_.p, work_ids.data(), nwork * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
+        const uint64_t batch_blocks = std::max<uint64_t>(1, max_blocks_ / per) * per;
+        const uint64_t count = 2ull << L_.b;
+        std::vector<uint64_t> hsz((m - 1) * max_blocks_);
+        for (uint64_t b0 = 0; b0 < nwork; b0 += batch_blocks, ++nbatches) {
+            const uint64_t nblk = std::min(batch_blocks, nwork - b0);
+            phase_event(4 * nbatches);
+            k_build_desc<<<grid_for(nblk), 256, 0, st_>>>(ids_.p + b0, nblk, off_.p, size_.p, arena_.base(), host_pool_,
+                                                          zero_hdr_.p, work_.p, pk_.p, L_.b, dec_.p, cmp_.p, 0);
+            ++counters_.kernel_launches;
+            launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
+                              &counters_.kernel_launches, 0);
+            phase_event(4 * nbatches + 1);
+            const QuantOut qo{pk_.p, cplan_.p, nch_, *tabs_, err_.p};
+            for (uint64_t j = 0; j < m; ++j) {
+                const GateProgram& prog = *fs.progs[j];
+                BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
+                const bool fused = run_program(st_, prog, work_.p, L_.b, false, nblk / per, &counters_.kernel_launches,
+                                               &qo, nullptr, nblk, nullptr, nch_, nullptr, nullptr);
+                if (j + 1 == m) phase_event(4 * nbatches + 2);
+                launch_compress_plan(st_, cmp_.p, nblk, nch_, *tabs_, bplan_.p, cplan_.p, fused, err_.p,
+                                     &counters_.kernel_launches);
+                if (fused) ++counters_.fused_batches;
+                counters_.lazy_cx += prog.lazy_cx;
+                counters_.perm_materialisations += prog.perms;
+                counters_.gate_passes += prog.passes.size();
+                for (const GatePass& gp : prog.passes) counters_.stream_passes += gp.sp && !stream_off() ? 1 : 0;
+                if (j + 1 == m) break;
+                k_plan_sizes<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, nblk, fsz_.p + j * max_blocks_);
+                const uint64_t nquads = nblk * count / 4;
+                k_round<<<static_cast<uint32_t>(std::min<uint64_t>((nquads + 255) / 256, 148ull * 16)), 256, 0, st_>>>(
+                    reinterpret_cast<const uint4*>(pk_.p), reinterpret_cast<double2*>(work_.p), nquads, tabs_->dequant);
+                counters_.kernel_launches += 2;
+            }
+            if (m > 1) {
+                BMQ_CUDA(cudaMemcpy2DAsync(hsz.data(), nblk * sizeof(uint64_t), fsz_.p, max_blocks_ * sizeof(uint64_t),
+                                           nblk * sizeof(uint64_t), m - 1, cudaMemcpyDeviceToHost, st_));
+            }
+            emit_batch(nblk, work_ids.data() + b0);
+            phase_event(4 * nbatches + 3);
+            BMQ_CUDA(cudaStreamSynchronize(st_));
+            for (uint64_t j = 0; j + 1 < m; ++j)
+                for (uint64_t i = 0; i < nblk; ++i) {
+                    const uint64_t v = hsz[j * nblk + i];
+                    after[j][work_ids[b0 + i]] = v == ~0ull ? kHeaderBytes : v;
+                }
+        }
+    }
+    check_device_error(("stages " + std::to_string(fs.s0) + ".." + std::to_string(fs.s1 - 1) + ": ").c_str());
+    sync_copies();
+    sync_meta_to_host();
+    collect_phase_times(nbatches);
+    uint64_t wr = 0;
+    for (uint64_t id : work_ids) wr += h_off_[id] == ~0ull ? 0 : h_size_[id];
+    // per stage: the store model's puts and the SURVEY 8(d) model bytes, each
+    // in that stage's own grouping
+    for (uint64_t j = 0; j < m; ++j) {
+        const uint64_t s = fs.s0 + j;
+        const uint64_t* before = j == 0 ? sizes[0].data() : after[j - 1].data();
+        const uint64_t* now = j + 1 == m ? h_size_.data() : after[j].data();
+        account_stage(s, now);
+        const GroupGeometry& sg = stage_plans_[s]->gg;
+        const uint64_t sper = sg.per_group();
+        std::vector<uint64_t> sin(sper);
+        for (uint64_t v = 0; v < sper; ++v) sin[v] = deposit_bits(v, sg.inner_mask);
+        uint64_t so = 0, mb = 0, mg = 0;
+        for (uint64_t g = 0; g < sg.groups(); ++g) {
+            bool nz = false;
+            for (uint64_t v = 0; v < sper && !nz; ++v) nz = before[so | sin[v]] > kHeaderBytes;
+            if (nz) {
+                for (uint64_t v = 0; v < sper; ++v) mb += before[so | sin[v]] + now[so | sin[v]];
+                ++mg;
+            }
+            so = ((so | ~sg.outer_mask) + 1) & sg.outer_mask;
+        }
+        counters_.model_bytes += mb + mg * sper * (32ull << L_.b);
+        counters_.model_groups += mg;
+        counters_.groups_processed += nwork / sper;
+        counters_.groups_skipped += sg.groups() - nwork / sper;
+        stage_compress_calls_ += nid;
+        stage_decompress_calls_ += nid;
+    }
+    // implementation bytes: one decode and one emit for the run, every
+    // stage's passes, and a round trip (8 B of codes in, 16 B out) per
+    // amplitude between stages
+    const uint64_t half_dense = nwork * (16ull << L_.b), pk_bytes = nwork * (8ull << L_.b);
+    counters_.payload_bytes_read += rd;
+    counters_.payload_bytes_written += wr;
+    counters_.decompress_bytes += rd + half_dense;
+    for (uint64_t j = 0; j < m; ++j)
+        counters_.gate_bytes += 2 * half_dense * (fs.progs[j]->passes.size() - 1) + half_dense + pk_bytes +
+                                (j + 1 < m ? pk_bytes + half_dense : 0);
+    counters_.compress_bytes += pk_bytes + wr;
+    for (uint64_t id : work_ids) sums_ok_[id] = 0;
+    counters_.blocks_processed += nwork * m;
+    counters_.dense_bytes += nwork * m * (32ull << L_.b);
+    counters_.fused_stages += m;
+    counters_.fused_sets += 1;
+}
+
 void Engine::run_stages(uint64_t first, uint64_t last) {
     BMQ_CUDA(cudaSetDevice(dev_));
     ensure_init();
@@ -1516,8 +1734,19 @@ void Engine::run(bmq_report* rep, double* stage_ms, uint64_t stage_cap) {
     ensure_init();
     counters_ = bmq_report{};
     BMQ_CUDA(cudaEventRecord(ev0_, st_));
+    if (!fusion_planned_) plan_fusion();
     for (uint64_t s = next_stage_; s < plan_.size(); ++s) {
         const double ts = now_ms();
+        const int64_t f = cfg_.compress ? fused_at_[s] : -1;
+        if (f >= 0) {  // a fused run: its time goes to its first stage
+            const FusedSet& fs = *fused_sets_[f];
+            run_fused(fs);
+            for (uint64_t j = fs.s0; j < fs.s1; ++j)
+                if (stage_ms && j < stage_cap) stage_ms[j] = j == s ? now_ms() - ts : 0.0;
+            next_stage_ = fs.s1;
+            s = fs.s1 - 1;
+            continue;
+        }
         run_stage(s);
         next_stage_ = s + 1;
         if (stage_ms && s < stage_cap) stage_ms[s] = now_ms() - ts;
@@ -1585,6 +1814,8 @@ void Engine::report(bmq_report* rep, double device_ms) {
     r.disk_read_bytes = counters_.disk_read_bytes;
     r.disk_peak_bytes = disk_.is_open() ? disk_.heap().high_water() : 0;
     r.disk_gds = disk_.gds() ? 1 : 0;
+    r.fused_stages = counters_.fused_stages;
+    r.fused_sets = counters_.fused_sets;
     *rep = r;
 }
 

@@ -117,6 +117,14 @@ struct StagePlan {
     std::vector<uint8_t> touched;  // diag_only: inner value v -> some gate acts on the block
 };
 
+// BMQ_FLAG_STAGE_FUSION: stages [s0, s1) run over the groups of the union of
+// their inner qubits; progs[j] is stage s0 + j's program on that layout.
+struct FusedSet {
+    uint64_t s0 = 0, s1 = 0;
+    GroupGeometry gg;
+    std::vector<std::unique_ptr<GateProgram>> progs;
+};
+
 class Engine {
 public:
     Engine(uint32_t n, const bmq_gate* gates, uint64_t ngates, const bmq_config& cfg);
@@ -189,6 +197,13 @@ private:
 
     void ensure_init();
     void run_stage(uint64_t s);
+    // stage fusion (BMQ_FLAG_STAGE_FUSION)
+    bool fusable(uint64_t s) const;
+    void plan_fusion();
+    void run_fused(const FusedSet& fs);
+    bool fusion_planned_ = false;
+    std::vector<std::unique_ptr<FusedSet>> fused_sets_;
+    std::vector<int64_t> fused_at_;  // stage -> index of the fused set starting there, else -1
     void raw_run_stage(uint64_t s);
     // Batches alternate between two buffer sets and two streams: the front
     // of batch k+1 (descriptors, decode, gate passes, plan) is queued before
@@ -338,6 +353,7 @@ private:
     DevArray<uint64_t> d_place2_, d_meta2_;
     PinnedVec<uint64_t> h_place2_, h_meta2_;
     DevArray<uint64_t> ids_;
+    DevArray<uint64_t> fsz_;  // stage fusion: payload sizes of the intermediate stages of a batch
     DevArray<uint32_t> vtab_;
     DevArray<DevError> err_;
     DevArray<double> red_;

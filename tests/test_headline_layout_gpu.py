@@ -43,11 +43,11 @@ def circuit_of(gpu, case):
 
 
 @pytest.mark.parametrize("case", cases(), ids=lambda c: "missing" if c is None else f"{c['name']}{c['n']}-b{c['b']}-i{c['inner']}-{c['error_bound']}")
-@pytest.mark.parametrize("identity_skip", [True, False], ids=["skip", "noskip"])
-def test_b20_matches_reference(gpu, port, case, identity_skip):
+@pytest.mark.parametrize("mode", ["skip", "noskip", "fuse"])
+def test_b20_matches_reference(gpu, port, case, mode):
     c = circuit_of(gpu, case)
     cfg = gpu.Config(block_bits=case["b"], inner_size=case["inner"], error_bound=case["error_bound"],
-                     identity_skip=identity_skip)
+                     identity_skip=mode != "noskip", fuse_stages=mode == "fuse")
     with gpu.Simulator(c, cfg) as sim:
         rep = sim.run()
         want = case["report"]
