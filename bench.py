@@ -466,6 +466,7 @@ def main_sharded_capi(args, world, rank, local, dist, circ, cfg):
         "config": {"workload": workload_tag(w), "stages": stages,
                    "parallelism": f"shard{world} (device qubits; C ABI driver, NCCL payload remaps)",
                    "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
+                   "stage_fusion": "off (sharded runs)",
                    "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},
         "sim_time_s": t_dev / 1e3, "compression_ratio": rep.compression_ratio,
         "max_footprint_bytes": rep.max_footprint_bytes, "fidelity": fidelity, "final_norm": rep.final_norm,
@@ -579,7 +580,8 @@ def e2e_once(args):
     from paper_2410_14088_b200 import _lib, cbq
     w = WORKLOAD
     circ = cbq.generate_benchmark(w["name"], w["n"], cbq.BenchmarkParams(layers=w["layers"]))
-    cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"])
+    cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"],
+                     fuse_stages=args.fuse_stages)
     gates = circ.c_array()
     ccfg = cfg.to_c()
     lib = _lib.lib
@@ -602,7 +604,7 @@ def cold_first_call(args):
     cmd = [sys.executable, os.path.abspath(__file__), "--e2e-once", "--workload", WORKLOAD["name"],
            "--qubits", str(WORKLOAD["n"]), "--block-bits", str(WORKLOAD["b"]), "--inner-size",
            str(WORKLOAD["inner"]), "--error-bound", repr(WORKLOAD["error_bound"]), "--layers",
-           str(WORKLOAD["layers"])]
+           str(WORKLOAD["layers"])] + ([] if args.fuse_stages else ["--no-fuse-stages"])
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
                            env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0")))
@@ -653,6 +655,9 @@ def main():
                     help="disk level beneath the host level (spill file, GiB); 0 = none")
     ap.add_argument("--device-plan", action="store_true",
                     help="plan with bmq_plan_device_aware (inner size chosen for the device, --inner-size caps it)")
+    ap.add_argument("--no-fuse-stages", dest="fuse_stages", action="store_false",
+                    help="turn off BMQ_FLAG_STAGE_FUSION (runs of consecutive FP stages decoded / emitted once; "
+                         "same payloads)")
     ap.add_argument("--py-shard", action="store_true",
                     help="N>1: the Python sharded driver (shard.py over torch.distributed) instead of the C ABI one")
     ap.add_argument("--e2e-once", action="store_true", help=argparse.SUPPRESS)
@@ -689,7 +694,8 @@ def main():
     cfg = cbq.Config(block_bits=w["b"], inner_size=w["inner"], error_bound=w["error_bound"], device=local,
                      identity_skip=not args.no_identity_skip, device_pool_bytes=int(args.device_pool_gib * 2**30),
                      host_pool_bytes=int(args.host_pool_gib * 2**30), arena=args.arena,
-                     disk_pool_bytes=int(args.disk_pool_gib * 2**30), device_plan=args.device_plan)
+                     disk_pool_bytes=int(args.disk_pool_gib * 2**30), device_plan=args.device_plan,
+                     fuse_stages=args.fuse_stages)
     sim = cbq.Simulator(circ, cfg)
     plan = sim.plan().stages
     stages = len(plan)
@@ -735,6 +741,8 @@ def main():
                    "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "zero_group_skip": True, "identity_skip": not args.no_identity_skip,
                    "device_pool": f"{args.device_pool_gib:g} GiB fixed" if args.device_pool_gib else "automatic",
+                   "stage_fusion": (f"{rep.device['fused_stages']} stages in {rep.device['fused_sets']} fused runs"
+                                    if args.fuse_stages else "off"),
                    "host_pool_gib": args.host_pool_gib, "arena": args.arena,
                    "l2": "working set (16 GiB batches) >> 126 MB L2; no flush needed"},
         "sim_time_s": t_dev / 1e3, "wall_ms_median": statistics.median(wall_ms),

@@ -386,6 +386,7 @@ struct Config {  // engine.hpp:23-37 (+ device knobs)
     bool zero_group_skip = true;
     bool code_domain = true;
     bool pool_grow = false;
+    bool fuse_stages = true;  // BMQ_FLAG_STAGE_FUSION (same payloads, fewer codec trips)
     enum class Arena { Auto, Heap, Bump } arena = Arena::Auto;  // device arena placement (BMQ_FLAG_*_ARENA)
     std::uint64_t device_pool_bytes = 0;  // 0 = automatic
     std::uint64_t work_bytes = 0;         // 0 = automatic
@@ -410,7 +411,8 @@ struct Config {  // engine.hpp:23-37 (+ device knobs)
         k.disk_dir = disk_dir.empty() ? nullptr : disk_dir.c_str();
         k.flags = (zero_group_skip ? BMQ_FLAG_ZERO_GROUP_SKIP : 0u) | (identity_skip ? BMQ_FLAG_IDENTITY_SKIP : 0u) |
                   (code_domain ? BMQ_FLAG_CODE_DOMAIN : 0u) | (pool_grow ? BMQ_FLAG_POOL_GROW : 0u) |
-                  (arena == Arena::Heap ? BMQ_FLAG_HEAP_ARENA : 0u) | (arena == Arena::Bump ? BMQ_FLAG_BUMP_ARENA : 0u);
+                  (arena == Arena::Heap ? BMQ_FLAG_HEAP_ARENA : 0u) | (arena == Arena::Bump ? BMQ_FLAG_BUMP_ARENA : 0u) |
+                  (fuse_stages ? BMQ_FLAG_STAGE_FUSION : 0u);
         return k;
     }
 };

@@ -612,7 +612,7 @@ class Config:
     arena: str = "auto"  # device arena placement: "auto", "heap" (extent per payload) or "bump" (cursor + compaction)
     host_pool_bytes: int = 0
     device_plan: bool = False  # plan with plan_device_aware (inner_size = cap) instead of partition_circuit
-    fuse_stages: bool = False  # BMQ_FLAG_STAGE_FUSION: consecutive FP stages decoded / emitted once
+    fuse_stages: bool = True  # BMQ_FLAG_STAGE_FUSION: consecutive FP stages decoded / emitted once
     disk_pool_bytes: int = 0   # third level: spill file beneath the host level (needs host_pool_bytes)
     disk_dir: str = ""         # directory of the spill file ("" = /tmp)
 

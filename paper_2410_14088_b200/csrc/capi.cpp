@@ -251,7 +251,7 @@ void bmq_config_default(bmq_config* cfg) {
     cfg->compress = 1;
     cfg->verify_cap_qubits = 24;
     cfg->device = 0;
-    cfg->flags = BMQ_FLAG_ZERO_GROUP_SKIP | BMQ_FLAG_CODE_DOMAIN;
+    cfg->flags = BMQ_FLAG_ZERO_GROUP_SKIP | BMQ_FLAG_CODE_DOMAIN | BMQ_FLAG_STAGE_FUSION;
 }
 
 int bmq_simulator_create(uint32_t num_qubits, const bmq_gate* gates, uint64_t ngates, const bmq_config* cfg,

@@ -1536,8 +1536,14 @@ void Engine::plan_fusion() {
     fused_at_.assign(plan_.size(), -1);
     if (!(cfg_.flags & BMQ_FLAG_STAGE_FUSION) || !cfg_.compress || sharded() || cfg_.host_pool_bytes || L_.b < 12)
         return;
-    // union inner sets up to 2^10 blocks per group and within one batch
-    uint32_t kcap = 10;
+    // union inner sets of at most kcap qubits (BMQ_FUSE_INNER, default 8):
+    // groups of up to 2^kcap blocks, within one batch; small enough that
+    // all-zero union groups of sparse states are still skipped
+    static const uint32_t fuse_inner = [] {
+        const char* e = getenv("BMQ_FUSE_INNER");
+        return e ? static_cast<uint32_t>(std::max(2, std::min(16, atoi(e)))) : 8u;
+    }();
+    uint32_t kcap = fuse_inner;
     while (kcap > 0 && (1ull << kcap) > max_blocks_) --kcap;
     for (uint64_t s = 0; s < plan_.size();) {
         if (!fusable(s)) {
@@ -1629,9 +1635,14 @@ void Engine::run_fused(const FusedSet& fs) {
             launch_decompress(st_, dec_.p, nblk, nch_, *tabs_, dinfo_.p, dchunk_.p, true, false, err_.p,
                               &counters_.kernel_launches, 0);
             phase_event(4 * nbatches + 1);
-            const QuantOut qo{pk_.p, cplan_.p, nch_, *tabs_, err_.p};
             for (uint64_t j = 0; j < m; ++j) {
                 const GateProgram& prog = *fs.progs[j];
+                // between stages a streaming last pass writes the dequantised
+                // values straight back (no code words, no k_round)
+                static const bool kround = getenv("BMQ_DBG_FUSE_KROUND") != nullptr;  // A/B: codes + k_round always
+                const bool rnd = j + 1 < m && !kround && last_pass_streams(prog, L_.b);
+                QuantOut qo{pk_.p, cplan_.p, nch_, *tabs_, err_.p};
+                qo.rnd = rnd ? work_.p : nullptr;
                 BMQ_CUDA(cudaMemsetAsync(cplan_.p, 0, nblk * nch_ * sizeof(ChunkPlan), st_));
                 const bool fused = run_program(st_, prog, work_.p, L_.b, false, nblk / per, &counters_.kernel_launches,
                                                &qo, nullptr, nblk, nullptr, nch_, nullptr, nullptr);
@@ -1645,10 +1656,12 @@ void Engine::run_fused(const FusedSet& fs) {
                 for (const GatePass& gp : prog.passes) counters_.stream_passes += gp.sp && !stream_off() ? 1 : 0;
                 if (j + 1 == m) break;
                 k_plan_sizes<<<grid_for(nblk), 256, 0, st_>>>(bplan_.p, nblk, fsz_.p + j * max_blocks_);
+                ++counters_.kernel_launches;
+                if (rnd && fused) continue;
                 const uint64_t nquads = nblk * count / 4;
                 k_round<<<static_cast<uint32_t>(std::min<uint64_t>((nquads + 255) / 256, 148ull * 16)), 256, 0, st_>>>(
                     reinterpret_cast<const uint4*>(pk_.p), reinterpret_cast<double2*>(work_.p), nquads, tabs_->dequant);
-                counters_.kernel_launches += 2;
+                ++counters_.kernel_launches;
             }
             if (m > 1) {
                 BMQ_CUDA(cudaMemcpy2DAsync(hsz.data(), nblk * sizeof(uint64_t), fsz_.p, max_blocks_ * sizeof(uint64_t),
@@ -1699,15 +1712,17 @@ void Engine::run_fused(const FusedSet& fs) {
         stage_decompress_calls_ += nid;
     }
     // implementation bytes: one decode and one emit for the run, every
-    // stage's passes, and a round trip (8 B of codes in, 16 B out) per
-    // amplitude between stages
+    // stage's passes; between stages either a streaming last pass writing
+    // doubles (16 B) or code words plus k_round (8 B out, 8 B in, 16 B out)
     const uint64_t half_dense = nwork * (16ull << L_.b), pk_bytes = nwork * (8ull << L_.b);
     counters_.payload_bytes_read += rd;
     counters_.payload_bytes_written += wr;
     counters_.decompress_bytes += rd + half_dense;
     for (uint64_t j = 0; j < m; ++j)
-        counters_.gate_bytes += 2 * half_dense * (fs.progs[j]->passes.size() - 1) + half_dense + pk_bytes +
-                                (j + 1 < m ? pk_bytes + half_dense : 0);
+        counters_.gate_bytes += 2 * half_dense * (fs.progs[j]->passes.size() - 1) + half_dense +
+                                (j + 1 == m ? pk_bytes
+                                            : (last_pass_streams(*fs.progs[j], L_.b) ? half_dense
+                                                                                       : 2 * pk_bytes + half_dense));
     counters_.compress_bytes += pk_bytes + wr;
     for (uint64_t id : work_ids) sums_ok_[id] = 0;
     counters_.blocks_processed += nwork * m;

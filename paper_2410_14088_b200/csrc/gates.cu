@@ -1697,11 +1697,21 @@ __global__ void __launch_bounds__(kStreamThreads, (kQuant && !kSame) ? 2 : 3) k_
                     pk[2 * r + 1] = quantize_pack_fast(a[r].im, q.t, qlo_d, span, bad, oow);
                 }
             }
+            if (q.rnd) {  // round trip in place (stage fusion), counters below as for codes
+#pragma unroll
+                for (int k = 0; k < 2 * kNV; ++k) {
+                    const uint32_t w = pk[k];
+                    const double m = (w & 1u) ? 0.0 : __ldg(q.t.dequant + (w >> 2));
+                    q.rnd[pb + pdep[k >> 1] + lane + ((k & 1) ? im_off : 0)] = (w & 3u) == 2u ? -m : m;
+                }
+            }
 #pragma unroll
             for (int r = 0; r < kNV; ++r) {
                 const uint64_t p = pb + pdep[r] + lane;
-                __stcs(q.pk + p, pk[2 * r]);
-                __stcs(q.pk + p + im_off, pk[2 * r + 1]);
+                if (!q.rnd) {
+                    __stcs(q.pk + p, pk[2 * r]);
+                    __stcs(q.pk + p + im_off, pk[2 * r + 1]);
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t w = pk[2 * r + h];
@@ -2361,6 +2371,10 @@ bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved) {
     for (const GatePass& p : prog.passes)
         if (!p.fast) return false;
     return true;
+}
+
+bool last_pass_streams(const GateProgram& prog, uint32_t lb) {
+    return !prog.passes.empty() && prog.passes.back().fast && prog.passes.back().sp && lb >= 12 && !stream_off();
 }
 
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,

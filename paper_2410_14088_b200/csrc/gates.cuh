@@ -202,6 +202,10 @@ struct QuantOut {
     uint32_t nch;      // chunks per block
     DevTables t;
     DevError* err;
+    // stage fusion: the streaming pass stores each quantised scalar back as
+    // its dequantised value (+-E[q], zero -> +0) at the same planar index of
+    // rnd instead of its code word in pk (counters as usual)
+    double* rnd = nullptr;
 };
 
 // First pass decodes its input rows itself (mode 3 of launch_decompress):
@@ -233,6 +237,9 @@ bool stream_off();  // BMQ_DBG_NO_STREAM
 // maintains them. nch is unused. wz (with zflag): device word, nonzero when
 // some flag may be 0; launch_decompress and the passes set it.
 bool program_zero_skip(const GateProgram& prog, uint32_t lb, bool interleaved);
+// The program's last pass runs as a (quantising) streaming pass on a
+// planar buffer of 2^lb-amplitude blocks, so QuantOut::rnd applies to it.
+bool last_pass_streams(const GateProgram& prog, uint32_t lb);
 bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t lb, bool interleaved,
                  uint64_t nreps, uint64_t* launches, const QuantOut* quant = nullptr,
                  const uint32_t* vtab = nullptr, uint64_t nblocks = 0, const uint8_t* zflag = nullptr,

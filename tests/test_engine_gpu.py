@@ -139,7 +139,7 @@ def test_arena_compaction_is_exact(gpu, port):
     biggest = max(len(p) for p in want.payloads)
     pool = 24 * (biggest + 16)  # the live state plus about two batches
     with gpu.Simulator(c, gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=pool, arena="bump",
-                                     work_bytes=4 * (16 << 12))) as sim:
+                                     work_bytes=4 * (16 << 12), fuse_stages=False)) as sim:
         rep = sim.run()
         assert rep.device["compactions"] > 0
         assert sim.payloads() == want.payloads
@@ -203,7 +203,7 @@ def test_in_place_compaction_keeps_live_payloads(gpu, port):
     state = sum((len(p) + 15) // 16 * 16 for p in want.payloads)
     biggest = max(len(p) for p in want.payloads)
     cfg = gpu.Config(block_bits=12, inner_size=2, device_pool_bytes=state + 5 * (biggest + 16),
-                     work_bytes=4 * (16 << 12), arena="bump")
+                     work_bytes=4 * (16 << 12), arena="bump", fuse_stages=False)
     with gpu.Simulator(c, cfg) as sim:
         rep = sim.run()
         assert rep.device["compactions"] >= rep.stage_count

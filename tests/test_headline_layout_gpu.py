@@ -47,7 +47,7 @@ def circuit_of(gpu, case):
 def test_b20_matches_reference(gpu, port, case, mode):
     c = circuit_of(gpu, case)
     cfg = gpu.Config(block_bits=case["b"], inner_size=case["inner"], error_bound=case["error_bound"],
-                     identity_skip=mode != "noskip", fuse_stages=mode == "fuse")
+                     identity_skip=mode != "noskip", fuse_stages=mode != "skip")
     with gpu.Simulator(c, cfg) as sim:
         rep = sim.run()
         want = case["report"]
