@@ -1446,7 +1446,9 @@ __device__ __forceinline__ C2 shfl_c2(C2 a, uint32_t m) {
 
 // kSame: every register row of a unit lies in the unit's 4096-scalar chunk
 // (the register bits are below bit 12), so one accumulator pair serves them.
-template <bool kQuant, bool kDecode, bool kSame = false>
+// kRound (stage fusion): the quantised scalars are stored back as their
+// dequantised values (QuantOut::rnd) instead of code words.
+template <bool kQuant, bool kDecode, bool kSame = false, bool kRound = false>
 __global__ void __launch_bounds__(kStreamThreads, (kQuant && !kSame) ? 2 : 3) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
                                                                 const __grid_constant__ StreamPass pass,
                                                                 const __grid_constant__ QuantOut q,
@@ -1697,18 +1699,18 @@ __global__ void __launch_bounds__(kStreamThreads, (kQuant && !kSame) ? 2 : 3) k_
                     pk[2 * r + 1] = quantize_pack_fast(a[r].im, q.t, qlo_d, span, bad, oow);
                 }
             }
-            if (q.rnd) {  // round trip in place (stage fusion), counters below as for codes
+            // round trip in place (stage fusion): the table gathers are issued
+            // here and land while the counters below are reduced
+            double ev[2 * kNV];
+            if constexpr (kRound) {
 #pragma unroll
-                for (int k = 0; k < 2 * kNV; ++k) {
-                    const uint32_t w = pk[k];
-                    const double m = (w & 1u) ? 0.0 : __ldg(q.t.dequant + (w >> 2));
-                    q.rnd[pb + pdep[k >> 1] + lane + ((k & 1) ? im_off : 0)] = (w & 3u) == 2u ? -m : m;
-                }
+                for (int k = 0; k < 2 * kNV; ++k)
+                    ev[k] = (pk[k] & 1u) ? 0.0 : __ldg(q.t.dequant + (pk[k] >> 2));
             }
 #pragma unroll
             for (int r = 0; r < kNV; ++r) {
                 const uint64_t p = pb + pdep[r] + lane;
-                if (!q.rnd) {
+                if constexpr (!kRound) {
                     __stcs(q.pk + p, pk[2 * r]);
                     __stcs(q.pk + p + im_off, pk[2 * r + 1]);
                 }
@@ -1720,6 +1722,11 @@ __global__ void __launch_bounds__(kStreamThreads, (kQuant && !kSame) ? 2 : 3) k_
                     amx[ra][h] = max(amx[ra][h], __reduce_max_sync(0xffffffffu, w));
                     azn[ra][h] += __reduce_add_sync(0xffffffffu, (w & 1u) | ((w & 2u) << 15));
                 }
+            }
+            if constexpr (kRound) {
+#pragma unroll
+                for (int k = 0; k < 2 * kNV; ++k)
+                    q.rnd[pb + pdep[k >> 1] + lane + ((k & 1) ? im_off : 0)] = (pk[k] & 3u) == 2u ? -ev[k] : ev[k];
             }
             ++run_len;
         } else {
@@ -2416,6 +2423,10 @@ bool run_program(cudaStream_t st, const GateProgram& prog, double* buf, uint32_t
             if (fuse && last) {
                 if (fd.rows)
                     k_stream_pass<true, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
+                else if (quant->rnd && p.sp->qbit[kStreamNQ - 1] < 12)
+                    k_stream_pass<true, false, true, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
+                else if (quant->rnd)
+                    k_stream_pass<true, false, false, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
                 else if (p.sp->qbit[kStreamNQ - 1] < 12)
                     k_stream_pass<true, false, true><<<g, b, 0, st>>>(buf, lb, units, *p.sp, *quant, vtab, zf, wz, fd);
                 else
