@@ -56,3 +56,24 @@ def test_fused_equals_unfused_with_budget(gpu, name):
     assert out[0][3] == 0 and out[1][3] > 0 and out[2][3] > 0
     for got in out[1:]:
         assert got[:3] == out[0][:3]
+
+
+@pytest.mark.parametrize("cut", [1, 3, 5])
+def test_fused_resume_from_checkpoint(gpu, port, tmp_path, cut):
+    """A checkpoint taken after `cut` stages (possibly inside what would be a
+    fused run) and resumed with run(): the remaining stages run unfused up to
+    the next fused run's first stage, then fused; the final payloads and the
+    peak equal the oracle's uninterrupted run."""
+    c = gpu.generate_benchmark("qaoa3reg", 16, gpu.BenchmarkParams(layers=2, seed=1))
+    want = port.simulate(16, [g.as_tuple() for g in c.gates], 12, 2, 1e-4)
+    cfg = gpu.Config(block_bits=12, inner_size=2, error_bound=1e-4)
+    path = str(tmp_path / "state.bmqckpt")
+    with gpu.Simulator(c, cfg) as a:
+        a.run_stages(0, cut)
+        a.save(path)
+    with gpu.Simulator(c, cfg) as b:
+        assert b.load(path) == cut
+        rep = b.run()
+        assert b.payloads() == want.payloads
+        assert rep.max_footprint_bytes == want.report["max_footprint_bytes"]
+        assert rep.final_norm == pytest.approx(want.report["final_norm"], rel=1e-10)
