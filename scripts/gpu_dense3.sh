@@ -1,0 +1,16 @@
+#!/bin/bash
+# Dense fused lines only (A/B of a streaming-pass variant change).
+mkdir -p gpurun_out; B=gpurun_out; T=${T:-d3}
+timeout 600 python -m pytest tests/test_fusion_gpu.py -m gpu -q -x 2>&1 | tail -1
+run() { timeout 900 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-link "$@" 2>> $B/${T}.err | tail -1 >> $B/${T}.jsonl; }
+: > $B/${T}.jsonl
+run --workload qaoa3reg --qubits 30 --error-bound 1e-4
+run --workload qaoa3reg --qubits 32 --error-bound 1e-3
+run --workload random --qubits 30 --layers 20
+python - <<'PY'
+import json, os
+for line in open(f"gpurun_out/{os.environ.get('T','d3')}.jsonl"):
+    if not line.startswith("{"): print("!!", line[:300]); continue
+    d = json.loads(line)
+    print(d["config"]["workload"], d["config"].get("stage_fusion"), "ms %.1f" % d["ms_per_step"], "frac %.3f" % d["roofline"]["frac"])
+PY
