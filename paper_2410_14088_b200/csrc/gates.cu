@@ -1449,7 +1449,7 @@ __device__ __forceinline__ C2 shfl_c2(C2 a, uint32_t m) {
 // kRound (stage fusion): the quantised scalars are stored back as their
 // dequantised values (QuantOut::rnd) instead of code words.
 template <bool kQuant, bool kDecode, bool kSame = false, bool kRound = false>
-__global__ void __launch_bounds__(kStreamThreads, (kQuant && (!kSame || kRound)) ? 2 : 3) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
+__global__ void __launch_bounds__(kStreamThreads, kQuant ? 2 : 3) k_stream_pass(double* __restrict__ buf, uint32_t lb, uint64_t nunits,
                                                                 const __grid_constant__ StreamPass pass,
                                                                 const __grid_constant__ QuantOut q,
                                                                 const uint32_t* __restrict__ vtab,
