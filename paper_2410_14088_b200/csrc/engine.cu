@@ -1541,7 +1541,10 @@ bool Engine::fusable(uint64_t s) const {
 void Engine::plan_fusion() {
     fusion_planned_ = true;
     fused_at_.assign(plan_.size(), -1);
-    if (!(cfg_.flags & BMQ_FLAG_STAGE_FUSION) || !cfg_.compress || sharded() || cfg_.host_pool_bytes || L_.b < 12)
+    // (a host level is fine: its payloads are read in place through the
+    // mapped pinned arena and written back by emit_to_host; a disk level is
+    // not, its payloads must be staged before a batch decodes them)
+    if (!(cfg_.flags & BMQ_FLAG_STAGE_FUSION) || !cfg_.compress || sharded() || cfg_.disk_pool_bytes || L_.b < 12)
         return;
     // union inner sets of at most kcap qubits (BMQ_FUSE_INNER, default 8):
     // groups of up to 2^kcap blocks, within one batch; small enough that
