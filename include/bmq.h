@@ -136,8 +136,8 @@ typedef struct bmq_config {
  * code_min / width), and the intermediate stage's payload sizes come from the
  * same per-chunk counters the emit would use, so the payloads, the peak and
  * every reported size equal the unfused run's (codec.hpp:227-344). Not used
- * with a host level, code-domain or identity-skipped (diagonal block-wise)
- * stages, or sharded runs. Default on (bmq_config_default). */
+ * with a disk level, on code-domain, identity-skipped (diagonal block-wise)
+ * or phase-chain stages, or in sharded runs. Default on (bmq_config_default). */
 #define BMQ_FLAG_STAGE_FUSION 0x80u
 
 /* cbq::SimulationReport (engine.hpp:39-53) plus device-side counters. */
